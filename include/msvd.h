@@ -1,0 +1,224 @@
+/*
+ * msvd.h -- C ABI of libmsvd_cuda.so, the B200-native RLOBPCG hot path.
+ *
+ * This is the drop-in boundary for the reference's C++ solve API
+ * (minsvd, /root/reference/proj/include/minsvd/solver.hpp).  Every function
+ * returns an msvd_status, never throws across the boundary, and records a
+ * thread-local message readable with msvd_last_error().  Status codes map 1:1
+ * onto the reference's exception classes (errors.hpp:9-38); the C++ wrapper
+ * include/minsvd_gpu.hpp rethrows them as those classes.
+ *
+ * Layout conventions
+ *   A            device, ROW-major, m_local x n, leading dimension ld >= n
+ *                (ld even enables the 16-byte TMA bulk path; every kernel
+ *                requires 8*ld*rows chunks to be 16-byte aligned).
+ *   n x b blocks column-major (leading dimension n), like minsvd::DenseMatrix.
+ *   m x b blocks column-major (leading dimension m_local).
+ *
+ * Reference interface each entry point replaces is cited beside it.
+ */
+#ifndef MSVD_H_
+#define MSVD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSVD_ABI_VERSION 1
+
+/* errors.hpp:9-38 -> status codes */
+typedef enum msvd_status {
+    MSVD_OK = 0,
+    MSVD_ERR_DIMENSION = 1,   /* minsvd::DimensionError   */
+    MSVD_ERR_IO = 2,          /* minsvd::IoError          */
+    MSVD_ERR_NUMERICAL = 3,   /* minsvd::NumericalError   */
+    MSVD_ERR_CONVERGENCE = 4, /* minsvd::ConvergenceError */
+    MSVD_ERR_CUDA = 5,        /* device failure  -> minsvd::Error */
+    MSVD_ERR_COMM = 6,        /* NCCL / comm failure -> minsvd::Error */
+    MSVD_ERR_INVALID = 7      /* bad handle / null pointer -> minsvd::Error */
+} msvd_status;
+
+/* solver.hpp:14 PrecondKind */
+typedef enum msvd_precond_kind {
+    MSVD_PRECOND_NONE = 0,
+    MSVD_PRECOND_DIAGONAL = 1,
+    MSVD_PRECOND_RANDOMIZED = 2
+} msvd_precond_kind;
+
+/* solver.hpp:25-78 SolverOptions, field by field (same defaults). */
+typedef struct msvd_options {
+    double tol;                 /* <0: default_tolerance(n) = 2 sqrt(n) eps   */
+    int32_t max_iter;           /* <0: 200 if block_size==1 else 100          */
+    int32_t check_every;        /* 5                                          */
+    double stagnation_factor;   /* 1.1                                        */
+    int64_t block_size;         /* 1                                          */
+    uint64_t seed;              /* 0                                          */
+    int64_t sketch_dim;         /* -1: round_up(4n, zeta), skip if m <= 4n     */
+    int32_t zeta;               /* 4                                          */
+    int32_t use_stagnation;     /* 1                                          */
+    int32_t record_timing;      /* 1                                          */
+    int32_t verify_cached_products; /* 0                                      */
+    int32_t store_iterates;     /* 0                                          */
+    int32_t precond_kind;       /* msvd_precond_kind, lobpcg_solve's `kind`   */
+} msvd_options;
+
+/* solver.hpp:93-102 RecordRow */
+typedef struct msvd_record_row {
+    int32_t iter;
+    int32_t pad_;
+    int64_t matvecs_a;
+    int64_t matvecs_at;
+    double wall_ms;
+    double theta;
+    double resid;
+    double relerr;     /* -1 when no truth */
+    double sin_angle;  /* -1 when no truth */
+} msvd_record_row;
+
+/* solver.hpp:87-90 GroundTruth (host memory) */
+typedef struct msvd_truth {
+    double sigma_min;
+    const double* v_min;  /* length n, host */
+} msvd_truth;
+
+/* store_iterates sink: kind 0 = trial basis T (n x k), kind 1 = target block V
+ * (n x b); data is host memory, column-major, valid during the call only.    */
+typedef void (*msvd_iterate_fn)(void* user, int32_t kind, int32_t iter,
+                                const double* data, int64_t rows, int64_t cols);
+
+/* solver.hpp:118-137 SolveResult.  Arrays are caller-owned HOST buffers;
+ * optional ones may be NULL.                                                  */
+typedef struct msvd_result {
+    double* sigma;              /* [b]  ascending from the smallest           */
+    double* v;                  /* [n*b] column-major, ordered like sigma     */
+    msvd_record_row* rows;      /* [rows_capacity]                            */
+    int32_t rows_capacity;      /* >= max_iter + 1 to receive every row       */
+    int32_t rows_count;         /* out: record.rows.size()                    */
+    int32_t status;             /* out: 0 converged, 1 max_iter_reached       */
+    int32_t iterations;         /* out: rows_count - 1                        */
+    double* vtilde;             /* optional [n*n] column-major Preconditioner::vtilde */
+    double* sigma_tilde;        /* optional [n]                               */
+    double sigma_max_estimate;  /* out */
+    int32_t floored;            /* out */
+    int32_t sketch_skipped;     /* out */
+    int64_t floor_count;        /* out */
+    int64_t sketch_dim;         /* out (0 when skipped) */
+    int32_t zeta;               /* out (0 when skipped) */
+    int32_t pad_;
+    int64_t verify_count;       /* out */
+    double max_cache_drift;     /* out */
+    int64_t degenerate_replacements; /* out */
+    msvd_iterate_fn iterate_cb; /* store_iterates sink, may be NULL           */
+    void* iterate_user;
+    /* timing breakdown (device events, ms); not part of the reference record */
+    double t_sketch_ms, t_svd_ms, t_init_ms, t_loop_ms, t_total_ms;
+} msvd_result;
+
+typedef struct msvd_ctx msvd_ctx;
+typedef struct msvd_matrix msvd_matrix;
+
+/* Communicator for row-sharded runs.  kind 0 = single rank,
+ * 1 = NCCL (unique id from rank 0, 128 bytes), 2 = in-process fake group
+ * (several host threads on one GPU, host-mediated reductions; for tests).   */
+typedef struct msvd_ctx_desc {
+    int32_t device;             /* CUDA ordinal                               */
+    int32_t comm_kind;          /* 0 none, 1 nccl, 2 fake                     */
+    int32_t nranks;
+    int32_t rank;
+    uint8_t nccl_id[128];       /* comm_kind 1                                */
+    void* fake_group;           /* comm_kind 2: from msvd_fake_group_create   */
+    void* stream;               /* cudaStream_t or NULL (library creates one) */
+} msvd_ctx_desc;
+
+/* ---- library / context ------------------------------------------------ */
+int32_t msvd_abi_version(void);
+const char* msvd_last_error(void);
+const char* msvd_status_name(int32_t status);
+void msvd_options_default(msvd_options* o);
+/* solver.hpp:83-85 */
+double msvd_default_tolerance(int64_t n);
+/* Host-only validation of solver.cpp:306-315 + prepare() 128-145 checks; the
+ * same status solve would return before touching the device.               */
+int32_t msvd_validate_options(int64_t m, int64_t n, const msvd_options* o,
+                              const msvd_truth* truth);
+/* row range [row0, row0+rows) owned by `rank` when m rows are split evenly */
+void msvd_shard_rows(int64_t m, int32_t nranks, int32_t rank, int64_t* row0,
+                     int64_t* rows);
+
+int32_t msvd_get_nccl_unique_id(uint8_t out[128]);
+int32_t msvd_fake_group_create(int32_t nranks, void** group);
+int32_t msvd_fake_group_destroy(void* group);
+int32_t msvd_ctx_create(const msvd_ctx_desc* desc, msvd_ctx** out);
+int32_t msvd_ctx_destroy(msvd_ctx* ctx);
+int32_t msvd_ctx_synchronize(msvd_ctx* ctx);
+
+/* ---- operator (operator.hpp:41-56 DenseOperator over device memory) ----- */
+/* Borrowed device pointer, row-major m_local x n with leading dim ld; row0 =
+ * global index of the first local row (keys the sketch), m_global = total.  */
+int32_t msvd_matrix_attach(msvd_ctx* ctx, const double* dA, int64_t m_local,
+                           int64_t n, int64_t ld, int64_t row0,
+                           int64_t m_global, msvd_matrix** out);
+int32_t msvd_matrix_detach(msvd_matrix* mat);
+/* operator.cpp:7-12 apply_block: dY (m_local x b) = A dX (n x b)           */
+int32_t msvd_apply(msvd_matrix* mat, const double* dX, int64_t b, double* dY);
+/* operator.cpp:14-19 apply_adjoint_block: dX (n x b) = A^T dY (m_local x b),
+ * summed over ranks (allreduce) for sharded matrices.                       */
+int32_t msvd_apply_adjoint(msvd_matrix* mat, const double* dY, int64_t b,
+                           double* dX);
+/* operator.cpp:151-161 column_norms: dNorms (n)                             */
+int32_t msvd_column_norms(msvd_matrix* mat, double* dNorms);
+
+/* ---- hot-path primitives --------------------------- */
+/* sketch.cpp:36-60 build_sparsestack into device arrays (m*zeta each)       */
+int32_t msvd_build_sparsestack(msvd_ctx* ctx, int64_t d, int64_t m, int32_t zeta,
+                               uint64_t seed, uint32_t* dPositions,
+                               int8_t* dSigns);
+/* sketch.cpp:75-95 / 120-126 sketch_apply(S, A): dSA (d x n, col-major),
+ * reduced over ranks.                                                       */
+int32_t msvd_sketch(msvd_matrix* mat, int64_t d, int32_t zeta, uint64_t seed,
+                    double* dSA);
+/* precond.cpp:11-36 build_preconditioner from dSA (rows x n col-major):
+ * dVt (n x n col-major), dSig (n), floored values raised.                   */
+int32_t msvd_precond_build(msvd_ctx* ctx, const double* dSA, int64_t rows,
+                           int64_t n, double* dVt, double* dSig,
+                           double* sigma_max_estimate, int64_t* floor_count);
+/* precond.cpp:38-48 precond_apply per column: dW = Vt diag(sig^-2) Vt^T dR  */
+int32_t msvd_precond_apply(msvd_ctx* ctx, const double* dVt, const double* dSig,
+                           int64_t n, const double* dR, int64_t b, double* dW);
+/* svd.cpp:21-55 householder_qr R factor of a tall dT (rows x k col-major),
+ * computed as a TSQR; dR (k x k col-major, upper).  Row signs are the
+ * reference's only up to +-1 (R^T R identical).                             */
+int32_t msvd_tsqr_r(msvd_ctx* ctx, const double* dT, int64_t rows, int64_t k,
+                    double* dR);
+/* svd.cpp:180-252 dense_svd(B, false) of a small square dB (k x k, k<=32)
+ * already reduced to R: sigma descending, V sign-fixed.                     */
+int32_t msvd_small_svd(msvd_ctx* ctx, const double* dB, int64_t k,
+                       double* dSigma, double* dV);
+
+/* ---- full solve (solver.cpp:301-477, 479-489) ------------------------- */
+int32_t msvd_lobpcg_solve(msvd_matrix* mat, const msvd_options* opts,
+                          const msvd_truth* truth, msvd_result* res);
+/* solver.cpp:479-484 (block size forced to 1) */
+int32_t msvd_rlobpcg_single(msvd_matrix* mat, const msvd_options* opts,
+                            const msvd_truth* truth, msvd_result* res);
+/* solver.cpp:486-489 (precond_kind forced to randomized) */
+int32_t msvd_rlobpcg_block(msvd_matrix* mat, const msvd_options* opts,
+                           const msvd_truth* truth, msvd_result* res);
+/* End-to-end convenience: A in HOST memory (row-major, pinned or pageable);
+ * copies the local rows to the device inside the call, then solves.        */
+int32_t msvd_solve_host(msvd_ctx* ctx, const double* hA, int64_t m_local,
+                        int64_t n, int64_t ld, int64_t row0, int64_t m_global,
+                        const msvd_options* opts, const msvd_truth* truth,
+                        msvd_result* res);
+
+/* Number of library kernels launched since ctx creation (bench evidence). */
+int64_t msvd_launch_count(msvd_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MSVD_H_ */
