@@ -214,6 +214,10 @@ int32_t msvd_solve_host(msvd_ctx* ctx, const double* hA, int64_t m_local,
                         const msvd_options* opts, const msvd_truth* truth,
                         msvd_result* res);
 
+/* sizeof of {msvd_options, msvd_record_row, msvd_truth, msvd_result,
+ * msvd_ctx_desc} into out[0..n) (binding self-check; host only). */
+void msvd_abi_sizes(int64_t* out, int32_t n);
+
 /* Number of library kernels launched since ctx creation (bench evidence). */
 int64_t msvd_launch_count(msvd_ctx* ctx);
 

@@ -889,6 +889,24 @@ int orc_synth_dense(const double *sigma, int64_t n, int64_t m, uint64_t seed, do
     LEAVE();
 }
 
+/* Same assembly without spectrum validation: configs with exact zeros (C3)
+ * are assembled directly, since spectrum() rejects them (matgen.cpp:41-47). */
+int orc_assemble_svd(const double *sigma, int64_t n, int64_t m, uint64_t seed, double *a_colmajor, double *v_min) {
+    ENTER();
+    if (m < n) raise_err(MSVD_ERR_DIMENSION, "synth: need rows >= columns");
+    sm64 ku = sm_keyed(seed, 0x55u), kv = sm_keyed(seed, 0x56u);
+    mat u = haar(m, n, sm_u64(&ku));
+    mat v = haar(n, n, sm_u64(&kv));
+    memcpy(v_min, col(v, n - 1), sizeof(double) * (size_t)n);
+    for (int64_t j = 0; j < n; ++j) {
+        double *c = col(u, j);
+        for (int64_t i = 0; i < m; ++i) c[i] *= sigma[j];
+    }
+    mat a = matmul(u, transpose(v));
+    memcpy(a_colmajor, a.p, sizeof(double) * (size_t)(m * n));
+    LEAVE();
+}
+
 int orc_lobpcg_solve(const double *a, int64_t m, int64_t n, const msvd_options *o, const msvd_truth *truth,
                      msvd_result *res) {
     ENTER();

@@ -151,6 +151,19 @@ class Oracle:
         self._check(self._synth(_p(sigma), n, m, seed, _p(a), _p(vmin)))
         return a, vmin
 
+    def assemble_svd(self, sigma, m, seed):
+        """U diag(sigma) V^T with synth's factors but no spectrum validation
+        (zeros allowed); port only."""
+        sigma = _f64(sigma)
+        n = sigma.size
+        a = np.empty((m, n), dtype=np.float64, order="F")
+        vmin = np.empty(n)
+        f = self.lib.orc_assemble_svd
+        f.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_int64, C.c_uint64, C.POINTER(C.c_double),
+                      C.POINTER(C.c_double)]
+        self._check(f(_p(sigma), n, m, seed, _p(a), _p(vmin)))
+        return a, vmin
+
     def haar_orthonormal(self, m, n, seed):
         q = np.empty((m, n), order="F")
         self._check(self._haar(m, n, seed, _p(q)))

@@ -1,0 +1,899 @@
+// Host side of libmsvd_cuda.so: the C ABI of include/msvd.h and the device
+// solve loop that replaces lobpcg_solve (solver.cpp:301-477).
+//
+// The host only orchestrates: it validates options exactly like the
+// reference (solver.cpp:306-315, prepare() :128-145, build_sparsestack
+// :36-41), launches the kernels of one iteration back to back on the context
+// stream, and synchronizes only at check iterations (solver.cpp:439) to read
+// the device stop/error word.  Every number the solver produces is computed
+// on the GPU; there is no CPU fallback.
+#include <algorithm>
+#include <cstddef>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "msvd_internal.h"
+
+namespace msvd {
+
+thread_local std::string g_last_error;
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Fail(code, msg); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(MSVD_ERR_CUDA, std::string(cudaGetErrorString(e)) + " in " + what);
+}
+
+void* Ctx::ensure_scratch(size_t bytes) {
+    if (bytes > scratch_bytes) {
+        if (scratch) MSVD_CUDA(cudaFree(scratch));
+        scratch = nullptr;
+        MSVD_CUDA(cudaMalloc(&scratch, bytes));
+        scratch_bytes = bytes;
+    }
+    return scratch;
+}
+
+namespace {
+
+template <class F>
+int32_t guard(F&& f) {
+    try {
+        f();
+        return MSVD_OK;
+    } catch (const Fail& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return MSVD_ERR_INVALID;
+    }
+}
+
+constexpr double kEps = 2.220446049250313e-16;
+
+double default_tol(int64_t n) { return 2.0 * std::sqrt(static_cast<double>(n)) * kEps; }
+
+struct Plan {
+    double tol;
+    int max_iter;
+    bool skip;
+    int64_t d;
+};
+
+// solver.cpp:306-315 + prepare() :128-145 + build_sparsestack :36-41, in order
+Plan validate(int64_t m, int64_t n, const msvd_options& o) {
+    const int64_t b = o.block_size;
+    if (m < n) fail(MSVD_ERR_DIMENSION, "solver: matrix must have at least as many rows as columns");
+    if (b < 1) fail(MSVD_ERR_DIMENSION, "solver: block size must be positive");
+    if (n < 3 * b) fail(MSVD_ERR_DIMENSION, "solver: need at least 3x block size columns");
+    Plan p{};
+    p.tol = o.tol < 0.0 ? default_tol(n) : o.tol;
+    if (!(p.tol >= 0.0 && p.tol < 1.0)) fail(MSVD_ERR_NUMERICAL, "solver: tol must lie in [0, 1)");
+    p.max_iter = o.max_iter < 0 ? (b == 1 ? 200 : 100) : o.max_iter;
+    if (p.max_iter < 0 || o.check_every < 1)
+        fail(MSVD_ERR_NUMERICAL, "solver: max_iter must be >= 0 and check_every >= 1");
+    p.skip = o.sketch_dim < 0 && m <= 4 * n;
+    if (!p.skip) {
+        if (o.sketch_dim < 0 && o.zeta <= 0)
+            fail(MSVD_ERR_DIMENSION, "round_up_to_multiple: zeta must be positive");
+        int64_t d = o.sketch_dim;
+        if (d < 0) d = (4 * n) % o.zeta == 0 ? 4 * n : 4 * n + (o.zeta - (4 * n) % o.zeta);
+        if (d < n) fail(MSVD_ERR_DIMENSION, "solver: sketch dimension below column count");
+        if (d <= 0 || m <= 0) fail(MSVD_ERR_DIMENSION, "build_sparsestack: dimensions must be positive");
+        if (o.zeta <= 0 || o.zeta > d) fail(MSVD_ERR_DIMENSION, "build_sparsestack: zeta must be in [1, d]");
+        if (d % o.zeta != 0)
+            fail(MSVD_ERR_DIMENSION, "build_sparsestack: zeta must divide d; use round_up_to_multiple(d, zeta) = " +
+                                         std::to_string(d + (o.zeta - d % o.zeta)));
+        p.d = d;
+    }
+    // limits of this build's register-tiled kernels (not reference errors)
+    if (b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size above 8 is not supported by this build");
+    if (n > kMaxN) fail(MSVD_ERR_DIMENSION, "msvd: more than 2048 columns is not supported by this build");
+    if (o.precond_kind < 0 || o.precond_kind > 2) fail(MSVD_ERR_INVALID, "msvd: unknown preconditioner kind");
+    return p;
+}
+
+// one cudaMalloc for all per-solve buffers
+struct Arena {
+    std::vector<std::pair<void**, size_t>> req;
+    void* base = nullptr;
+    template <class T>
+    void add(T** p, size_t count) {
+        req.push_back({reinterpret_cast<void**>(p), ((sizeof(T) * std::max<size_t>(count, 1) + 255) / 256) * 256});
+    }
+    void commit() {
+        size_t tot = 0;
+        for (auto& r : req) tot += r.second;
+        MSVD_CUDA(cudaMalloc(&base, tot));
+        size_t off = 0;
+        for (auto& r : req) {
+            *r.first = static_cast<unsigned char*>(base) + off;
+            off += r.second;
+        }
+    }
+    ~Arena() {
+        if (base) cudaFree(base);
+    }
+};
+
+std::string err_message(const DevState& s) {
+    char buf[160];
+    switch (s.err_code) {
+        case kErrNonfiniteW:
+            std::snprintf(buf, sizeof buf, "solver: non-finite preconditioned residual at iteration %d", s.err_iter);
+            return buf;
+        case kErrNonfiniteAT:
+            std::snprintf(buf, sizeof buf, "solver: non-finite trial products at iteration %d", s.err_iter);
+            return buf;
+        case kErrJacobi:
+            return "one_sided_jacobi: no convergence after 60 sweeps";
+        case kErrCgs2:
+            return "cgs2: could not complete an orthonormal block";
+        case kErrOrth:
+            return "solver: history update basis collapsed";
+        case kErrDrift:
+            std::snprintf(buf, sizeof buf, "solver: cached product drifted from a fresh one at iteration %d",
+                          s.err_iter);
+            return buf;
+        case kErrNonfiniteA:
+            return "DenseOperator: non-finite entry";
+        default:
+            return "msvd: device error " + std::to_string(s.err_code);
+    }
+}
+
+DevState read_state(Ctx& c, const DevState* st) {
+    DevState h;
+    MSVD_CUDA(cudaMemcpyAsync(&h, st, sizeof(DevState), cudaMemcpyDeviceToHost, c.stream));
+    MSVD_CUDA(cudaStreamSynchronize(c.stream));
+    if (h.err_code != kErrNone) fail(MSVD_ERR_NUMERICAL, err_message(h));
+    return h;
+}
+
+void set_device(const Ctx& c) { MSVD_CUDA(cudaSetDevice(c.device)); }
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+// ---------------------------------------------------------------------------
+// lobpcg_solve on a device (row-sharded) dense operator
+// ---------------------------------------------------------------------------
+void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_result* res) {
+    Ctx& c = M->ctx->c;
+    set_device(c);
+    Comm& comm = *c.comm;
+    const int64_t n = M->n, m = M->m_global, ml = M->m_local;
+    const Plan plan = validate(m, n, o);
+    const int b = static_cast<int>(o.block_size);
+    const int max_iter = plan.max_iter;
+    const int kind = o.precond_kind;
+    if (!res || !res->sigma || !res->v) fail(MSVD_ERR_INVALID, "msvd: result buffers missing");
+    if (truth && !truth->v_min) fail(MSVD_ERR_DIMENSION, "solver: ground-truth vector length mismatch");
+    const StreamGeom geom = make_geom(c, M->A, ml, static_cast<int32_t>(n), M->ld);
+    const int nparts = tsqr_parts(c);
+    const int ranks = comm.nranks();
+    const int kmax = 3 * b;
+    const int nblk = static_cast<int>(ceil_div(n, 256));
+
+    for (int i = 0; i < 6; ++i)
+        if (!c.ev[i]) MSVD_CUDA(cudaEventCreate(&c.ev[i]));
+    MSVD_CUDA(cudaEventRecord(c.ev[0], c.stream));
+
+    Arena ar;
+    DevState* st;
+    msvd_record_row* rows;
+    double *rh, *th, *Vcol, *Vrow, *sig, *AVb[2], *AXb[2], *AW, *Vb[2], *Xb[2], *W, *Rres, *tmp, *Cm, *Gpart,
+        *Gout, *nrm, *Rparts, *Rall, *tv, *dinv, *cpart, *fresh;
+    ar.add(&st, 1);
+    ar.add(&rows, max_iter + 2);
+    ar.add(&rh, max_iter + 2);
+    ar.add(&th, max_iter + 2);
+    ar.add(&Vcol, n * n);
+    ar.add(&Vrow, n * n);
+    ar.add(&sig, n);
+    for (int i = 0; i < 2; ++i) {
+        ar.add(&AVb[i], ml * b);
+        ar.add(&AXb[i], ml * b);
+        ar.add(&Vb[i], n * b);
+        ar.add(&Xb[i], n * b);
+    }
+    ar.add(&AW, ml * b);
+    ar.add(&W, n * b);
+    ar.add(&Rres, n * b);
+    ar.add(&tmp, n * b);
+    ar.add(&Cm, kMaxK * 2 * kMaxB);
+    ar.add(&Gpart, static_cast<size_t>(geom.grid) * b * n);
+    ar.add(&Gout, n * b);
+    ar.add(&nrm, static_cast<size_t>(b) * nblk);
+    ar.add(&Rparts, static_cast<size_t>(nparts) * kmax * kmax);
+    ar.add(&Rall, static_cast<size_t>(ranks) * nparts * kmax * kmax);
+    ar.add(&tv, n);
+    ar.add(&dinv, n);
+    ar.add(&cpart, static_cast<size_t>(c.num_sms) * n);
+    ar.add(&fresh, o.verify_cached_products ? ml * b : 1);
+    ar.commit();
+
+    launch_state_init(c, st, o.seed);
+    double* theta_dev =
+        reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(st) + offsetof(DevState, theta));
+    if (truth) MSVD_CUDA(cudaMemcpyAsync(tv, truth->v_min, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+
+    // ---- prepare (solver.cpp:128-145) ----
+    double sigma1 = 0.0;
+    int64_t nfloor = 0;
+    {
+        double* SA = nullptr;
+        int64_t sa_rows = 0;
+        if (plan.skip) {
+            // m <= 4n: P from a direct SVD of A (solver.cpp:132-134).  Assemble the
+            // global A (exact: other ranks contribute zeros) and transpose it.
+            double* Arm = nullptr;
+            MSVD_CUDA(cudaMalloc(&Arm, sizeof(double) * m * n));
+            MSVD_CUDA(cudaMalloc(&SA, sizeof(double) * m * n));
+            MSVD_CUDA(cudaMemsetAsync(Arm, 0, sizeof(double) * m * n, c.stream));
+            if (ml > 0)
+                MSVD_CUDA(cudaMemcpy2DAsync(Arm + M->row0 * n, sizeof(double) * n, M->A, sizeof(double) * M->ld,
+                                            sizeof(double) * n, ml, cudaMemcpyDeviceToDevice, c.stream));
+            comm.allreduce_sum(Arm, static_cast<size_t>(m * n), c.stream);
+            launch_transpose_rm_to_cm(c, Arm, m, n, n, SA);
+            MSVD_CUDA(cudaStreamSynchronize(c.stream));
+            MSVD_CUDA(cudaFree(Arm));
+            sa_rows = m;
+            // DenseOperator construction rejects non-finite data (operator.cpp:35-37)
+            launch_colnorms(c, make_geom(c, M->A, ml, static_cast<int32_t>(n), M->ld), cpart, tmp);
+        } else {
+            MSVD_CUDA(cudaMalloc(&SA, sizeof(double) * plan.d * n));
+            sketch_dev(c, geom, M->row0, plan.d, o.zeta, o.seed, SA, st);
+            comm.allreduce_sum(SA, static_cast<size_t>(plan.d * n), c.stream);
+            sa_rows = plan.d;
+        }
+        MSVD_CUDA(cudaEventRecord(c.ev[1], c.stream));
+        try {
+            read_state(c, st);  // non-finite A surfaces here, like the DenseOperator ctor
+            if (plan.skip) {
+                // finite check of A for the skip path: column sums of squares
+                std::vector<double> h(n);
+                MSVD_CUDA(cudaMemcpy(h.data(), tmp, sizeof(double) * n, cudaMemcpyDeviceToHost));
+                for (double v : h)
+                    if (!std::isfinite(v)) fail(MSVD_ERR_NUMERICAL, "DenseOperator: non-finite entry");
+            }
+            precond_build_dev(c, SA, sa_rows, n, Vcol, Vrow, sig, &sigma1, &nfloor);
+        } catch (...) {
+            cudaFree(SA);
+            throw;
+        }
+        MSVD_CUDA(cudaFree(SA));
+        if (ranks > 1) {  // every rank uses rank 0's factorization bit for bit
+            comm.bcast(Vcol, static_cast<size_t>(n * n), 0, c.stream);
+            comm.bcast(Vrow, static_cast<size_t>(n * n), 0, c.stream);
+            comm.bcast(sig, static_cast<size_t>(n), 0, c.stream);
+            double hs[2] = {sigma1, static_cast<double>(nfloor)};
+            MSVD_CUDA(cudaMemcpyAsync(tmp, hs, sizeof(hs), cudaMemcpyHostToDevice, c.stream));
+            comm.bcast(tmp, 2, 0, c.stream);
+            MSVD_CUDA(cudaMemcpyAsync(hs, tmp, sizeof(hs), cudaMemcpyDeviceToHost, c.stream));
+            MSVD_CUDA(cudaStreamSynchronize(c.stream));
+            sigma1 = hs[0];
+            nfloor = static_cast<int64_t>(hs[1]);
+        }
+    }
+    MSVD_CUDA(cudaEventRecord(c.ev[2], c.stream));
+    if (kind == MSVD_PRECOND_DIAGONAL) {  // solver.cpp:336-340
+        launch_colnorms(c, geom, cpart, dinv);
+        comm.allreduce_sum(dinv, static_cast<size_t>(n), c.stream);
+        std::vector<double> h(n);
+        MSVD_CUDA(cudaMemcpyAsync(h.data(), dinv, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+        for (double& v : h) {
+            const double cn = std::sqrt(v);
+            v = cn > 0.0 ? 1.0 / (cn * cn) : 1.0;
+        }
+        MSVD_CUDA(cudaMemcpyAsync(dinv, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+    }
+
+    auto cols_m = [&](std::initializer_list<std::pair<double*, int>> parts) {
+        Cols t{};
+        int at = 0;
+        for (auto& pr : parts)
+            for (int j = 0; j < pr.second; ++j) t.p[at++] = pr.first + static_cast<int64_t>(j) * ml;
+        return t;
+    };
+    auto cols_n = [&](std::initializer_list<std::pair<double*, int>> parts) {
+        Cols t{};
+        int at = 0;
+        for (auto& pr : parts)
+            for (int j = 0; j < pr.second; ++j) t.p[at++] = pr.first + static_cast<int64_t>(j) * n;
+        return t;
+    };
+    auto tsqr_all = [&](Cols T, int k, int iter) -> std::pair<const double*, int> {
+        launch_tsqr(c, T, ml, k, Rparts, st, iter);
+        if (ranks == 1) return {Rparts, nparts};
+        comm.allgather(Rparts, Rall, static_cast<size_t>(nparts) * k * k, c.stream);
+        return {Rall, nparts * ranks};
+    };
+    auto residual = [&](const double* V) {  // G = A^T Y summed over ranks; R = G - theta^2 V
+        if (ranks == 1) {
+            launch_reduce_g(c, Gpart, geom.grid, n, b, V, st, 1, Rres, nrm, nblk);
+        } else {
+            launch_reduce_g(c, Gpart, geom.grid, n, b, V, st, 0, Gout, nrm, nblk);
+            comm.allreduce_sum(Gout, static_cast<size_t>(n * b), c.stream);
+            launch_reduce_g(c, Gout, 1, n, b, V, st, 1, Rres, nrm, nblk);
+        }
+    };
+    ControlArgs ca{};
+    ca.nblk = nblk;
+    ca.nrm_part = nrm;
+    ca.b = b;
+    ca.n = n;
+    ca.truth_v = truth ? tv : nullptr;
+    ca.truth_sigma = truth ? truth->sigma_min : 0.0;
+    ca.st = st;
+    ca.rows = rows;
+    ca.rh = rh;
+    ca.th = th;
+    ca.sigma1 = sigma1;
+    ca.tol = plan.tol;
+    ca.factor = o.stagnation_factor;
+    ca.use_stag = o.use_stagnation;
+    ca.timing = o.record_timing;
+
+    std::vector<double> host_t, host_v;
+    auto emit = [&](int kindv, int iter, std::initializer_list<std::pair<double*, int>> parts) {
+        if (!res->iterate_cb) return;
+        int cols = 0;
+        for (auto& pr : parts) cols += pr.second;
+        std::vector<double>& h = kindv == 0 ? host_t : host_v;
+        h.resize(static_cast<size_t>(n) * cols);
+        int at = 0;
+        for (auto& pr : parts) {
+            if (pr.second)
+                MSVD_CUDA(cudaMemcpyAsync(h.data() + static_cast<size_t>(at) * n, pr.first,
+                                          sizeof(double) * n * pr.second, cudaMemcpyDeviceToHost, c.stream));
+            at += pr.second;
+        }
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+        res->iterate_cb(res->iterate_user, kindv, iter, h.data(), n, cols);
+    };
+
+    // ---- initial block and Rayleigh-Ritz (solver.cpp:349-371) ----
+    launch_copy_cols(c, Vcol, n, n - b, n, b, W);  // sketch_and_solve_init: last b columns
+    OutCols out{};
+    for (int j = 0; j < b; ++j) out.p[j] = AW + static_cast<int64_t>(j) * ml;
+    launch_apply(c, geom, W, b, out);
+    {
+        auto parts = tsqr_all(cols_m({{AW, b}}), b, -1);
+        RRArgs ra{};
+        ra.Rparts = parts.first;
+        ra.nparts = parts.second;
+        ra.k = b;
+        ra.b = b;
+        ra.mode = 0;
+        ra.T = cols_n({{W, b}});
+        ra.n = n;
+        ra.Vout = Vb[0];
+        ra.Xout = nullptr;
+        ra.Cm = Cm;
+        ra.theta_out = theta_dev;
+        ra.st = st;
+        ra.iter = -1;
+        launch_rr(c, ra);
+        OutCols yo{};
+        for (int j = 0; j < b; ++j) yo.p[j] = AVb[0] + static_cast<int64_t>(j) * ml;
+        launch_gram(c, geom, cols_m({{AW, b}}), b, Cm, b, b, yo, false, Gpart);
+        residual(Vb[0]);
+        ca.V = Vb[0];
+        ca.row = 0;
+        ca.check = 0;
+        launch_control(c, ca);
+    }
+    if (o.store_iterates) emit(1, 0, {{Vb[0], b}});
+    MSVD_CUDA(cudaEventRecord(c.ev[3], c.stream));
+
+    int cur = 0;  // index of the current V / X / AV / AX buffers
+    int status = 1;
+    int last_row = 0;
+    int64_t verify_count = 0;
+    for (int i = 0; i < max_iter; ++i) {
+        const bool first = (i == 0);
+        const int nx = first ? 0 : b;
+        const int k = b + nx + b;
+        const int nxt = cur ^ 1;
+        launch_precond(c, kind, Vcol, Vrow, sig, dinv, n, Rres, b, tmp, W, st, i);
+        launch_cgs2(c, W, n, b, cols_n({{Vb[cur], b}, {Xb[cur], nx}}), b + nx, st, i);
+        for (int j = 0; j < b; ++j) out.p[j] = AW + static_cast<int64_t>(j) * ml;
+        launch_apply(c, geom, W, b, out);
+        const Cols Tm = cols_m({{AVb[cur], b}, {AXb[cur], nx}, {AW, b}});
+        auto parts = tsqr_all(Tm, k, i);
+        RRArgs ra{};
+        ra.Rparts = parts.first;
+        ra.nparts = parts.second;
+        ra.k = k;
+        ra.b = b;
+        ra.mode = 1;
+        ra.T = cols_n({{Vb[cur], b}, {Xb[cur], nx}, {W, b}});
+        ra.n = n;
+        ra.Vout = Vb[nxt];
+        ra.Xout = Xb[nxt];
+        ra.Cm = Cm;
+        ra.theta_out = theta_dev;
+        ra.st = st;
+        ra.iter = i;
+        launch_rr(c, ra);
+        OutCols yo{};
+        for (int j = 0; j < b; ++j) {
+            yo.p[j] = AVb[nxt] + static_cast<int64_t>(j) * ml;
+            yo.p[b + j] = AXb[nxt] + static_cast<int64_t>(j) * ml;
+        }
+        launch_gram(c, geom, Tm, k, Cm, 2 * b, b, yo, false, Gpart);
+        residual(Vb[nxt]);
+        ca.V = Vb[nxt];
+        ca.row = i + 1;
+        ca.check = (i % o.check_every) == 0;
+        launch_control(c, ca);
+        last_row = i + 1;
+        if (o.store_iterates) {
+            emit(0, i, {{Vb[cur], b}, {Xb[cur], nx}, {W, b}});
+            emit(1, i + 1, {{Vb[nxt], b}});
+        }
+        if (o.verify_cached_products && (i + 1) % 25 == 0) {  // solver.cpp:430-436
+            OutCols fo{};
+            for (int j = 0; j < b; ++j) fo.p[j] = fresh + static_cast<int64_t>(j) * ml;
+            launch_apply(c, geom, Vb[nxt], b, fo);
+            launch_drift(c, fresh, AVb[nxt], ml * b, st, 1e-10 * sigma1, i);
+            if (ranks > 1) {
+                double* dm = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(st) +
+                                                       offsetof(DevState, max_drift));
+                comm.allreduce_max(dm, 1, c.stream);
+                launch_drift(c, fresh, fresh, 0, st, 1e-10 * sigma1, i);
+            }
+            verify_count += b;
+        }
+        cur = nxt;
+        if (ca.check) {
+            const DevState h = read_state(c, st);
+            if (h.stop) {
+                status = 0;
+                break;
+            }
+        }
+    }
+    MSVD_CUDA(cudaEventRecord(c.ev[4], c.stream));
+    const DevState hs = read_state(c, st);
+
+    // ---- results (solver.cpp:469-476): ascending from the smallest ----
+    std::vector<double> V(static_cast<size_t>(n) * b);
+    MSVD_CUDA(cudaMemcpyAsync(V.data(), Vb[cur], sizeof(double) * n * b, cudaMemcpyDeviceToHost, c.stream));
+    const int nrows = last_row + 1;
+    std::vector<msvd_record_row> hrows(nrows);
+    MSVD_CUDA(cudaMemcpyAsync(hrows.data(), rows, sizeof(msvd_record_row) * nrows, cudaMemcpyDeviceToHost, c.stream));
+    if (res->vtilde)
+        MSVD_CUDA(cudaMemcpyAsync(res->vtilde, Vcol, sizeof(double) * n * n, cudaMemcpyDeviceToHost, c.stream));
+    if (res->sigma_tilde)
+        MSVD_CUDA(cudaMemcpyAsync(res->sigma_tilde, sig, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+    MSVD_CUDA(cudaEventRecord(c.ev[5], c.stream));
+    MSVD_CUDA(cudaStreamSynchronize(c.stream));
+    for (int j = 0; j < b; ++j) {
+        res->sigma[j] = hs.theta[b - 1 - j];
+        std::memcpy(res->v + static_cast<size_t>(j) * n, V.data() + static_cast<size_t>(b - 1 - j) * n,
+                    sizeof(double) * n);
+    }
+    res->rows_count = nrows;
+    res->iterations = nrows - 1;
+    for (int r = 0; r < nrows && r < res->rows_capacity; ++r) res->rows[r] = hrows[r];
+    res->status = status;
+    res->sigma_max_estimate = sigma1;
+    res->floored = nfloor > 0;
+    res->floor_count = nfloor;
+    res->sketch_skipped = plan.skip;
+    res->sketch_dim = plan.skip ? 0 : plan.d;
+    res->zeta = plan.skip ? 0 : o.zeta;
+    res->verify_count = verify_count;
+    res->max_cache_drift = hs.max_drift;
+    res->degenerate_replacements = hs.replacements;
+    res->t_sketch_ms = ev_ms(c.ev[0], c.ev[1]);
+    res->t_svd_ms = ev_ms(c.ev[1], c.ev[2]);
+    res->t_init_ms = ev_ms(c.ev[2], c.ev[3]);
+    res->t_loop_ms = ev_ms(c.ev[3], c.ev[4]);
+    res->t_total_ms = ev_ms(c.ev[0], c.ev[5]);
+}
+
+DevState* prim_state(Ctx& c) {
+    if (!c.pstate) {
+        MSVD_CUDA(cudaMalloc(&c.pstate, sizeof(DevState)));
+        MSVD_CUDA(cudaMemsetAsync(c.pstate, 0, sizeof(DevState), c.stream));
+    }
+    return c.pstate;
+}
+
+void need(const void* p, const char* what) {
+    if (!p) fail(MSVD_ERR_INVALID, std::string("msvd: null ") + what);
+}
+
+}  // namespace
+}  // namespace msvd
+
+using namespace msvd;
+
+extern "C" {
+
+int32_t msvd_abi_version(void) { return MSVD_ABI_VERSION; }
+const char* msvd_last_error(void) { return g_last_error.c_str(); }
+
+const char* msvd_status_name(int32_t s) {
+    switch (s) {
+        case MSVD_OK: return "ok";
+        case MSVD_ERR_DIMENSION: return "DimensionError";
+        case MSVD_ERR_IO: return "IoError";
+        case MSVD_ERR_NUMERICAL: return "NumericalError";
+        case MSVD_ERR_CONVERGENCE: return "ConvergenceError";
+        case MSVD_ERR_CUDA: return "CudaError";
+        case MSVD_ERR_COMM: return "CommError";
+        default: return "Error";
+    }
+}
+
+void msvd_options_default(msvd_options* o) {
+    if (!o) return;
+    o->tol = -1.0;
+    o->max_iter = -1;
+    o->check_every = 5;
+    o->stagnation_factor = 1.1;
+    o->block_size = 1;
+    o->seed = 0;
+    o->sketch_dim = -1;
+    o->zeta = 4;
+    o->use_stagnation = 1;
+    o->record_timing = 1;
+    o->verify_cached_products = 0;
+    o->store_iterates = 0;
+    o->precond_kind = MSVD_PRECOND_RANDOMIZED;
+}
+
+double msvd_default_tolerance(int64_t n) { return default_tol(n); }
+
+int32_t msvd_validate_options(int64_t m, int64_t n, const msvd_options* o, const msvd_truth* truth) {
+    return guard([&] {
+        need(o, "options");
+        validate(m, n, *o);
+        if (truth && !truth->v_min) fail(MSVD_ERR_DIMENSION, "solver: ground-truth vector length mismatch");
+    });
+}
+
+void msvd_shard_rows(int64_t m, int32_t nranks, int32_t rank, int64_t* row0, int64_t* rows) {
+    const int64_t a = (m * rank) / nranks, b = (m * (rank + 1)) / nranks;
+    if (row0) *row0 = a;
+    if (rows) *rows = b - a;
+}
+
+int32_t msvd_get_nccl_unique_id(uint8_t out[128]) {
+    return guard([&] { nccl_unique_id(out); });
+}
+
+int32_t msvd_fake_group_create(int32_t nranks, void** group) {
+    return guard([&] {
+        need(group, "group");
+        if (nranks < 1) fail(MSVD_ERR_INVALID, "msvd: nranks must be positive");
+        *group = fake_group_create(nranks);
+    });
+}
+int32_t msvd_fake_group_destroy(void* group) {
+    return guard([&] {
+        if (group) fake_group_destroy(group);
+    });
+}
+
+int32_t msvd_ctx_create(const msvd_ctx_desc* desc, msvd_ctx** out) {
+    return guard([&] {
+        need(desc, "descriptor");
+        need(out, "output handle");
+        *out = nullptr;
+        int count = 0;
+        MSVD_CUDA(cudaGetDeviceCount(&count));
+        if (desc->device < 0 || desc->device >= count) fail(MSVD_ERR_INVALID, "msvd: no such CUDA device");
+        auto* h = new msvd_ctx();
+        Ctx& c = h->c;
+        try {
+            c.device = desc->device;
+            MSVD_CUDA(cudaSetDevice(c.device));
+            int major = 0;
+            MSVD_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c.device));
+            if (major != 10) fail(MSVD_ERR_CUDA, "msvd: this build targets sm_100a (B200) only");
+            MSVD_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, c.device));
+            int optin = 0;
+            MSVD_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+            c.smem_optin = static_cast<size_t>(optin);
+            if (desc->stream) {
+                c.stream = static_cast<cudaStream_t>(desc->stream);
+            } else {
+                MSVD_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+                c.own_stream = true;
+            }
+            c.comm = make_comm(*desc, c.stream);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int32_t msvd_ctx_destroy(msvd_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        Ctx& c = ctx->c;
+        cudaSetDevice(c.device);
+        cudaStreamSynchronize(c.stream);
+        delete c.comm;
+        if (c.solver) cusolverDnDestroy(c.solver);
+        if (c.scratch) cudaFree(c.scratch);
+        if (c.pstate) cudaFree(c.pstate);
+        for (auto& e : c.ev)
+            if (e) cudaEventDestroy(e);
+        if (c.own_stream) cudaStreamDestroy(c.stream);
+        delete ctx;
+    });
+}
+
+int32_t msvd_ctx_synchronize(msvd_ctx* ctx) {
+    return guard([&] {
+        need(ctx, "context");
+        set_device(ctx->c);
+        MSVD_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
+int64_t msvd_launch_count(msvd_ctx* ctx) { return ctx ? ctx->c.launches : -1; }
+
+void msvd_abi_sizes(int64_t* out, int32_t n) {
+    const int64_t s[5] = {sizeof(msvd_options), sizeof(msvd_record_row), sizeof(msvd_truth), sizeof(msvd_result),
+                          sizeof(msvd_ctx_desc)};
+    for (int i = 0; i < n && i < 5; ++i) out[i] = s[i];
+}
+
+int32_t msvd_matrix_attach(msvd_ctx* ctx, const double* dA, int64_t m_local, int64_t n, int64_t ld, int64_t row0,
+                           int64_t m_global, msvd_matrix** out) {
+    return guard([&] {
+        need(ctx, "context");
+        need(out, "output handle");
+        if (m_local > 0) need(dA, "matrix pointer");
+        if (m_local < 0 || n < 0) fail(MSVD_ERR_DIMENSION, "DenseMatrix: negative dimension");
+        if (ld < n) fail(MSVD_ERR_DIMENSION, "msvd: leading dimension below column count");
+        if (row0 < 0 || row0 + m_local > m_global) fail(MSVD_ERR_DIMENSION, "msvd: local rows outside the global range");
+        auto* M = new msvd_matrix{ctx, dA, m_local, n, ld, row0, m_global};
+        *out = M;
+    });
+}
+
+int32_t msvd_matrix_detach(msvd_matrix* mat) {
+    return guard([&] { delete mat; });
+}
+
+int32_t msvd_apply(msvd_matrix* M, const double* dX, int64_t b, double* dY) {
+    return guard([&] {
+        need(M, "matrix");
+        Ctx& c = M->ctx->c;
+        set_device(c);
+        if (b < 1 || b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size must lie in [1, 8]");
+        const StreamGeom g = make_geom(c, M->A, M->m_local, static_cast<int32_t>(M->n), M->ld);
+        OutCols out{};
+        for (int j = 0; j < b; ++j) out.p[j] = dY + j * M->m_local;
+        launch_apply(c, g, dX, static_cast<int>(b), out);
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int32_t msvd_apply_adjoint(msvd_matrix* M, const double* dY, int64_t b, double* dX) {
+    return guard([&] {
+        need(M, "matrix");
+        Ctx& c = M->ctx->c;
+        set_device(c);
+        if (b < 1 || b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size must lie in [1, 8]");
+        const int64_t n = M->n;
+        const StreamGeom g = make_geom(c, M->A, M->m_local, static_cast<int32_t>(n), M->ld);
+        const int nblk = static_cast<int>(ceil_div(n, 256));
+        const size_t gp = static_cast<size_t>(g.grid) * b * n;
+        double* s = static_cast<double*>(c.ensure_scratch(sizeof(double) * (gp + static_cast<size_t>(b) * nblk)));
+        Cols T{};
+        for (int j = 0; j < b; ++j) T.p[j] = dY + j * M->m_local;
+        launch_gram(c, g, T, static_cast<int>(b), nullptr, static_cast<int>(b), static_cast<int>(b), OutCols{},
+                    true, s);
+        launch_reduce_g(c, s, g.grid, n, static_cast<int>(b), nullptr, nullptr, 0, dX, s + gp, nblk);
+        c.comm->allreduce_sum(dX, static_cast<size_t>(n * b), c.stream);
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int32_t msvd_column_norms(msvd_matrix* M, double* dNorms) {
+    return guard([&] {
+        need(M, "matrix");
+        Ctx& c = M->ctx->c;
+        set_device(c);
+        const StreamGeom g = make_geom(c, M->A, M->m_local, static_cast<int32_t>(M->n), M->ld);
+        double* part = static_cast<double*>(c.ensure_scratch(sizeof(double) * c.num_sms * M->n));
+        launch_colnorms(c, g, part, dNorms);
+        c.comm->allreduce_sum(dNorms, static_cast<size_t>(M->n), c.stream);
+        std::vector<double> h(M->n);
+        MSVD_CUDA(cudaMemcpyAsync(h.data(), dNorms, sizeof(double) * M->n, cudaMemcpyDeviceToHost, c.stream));
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+        for (double& v : h) v = std::sqrt(v);
+        MSVD_CUDA(cudaMemcpy(dNorms, h.data(), sizeof(double) * M->n, cudaMemcpyHostToDevice));
+    });
+}
+
+int32_t msvd_build_sparsestack(msvd_ctx* ctx, int64_t d, int64_t m, int32_t zeta, uint64_t seed,
+                               uint32_t* dPositions, int8_t* dSigns) {
+    return guard([&] {
+        need(ctx, "context");
+        Ctx& c = ctx->c;
+        set_device(c);
+        if (d <= 0 || m <= 0) fail(MSVD_ERR_DIMENSION, "build_sparsestack: dimensions must be positive");
+        if (zeta <= 0 || zeta > d) fail(MSVD_ERR_DIMENSION, "build_sparsestack: zeta must be in [1, d]");
+        if (d % zeta != 0)
+            fail(MSVD_ERR_DIMENSION, "build_sparsestack: zeta must divide d; use round_up_to_multiple(d, zeta) = " +
+                                         std::to_string(d + (zeta - d % zeta)));
+        build_sparsestack_dev(c, d, m, zeta, seed, dPositions, dSigns);
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int32_t msvd_sketch(msvd_matrix* M, int64_t d, int32_t zeta, uint64_t seed, double* dSA) {
+    return guard([&] {
+        need(M, "matrix");
+        Ctx& c = M->ctx->c;
+        set_device(c);
+        if (d <= 0 || M->m_global <= 0) fail(MSVD_ERR_DIMENSION, "build_sparsestack: dimensions must be positive");
+        if (zeta <= 0 || zeta > d) fail(MSVD_ERR_DIMENSION, "build_sparsestack: zeta must be in [1, d]");
+        if (d % zeta != 0)
+            fail(MSVD_ERR_DIMENSION, "build_sparsestack: zeta must divide d; use round_up_to_multiple(d, zeta) = " +
+                                         std::to_string(d + (zeta - d % zeta)));
+        const StreamGeom g = make_geom(c, M->A, M->m_local, static_cast<int32_t>(M->n), M->ld);
+        DevState* st = prim_state(c);
+        MSVD_CUDA(cudaMemsetAsync(st, 0, sizeof(DevState), c.stream));
+        sketch_dev(c, g, M->row0, d, zeta, seed, dSA, st);
+        c.comm->allreduce_sum(dSA, static_cast<size_t>(d * M->n), c.stream);
+        read_state(c, st);
+    });
+}
+
+int32_t msvd_precond_build(msvd_ctx* ctx, const double* dSA, int64_t rows, int64_t n, double* dVt, double* dSig,
+                           double* sigma_max_estimate, int64_t* floor_count) {
+    return guard([&] {
+        need(ctx, "context");
+        Ctx& c = ctx->c;
+        set_device(c);
+        double* Vrow = nullptr;
+        MSVD_CUDA(cudaMalloc(&Vrow, sizeof(double) * std::max<int64_t>(n * n, 1)));
+        double smax = 0.0;
+        int64_t nf = 0;
+        try {
+            precond_build_dev(c, dSA, rows, n, dVt, Vrow, dSig, &smax, &nf);
+        } catch (...) {
+            cudaFree(Vrow);
+            throw;
+        }
+        cudaFree(Vrow);
+        if (sigma_max_estimate) *sigma_max_estimate = smax;
+        if (floor_count) *floor_count = nf;
+    });
+}
+
+int32_t msvd_precond_apply(msvd_ctx* ctx, const double* dVt, const double* dSig, int64_t n, const double* dR,
+                           int64_t b, double* dW) {
+    return guard([&] {
+        need(ctx, "context");
+        Ctx& c = ctx->c;
+        set_device(c);
+        if (b < 1 || b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size must lie in [1, 8]");
+        double* s = static_cast<double*>(c.ensure_scratch(sizeof(double) * (n * n + n * b)));
+        launch_transpose_rm_to_cm(c, dVt, n, n, n, s);  // column-major Vt -> row-major copy
+        DevState* st = prim_state(c);
+        launch_precond(c, MSVD_PRECOND_RANDOMIZED, dVt, s, dSig, nullptr, n, dR, static_cast<int>(b), s + n * n, dW,
+                       st, 0);
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int32_t msvd_tsqr_r(msvd_ctx* ctx, const double* dT, int64_t rows, int64_t k, double* dR) {
+    return guard([&] {
+        need(ctx, "context");
+        Ctx& c = ctx->c;
+        set_device(c);
+        if (k < 1 || k > kMaxK) fail(MSVD_ERR_DIMENSION, "msvd: tsqr width must lie in [1, 24]");
+        if (rows < k) fail(MSVD_ERR_DIMENSION, "householder_qr: requires rows >= cols");
+        const int np = tsqr_parts(c);
+        double* parts = static_cast<double*>(c.ensure_scratch(sizeof(double) * np * k * k));
+        DevState* st = prim_state(c);
+        MSVD_CUDA(cudaMemsetAsync(st, 0, sizeof(DevState), c.stream));
+        Cols T{};
+        for (int l = 0; l < k; ++l) T.p[l] = dT + l * rows;
+        launch_tsqr(c, T, rows, static_cast<int>(k), parts, st, 0);
+        RRArgs ra{};
+        ra.Rparts = parts;
+        ra.nparts = np;
+        ra.k = static_cast<int>(k);
+        ra.b = 1;
+        ra.mode = 2;
+        ra.R_out = dR;
+        ra.st = st;
+        launch_rr(c, ra);
+        const DevState h = read_state(c, st);
+        (void)h;
+    });
+}
+
+int32_t msvd_small_svd(msvd_ctx* ctx, const double* dB, int64_t k, double* dSigma, double* dV) {
+    return guard([&] {
+        need(ctx, "context");
+        Ctx& c = ctx->c;
+        set_device(c);
+        if (k < 1 || k > kMaxK) fail(MSVD_ERR_DIMENSION, "msvd: small svd size must lie in [1, 24]");
+        DevState* st = prim_state(c);
+        MSVD_CUDA(cudaMemsetAsync(st, 0, sizeof(DevState), c.stream));
+        launch_small_svd(c, dB, static_cast<int>(k), dSigma, dV, st);
+        read_state(c, st);
+    });
+}
+
+int32_t msvd_lobpcg_solve(msvd_matrix* mat, const msvd_options* opts, const msvd_truth* truth, msvd_result* res) {
+    return guard([&] {
+        need(mat, "matrix");
+        need(opts, "options");
+        solve(mat, *opts, truth, res);
+    });
+}
+
+int32_t msvd_rlobpcg_single(msvd_matrix* mat, const msvd_options* opts, const msvd_truth* truth, msvd_result* res) {
+    return guard([&] {
+        need(mat, "matrix");
+        need(opts, "options");
+        msvd_options o = *opts;
+        o.block_size = 1;
+        o.precond_kind = MSVD_PRECOND_RANDOMIZED;
+        solve(mat, o, truth, res);
+    });
+}
+
+int32_t msvd_rlobpcg_block(msvd_matrix* mat, const msvd_options* opts, const msvd_truth* truth, msvd_result* res) {
+    return guard([&] {
+        need(mat, "matrix");
+        need(opts, "options");
+        msvd_options o = *opts;
+        o.precond_kind = MSVD_PRECOND_RANDOMIZED;
+        solve(mat, o, truth, res);
+    });
+}
+
+int32_t msvd_solve_host(msvd_ctx* ctx, const double* hA, int64_t m_local, int64_t n, int64_t ld, int64_t row0,
+                        int64_t m_global, const msvd_options* opts, const msvd_truth* truth, msvd_result* res) {
+    return guard([&] {
+        need(ctx, "context");
+        need(opts, "options");
+        Ctx& c = ctx->c;
+        set_device(c);
+        if (m_local > 0) need(hA, "host matrix");
+        if (ld < n) fail(MSVD_ERR_DIMENSION, "msvd: leading dimension below column count");
+        const int64_t ldd = (n % 2 == 0) ? n : n + 1;  // even pitch keeps the TMA path
+        double* dA = nullptr;
+        MSVD_CUDA(cudaMalloc(&dA, sizeof(double) * std::max<int64_t>(m_local * ldd, 1)));
+        try {
+            if (m_local > 0)
+                MSVD_CUDA(cudaMemcpy2DAsync(dA, sizeof(double) * ldd, hA, sizeof(double) * ld, sizeof(double) * n,
+                                            m_local, cudaMemcpyHostToDevice, c.stream));
+            msvd_matrix M{ctx, dA, m_local, n, ldd, row0, m_global};
+            solve(&M, *opts, truth, res);
+        } catch (...) {
+            cudaFree(dA);
+            throw;
+        }
+        cudaFree(dA);
+    });
+}
+
+}  // extern "C"

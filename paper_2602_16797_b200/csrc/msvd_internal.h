@@ -1,0 +1,207 @@
+// Internal declarations shared by the msvd CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "msvd.h"
+
+namespace msvd {
+
+constexpr int kMaxB = 8;              // block size limit of the register-tiled kernels
+constexpr int kMaxK = 3 * kMaxB;      // trial width limit
+constexpr int kMaxPairs = 4;          // column pairs per consumer thread (n <= 2048)
+constexpr int kConsumers = 256;       // consumer threads per stream CTA
+constexpr int kMaxN = 2 * kMaxPairs * kConsumers;
+
+// thrown inside the library; converted to a status at the C boundary
+struct Fail : std::runtime_error {
+    int code;
+    Fail(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+#define MSVD_CUDA(x) ::msvd::cuda_check((x), #x)
+
+// ---- device-side solver state (one per solve, in device memory) ----------
+enum DevErr : int32_t {
+    kErrNone = 0,
+    kErrNonfiniteW = 1,      // solver.cpp:407
+    kErrNonfiniteAT = 2,     // solver.cpp:414
+    kErrJacobi = 3,          // svd.cpp:147-149
+    kErrCgs2 = 4,            // solver.cpp:254
+    kErrOrth = 5,            // solver.cpp:112
+    kErrDrift = 6,           // solver.cpp:435
+    kErrNonfiniteA = 7,      // operator.cpp:35-37 (DenseOperator ctor)
+};
+
+struct DevState {
+    int32_t stop;
+    int32_t err_code;
+    int32_t err_iter;
+    int32_t have_spare;     // SplitMix64 Box-Muller spare (rng.hpp:40-52)
+    uint64_t rng_state;
+    double spare;
+    int64_t replacements;   // SolveResult::degenerate_replacements
+    unsigned long long t0_ns;
+    double theta[kMaxB];    // Ritz values of the current target block (descending)
+    double max_drift;
+    double worst_jacobi;
+};
+
+// column-pointer bundles passed by value to kernels
+struct Cols {
+    const double* p[kMaxK];
+};
+struct OutCols {
+    double* p[2 * kMaxB];
+};
+
+// ---- stream geometry of a row-major A on one rank -------------------------
+struct StreamGeom {
+    const double* A;
+    int64_t m;       // local rows
+    int32_t n;       // columns
+    int64_t ld;      // leading dimension (elements)
+    int32_t ld_s;    // shared-memory row stride (elements, even)
+    int32_t rc;      // rows per chunk
+    int32_t stages;  // pipeline depth
+    int32_t tma;     // 1: cp.async.bulk producer, 0: LDG producer
+    int32_t grid;    // persistent CTAs
+    size_t stage_bytes;
+};
+
+struct Ctx;
+
+// ---- launchers (kernels.cu) -----------------------------------------------
+StreamGeom make_geom(const Ctx& c, const double* A, int64_t m, int32_t n, int64_t ld);
+// Y (m x b, out cols) = A W (W n x b col-major)
+void launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out);
+// Gpart[grid][b][n]: A^T Y with Y = T C (gram mode, writes Y cols + extra cols)
+// or Y = T (direct mode, q == b, no writes)
+void launch_gram(Ctx& c, const StreamGeom& g, Cols T, int k, const double* Cm, int q, int b,
+                 OutCols out, bool direct, double* Gpart);
+// per-CTA Householder R of the m x k column block T, Rparts[nparts][k][k]
+int tsqr_parts(const Ctx& c);  // number of partial R factors launch_tsqr produces
+void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st, int iter);
+
+// single-CTA Rayleigh-Ritz: merge R parts, Jacobi SVD, C / theta / mix, V' = T C, X' = T mix
+struct RRArgs {
+    const double* Rparts;
+    int nparts;
+    int k, b;
+    int mode;            // 0 init (C = all of V, theta = all sigma), 1 iteration, 2 merge only
+    Cols T;              // n-side trial basis columns [V X W]
+    int64_t n;
+    double* Vout;        // n x b
+    double* Xout;        // n x b (mode 1)
+    double* Cm;          // k x 2b (C | mix), ld k
+    double* theta_out;   // b, descending (theta_next)
+    double* sig_out;     // optional k: all Ritz sigma (tests)
+    double* Vfull_out;   // optional k x k sorted, sign-fixed V (tests)
+    double* R_out;       // optional k x k merged R factor (tests / msvd_tsqr_r)
+    DevState* st;
+    int iter;
+};
+void launch_rr(Ctx& c, const RRArgs& a);
+
+void launch_reduce_g(Ctx& c, const double* Gpart, int nparts, int64_t n, int b, const double* V,
+                     const DevState* st, int residual, double* Gout, double* nrm_part, int nblk);
+struct ControlArgs {
+    const double* nrm_part;  // b x nblk partial sums of squares
+    int nblk;
+    int b;
+    int64_t n;
+    const double* V;         // n x b current target block
+    const double* truth_v;   // n or null
+    double truth_sigma;
+    DevState* st;
+    msvd_record_row* rows;
+    double* rh;
+    double* th;
+    int row;                 // record row index (= iteration + 1, or 0)
+    int check;               // evaluate stop rule at loop counter row-1
+    double sigma1, tol, factor;
+    int use_stag;
+    int timing;
+};
+void launch_control(Ctx& c, const ControlArgs& a);
+
+void launch_precond(Ctx& c, int kind, const double* Vcol, const double* Vrow, const double* sig,
+                    const double* dinv, int64_t n, const double* R, int b, double* tmp, double* W,
+                    DevState* st, int iter);
+void launch_cgs2(Ctx& c, double* W, int64_t n, int b, Cols basis, int nb, DevState* st, int iter);
+void launch_state_init(Ctx& c, DevState* st, uint64_t seed);
+void launch_drift(Ctx& c, const double* fresh, const double* cached, int64_t count, DevState* st,
+                  double limit, int iter);
+void launch_colnorms(Ctx& c, const StreamGeom& g, double* part, double* out);
+void launch_transpose_rm_to_cm(Ctx& c, const double* A, int64_t m, int64_t n, int64_t ld,
+                               double* out);
+void launch_copy_cols(Ctx& c, const double* src, int64_t ld_src, int64_t col0, int64_t rows,
+                      int64_t cols, double* dst);
+void launch_small_svd(Ctx& c, const double* B, int k, double* sigma, double* V, DevState* st);
+
+// ---- sketch (sketch.cu) ---------------------------------------------------
+void build_sparsestack_dev(Ctx& c, int64_t d, int64_t m, int zeta, uint64_t seed, uint32_t* pos,
+                           int8_t* sgn);
+void sketch_dev(Ctx& c, const StreamGeom& g, int64_t row0, int64_t d, int zeta, uint64_t seed,
+                double* SA, DevState* st);
+
+// ---- preconditioner factorization (svd.cu) --------------------------------
+void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double* Vcol,
+                       double* Vrow, double* sig, double* sigma_max, int64_t* nfloor);
+
+// ---- communicator (comm.cu) ----------------------------------------------
+struct Comm {
+    virtual ~Comm() = default;
+    virtual int nranks() const = 0;
+    virtual int rank() const = 0;
+    virtual void allreduce_sum(double* d, size_t count, cudaStream_t s) = 0;
+    virtual void allgather(const double* send, double* recv, size_t count, cudaStream_t s) = 0;
+    virtual void bcast(double* d, size_t count, int root, cudaStream_t s) = 0;
+    virtual void allreduce_max(double* d, size_t count, cudaStream_t s) = 0;
+};
+Comm* make_comm(const msvd_ctx_desc& desc, cudaStream_t s);
+
+// ---- context ---------------------------------------------------------------
+struct Ctx {
+    int device = 0;
+    int num_sms = 148;
+    size_t smem_optin = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    Comm* comm = nullptr;
+    cusolverDnHandle_t solver = nullptr;
+    int64_t launches = 0;
+    cudaEvent_t ev[8] = {};
+    // reusable device scratch
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    void* ensure_scratch(size_t bytes);
+    DevState* pstate = nullptr;  // error word for primitive entry points
+};
+
+void* fake_group_create(int n);
+void fake_group_destroy(void* g);
+int nccl_unique_id(uint8_t out[128]);
+
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace msvd
+
+struct msvd_ctx {
+    msvd::Ctx c;
+};
+struct msvd_matrix {
+    msvd_ctx* ctx;
+    const double* A;
+    int64_t m_local, n, ld, row0, m_global;
+};

@@ -1,0 +1,170 @@
+// SparseStack sketch S A (SURVEY 2.3 K1; sketch.cpp:36-60, :75-95).
+//
+// S is never stored: each row r of A regenerates its zeta (position, sign)
+// pairs from SplitMix64(seed, row0 + r), exactly as build_sparsestack keys a
+// column of S.  The scatter  SA[blk*k + pos] += sign * zeta^-1/2 * A[r, :]  is
+// turned into a deterministic gather: the (sketch row, source row) pairs are
+// radix-sorted by sketch row (stable, so source rows stay ascending), and one
+// CTA per sketch row sums its source rows in that order with unfused
+// multiply/add -- the reference's accumulation order, so on one rank SA is
+// bit-identical to sketch_apply(S, A).
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "msvd_internal.h"
+
+namespace msvd {
+
+namespace {
+
+// next_below without modulo bias (rng.hpp:27-32)
+__device__ __forceinline__ uint64_t below(uint64_t& s, uint64_t bound) {
+    const uint64_t lim = UINT64_MAX - UINT64_MAX % bound;
+    uint64_t x;
+    do {
+        s += kGolden;
+        x = sm_mix(s);
+    } while (x >= lim);
+    return x % bound;
+}
+
+// one thread per local row: zeta (sketch row, signed source row) pairs
+__global__ void keys_kernel(int64_t m, int64_t row0, int64_t d, int zeta, uint64_t seed, uint32_t* keys,
+                            uint32_t* vals, uint32_t* pos_out, int8_t* sgn_out) {
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= m) return;
+    uint64_t s = sm_keyed_state(seed, static_cast<uint64_t>(row0 + r));
+    const uint64_t blk = static_cast<uint64_t>(d / zeta);
+    for (int k = 0; k < zeta; ++k) {
+        const uint32_t pos = static_cast<uint32_t>(below(s, blk));
+        s += kGolden;
+        const bool neg = (sm_mix(s) >> 63) != 0;
+        const int64_t at = r * zeta + k;
+        if (keys) {
+            keys[at] = static_cast<uint32_t>(k * blk + pos);
+            vals[at] = static_cast<uint32_t>(r) | (neg ? 0x80000000u : 0u);
+        }
+        if (pos_out) {
+            pos_out[at] = pos;
+            sgn_out[at] = neg ? -1 : 1;
+        }
+    }
+}
+
+// offs[s] = first index with key >= s (binary search), s in [0, d]
+__global__ void offsets_kernel(const uint32_t* keys, int64_t cnt, int64_t d, int64_t* offs) {
+    const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s > d) return;
+    int64_t lo = 0, hi = cnt;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (static_cast<int64_t>(keys[mid]) < s) lo = mid + 1;
+        else hi = mid;
+    }
+    offs[s] = lo;
+}
+
+constexpr int kGatherT = 256;
+constexpr int kGatherUnroll = 4;
+
+// one CTA per sketch row; threads own column pairs; rows summed in source order
+__global__ void __launch_bounds__(kGatherT) gather_kernel(const double* A, int64_t ld, int n, int64_t d,
+                                                          const int64_t* offs, const uint32_t* vals, double val,
+                                                          double* SA, DevState* st, int vec) {
+    const int64_t s = blockIdx.x;
+    const int64_t e0 = offs[s], e1 = offs[s + 1];
+    const int npairs = (n + 1) >> 1;
+    bool finite = true;
+    for (int pi = threadIdx.x; pi < npairs; pi += kGatherT) {
+        const int c0 = 2 * pi;
+        const bool has1 = c0 + 1 < n;
+        double acc0 = 0.0, acc1 = 0.0;
+        int64_t e = e0;
+        for (; e + kGatherUnroll <= e1; e += kGatherUnroll) {
+            double x0[kGatherUnroll], x1[kGatherUnroll], sv[kGatherUnroll];
+#pragma unroll
+            for (int u = 0; u < kGatherUnroll; ++u) {
+                const uint32_t v = __ldg(vals + e + u);
+                const int64_t r = v & 0x7fffffffu;
+                sv[u] = (v >> 31) ? -val : val;
+                const double* row = A + r * ld + c0;
+                if (vec && has1) {
+                    const double2 x = __ldg(reinterpret_cast<const double2*>(row));
+                    x0[u] = x.x;
+                    x1[u] = x.y;
+                } else {
+                    x0[u] = __ldg(row);
+                    x1[u] = has1 ? __ldg(row + 1) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kGatherUnroll; ++u) {
+                acc0 = __dadd_rn(acc0, __dmul_rn(sv[u], x0[u]));
+                acc1 = __dadd_rn(acc1, __dmul_rn(sv[u], x1[u]));
+                finite = finite && isfinite(x0[u]) && isfinite(x1[u]);
+            }
+        }
+        for (; e < e1; ++e) {
+            const uint32_t v = __ldg(vals + e);
+            const int64_t r = v & 0x7fffffffu;
+            const double svv = (v >> 31) ? -val : val;
+            const double* row = A + r * ld + c0;
+            const double x0 = __ldg(row);
+            const double x1 = has1 ? __ldg(row + 1) : 0.0;
+            acc0 = __dadd_rn(acc0, __dmul_rn(svv, x0));
+            acc1 = __dadd_rn(acc1, __dmul_rn(svv, x1));
+            finite = finite && isfinite(x0) && isfinite(x1);
+        }
+        SA[s + static_cast<int64_t>(c0) * d] = acc0;
+        if (has1) SA[s + static_cast<int64_t>(c0 + 1) * d] = acc1;
+    }
+    if (!finite && st) atomicCAS(&st->err_code, 0, kErrNonfiniteA);
+}
+
+}  // namespace
+
+void build_sparsestack_dev(Ctx& c, int64_t d, int64_t m, int zeta, uint64_t seed, uint32_t* pos, int8_t* sgn) {
+    if (m == 0) return;
+    keys_kernel<<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, c.stream>>>(m, 0, d, zeta, seed, nullptr,
+                                                                              nullptr, pos, sgn);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void sketch_dev(Ctx& c, const StreamGeom& g, int64_t row0, int64_t d, int zeta, uint64_t seed, double* SA,
+                DevState* st) {
+    const int64_t m = g.m;
+    if (m == 0) {
+        MSVD_CUDA(cudaMemsetAsync(SA, 0, sizeof(double) * d * g.n, c.stream));
+        return;
+    }
+    if (m > 0x7fffffffLL) fail(MSVD_ERR_DIMENSION, "msvd: more than 2^31-1 local rows in one sketch");
+    const int64_t cnt = m * zeta;
+    int bits = 1;
+    while ((1LL << bits) < d) ++bits;
+    size_t temp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, static_cast<uint32_t*>(nullptr),
+                                    static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr),
+                                    static_cast<uint32_t*>(nullptr), cnt, 0, bits, c.stream);
+    const size_t arr = ((sizeof(uint32_t) * cnt + 255) / 256) * 256;
+    const size_t offb = ((sizeof(int64_t) * (d + 1) + 255) / 256) * 256;
+    unsigned char* base = static_cast<unsigned char*>(c.ensure_scratch(4 * arr + offb + temp_bytes + 256));
+    uint32_t* k_in = reinterpret_cast<uint32_t*>(base);
+    uint32_t* v_in = reinterpret_cast<uint32_t*>(base + arr);
+    uint32_t* k_out = reinterpret_cast<uint32_t*>(base + 2 * arr);
+    uint32_t* v_out = reinterpret_cast<uint32_t*>(base + 3 * arr);
+    int64_t* offs = reinterpret_cast<int64_t*>(base + 4 * arr);
+    void* temp = base + 4 * arr + offb;
+    keys_kernel<<<static_cast<unsigned>(ceil_div(m, 256)), 256, 0, c.stream>>>(m, row0, d, zeta, seed, k_in, v_in,
+                                                                              nullptr, nullptr);
+    MSVD_CUDA(cudaGetLastError());
+    MSVD_CUDA(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, k_in, k_out, v_in, v_out, cnt, 0, bits, c.stream));
+    offsets_kernel<<<static_cast<unsigned>(ceil_div(d + 1, 256)), 256, 0, c.stream>>>(k_out, cnt, d, offs);
+    const double val = 1.0 / sqrt(static_cast<double>(zeta));  // sketch.cpp:12-14
+    gather_kernel<<<static_cast<unsigned>(d), kGatherT, 0, c.stream>>>(g.A, g.ld, g.n, d, offs, v_out, val, SA, st,
+                                                                   g.tma);
+    MSVD_CUDA(cudaGetLastError());
+    c.launches += 4;  // keys, radix sort (counted once), offsets, gather
+}
+
+}  // namespace msvd

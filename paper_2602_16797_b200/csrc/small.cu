@@ -1,0 +1,891 @@
+// TSQR, Rayleigh-Ritz and the n-scale control kernels.
+//
+// Everything between the two A passes stays on the device: the host only
+// launches and, at check iterations, reads the stop/error words.
+#include <cmath>
+
+#include "common.cuh"
+#include "msvd_internal.h"
+
+namespace msvd {
+
+namespace {
+
+constexpr double kEps = 2.220446049250313e-16;
+
+// ---------------------------------------------------------------------------
+// Householder fold of a 32-row block X into an upper-triangular R held in
+// shared memory (column-major, leading dimension KM): the QR step of a TSQR
+// on [R; X].  Lane i holds row i of X in x[].  The reflector sign convention
+// follows svd.cpp:37 (alpha = -sign(x_k) ||x||), so every R produced here is
+// the reference's householder_qr R up to roundoff and row signs -- and the
+// Jacobi SVD that consumes it depends only on R^T R (svd.cpp:113-117).
+// ---------------------------------------------------------------------------
+template <int KM>
+__device__ void fold_rows(double* R, double (&x)[KM], int k) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int j = 0; j < KM; ++j) {
+        if (j >= k) break;
+        const double rjj = R[j + j * KM];
+        const double xj = x[j];
+        const double ss = warp_sum(xj * xj);
+        const double nrm2 = rjj * rjj + ss;
+        if (nrm2 == 0.0) continue;  // svd.cpp:33-36 (zero column: beta = 0)
+        const double xnorm = sqrt(nrm2);
+        const double alpha = rjj >= 0.0 ? -xnorm : xnorm;
+        const double v0 = rjj - alpha;
+        const double vi = xj / v0;
+        const double beta = -v0 / alpha;
+        double d[KM];
+#pragma unroll
+        for (int l = j + 1; l < KM; ++l) d[l] = l < k ? vi * x[l] : 0.0;
+#pragma unroll
+        for (int l = j + 1; l < KM; ++l)
+            if (l < k) d[l] = warp_sum(d[l]);
+#pragma unroll
+        for (int l = j + 1; l < KM; ++l) {
+            if (l < k) {
+                const double rjl = R[j + l * KM];
+                const double s = (rjl + d[l]) * beta;
+                d[l] = rjl - s;  // new R(j, l)
+                x[l] -= s * vi;
+            }
+        }
+        x[j] = 0.0;
+        __syncwarp();
+        if (lane == 0) {
+            R[j + j * KM] = alpha;
+#pragma unroll
+            for (int l = j + 1; l < KM; ++l)
+                if (l < k) R[j + l * KM] = d[l];
+        }
+        __syncwarp();
+    }
+}
+
+// rows of another upper-triangular R2 (ld KM) as the X block of a fold
+template <int KM>
+__device__ __forceinline__ void rows_of(const double* R2, int k, double (&x)[KM]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int l = 0; l < KM; ++l) x[l] = (lane < k && l >= lane && l < k) ? R2[lane + l * KM] : 0.0;
+}
+
+struct TsqrArgs {
+    Cols T;
+    int64_t m;
+    int k;
+    double* Rparts;  // [grid][k][k]
+    DevState* st;
+    int iter;
+};
+
+// per-CTA TSQR: 8 warps fold 32-row tiles round-robin, then a 3-level tree
+template <int KM>
+__global__ void __launch_bounds__(256) tsqr_kernel(TsqrArgs a) {
+    __shared__ double Rw[8][KM * KM];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = lane; i < KM * KM; i += 32) Rw[warp][i] = 0.0;
+    __syncwarp();
+    const int64_t r0 = (a.m * blockIdx.x) / gridDim.x;
+    const int64_t r1 = (a.m * (blockIdx.x + 1)) / gridDim.x;
+    const int64_t ntiles = ceil_div(r1 - r0, 32);
+    bool finite = true;
+    for (int64_t t = warp; t < ntiles; t += 8) {
+        const int64_t row = r0 + t * 32 + lane;
+        double x[KM];
+#pragma unroll
+        for (int l = 0; l < KM; ++l) {
+            x[l] = (l < a.k && row < r1) ? a.T.p[l][row] : 0.0;
+            finite = finite && isfinite(x[l]);
+        }
+        fold_rows<KM>(Rw[warp], x, a.k);
+    }
+    if (!__all_sync(kFull, finite) && lane == 0 && a.st) {
+        if (atomicCAS(&a.st->err_code, 0, kErrNonfiniteAT) == 0) a.st->err_iter = a.iter;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s = 1; s < 8; s <<= 1) {
+        if ((warp % (2 * s)) == 0) {
+            double x[KM];
+            rows_of<KM>(Rw[warp + s], a.k, x);
+            fold_rows<KM>(Rw[warp], x, a.k);
+        }
+        __syncthreads();
+    }
+    double* out = a.Rparts + static_cast<size_t>(blockIdx.x) * a.k * a.k;
+    for (int i = threadIdx.x; i < a.k * a.k; i += blockDim.x) {
+        const int r = i % a.k, cc = i / a.k;
+        out[i] = r <= cc ? Rw[0][r + cc * KM] : 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// One-sided Jacobi SVD of a k x k (k <= 24) matrix in shared memory with a
+// round-robin parallel pair order (one warp per pair, lanes over rows); the
+// per-pair rotation, the 1e-15 tolerance, the 60-sweep cap and the
+// convergence test are svd.cpp:99-150.  Then sigma = column norms, stable
+// descending sort, largest-|entry|-positive signs (svd.cpp:200-248).
+// Must be called by all threads of the CTA (blockDim >= 32 * 12).
+// ---------------------------------------------------------------------------
+template <int KM>
+__device__ bool jacobi_svd(double* Bm, double* V, int k, double* sig, double* Vs, int* ord,
+                           double* worst_s) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < KM * KM; i += blockDim.x) V[i] = ((i % KM) == (i / KM)) ? 1.0 : 0.0;
+    const int K2 = k + (k & 1);
+    bool converged = (k <= 1);
+    __syncthreads();
+    for (int sweep = 0; sweep < 60 && !converged; ++sweep) {
+        if (threadIdx.x == 0) *worst_s = 0.0;
+        __syncthreads();
+        for (int r = 0; r < K2 - 1; ++r) {
+            if (warp < K2 / 2) {
+                int p, q;
+                if (warp == 0) {
+                    p = r;
+                    q = K2 - 1;
+                } else {
+                    p = (r + warp) % (K2 - 1);
+                    q = (r - warp + (K2 - 1)) % (K2 - 1);
+                }
+                if (p > q) {
+                    const int t = p;
+                    p = q;
+                    q = t;
+                }
+                if (q < k) {
+                    const double bp = lane < k ? Bm[lane + p * KM] : 0.0;
+                    const double bq = lane < k ? Bm[lane + q * KM] : 0.0;
+                    const double app = warp_sum(bp * bp);
+                    const double aqq = warp_sum(bq * bq);
+                    const double apq = warp_sum(bp * bq);
+                    if (!(app == 0.0 || aqq == 0.0 || apq == 0.0)) {
+                        const double rel = fabs(apq) / sqrt(app * aqq);
+                        if (lane == 0) atomic_max_pos(worst_s, rel);
+                        if (rel > 1e-15) {
+                            const double tau = (aqq - app) / (2.0 * apq);
+                            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                            const double c = 1.0 / sqrt(1.0 + t * t);
+                            const double sn = c * t;
+                            if (lane < k) {
+                                Bm[lane + p * KM] = c * bp - sn * bq;
+                                Bm[lane + q * KM] = sn * bp + c * bq;
+                                const double vp = V[lane + p * KM], vq = V[lane + q * KM];
+                                V[lane + p * KM] = c * vp - sn * vq;
+                                V[lane + q * KM] = sn * vp + c * vq;
+                            }
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        converged = *worst_s <= 1e-15;
+        __syncthreads();
+    }
+    if (threadIdx.x < k) {
+        double s = 0.0;
+        for (int i = 0; i < k; ++i) s += Bm[i + threadIdx.x * KM] * Bm[i + threadIdx.x * KM];
+        sig[threadIdx.x] = sqrt(s);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int j = 0; j < k; ++j) ord[j] = j;
+        for (int j = 1; j < k; ++j) {
+            const int key = ord[j];
+            int i = j - 1;
+            while (i >= 0 && sig[key] > sig[ord[i]]) {
+                ord[i + 1] = ord[i];
+                --i;
+            }
+            ord[i + 1] = key;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < k) {
+        const int j = threadIdx.x, src = ord[j];
+        int imax = 0;
+        double amax = -1.0;
+        for (int i = 0; i < k; ++i) {
+            const double v = fabs(V[i + src * KM]);
+            if (v > amax) {
+                amax = v;
+                imax = i;
+            }
+        }
+        const double sgn = V[imax + src * KM] < 0.0 ? -1.0 : 1.0;
+        for (int i = 0; i < k; ++i) Vs[i + j * KM] = sgn * V[i + src * KM];
+    }
+    __syncthreads();
+    const double s_sorted = threadIdx.x < k ? sig[ord[threadIdx.x]] : 0.0;
+    __syncthreads();
+    if (threadIdx.x < k) sig[threadIdx.x] = s_sorted;
+    __syncthreads();
+    return converged;
+}
+
+// ---------------------------------------------------------------------------
+// Rayleigh-Ritz (solver.cpp:352-355 init, :417-421 and :453-462 iteration)
+// ---------------------------------------------------------------------------
+template <int KM>
+__global__ void __launch_bounds__(512) rr_kernel(RRArgs a) {
+    extern __shared__ __align__(16) double sh[];
+    double* Rw = sh;                      // [16][KM*KM]
+    double* Bm = Rw + 16 * KM * KM;       // KM*KM
+    double* V = Bm + KM * KM;             // KM*KM
+    double* Vs = V + KM * KM;             // KM*KM sorted/sign-fixed
+    double* sig = Vs + KM * KM;           // KM
+    double* q = sig + KM;                 // KM*KMAXB  orth coefficients (lead x b)
+    double* mix = q + KM * kMaxB;         // KM*kMaxB
+    double* worst = mix + KM * kMaxB;     // 1
+    int* ord = reinterpret_cast<int*>(worst + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int k = a.k, b = a.b;
+
+    // 1. merge the partial R factors: warp w folds parts w, w+32, ...; then a tree
+    for (int i = lane; i < KM * KM; i += 32) Rw[warp * KM * KM + i] = 0.0;
+    __syncwarp();
+    const int nw = blockDim.x >> 5;
+    for (int pi = warp; pi < a.nparts; pi += nw) {
+        double x[KM];
+        const double* R2 = a.Rparts + static_cast<size_t>(pi) * k * k;
+#pragma unroll
+        for (int l = 0; l < KM; ++l) x[l] = (lane < k && l >= lane && l < k) ? R2[lane + l * k] : 0.0;
+        fold_rows<KM>(Rw + warp * KM * KM, x, k);
+    }
+    __syncthreads();
+    for (int s = 1; s < nw; s <<= 1) {
+        if ((warp % (2 * s)) == 0 && warp + s < nw) {
+            double x[KM];
+            rows_of<KM>(Rw + (warp + s) * KM * KM, k, x);
+            fold_rows<KM>(Rw + warp * KM * KM, x, k);
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < KM * KM; i += blockDim.x) {
+        const int r = i % KM, c = i / KM;
+        Bm[i] = (r < k && c < k && r <= c) ? Rw[i] : 0.0;
+    }
+    __syncthreads();
+    if (a.R_out)
+        for (int i = threadIdx.x; i < k * k; i += blockDim.x) a.R_out[i] = Bm[(i % k) + (i / k) * KM];
+    if (a.mode == 2) return;
+
+    // 2. SVD of R (svd.cpp:180-252)
+    const bool ok = jacobi_svd<KM>(Bm, V, k, sig, Vs, ord, worst);
+    if (!ok && threadIdx.x == 0) {
+        if (atomicCAS(&a.st->err_code, 0, kErrJacobi) == 0) a.st->err_iter = a.iter;
+    }
+    if (a.sig_out && threadIdx.x < k) a.sig_out[threadIdx.x] = sig[threadIdx.x];
+    if (a.Vfull_out)
+        for (int i = threadIdx.x; i < k * k; i += blockDim.x) a.Vfull_out[i] = Vs[(i % k) + (i / k) * KM];
+
+    // 3. target block: last b Ritz pairs
+    const int lead = k - b;
+    if (threadIdx.x < b) {
+        const double th = sig[lead + threadIdx.x];
+        a.theta_out[threadIdx.x] = th;
+    }
+    for (int i = threadIdx.x; i < k * b; i += blockDim.x) {
+        const int r = i % k, j = i / k;
+        a.Cm[r + j * k] = Vs[r + (lead + j) * KM];
+    }
+    // 4. history coefficients: q = orth_coefficients(C(0:b, 0:lead)^T), mix = V(:,0:lead) q
+    if (a.mode == 1 && warp == 0) {
+        // g (lead x b): g(j,l) = Vs(l, j); lane = row j of g
+        double sref = 0.0;
+        for (int l = 0; l < b; ++l) {
+            const double gv = lane < lead ? Vs[l + lane * KM] : 0.0;
+            sref = fmax(sref, sqrt(warp_sum(gv * gv)));
+        }
+        bool collapsed = false;
+        for (int j = 0; j < b; ++j) {
+            double w = lane < lead ? Vs[j + lane * KM] : 0.0;
+            for (int pass = 0; pass < 2; ++pass)
+                for (int l = 0; l < j; ++l) {
+                    const double ql = lane < lead ? q[lane + l * KM] : 0.0;
+                    const double pr = warp_sum(ql * w);
+                    w -= pr * ql;
+                }
+            const double nrm = sqrt(warp_sum(w * w));
+            if (nrm <= 1e-14 * fmax(1.0, sref)) {
+                bool placed = false;
+                for (int cand = 0; cand < lead && !placed; ++cand) {
+                    double e = lane == cand ? 1.0 : 0.0;
+                    for (int pass = 0; pass < 2; ++pass)
+                        for (int l = 0; l < j; ++l) {
+                            const double ql = lane < lead ? q[lane + l * KM] : 0.0;
+                            const double pr = warp_sum(ql * e);
+                            e -= pr * ql;
+                        }
+                    const double en = sqrt(warp_sum(e * e));
+                    if (en > 1e-8) {
+                        w = e * (1.0 / en);
+                        placed = true;
+                    }
+                }
+                if (!placed) collapsed = true;
+            } else {
+                w *= 1.0 / nrm;
+            }
+            if (lane < lead) q[lane + j * KM] = w;
+            __syncwarp();
+        }
+        if (collapsed && lane == 0)
+            if (atomicCAS(&a.st->err_code, 0, kErrOrth) == 0) a.st->err_iter = a.iter;
+    }
+    __syncthreads();
+    if (a.mode == 1) {
+        for (int i = threadIdx.x; i < k * b; i += blockDim.x) {
+            const int r = i % k, j = i / k;
+            double s = 0.0;
+            for (int l = 0; l < lead; ++l) s += Vs[r + l * KM] * q[l + j * KM];
+            mix[r + j * KM] = s;
+            a.Cm[r + (b + j) * k] = s;
+        }
+    }
+    __syncthreads();
+    // 5. n-side products V' = T C, X' = T mix (dense.cpp:75-89 matmul)
+    for (int64_t i = threadIdx.x; i < a.n; i += blockDim.x) {
+        double t[KM];
+#pragma unroll
+        for (int l = 0; l < KM; ++l) t[l] = l < k ? a.T.p[l][i] : 0.0;
+        for (int j = 0; j < b; ++j) {
+            double v = 0.0, xv = 0.0;
+#pragma unroll
+            for (int l = 0; l < KM; ++l)
+                if (l < k) {
+                    v = fma(Vs[l + (lead + j) * KM], t[l], v);
+                    if (a.mode == 1) xv = fma(mix[l + j * KM], t[l], xv);
+                }
+            a.Vout[i + j * a.n] = v;
+            if (a.mode == 1) a.Xout[i + j * a.n] = xv;
+        }
+    }
+}
+
+// G = sum of per-CTA partials (fixed order); R = G - theta^2 V; partial norms
+__global__ void __launch_bounds__(256) reduce_g_kernel(const double* Gpart, int nparts, int64_t n, int b,
+                                                       const double* V, const DevState* st, int residual,
+                                                       double* Gout, double* nrm_part) {
+    __shared__ double red[8];
+    const int j = blockIdx.y;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    double v = 0.0;
+    if (i < n) {
+        double s = 0.0;
+        for (int p = 0; p < nparts; ++p) s += Gpart[(static_cast<size_t>(p) * b + j) * n + i];
+        if (residual) {
+            const double th = st->theta[j];
+            s -= (th * th) * V[i + j * n];
+        }
+        Gout[i + j * n] = s;
+        v = s * s;
+    }
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        nrm_part[j * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+// record row + stop rule (solver.cpp:376-397, :177-211)
+__global__ void __launch_bounds__(256) control_kernel(ControlArgs a) {
+    __shared__ double red[8];
+    __shared__ double resid_s;
+    if (threadIdx.x == 0) {
+        double best = 0.0;
+        for (int j = 0; j < a.b; ++j) {
+            double s = 0.0;
+            for (int x = 0; x < a.nblk; ++x) s += a.nrm_part[j * a.nblk + x];
+            best = fmax(best, sqrt(s));
+        }
+        resid_s = best;
+    }
+    double c = 0.0;
+    if (a.truth_v) {
+        const double* vc = a.V + static_cast<int64_t>(a.b - 1) * a.n;
+        for (int64_t i = threadIdx.x; i < a.n; i += blockDim.x) c += vc[i] * a.truth_v[i];
+        c = warp_sum(c);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    DevState* st = a.st;
+    msvd_record_row row;
+    row.iter = a.row;
+    row.pad_ = 0;
+    row.matvecs_a = static_cast<int64_t>(a.b) * (a.row + 1);
+    row.matvecs_at = static_cast<int64_t>(a.b) * (a.row + 1);
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    row.wall_ms = a.timing ? static_cast<double>(now - st->t0_ns) * 1e-6 : 0.0;
+    row.theta = st->theta[a.b - 1];
+    row.resid = resid_s;
+    row.relerr = -1.0;
+    row.sin_angle = -1.0;
+    if (a.truth_v) {
+        double cc = 0.0;
+        for (int w = 0; w < 8; ++w) cc += red[w];
+        cc = fmin(1.0, fmax(-1.0, cc));
+        const double sn = a.truth_sigma;
+        row.relerr = sn > 0.0 ? fabs(row.theta - sn) / sn : fabs(row.theta);
+        row.sin_angle = sqrt(fmax(0.0, 1.0 - cc * cc));
+    }
+    a.rows[a.row] = row;
+    a.rh[a.row] = resid_s;
+    a.th[a.row] = st->theta[0];
+    if (a.check) {
+        const int i = a.row - 1;
+        const double* rh = a.rh;
+        const double* th = a.th;
+        const bool tol_ok = rh[i + 1] <= a.sigma1 * a.sigma1 * a.tol;
+        bool stop = tol_ok;
+        if (a.use_stag) {
+            bool rs = false, ps = false;
+            if (i >= 4) rs = a.factor * rh[i + 1] >= rh[i - 4];
+            if (i >= 9) {
+                const double dn = th[i] > 0.0 ? th[i] : 1.0;
+                const double dt = th[i - 4] > 0.0 ? th[i - 4] : 1.0;
+                const double recent = (th[i - 4] - th[i + 1]) / dn;
+                const double earlier = (th[i - 9] - th[i - 4]) / dt;
+                ps = a.factor * recent >= earlier;
+            }
+            stop = tol_ok && rs && ps;
+        }
+        st->stop = stop ? 1 : 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// preconditioner apply (precond.cpp:38-48): t = Vt^T r / sig^2, w = Vt t.
+// Vt is held column-major (Vcol) and row-major (Vrow) so both passes are
+// warp-per-vector coalesced dot products over an L2-resident n x n matrix.
+// ---------------------------------------------------------------------------
+template <int B>
+__global__ void __launch_bounds__(256) dots_kernel(const double* M, int64_t n, const double* X,
+                                                   const double* sig, double* out, DevState* st, int iter,
+                                                   int check_finite) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    if (c >= n) return;
+    const double* mc = M + c * n;
+    double acc[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) acc[j] = 0.0;
+    for (int64_t i = lane; i < n; i += 32) {
+        const double mv = mc[i];
+#pragma unroll
+        for (int j = 0; j < B; ++j) acc[j] = fma(mv, X[i + j * n], acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j) acc[j] = warp_sum(acc[j]);
+    if (lane == 0) {
+        bool finite = true;
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            double v = acc[j];
+            if (sig) {
+                const double s = sig[c];
+                v /= s * s;
+            }
+            out[c + j * n] = v;
+            finite = finite && isfinite(v);
+        }
+        if (check_finite && !finite)
+            if (atomicCAS(&st->err_code, 0, kErrNonfiniteW) == 0) st->err_iter = iter;
+    }
+}
+
+__global__ void diag_scale_kernel(int kind, const double* R, const double* dinv, int64_t n, int b, double* W,
+                                  DevState* st, int iter) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n * b) return;
+    const double v = kind == MSVD_PRECOND_DIAGONAL ? R[i] * dinv[i % n] : R[i];
+    W[i] = v;
+    if (!isfinite(v))
+        if (atomicCAS(&st->err_code, 0, kErrNonfiniteW) == 0) st->err_iter = iter;
+}
+
+// ---------------------------------------------------------------------------
+// BCGS2 (solver.cpp:213-261), single CTA.  Each pass projects against all
+// basis columns and all earlier W columns at once (one multi-dot per pass);
+// degenerate columns are replaced from the solver's SplitMix64 Gaussian
+// stream, generated counter-style so every thread draws its own entries.
+// ---------------------------------------------------------------------------
+constexpr int kCgsT = 512;
+
+__device__ double gauss_at(uint64_t s, int have_spare, double spare, int64_t e) {
+    int64_t idx = e;
+    if (have_spare) {
+        if (e == 0) return spare;
+        idx = e - 1;
+    }
+    const int64_t pr = idx / 2;
+    const uint64_t d1 = sm_mix(s + kGolden * static_cast<uint64_t>(2 * pr + 1));
+    const uint64_t d2 = sm_mix(s + kGolden * static_cast<uint64_t>(2 * pr + 2));
+    const double u1 = static_cast<double>((d1 >> 11) + 1) * 0x1.0p-53;
+    const double u2 = static_cast<double>((d2 >> 11) + 1) * 0x1.0p-53;
+    const double rad = sqrt(-2.0 * log(u1));
+    const double ang = 6.283185307179586476925286766559 * u2;
+    return (idx & 1) ? rad * sin(ang) : rad * cos(ang);
+}
+
+// block-wide sums of cnt (<= 32) per-thread values; result in out[0..cnt)
+__device__ void block_multi_sum(double (&v)[32], int cnt, double* red, double* out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const double t = warp_transpose_reduce32(v);
+    red[warp * 32 + lane] = t;
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w * 32 + threadIdx.x];
+        out[threadIdx.x] = s;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kCgsT) cgs2_kernel(double* W, int64_t n, int b, Cols basis, int nb,
+                                                     DevState* st, int iter) {
+    __shared__ double red[32 * 32];
+    __shared__ double sums[32];
+    __shared__ double scale_ref;
+    // scale_ref = max column norm of the incoming W (solver.cpp:217)
+    {
+        double v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.0;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x)
+#pragma unroll
+            for (int j = 0; j < kMaxB; ++j)
+                if (j < b) v[j] += W[i + j * n] * W[i + j * n];
+        block_multi_sum(v, b, red, sums);
+        if (threadIdx.x == 0) {
+            double best = 0.0;
+            for (int j = 0; j < b; ++j) best = fmax(best, sqrt(sums[j]));
+            scale_ref = best;
+        }
+        __syncthreads();
+    }
+    const double drop = static_cast<double>(n) * kEps * scale_ref;
+    for (int j = 0; j < b; ++j) {
+        double* x = W + j * n;
+        const int cnt = nb + j;
+        bool replaced = false;
+        for (int attempt = -1; attempt < 8; ++attempt) {
+            if (attempt >= 0) {
+                // x = fresh Gaussian draws (rng.hpp:40-52 stream continued)
+                const uint64_t s0 = st->rng_state;
+                const int hs = st->have_spare;
+                const double sp = st->spare;
+                for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] = gauss_at(s0, hs, sp, i);
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    const int64_t fresh = hs ? n - 1 : n;
+                    const int64_t pairs = (fresh + 1) / 2;
+                    if (fresh & 1) {
+                        st->spare = gauss_at(s0, 0, 0.0, 2 * pairs - 1);
+                        st->have_spare = 1;
+                    } else {
+                        st->have_spare = 0;
+                    }
+                    st->rng_state = s0 + kGolden * static_cast<uint64_t>(2 * pairs);
+                }
+            }
+            for (int pass = 0; pass < 2; ++pass) {
+                double v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.0;
+                for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+                    const double xi = x[i];
+#pragma unroll
+                    for (int l = 0; l < 2 * kMaxB + kMaxB; ++l) {
+                        if (l < cnt) {
+                            const double cl = l < nb ? basis.p[l][i] : W[i + (l - nb) * n];
+                            v[l] = fma(cl, xi, v[l]);
+                        }
+                    }
+                }
+                block_multi_sum(v, cnt, red, sums);
+                for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+                    double xi = x[i];
+                    for (int l = 0; l < cnt; ++l) {
+                        const double cl = l < nb ? basis.p[l][i] : W[i + (l - nb) * n];
+                        xi -= sums[l] * cl;
+                    }
+                    x[i] = xi;
+                }
+                __syncthreads();
+            }
+            double v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.0;
+            for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v[0] += x[i] * x[i];
+            block_multi_sum(v, 1, red, sums);
+            const double nrm = sqrt(sums[0]);
+            const bool accept = attempt < 0 ? nrm > drop : nrm > 1e-3 * sqrt(static_cast<double>(n));
+            if (accept) {
+                const double inv = 1.0 / nrm;
+                for (int64_t i = threadIdx.x; i < n; i += blockDim.x) x[i] *= inv;
+                __syncthreads();
+                if (attempt >= 0) replaced = true;
+                break;
+            }
+            if (attempt == 7) {
+                if (threadIdx.x == 0)
+                    if (atomicCAS(&st->err_code, 0, kErrCgs2) == 0) st->err_iter = iter;
+                return;
+            }
+        }
+        if (replaced && threadIdx.x == 0) st->replacements += 1;
+        __syncthreads();
+    }
+}
+
+__global__ void state_init_kernel(DevState* st, uint64_t seed) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    st->stop = 0;
+    st->err_code = 0;
+    st->err_iter = -1;
+    st->have_spare = 0;
+    st->rng_state = sm_keyed_state(seed, 0x9e3779b97f4a7c15ULL);  // solver.cpp:342
+    st->spare = 0.0;
+    st->replacements = 0;
+    st->t0_ns = now;
+    st->max_drift = 0.0;
+    st->worst_jacobi = 0.0;
+    for (int j = 0; j < kMaxB; ++j) st->theta[j] = 0.0;
+}
+
+__global__ void drift_kernel(const double* fresh, const double* cached, int64_t count, DevState* st) {
+    double v = 0.0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        v = fmax(v, fabs(fresh[i] - cached[i]));
+    v = warp_max(v);
+    if ((threadIdx.x & 31) == 0) atomic_max_pos(&st->max_drift, v);
+}
+
+__global__ void drift_check_kernel(DevState* st, double limit, int iter) {
+    if (st->max_drift > limit)
+        if (atomicCAS(&st->err_code, 0, kErrDrift) == 0) st->err_iter = iter;
+}
+
+// column sums of squares of a row-major A: per-CTA partials then a fixed-order sum
+__global__ void colsq_kernel(const double* A, int64_t m, int n, int64_t ld, double* part) {
+    const int64_t r0 = (m * blockIdx.y) / gridDim.y, r1 = (m * (blockIdx.y + 1)) / gridDim.y;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    double s = 0.0;
+    for (int64_t r = r0; r < r1; ++r) {
+        const double v = A[r * ld + c];
+        s += v * v;
+    }
+    part[static_cast<int64_t>(blockIdx.y) * n + c] = s;
+}
+__global__ void colsq_finish_kernel(const double* part, int np, int n, double* out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n) return;
+    double s = 0.0;
+    for (int p = 0; p < np; ++p) s += part[static_cast<int64_t>(p) * n + c];
+    out[c] = s;
+}
+
+__global__ void transpose_kernel(const double* A, int64_t m, int64_t n, int64_t ld, double* out) {
+    __shared__ double tile[32][33];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32, c0 = static_cast<int64_t>(blockIdx.x) * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        tile[i][threadIdx.x] = (r < m && c < n) ? A[r * ld + c] : 0.0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < m && c < n) out[c * m + r] = tile[threadIdx.x][i];
+    }
+}
+
+__global__ void copy_cols_kernel(const double* src, int64_t ld, int64_t col0, int64_t rows, int64_t cols,
+                                 double* dst) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows * cols) return;
+    const int64_t r = i % rows, c = i / rows;
+    dst[i] = src[r + (col0 + c) * ld];
+}
+
+template <int KM>
+__global__ void __launch_bounds__(512) small_svd_kernel(const double* B, int k, double* sigma, double* Vout,
+                                                         DevState* st) {
+    __shared__ double Bm[KM * KM], V[KM * KM], Vs[KM * KM], sig[KM], worst[2];
+    __shared__ int ord[KM];
+    for (int i = threadIdx.x; i < KM * KM; i += blockDim.x) {
+        const int r = i % KM, c = i / KM;
+        Bm[i] = (r < k && c < k) ? B[r + c * k] : 0.0;
+    }
+    __syncthreads();
+    const bool ok = jacobi_svd<KM>(Bm, V, k, sig, Vs, ord, worst);
+    if (!ok && threadIdx.x == 0) st->err_code = kErrJacobi;
+    if (threadIdx.x < k) sigma[threadIdx.x] = sig[threadIdx.x];
+    for (int i = threadIdx.x; i < k * k; i += blockDim.x) Vout[i] = Vs[(i % k) + (i / k) * KM];
+}
+
+template <int KM>
+size_t rr_smem() {
+    return sizeof(double) * (16 * KM * KM + 3 * KM * KM + KM + 2 * KM * kMaxB + 2) + sizeof(int) * KM + 64;
+}
+
+int km_for(int k) {
+    if (k <= 4) return 4;
+    if (k <= 8) return 8;
+    if (k <= 16) return 16;
+    if (k <= 24) return 24;
+    fail(MSVD_ERR_DIMENSION, "msvd: trial width above 24 is not supported");
+}
+
+template <int KM>
+void rr_launch(Ctx& c, const RRArgs& a) {
+    const size_t sm = rr_smem<KM>();
+    MSVD_CUDA(cudaFuncSetAttribute(rr_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    rr_kernel<KM><<<1, 512, sm, c.stream>>>(a);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+}  // namespace
+
+int tsqr_parts(const Ctx& c) { return c.num_sms; }
+
+void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st, int iter) {
+    TsqrArgs a{T, m, k, Rparts, st, iter};
+    const int grid = tsqr_parts(c);
+    switch (km_for(k)) {
+        case 4: tsqr_kernel<4><<<grid, 256, 0, c.stream>>>(a); break;
+        case 8: tsqr_kernel<8><<<grid, 256, 0, c.stream>>>(a); break;
+        case 16: tsqr_kernel<16><<<grid, 256, 0, c.stream>>>(a); break;
+        default: tsqr_kernel<24><<<grid, 256, 0, c.stream>>>(a); break;
+    }
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void launch_rr(Ctx& c, const RRArgs& a) {
+    switch (km_for(a.k)) {
+        case 4: rr_launch<4>(c, a); break;
+        case 8: rr_launch<8>(c, a); break;
+        case 16: rr_launch<16>(c, a); break;
+        default: rr_launch<24>(c, a); break;
+    }
+}
+
+void launch_small_svd(Ctx& c, const double* B, int k, double* sigma, double* V, DevState* st) {
+    switch (km_for(k)) {
+        case 4: small_svd_kernel<4><<<1, 512, 0, c.stream>>>(B, k, sigma, V, st); break;
+        case 8: small_svd_kernel<8><<<1, 512, 0, c.stream>>>(B, k, sigma, V, st); break;
+        case 16: small_svd_kernel<16><<<1, 512, 0, c.stream>>>(B, k, sigma, V, st); break;
+        default: small_svd_kernel<24><<<1, 512, 0, c.stream>>>(B, k, sigma, V, st); break;
+    }
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void launch_reduce_g(Ctx& c, const double* Gpart, int nparts, int64_t n, int b, const double* V,
+                     const DevState* st, int residual, double* Gout, double* nrm_part, int nblk) {
+    dim3 grid(static_cast<unsigned>(nblk), static_cast<unsigned>(b));
+    reduce_g_kernel<<<grid, 256, 0, c.stream>>>(Gpart, nparts, n, b, V, st, residual, Gout, nrm_part);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void launch_control(Ctx& c, const ControlArgs& a) {
+    control_kernel<<<1, 256, 0, c.stream>>>(a);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+template <int B>
+static void precond_b(Ctx& c, const double* Vcol, const double* Vrow, const double* sig, int64_t n,
+                      const double* R, double* tmp, double* W, DevState* st, int iter) {
+    const unsigned grid = static_cast<unsigned>(ceil_div(n, 8));
+    dots_kernel<B><<<grid, 256, 0, c.stream>>>(Vcol, n, R, sig, tmp, st, iter, 0);
+    dots_kernel<B><<<grid, 256, 0, c.stream>>>(Vrow, n, tmp, nullptr, W, st, iter, 1);
+    MSVD_CUDA(cudaGetLastError());
+    c.launches += 2;
+}
+
+void launch_precond(Ctx& c, int kind, const double* Vcol, const double* Vrow, const double* sig,
+                    const double* dinv, int64_t n, const double* R, int b, double* tmp, double* W,
+                    DevState* st, int iter) {
+    if (kind != MSVD_PRECOND_RANDOMIZED) {
+        const int64_t tot = n * b;
+        diag_scale_kernel<<<static_cast<unsigned>(ceil_div(tot, 256)), 256, 0, c.stream>>>(kind, R, dinv, n, b, W,
+                                                                                           st, iter);
+        MSVD_CUDA(cudaGetLastError());
+        ++c.launches;
+        return;
+    }
+    switch (b) {
+        case 1: precond_b<1>(c, Vcol, Vrow, sig, n, R, tmp, W, st, iter); break;
+        case 2: precond_b<2>(c, Vcol, Vrow, sig, n, R, tmp, W, st, iter); break;
+        case 3: precond_b<3>(c, Vcol, Vrow, sig, n, R, tmp, W, st, iter); break;
+        case 4: precond_b<4>(c, Vcol, Vrow, sig, n, R, tmp, W, st, iter); break;
+        case 5: precond_b<5>(c, Vcol, Vrow, sig, n, R, tmp, W, st, iter); break;
+        case 6: precond_b<6>(c, Vcol, Vrow, sig, n, R, tmp, W, st, iter); break;
+        case 7: precond_b<7>(c, Vcol, Vrow, sig, n, R, tmp, W, st, iter); break;
+        default: precond_b<8>(c, Vcol, Vrow, sig, n, R, tmp, W, st, iter); break;
+    }
+}
+
+void launch_cgs2(Ctx& c, double* W, int64_t n, int b, Cols basis, int nb, DevState* st, int iter) {
+    cgs2_kernel<<<1, kCgsT, 0, c.stream>>>(W, n, b, basis, nb, st, iter);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void launch_state_init(Ctx& c, DevState* st, uint64_t seed) {
+    state_init_kernel<<<1, 1, 0, c.stream>>>(st, seed);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void launch_drift(Ctx& c, const double* fresh, const double* cached, int64_t count, DevState* st, double limit,
+                  int iter) {
+    drift_kernel<<<c.num_sms * 2, 256, 0, c.stream>>>(fresh, cached, count, st);
+    drift_check_kernel<<<1, 1, 0, c.stream>>>(st, limit, iter);
+    MSVD_CUDA(cudaGetLastError());
+    c.launches += 2;
+}
+
+void launch_colnorms(Ctx& c, const StreamGeom& g, double* part, double* out) {
+    const int np = c.num_sms;
+    dim3 grid(static_cast<unsigned>(ceil_div(g.n, 256)), static_cast<unsigned>(np));
+    colsq_kernel<<<grid, 256, 0, c.stream>>>(g.A, g.m, g.n, g.ld, part);
+    colsq_finish_kernel<<<static_cast<unsigned>(ceil_div(g.n, 256)), 256, 0, c.stream>>>(part, np, g.n, out);
+    MSVD_CUDA(cudaGetLastError());
+    c.launches += 2;
+}
+
+void launch_transpose_rm_to_cm(Ctx& c, const double* A, int64_t m, int64_t n, int64_t ld, double* out) {
+    dim3 grid(static_cast<unsigned>(ceil_div(n, 32)), static_cast<unsigned>(ceil_div(m, 32)));
+    transpose_kernel<<<grid, dim3(32, 8), 0, c.stream>>>(A, m, n, ld, out);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void launch_copy_cols(Ctx& c, const double* src, int64_t ld_src, int64_t col0, int64_t rows, int64_t cols,
+                      double* dst) {
+    const int64_t tot = rows * cols;
+    if (tot == 0) return;
+    copy_cols_kernel<<<static_cast<unsigned>(ceil_div(tot, 256)), 256, 0, c.stream>>>(src, ld_src, col0, rows, cols,
+                                                                                      dst);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+}  // namespace msvd

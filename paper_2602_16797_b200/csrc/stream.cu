@@ -1,0 +1,404 @@
+// The two O(mn) passes over the tall row-major A.
+//
+// Both kernels are persistent (one CTA per SM, contiguous row range per CTA)
+// and share one producer: warp 0 streams the CTA's rows HBM -> shared memory
+// through a ring of `stages` buffers with 1-D TMA bulk copies
+// (cp.async.bulk ... mbarrier::complete_tx, L2 evict_first) or, when A's rows
+// are not 16-byte aligned, with plain coalesced loads.  Consumer threads own
+// fixed column pairs (16-byte shared loads, conflict free), so A is read from
+// HBM exactly once per pass for all b right-hand sides.
+//
+//   apply_kernel  (K3)  Y = A W           -- operator.cpp:7-12 / dense.cpp:50-60
+//   gram_kernel   (K2)  G = A^T (T C)     -- solver.cpp:357-369 residual_of with
+//                        the recurrence products AV' = AT C, AX' = AT mix
+//                        (solver.cpp:421, :462) formed in-tile by a Y warp.
+#include "common.cuh"
+#include "msvd_internal.h"
+
+namespace msvd {
+
+namespace {
+
+constexpr int kStageTarget = 32 * 1024;
+constexpr int kStageBudget = 160 * 1024;
+
+struct Pipe {
+    uint64_t* full;
+    uint64_t* empty;
+    unsigned char* stage0;
+    size_t stage_bytes;
+};
+
+__device__ __forceinline__ void cta_rows(int64_t m, int64_t& r0, int64_t& r1) {
+    r0 = (m * blockIdx.x) / gridDim.x;
+    r1 = (m * (blockIdx.x + 1)) / gridDim.x;
+}
+
+// Warp 0: fill stage c % S with rows [r_begin + c*rc, ...) of A.
+__device__ void produce(const StreamGeom& g, const Pipe& p, int64_t r_begin, int64_t r_end) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nrows = r_end - r_begin;
+    const int64_t nchunks = ceil_div(nrows, g.rc);
+    if (g.tma) {
+        if (lane != 0) return;
+        const uint64_t pol = l2_evict_first_policy();
+        for (int64_t c = 0; c < nchunks; ++c) {
+            const int s = static_cast<int>(c % g.stages);
+            const int64_t it = c / g.stages;
+            if (c >= g.stages) mbar_wait(&p.empty[s], static_cast<uint32_t>((it - 1) & 1));
+            const int64_t r0 = r_begin + c * g.rc;
+            const int64_t rc = min(static_cast<int64_t>(g.rc), r_end - r0);
+            const uint32_t bytes = static_cast<uint32_t>(rc * g.ld * 8);
+            mbar_arrive_expect_tx(&p.full[s], bytes);
+            bulk_g2s(p.stage0 + s * p.stage_bytes, g.A + r0 * g.ld, bytes, &p.full[s], pol);
+        }
+    } else {
+        for (int64_t c = 0; c < nchunks; ++c) {
+            const int s = static_cast<int>(c % g.stages);
+            const int64_t it = c / g.stages;
+            if (c >= g.stages) mbar_wait(&p.empty[s], static_cast<uint32_t>((it - 1) & 1));
+            const int64_t r0 = r_begin + c * g.rc;
+            const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
+            double* dst = reinterpret_cast<double*>(p.stage0 + s * p.stage_bytes);
+            for (int r = 0; r < rc; ++r) {
+                const double* src = g.A + (r0 + r) * g.ld;
+                for (int e = lane; e < g.ld_s; e += 32) dst[r * g.ld_s + e] = e < g.n ? __ldg(src + e) : 0.0;
+            }
+            __syncwarp();
+            mbar_arrive(&p.full[s]);  // all 32 lanes arrive (count includes them)
+        }
+    }
+}
+
+// shared-memory carve-up common to both kernels
+__device__ __forceinline__ Pipe carve(unsigned char* smem, const StreamGeom& g, size_t extra_bytes,
+                                      unsigned char** extra) {
+    Pipe p;
+    p.full = reinterpret_cast<uint64_t*>(smem);
+    p.empty = p.full + g.stages;
+    *extra = smem + 256;
+    p.stage0 = smem + 256 + ((extra_bytes + 127) / 128) * 128;
+    p.stage_bytes = g.stage_bytes;
+    return p;
+}
+
+struct ApplyArgs {
+    StreamGeom g;
+    const double* W;  // n x b col-major
+    OutCols out;      // b columns of length m
+};
+
+// K3: Y = A W.  Warps 1..8 consume; each row's b partial dots are reduced
+// across the 256 consumer threads with a warp transpose-reduce + one named
+// barrier per group of floor(32/B) rows.
+template <int B>
+__global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const StreamGeom& g = a.g;
+    unsigned char* extra;
+    Pipe p = carve(smem, g, sizeof(double) * 2 * 8 * 32, &extra);
+    double* red = reinterpret_cast<double*>(extra);  // [2][8][32]
+    int64_t r_begin, r_end;
+    cta_rows(g.m, r_begin, r_end);
+    if (threadIdx.x == 0) {
+        const uint32_t full_count = g.tma ? 1u : 32u;
+        for (int s = 0; s < g.stages; ++s) {
+            mbar_init(&p.full[s], full_count);
+            mbar_init(&p.empty[s], kConsumers / 32);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp == 0) {
+        produce(g, p, r_begin, r_end);
+        return;
+    }
+    const int ct = threadIdx.x - 32;
+    const int cw = ct >> 5;
+    const int n = g.n;
+    const int npairs = (n + 1) >> 1;
+    double w[kMaxPairs][2][B];
+#pragma unroll
+    for (int i = 0; i < kMaxPairs; ++i) {
+        const int c0 = 2 * (ct + i * kConsumers);
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            w[i][0][j] = c0 < n ? a.W[c0 + static_cast<int64_t>(j) * n] : 0.0;
+            w[i][1][j] = c0 + 1 < n ? a.W[c0 + 1 + static_cast<int64_t>(j) * n] : 0.0;
+        }
+    }
+    constexpr int NV = B >= 5 ? 16 : 32;  // transpose-reduce slots
+    constexpr int GR = NV / B;            // rows per reduction group
+    const int64_t nchunks = ceil_div(r_end - r_begin, g.rc);
+    int buf = 0;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int s = static_cast<int>(c % g.stages);
+        mbar_wait(&p.full[s], static_cast<uint32_t>((c / g.stages) & 1));
+        const double* As = reinterpret_cast<const double*>(p.stage0 + s * p.stage_bytes);
+        const int64_t r0 = r_begin + c * g.rc;
+        const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
+        for (int g0 = 0; g0 < rc; g0 += GR) {
+            const int gn = min(GR, rc - g0);
+            double v[NV];
+#pragma unroll
+            for (int i = 0; i < NV; ++i) v[i] = 0.0;
+#pragma unroll
+            for (int rr = 0; rr < GR; ++rr) {
+                if (rr < gn) {
+                    const double* row = As + static_cast<int64_t>(g0 + rr) * g.ld_s;
+#pragma unroll
+                    for (int i = 0; i < kMaxPairs; ++i) {
+                        const int pi = ct + i * kConsumers;
+                        if (pi < npairs) {
+                            const double2 x = *reinterpret_cast<const double2*>(row + 2 * pi);
+                            const double xy = (2 * pi + 1 < n) ? x.y : 0.0;
+#pragma unroll
+                            for (int j = 0; j < B; ++j) {
+                                v[rr * B + j] = fma(x.x, w[i][0][j], v[rr * B + j]);
+                                v[rr * B + j] = fma(xy, w[i][1][j], v[rr * B + j]);
+                            }
+                        }
+                    }
+                }
+            }
+            const double tot = warp_transpose_reduce<NV>(v);
+            red[(buf * 8 + cw) * 32 + lane] = tot;
+            named_sync(1, kConsumers);
+            if (ct < gn * B) {
+                double sum = 0.0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) sum += red[(buf * 8 + q) * 32 + ct];
+                const int rr = ct / B, j = ct - (ct / B) * B;
+                a.out.p[j][r0 + g0 + rr] = sum;
+            }
+            buf ^= 1;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p.empty[s]);
+    }
+}
+
+struct GramArgs {
+    StreamGeom g;
+    Cols T;            // k columns of length m
+    int k;
+    const double* Cm;  // k x q, ld k (gram mode)
+    int q;             // Y columns produced (<= 2B); the first B feed G
+    OutCols out;       // q output columns (gram mode)
+    int direct;        // Y = T (k == B), no outputs
+    double* Gpart;     // [grid][B][n]
+};
+
+// K2: Gpart = A_cta^T Y_cta.  Warp 1 (the Y warp) forms Y rows for each
+// stage from the skinny trial block and writes the new recurrence products;
+// warps 2..9 stream the stage and accumulate in registers.
+template <int B>
+__global__ void __launch_bounds__(64 + kConsumers, 1) gram_kernel(GramArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const StreamGeom& g = a.g;
+    const size_t cm_bytes = sizeof(double) * kMaxK * 2 * kMaxB;
+    const size_t ys_bytes = sizeof(double) * g.stages * g.rc * B;
+    unsigned char* extra;
+    Pipe p = carve(smem, g, cm_bytes + ys_bytes, &extra);
+    double* Cs = reinterpret_cast<double*>(extra);
+    double* Ys = Cs + kMaxK * 2 * kMaxB;
+    int64_t r_begin, r_end;
+    cta_rows(g.m, r_begin, r_end);
+    if (threadIdx.x == 0) {
+        const uint32_t full_count = (g.tma ? 1u : 32u) + 32u;
+        for (int s = 0; s < g.stages; ++s) {
+            mbar_init(&p.full[s], full_count);
+            mbar_init(&p.empty[s], kConsumers / 32);
+        }
+        mbar_fence_init();
+    }
+    if (!a.direct)
+        for (int i = threadIdx.x; i < a.k * a.q; i += blockDim.x) Cs[i] = a.Cm[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nchunks = ceil_div(r_end - r_begin, g.rc);
+    if (warp == 0) {
+        produce(g, p, r_begin, r_end);
+        return;
+    }
+    if (warp == 1) {
+        for (int64_t c = 0; c < nchunks; ++c) {
+            const int s = static_cast<int>(c % g.stages);
+            const int64_t it = c / g.stages;
+            if (c >= g.stages) mbar_wait(&p.empty[s], static_cast<uint32_t>((it - 1) & 1));
+            const int64_t r0 = r_begin + c * g.rc;
+            const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
+            double* ys = Ys + static_cast<size_t>(s) * g.rc * B;
+            for (int r = lane; r < rc; r += 32) {
+                const int64_t gr = r0 + r;
+                if (a.direct) {
+#pragma unroll
+                    for (int j = 0; j < B; ++j) ys[r * B + j] = a.T.p[j][gr];
+                } else {
+                    double t[kMaxK];
+#pragma unroll
+                    for (int l = 0; l < kMaxK; ++l) t[l] = l < a.k ? a.T.p[l][gr] : 0.0;
+                    for (int j = 0; j < a.q; ++j) {
+                        double y = 0.0;
+#pragma unroll
+                        for (int l = 0; l < kMaxK; ++l)
+                            if (l < a.k) y = fma(Cs[l + j * a.k], t[l], y);
+                        if (j < B) ys[r * B + j] = y;
+                        a.out.p[j][gr] = y;
+                    }
+                }
+            }
+            __syncwarp();
+            mbar_arrive(&p.full[s]);
+        }
+        return;
+    }
+    const int ct = threadIdx.x - 64;
+    const int n = g.n;
+    const int npairs = (n + 1) >> 1;
+    double acc[kMaxPairs][2][B];
+#pragma unroll
+    for (int i = 0; i < kMaxPairs; ++i)
+#pragma unroll
+        for (int j = 0; j < B; ++j) acc[i][0][j] = acc[i][1][j] = 0.0;
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int s = static_cast<int>(c % g.stages);
+        mbar_wait(&p.full[s], static_cast<uint32_t>((c / g.stages) & 1));
+        const double* As = reinterpret_cast<const double*>(p.stage0 + s * p.stage_bytes);
+        const double* ys = Ys + static_cast<size_t>(s) * g.rc * B;
+        const int64_t r0 = r_begin + c * g.rc;
+        const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
+#pragma unroll 2
+        for (int r = 0; r < rc; ++r) {
+            double y[B];
+#pragma unroll
+            for (int j = 0; j < B; ++j) y[j] = ys[r * B + j];
+            const double* row = As + static_cast<int64_t>(r) * g.ld_s;
+#pragma unroll
+            for (int i = 0; i < kMaxPairs; ++i) {
+                const int pi = ct + i * kConsumers;
+                if (pi < npairs) {
+                    const double2 x = *reinterpret_cast<const double2*>(row + 2 * pi);
+                    const double xy = (2 * pi + 1 < n) ? x.y : 0.0;
+#pragma unroll
+                    for (int j = 0; j < B; ++j) {
+                        acc[i][0][j] = fma(x.x, y[j], acc[i][0][j]);
+                        acc[i][1][j] = fma(xy, y[j], acc[i][1][j]);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p.empty[s]);
+    }
+    double* gp = a.Gpart + static_cast<size_t>(blockIdx.x) * B * n;
+#pragma unroll
+    for (int i = 0; i < kMaxPairs; ++i) {
+        const int c0 = 2 * (ct + i * kConsumers);
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            if (c0 < n) gp[static_cast<size_t>(j) * n + c0] = acc[i][0][j];
+            if (c0 + 1 < n) gp[static_cast<size_t>(j) * n + c0 + 1] = acc[i][1][j];
+        }
+    }
+}
+
+size_t apply_smem(const StreamGeom& g) {
+    return 256 + ((sizeof(double) * 2 * 8 * 32 + 127) / 128) * 128 + g.stages * g.stage_bytes;
+}
+size_t gram_smem(const StreamGeom& g, int B) {
+    const size_t extra = sizeof(double) * kMaxK * 2 * kMaxB + sizeof(double) * g.stages * g.rc * B;
+    return 256 + ((extra + 127) / 128) * 128 + g.stages * g.stage_bytes;
+}
+
+template <int B>
+void apply_b(Ctx& c, const ApplyArgs& a) {
+    const size_t sm = apply_smem(a.g);
+    static bool attr = false;
+    if (!attr) {
+        MSVD_CUDA(cudaFuncSetAttribute(apply_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(c.smem_optin)));
+        attr = true;
+    }
+    apply_kernel<B><<<a.g.grid, 32 + kConsumers, sm, c.stream>>>(a);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+template <int B>
+void gram_b(Ctx& c, const GramArgs& a) {
+    const size_t sm = gram_smem(a.g, B);
+    static bool attr = false;
+    if (!attr) {
+        MSVD_CUDA(cudaFuncSetAttribute(gram_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(c.smem_optin)));
+        attr = true;
+    }
+    gram_kernel<B><<<a.g.grid, 64 + kConsumers, sm, c.stream>>>(a);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+}  // namespace
+
+StreamGeom make_geom(const Ctx& c, const double* A, int64_t m, int32_t n, int64_t ld) {
+    if (n < 1 || n > kMaxN)
+        fail(MSVD_ERR_DIMENSION, "msvd: column count " + std::to_string(n) +
+                                     " outside the supported range [1, " + std::to_string(kMaxN) + "]");
+    StreamGeom g{};
+    g.A = A;
+    g.m = m;
+    g.n = n;
+    g.ld = ld;
+    g.tma = (ld % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) ? 1 : 0;
+    g.ld_s = g.tma ? static_cast<int32_t>(ld) : static_cast<int32_t>((n + 1) & ~1);
+    const int64_t row_bytes = static_cast<int64_t>(g.ld_s) * 8;
+    if (row_bytes > kStageBudget / 2)
+        fail(MSVD_ERR_DIMENSION, "msvd: leading dimension too large for the stream pipeline");
+    g.rc = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(kStageTarget / row_bytes, 64)));
+    g.stage_bytes = ((static_cast<size_t>(g.rc) * row_bytes + 127) / 128) * 128;
+    g.stages = static_cast<int32_t>(std::max<size_t>(2, std::min<size_t>(8, kStageBudget / g.stage_bytes)));
+    g.grid = c.num_sms;
+    return g;
+}
+
+void launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out) {
+    if (g.m == 0) return;
+    ApplyArgs a{g, W, out};
+    switch (b) {
+        case 1: apply_b<1>(c, a); break;
+        case 2: apply_b<2>(c, a); break;
+        case 3: apply_b<3>(c, a); break;
+        case 4: apply_b<4>(c, a); break;
+        case 5: apply_b<5>(c, a); break;
+        case 6: apply_b<6>(c, a); break;
+        case 7: apply_b<7>(c, a); break;
+        case 8: apply_b<8>(c, a); break;
+        default: fail(MSVD_ERR_DIMENSION, "msvd: block size above 8 is not supported");
+    }
+}
+
+void launch_gram(Ctx& c, const StreamGeom& g, Cols T, int k, const double* Cm, int q, int b,
+                 OutCols out, bool direct, double* Gpart) {
+    GramArgs a{g, T, k, Cm, q, out, direct ? 1 : 0, Gpart};
+    if (g.m == 0) {
+        MSVD_CUDA(cudaMemsetAsync(Gpart, 0, sizeof(double) * g.grid * b * g.n, c.stream));
+        return;
+    }
+    switch (b) {
+        case 1: gram_b<1>(c, a); break;
+        case 2: gram_b<2>(c, a); break;
+        case 3: gram_b<3>(c, a); break;
+        case 4: gram_b<4>(c, a); break;
+        case 5: gram_b<5>(c, a); break;
+        case 6: gram_b<6>(c, a); break;
+        case 7: gram_b<7>(c, a); break;
+        case 8: gram_b<8>(c, a); break;
+        default: fail(MSVD_ERR_DIMENSION, "msvd: block size above 8 is not supported");
+    }
+}
+
+}  // namespace msvd

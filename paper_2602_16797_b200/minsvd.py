@@ -1,0 +1,550 @@
+"""Python mirror of the reference's solve API over libmsvd_cuda.so.
+
+Same names, argument meaning and error behaviour as minsvd's C++ API
+(/root/reference/proj/include/minsvd/solver.hpp:25-190, operator.hpp:15-56,
+errors.hpp:9-38), so tests read like the reference's own:
+
+    opts = SolverOptions(seed=7, block_size=4, tol=1e-10, use_stagnation=False)
+    res = rlobpcg_block(DeviceDenseOperator(A_cuda), opts, truth)
+    res.sigma, res.v, res.record.to_csv(), res.iterations()
+
+Device memory is plumbing from torch; every computation runs in the CUDA
+library.  There is no CPU path: importing works anywhere, but any call that
+needs the GPU raises when the extension or the device is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmsvd_cuda.so")
+CSRC = os.path.join(HERE, "csrc")
+
+
+# --------------------------------------------------------------- errors.hpp
+class Error(RuntimeError):
+    """minsvd::Error"""
+
+
+class DimensionError(Error):
+    """minsvd::DimensionError"""
+
+
+class IoError(Error):
+    """minsvd::IoError"""
+
+
+class NumericalError(Error):
+    """minsvd::NumericalError"""
+
+
+class ConvergenceError(Error):
+    """minsvd::ConvergenceError"""
+
+
+_STATUS_EXC = {
+    abi.MSVD_ERR_DIMENSION: DimensionError,
+    abi.MSVD_ERR_IO: IoError,
+    abi.MSVD_ERR_NUMERICAL: NumericalError,
+    abi.MSVD_ERR_CONVERGENCE: ConvergenceError,
+}
+
+
+# ----------------------------------------------------------------- library
+_lib = None
+
+
+def build(force=False, quiet=True):
+    """Compile libmsvd_cuda.so in-tree (nvcc, sm_100a)."""
+    args = ["make", "-C", CSRC, "-j8"]
+    if force:
+        subprocess.run(["make", "-C", CSRC, "clean"], check=True, capture_output=quiet)
+    out = subprocess.run(args, capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError(f"libmsvd_cuda build failed:\n{out.stdout[-4000:]}\n{out.stderr[-4000:]}")
+    return LIB_PATH
+
+
+def _declare(lib):
+    P = C.POINTER
+    d = C.c_double
+    i64 = C.c_int64
+    i32 = C.c_int32
+    vp = C.c_void_p
+    sig = {
+        "msvd_abi_version": (i32, []),
+        "msvd_last_error": (C.c_char_p, []),
+        "msvd_status_name": (C.c_char_p, [i32]),
+        "msvd_options_default": (None, [P(abi.Options)]),
+        "msvd_default_tolerance": (d, [i64]),
+        "msvd_validate_options": (i32, [i64, i64, P(abi.Options), P(abi.Truth)]),
+        "msvd_shard_rows": (None, [i64, i32, i32, P(i64), P(i64)]),
+        "msvd_get_nccl_unique_id": (i32, [P(C.c_uint8)]),
+        "msvd_fake_group_create": (i32, [i32, P(vp)]),
+        "msvd_fake_group_destroy": (i32, [vp]),
+        "msvd_ctx_create": (i32, [P(abi.CtxDesc), P(vp)]),
+        "msvd_ctx_destroy": (i32, [vp]),
+        "msvd_ctx_synchronize": (i32, [vp]),
+        "msvd_matrix_attach": (i32, [vp, vp, i64, i64, i64, i64, i64, P(vp)]),
+        "msvd_matrix_detach": (i32, [vp]),
+        "msvd_apply": (i32, [vp, vp, i64, vp]),
+        "msvd_apply_adjoint": (i32, [vp, vp, i64, vp]),
+        "msvd_column_norms": (i32, [vp, vp]),
+        "msvd_build_sparsestack": (i32, [vp, i64, i64, i32, C.c_uint64, vp, vp]),
+        "msvd_sketch": (i32, [vp, i64, i32, C.c_uint64, vp]),
+        "msvd_precond_build": (i32, [vp, vp, i64, i64, vp, vp, P(d), P(i64)]),
+        "msvd_precond_apply": (i32, [vp, vp, vp, i64, vp, i64, vp]),
+        "msvd_tsqr_r": (i32, [vp, vp, i64, i64, vp]),
+        "msvd_small_svd": (i32, [vp, vp, i64, vp, vp]),
+        "msvd_lobpcg_solve": (i32, [vp, P(abi.Options), P(abi.Truth), P(abi.Result)]),
+        "msvd_rlobpcg_single": (i32, [vp, P(abi.Options), P(abi.Truth), P(abi.Result)]),
+        "msvd_rlobpcg_block": (i32, [vp, P(abi.Options), P(abi.Truth), P(abi.Result)]),
+        "msvd_solve_host": (i32, [vp, vp, i64, i64, i64, i64, i64, P(abi.Options), P(abi.Truth),
+                                  P(abi.Result)]),
+        "msvd_launch_count": (i64, [vp]),
+        "msvd_abi_sizes": (None, [P(i64), i32]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+EXPORTED = (
+    "msvd_abi_version msvd_last_error msvd_status_name msvd_options_default msvd_default_tolerance "
+    "msvd_validate_options msvd_shard_rows msvd_get_nccl_unique_id msvd_fake_group_create "
+    "msvd_fake_group_destroy msvd_ctx_create msvd_ctx_destroy msvd_ctx_synchronize msvd_matrix_attach "
+    "msvd_matrix_detach msvd_apply msvd_apply_adjoint msvd_column_norms msvd_build_sparsestack msvd_sketch "
+    "msvd_precond_build msvd_precond_apply msvd_tsqr_r msvd_small_svd msvd_lobpcg_solve msvd_rlobpcg_single "
+    "msvd_rlobpcg_block msvd_solve_host msvd_launch_count msvd_abi_sizes"
+).split()
+
+
+def lib():
+    """Load the CUDA extension; fails loudly if it is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run paper_2602_16797_b200.minsvd.build() "
+                              "(the solver has no CPU fallback)")
+        _lib = _declare(C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL))
+        if _lib.msvd_abi_version() != 1:
+            raise ImportError("libmsvd_cuda ABI version mismatch")
+    return _lib
+
+
+def check(rc):
+    if rc != 0:
+        msg = lib().msvd_last_error().decode(errors="replace")
+        raise _STATUS_EXC.get(rc, Error)(msg)
+
+
+def default_tolerance(n):
+    """solver.hpp:83-85"""
+    return 2.0 * np.sqrt(float(n)) * np.finfo(np.float64).eps
+
+
+# --------------------------------------------------------- solver.hpp types
+@dataclass
+class SolverOptions:
+    """solver.hpp:25-78, same fields and defaults."""
+
+    tol: float = -1.0
+    max_iter: int = -1
+    check_every: int = 5
+    stagnation_factor: float = 1.1
+    block_size: int = 1
+    seed: int = 0
+    sketch_dim: int = -1
+    zeta: int = 4
+    use_stagnation: bool = True
+    record_timing: bool = True
+    verify_cached_products: bool = False
+    store_iterates: bool = False
+
+    def to_abi(self, kind=abi.PRECOND_RANDOMIZED):
+        return abi.Options(tol=float(self.tol), max_iter=int(self.max_iter), check_every=int(self.check_every),
+                           stagnation_factor=float(self.stagnation_factor), block_size=int(self.block_size),
+                           seed=int(self.seed) & 0xFFFFFFFFFFFFFFFF, sketch_dim=int(self.sketch_dim),
+                           zeta=int(self.zeta), use_stagnation=int(bool(self.use_stagnation)),
+                           record_timing=int(bool(self.record_timing)),
+                           verify_cached_products=int(bool(self.verify_cached_products)),
+                           store_iterates=int(bool(self.store_iterates)), precond_kind=int(kind))
+
+
+class PrecondKind:
+    """solver.hpp:14"""
+
+    none = abi.PRECOND_NONE
+    diagonal = abi.PRECOND_DIAGONAL
+    randomized = abi.PRECOND_RANDOMIZED
+
+
+@dataclass
+class GroundTruth:
+    sigma_min: float
+    v_min: np.ndarray
+
+
+@dataclass
+class RecordRow:
+    iter: int
+    matvecs_a: int
+    matvecs_at: int
+    wall_ms: float
+    theta: float
+    resid: float
+    relerr: float = -1.0
+    sin_angle: float = -1.0
+
+
+def format_double(x):
+    """io.cpp:11-15 (%.17g)"""
+    return "%.17g" % x
+
+
+@dataclass
+class ConvergenceRecord:
+    rows: List[RecordRow] = field(default_factory=list)
+    has_truth: bool = False
+
+    def to_csv(self):
+        """solver.cpp:149-171"""
+        out = ["iter,matvecs_A,matvecs_At,wall_ms,theta,resid_norm,singval_relerr,sin_angle\n"]
+        for r in self.rows:
+            line = f"{r.iter},{r.matvecs_a},{r.matvecs_at},{format_double(r.wall_ms)},"
+            line += f"{format_double(r.theta)},{format_double(r.resid)},"
+            line += (f"{format_double(r.relerr)},{format_double(r.sin_angle)}" if self.has_truth else ",")
+            out.append(line + "\n")
+        return "".join(out)
+
+
+@dataclass
+class Preconditioner:
+    vtilde: Optional[np.ndarray]
+    sigma_tilde: Optional[np.ndarray]
+    sigma_max_estimate: float
+    floored: bool
+    floor_count: int
+
+
+@dataclass
+class SolveResult:
+    """solver.hpp:118-137"""
+
+    v: np.ndarray
+    sigma: np.ndarray
+    status: str
+    record: ConvergenceRecord
+    precond: Preconditioner
+    sigma_max_estimate: float
+    sketch_skipped: bool
+    sketch_dim: int
+    zeta: int
+    verify_count: int
+    max_cache_drift: float
+    degenerate_replacements: int
+    trail_t: list = field(default_factory=list)
+    trail_v: list = field(default_factory=list)
+    timings_ms: dict = field(default_factory=dict)
+
+    def iterations(self):
+        return len(self.record.rows) - 1
+
+
+# ----------------------------------------------------------------- context
+class Context:
+    """A CUDA device + stream + communicator (msvd_ctx)."""
+
+    def __init__(self, device=0, comm_kind=0, nranks=1, rank=0, nccl_id=None, fake_group=None, stream=None):
+        desc = abi.CtxDesc()
+        desc.device = device
+        desc.comm_kind = comm_kind
+        desc.nranks = nranks
+        desc.rank = rank
+        if nccl_id is not None:
+            for i, byte in enumerate(bytes(nccl_id)[:128]):
+                desc.nccl_id[i] = byte
+        desc.fake_group = fake_group
+        desc.stream = stream
+        h = C.c_void_p()
+        check(lib().msvd_ctx_create(C.byref(desc), C.byref(h)))
+        self.handle = h
+        self.device = device
+        self.nranks = nranks
+        self.rank = rank
+
+    def synchronize(self):
+        check(lib().msvd_ctx_synchronize(self.handle))
+
+    def launch_count(self):
+        return lib().msvd_launch_count(self.handle)
+
+    def close(self):
+        if self.handle:
+            lib().msvd_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx = {}
+
+
+def default_context(device=0):
+    if device not in _default_ctx:
+        _default_ctx[device] = Context(device)
+    return _default_ctx[device]
+
+
+def nccl_unique_id():
+    buf = (C.c_uint8 * 128)()
+    check(lib().msvd_get_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class FakeGroup:
+    """In-process group of `nranks` contexts on one GPU (test communicator)."""
+
+    def __init__(self, nranks):
+        h = C.c_void_p()
+        check(lib().msvd_fake_group_create(nranks, C.byref(h)))
+        self.handle = h
+        self.nranks = nranks
+
+    def context(self, rank, device=0):
+        return Context(device, comm_kind=2, nranks=self.nranks, rank=rank, fake_group=self.handle)
+
+    def close(self):
+        if self.handle:
+            lib().msvd_fake_group_destroy(self.handle)
+            self.handle = None
+
+
+def shard_rows(m, nranks, rank):
+    """Contiguous row block owned by `rank`."""
+    r0, rows = C.c_int64(), C.c_int64()
+    lib().msvd_shard_rows(m, nranks, rank, C.byref(r0), C.byref(rows))
+    return r0.value, rows.value
+
+
+# --------------------------------------------------------------- operator
+def _torch():
+    import torch
+
+    return torch
+
+
+class DeviceDenseOperator:
+    """operator.hpp:41-56 DenseOperator over device memory (row-major A).
+
+    `a` is a CUDA float64 torch tensor holding this rank's rows (m_local x n,
+    row stride `ld`); row0/m_global place them in the global matrix.
+    Products are deterministic for a fixed device and rank count.
+    """
+
+    def __init__(self, a, ctx: Optional[Context] = None, row0=0, m_global=None):
+        torch = _torch()
+        if not (isinstance(a, torch.Tensor) and a.is_cuda and a.dtype == torch.float64 and a.dim() == 2):
+            raise DimensionError("DeviceDenseOperator needs a 2-D float64 CUDA tensor")
+        if a.stride(1) != 1:
+            raise DimensionError("DeviceDenseOperator needs row-major storage (unit column stride)")
+        self.a = a
+        self.ctx = ctx or default_context(a.device.index or 0)
+        self.m_local, self.n = a.shape
+        self.ld = a.stride(0) if self.m_local > 1 else self.n
+        self.row0 = row0
+        self.m_global = self.m_local if m_global is None else m_global
+        h = C.c_void_p()
+        check(lib().msvd_matrix_attach(self.ctx.handle, C.c_void_p(a.data_ptr()), self.m_local, self.n,
+                                       max(self.ld, self.n), row0, self.m_global, C.byref(h)))
+        self.handle = h
+
+    def rows(self):
+        return self.m_global
+
+    def cols(self):
+        return self.n
+
+    def nnz(self):
+        return self.m_global * self.n
+
+    def _cm(self, x, rows):
+        """column-major (rows x b) device copy of x"""
+        torch = _torch()
+        x = torch.as_tensor(x, dtype=torch.float64, device=self.a.device)
+        if x.dim() == 1:
+            x = x.reshape(-1, 1)
+        if x.shape[0] != rows:
+            raise DimensionError("apply_block: dimension mismatch")
+        return x.t().contiguous(), x.shape[1]
+
+    def apply_block(self, x):
+        """operator.cpp:7-12: Y = A X (local rows)."""
+        torch = _torch()
+        xt, b = self._cm(x, self.n)
+        y = torch.empty((b, self.m_local), dtype=torch.float64, device=self.a.device)
+        check(lib().msvd_apply(self.handle, C.c_void_p(xt.data_ptr()), b, C.c_void_p(y.data_ptr())))
+        return y.t()
+
+    def apply_adjoint_block(self, y):
+        """operator.cpp:14-19: X = A^T Y (summed over ranks)."""
+        torch = _torch()
+        yt, b = self._cm(y, self.m_local)
+        x = torch.empty((b, self.n), dtype=torch.float64, device=self.a.device)
+        check(lib().msvd_apply_adjoint(self.handle, C.c_void_p(yt.data_ptr()), b, C.c_void_p(x.data_ptr())))
+        return x.t()
+
+    def apply(self, x):
+        return self.apply_block(x)[:, 0]
+
+    def apply_adjoint(self, y):
+        return self.apply_adjoint_block(y)[:, 0]
+
+    def column_norms(self):
+        torch = _torch()
+        out = torch.empty(self.n, dtype=torch.float64, device=self.a.device)
+        check(lib().msvd_column_norms(self.handle, C.c_void_p(out.data_ptr())))
+        return out
+
+    def to_dense(self):
+        return self.a[:, : self.n]
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().msvd_matrix_detach(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ solve
+class _ResultBuffers:
+    def __init__(self, n, b, max_iter, want_precond, store):
+        cap = max_iter + 2
+        self.sigma = np.zeros(b)
+        self.v = np.zeros((b, n))  # row j = column j (column-major n x b)
+        self.rows = (abi.RecordRow * cap)()
+        self.res = abi.Result()
+        self.res.sigma = self.sigma.ctypes.data_as(C.POINTER(C.c_double))
+        self.res.v = self.v.ctypes.data_as(C.POINTER(C.c_double))
+        self.res.rows = self.rows
+        self.res.rows_capacity = cap
+        self.vt = self.sg = None
+        if want_precond:
+            self.vt = np.zeros((n, n))  # [j, i] = V(i, j) (column-major)
+            self.sg = np.zeros(n)
+            self.res.vtilde = self.vt.ctypes.data_as(C.POINTER(C.c_double))
+            self.res.sigma_tilde = self.sg.ctypes.data_as(C.POINTER(C.c_double))
+        self.trail = {"t": [], "v": []}
+
+        def sink(_u, kind, it, data, r, c):
+            arr = np.ctypeslib.as_array(data, shape=(int(c), int(r))).T.copy()
+            self.trail["t" if kind == 0 else "v"].append(arr)
+
+        self._cb = abi.ITERATE_FN(sink) if store else abi.ITERATE_FN()
+        self.res.iterate_cb = self._cb
+
+    def result(self, has_truth):
+        r = self.res
+        rows = [RecordRow(x.iter, x.matvecs_a, x.matvecs_at, x.wall_ms, x.theta, x.resid, x.relerr, x.sin_angle)
+                for x in self.rows[: min(r.rows_count, r.rows_capacity)]]
+        pre = Preconditioner(self.vt.T.copy() if self.vt is not None else None,
+                             self.sg.copy() if self.sg is not None else None, r.sigma_max_estimate,
+                             bool(r.floored), r.floor_count)
+        return SolveResult(v=self.v.T.copy(), sigma=self.sigma.copy(),
+                           status="converged" if r.status == 0 else "max_iter_reached",
+                           record=ConvergenceRecord(rows, has_truth), precond=pre,
+                           sigma_max_estimate=r.sigma_max_estimate, sketch_skipped=bool(r.sketch_skipped),
+                           sketch_dim=r.sketch_dim, zeta=r.zeta, verify_count=r.verify_count,
+                           max_cache_drift=r.max_cache_drift, degenerate_replacements=r.degenerate_replacements,
+                           trail_t=self.trail["t"], trail_v=self.trail["v"],
+                           timings_ms=dict(sketch=r.t_sketch_ms, svd=r.t_svd_ms, init=r.t_init_ms,
+                                           loop=r.t_loop_ms, total=r.t_total_ms))
+
+
+def _truth(truth, n):
+    if truth is None:
+        return None, None
+    v = np.ascontiguousarray(truth.v_min, dtype=np.float64)
+    if v.size != n:
+        raise DimensionError("solver: ground-truth vector length mismatch")
+    t = abi.Truth(float(truth.sigma_min), v.ctypes.data_as(C.POINTER(C.c_double)))
+    return t, v
+
+
+def _run(fn, a, kind, opts, truth, want_precond):
+    if not isinstance(a, DeviceDenseOperator):
+        raise DimensionError("msvd: the GPU solver accepts a DeviceDenseOperator only (no CPU fallback)")
+    opts = opts or SolverOptions()
+    o = opts.to_abi(kind)
+    if fn == "msvd_rlobpcg_single":
+        o.block_size = 1
+    b = max(int(o.block_size), 1)
+    max_iter = o.max_iter if o.max_iter >= 0 else (200 if b == 1 else 100)
+    t, keep = _truth(truth, a.n)
+    bufs = _ResultBuffers(a.n, b, max(max_iter, 0), want_precond, bool(o.store_iterates))
+    check(getattr(lib(), fn)(a.handle, C.byref(o), C.byref(t) if t is not None else None, C.byref(bufs.res)))
+    del keep
+    return bufs.result(truth is not None)
+
+
+def lobpcg_solve(a, kind=PrecondKind.randomized, opts=None, truth=None, want_precond=False):
+    """solver.hpp:172-173"""
+    return _run("msvd_lobpcg_solve", a, kind, opts, truth, want_precond)
+
+
+def rlobpcg_single(a, opts=None, truth=None, want_precond=False):
+    """solver.hpp:176-177 (block size forced to 1)"""
+    return _run("msvd_rlobpcg_single", a, abi.PRECOND_RANDOMIZED, opts, truth, want_precond)
+
+
+def rlobpcg_block(a, opts=None, truth=None, want_precond=False):
+    """solver.hpp:180-181"""
+    return _run("msvd_rlobpcg_block", a, abi.PRECOND_RANDOMIZED, opts, truth, want_precond)
+
+
+def solve_host(a_host, opts=None, truth=None, ctx=None, row0=0, m_global=None, kind=abi.PRECOND_RANDOMIZED,
+               want_precond=False):
+    """End-to-end entry (msvd_solve_host): A in host memory (row-major numpy,
+    ideally pinned), copied to the device inside the call."""
+    a_host = np.asarray(a_host)
+    if a_host.dtype != np.float64 or a_host.ndim != 2 or a_host.strides[1] != 8:
+        raise DimensionError("solve_host needs a row-major float64 2-D array")
+    ctx = ctx or default_context(0)
+    m, n = a_host.shape
+    ld = a_host.strides[0] // 8 if m > 1 else n
+    opts = opts or SolverOptions()
+    o = opts.to_abi(kind)
+    b = max(int(o.block_size), 1)
+    max_iter = o.max_iter if o.max_iter >= 0 else (200 if b == 1 else 100)
+    t, keep = _truth(truth, n)
+    bufs = _ResultBuffers(n, b, max(max_iter, 0), want_precond, bool(o.store_iterates))
+    check(lib().msvd_solve_host(ctx.handle, C.c_void_p(a_host.ctypes.data), m, n, ld, row0,
+                                m if m_global is None else m_global, C.byref(o),
+                                C.byref(t) if t is not None else None, C.byref(bufs.res)))
+    del keep
+    return bufs.result(truth is not None)
+
+
+def validate_options(m, n, opts: SolverOptions, kind=abi.PRECOND_RANDOMIZED):
+    """Host-only check of the reference's option/shape validation order."""
+    o = opts.to_abi(kind)
+    check(lib().msvd_validate_options(m, n, C.byref(o), None))

@@ -1,0 +1,135 @@
+"""The five BASELINE.json configurations and an on-device input generator.
+
+A = U diag(sigma) V^T in fp64, row-major on the device.  U is the sign-fixed
+(R_jj > 0) Householder Q of an m x n i.i.d. N(0,1) matrix and V the same for
+n x n, as in matgen.cpp:126-139 / :141-176; the Gaussians come from torch's
+seeded CUDA generator and the QR from cuSOLVER (via torch), so generation
+takes seconds instead of the hours a CPU Householder would need at m = 1e6.
+The parity tests hand the SAME bytes to the CPU oracle ("one
+buffer for both solvers").  Generation is harness, not the measured path.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+DATA_SEED = 20260216   # S in SURVEY 8d
+SOLVER_SEED = 7        # SolverOptions::seed for every config
+
+
+def geometric(first, last, count):
+    """matgen.cpp:30-39 geometric_fill: first..last inclusive, geometric."""
+    if count == 1:
+        return np.array([first], dtype=np.float64)
+    i = np.arange(count, dtype=np.float64)
+    return first * np.power(last / first, i / float(count - 1))
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    m: int
+    n: int
+    b: int
+    d_factor: int      # d = d_factor * n
+    tol: float
+    note: str = ""
+
+    @property
+    def d(self):
+        return self.d_factor * self.n
+
+    def spectrum(self, n=None):
+        return spectrum(self.name, self.n if n is None else n)
+
+    def scaled(self, m=None, n=None):
+        """Same recipe at a smaller shape (parity-test sizes)."""
+        return Config(self.name, m or self.m, n or self.n, self.b, self.d_factor, self.tol, self.note)
+
+
+CONFIGS = {
+    "c1": Config("c1", 10_000, 100, 1, 2, 1e-12, "CPU-oracle size"),
+    "c2": Config("c2", 1_000_000, 1_000, 1, 4, 1e-12, "headline"),
+    "c3": Config("c3", 1_000_000, 2_000, 5, 2, 1e-12, "5-dim exact nullspace"),
+    "c4": Config("c4", 500_000, 500, 4, 4, 1e-10, "small gap, ill-conditioned"),
+    "c5": Config("c5", 8_000_000, 1_000, 2, 4, 1e-12, "multi-GPU scaling; tol unspecified -> 1e-12"),
+}
+
+
+def spectrum(name, n):
+    """Descending singular values per BASELINE.json configs[0..4]."""
+    if name == "c1":
+        return np.concatenate([geometric(1.0, 1e-6, n - 1), [1e-8]])
+    if name == "c2":
+        return np.concatenate([geometric(1.0, 1e-4, n - 1), [1e-6]])
+    if name == "c3":
+        return np.concatenate([geometric(1.0, 1e-3, n - 5), np.zeros(5)])
+    if name == "c4":
+        return np.concatenate([geometric(1.0, 1e-3, n - 4), [1.3e-4, 1.2e-4, 1.1e-4, 1.0e-4]])
+    if name == "c5":
+        return np.concatenate([geometric(1.0, 1e-5, n - 1), [1e-7]])
+    raise KeyError(name)
+
+
+def _haar_gpu(torch, rows, cols, gen, device, block_rows=None):
+    """Sign-fixed Q of a seeded Gaussian rows x cols, on the device.  Tall
+    inputs larger than `block_rows` are orthonormalised as a two-level TSQR
+    (local QR per block, QR of the stacked R factors), so peak memory stays
+    near one copy of Q."""
+    if block_rows is None or rows <= block_rows:
+        g = torch.randn(rows, cols, dtype=torch.float64, device=device, generator=gen)
+        q, r = torch.linalg.qr(g)
+        del g
+        s = torch.sign(torch.diagonal(r))
+        s[s == 0] = 1.0
+        q *= s
+        return q
+    nb = (rows + block_rows - 1) // block_rows
+    q = torch.empty(rows, cols, dtype=torch.float64, device=device)
+    rs = []
+    for i in range(nb):
+        r0, r1 = i * block_rows, min(rows, (i + 1) * block_rows)
+        g = torch.randn(r1 - r0, cols, dtype=torch.float64, device=device, generator=gen)
+        qi, ri = torch.linalg.qr(g)
+        q[r0:r1] = qi
+        rs.append(ri)
+        del g, qi
+    q2, r2 = torch.linalg.qr(torch.cat(rs, 0))
+    s = torch.sign(torch.diagonal(r2))
+    s[s == 0] = 1.0
+    q2 *= s
+    for i in range(nb):
+        r0, r1 = i * block_rows, min(rows, (i + 1) * block_rows)
+        q[r0:r1] = q[r0:r1] @ q2[i * cols:(i + 1) * cols]
+    return q
+
+
+def make_problem_gpu(m, n, sigma, seed=DATA_SEED, device="cuda:0", block_rows=2_000_000, ld=None):
+    """Row-major A (m x n, leading dimension ld >= n) on the device plus the
+    true v_min (numpy).  A = U diag(sigma) V^T is formed block by block in
+    U's own storage."""
+    import torch
+
+    gen = torch.Generator(device=device)
+    gen.manual_seed(int(seed))
+    v = _haar_gpu(torch, n, n, gen, device)
+    u = _haar_gpu(torch, m, n, gen, device, block_rows=block_rows)
+    sig = torch.as_tensor(np.asarray(sigma, dtype=np.float64), device=device)
+    vt_scaled = sig[:, None] * v.t()  # diag(sigma) V^T
+    step = max(1, min(m, 1 << 18))
+    ldv = n if ld is None else ld
+    if ldv != n:
+        a = torch.zeros(m, ldv, dtype=torch.float64, device=device)
+        for r0 in range(0, m, step):
+            r1 = min(m, r0 + step)
+            a[r0:r1, :n] = u[r0:r1] @ vt_scaled
+        del u
+        out = a[:, :n]
+    else:
+        for r0 in range(0, m, step):
+            r1 = min(m, r0 + step)
+            u[r0:r1] = u[r0:r1] @ vt_scaled
+        out = u
+    vmin = v[:, n - 1].cpu().numpy().copy()
+    return out, vmin

@@ -1,0 +1,405 @@
+"""End-to-end parity of the device RLOBPCG solve against the CPU oracle.
+
+Gates (BASELINE.json north_star): |sigma_gpu - sigma_ref| <=
+1e-10 sigma_max, subspace angle <= 1e-8, iteration count within +-1, in
+tolerance-only mode.  Property tests port the reference's solver tests
+(test_solver.cpp:147-477) to the device operator.
+"""
+import numpy as np
+import pytest
+
+from paper_2602_16797_b200 import problems
+
+pytestmark = pytest.mark.gpu
+
+SIGMA_TOL = 1e-10
+ANGLE_TOL = 1e-8
+
+
+def subspace_sin(v_ref, v_got):
+    """||V_ref - V_got (V_got^T V_ref)||_2 (not sqrt(1 - c^2))."""
+    v_ref = np.asarray(v_ref).reshape(v_ref.shape[0], -1)
+    v_got = np.asarray(v_got).reshape(v_got.shape[0], -1)
+    return np.linalg.norm(v_ref - v_got @ (v_got.T @ v_ref), 2)
+
+
+def to_device(a_colmajor, cuda):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(a_colmajor)).to(cuda)
+
+
+def gpu_solve(msvd, a_dev, opts, truth=None, single=False):
+    op = msvd.DeviceDenseOperator(a_dev)
+    fn = msvd.rlobpcg_single if single else msvd.rlobpcg_block
+    return fn(op, opts, truth)
+
+
+def assert_parity(res, ref, b, gate_vectors=None, iters_exact=False):
+    smax = ref["sigma_max_estimate"]
+    assert abs(res.sigma_max_estimate - smax) <= 1e-12 * smax
+    assert np.all(np.abs(res.sigma - ref["sigma"]) <= SIGMA_TOL * smax), (res.sigma, ref["sigma"])
+    gate = range(b) if gate_vectors is None else gate_vectors
+    for j in gate:
+        assert subspace_sin(ref["v"][:, j], res.v[:, j]) <= ANGLE_TOL, j
+    if iters_exact:
+        assert res.iterations() == ref["iterations"]
+    else:
+        assert abs(res.iterations() - ref["iterations"]) <= 1
+    assert res.status == ref["status"]
+
+
+def c1_problem(port):
+    cfg = problems.CONFIGS["c1"]
+    sig = cfg.spectrum()
+    a, vmin = port.synth_dense(sig, cfg.m, problems.DATA_SEED)
+    return cfg, sig, a, vmin
+
+
+# ------------------------------------------------------------- C1 (full)
+def test_c1_full_parity(msvd, cuda, port):
+    cfg, sig, a, vmin = c1_problem(port)
+    opts = msvd.SolverOptions(seed=problems.SOLVER_SEED, sketch_dim=cfg.d, tol=cfg.tol, use_stagnation=False,
+                              record_timing=False)
+    truth = msvd.GroundTruth(sig[-1], vmin)
+    res = gpu_solve(msvd, to_device(a, cuda), opts, truth, single=True)
+    ref = port.lobpcg_solve(a, opts.to_abi(), truth=(sig[-1], vmin))
+    assert ref["iterations"] == 21
+    assert_parity(res, ref, 1, iters_exact=True)
+    # record rows line up: same products, theta and residual to roundoff
+    assert len(res.record.rows) == len(ref["record"])
+    for g, r in zip(res.record.rows, ref["record"]):
+        assert (g.iter, g.matvecs_a, g.matvecs_at) == (r["iter"], r["matvecs_a"], r["matvecs_at"])
+        assert abs(g.theta - r["theta"]) <= 1e-12 * ref["sigma_max_estimate"]
+        assert abs(g.resid - r["resid"]) <= 1e-3 * r["resid"] + 1e-15
+    assert res.record.rows[-1].relerr <= 1e-6
+    assert res.sketch_dim == 200 and res.zeta == 4 and not res.sketch_skipped
+
+
+def test_c1_stagnation_mode(msvd, cuda, port):
+    """Default stopping rule: roundoff-floor stop, compared within one check period."""
+    cfg, sig, a, vmin = c1_problem(port)
+    opts = msvd.SolverOptions(seed=problems.SOLVER_SEED, sketch_dim=cfg.d, tol=cfg.tol, record_timing=False)
+    res = gpu_solve(msvd, to_device(a, cuda), opts, single=True)
+    ref = port.lobpcg_solve(a, opts.to_abi())
+    smax = ref["sigma_max_estimate"]
+    assert abs(res.sigma[0] - ref["sigma"][0]) <= SIGMA_TOL * smax
+    assert subspace_sin(ref["v"], res.v) <= ANGLE_TOL
+    assert abs(res.iterations() - ref["iterations"]) <= 2 * opts.check_every
+
+
+# -------------------------------------------- config-shaped runs (reduced m)
+SHAPES = {
+    "c2": dict(m=100_000, n=500),
+    "c3": dict(m=40_000, n=400),
+    "c4": dict(m=50_000, n=500),
+    "c5": dict(m=40_000, n=500),
+}
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_config_shape_parity(msvd, cuda, port, name):
+    import torch
+
+    cfg = problems.CONFIGS[name].scaled(**SHAPES[name])
+    sig = cfg.spectrum()
+    a_dev, vmin = problems.make_problem_gpu(cfg.m, cfg.n, sig, device=cuda)
+    opts = msvd.SolverOptions(seed=problems.SOLVER_SEED, sketch_dim=cfg.d, tol=cfg.tol, block_size=cfg.b,
+                              use_stagnation=False, record_timing=False)
+    res = gpu_solve(msvd, a_dev, opts)
+    a_host = a_dev.cpu().numpy()  # the SAME bytes go to the oracle
+    ref = port.lobpcg_solve(a_host, opts.to_abi())
+    smax = ref["sigma_max_estimate"]
+    if name == "c3":
+        # 5-dim exact nullspace: gate on the returned sigmas and the 5-D subspace
+        assert np.all(np.abs(res.sigma - ref["sigma"]) <= SIGMA_TOL * smax)
+        assert subspace_sin(ref["v"], res.v) <= ANGLE_TOL
+        assert abs(res.iterations() - ref["iterations"]) <= 1
+    elif name == "c5":
+        # v_{n-1} is roundoff-chaotic in the reference itself:
+        # gate sigma_n, sigma_{n-1} and v_min only
+        assert_parity(res, ref, 2, gate_vectors=[0])
+    else:
+        assert_parity(res, ref, cfg.b)
+    del torch
+
+
+# ------------------------------------- reference solver tests on the device
+def test_tiny_diagonal_instance(msvd, cuda):
+    """test_solver.cpp:147-165"""
+    import torch
+
+    a = torch.zeros((50, 5), dtype=torch.float64, device=cuda)
+    for j in range(5):
+        a[j, j] = 5.0 - j
+    vmin = np.zeros(5)
+    vmin[4] = 1.0
+    res = gpu_solve(msvd, a, msvd.SolverOptions(seed=7), msvd.GroundTruth(1.0, vmin), single=True)
+    assert res.status == "converged"
+    assert abs(res.sigma[0] - 1.0) <= 1e-12
+    assert res.record.rows[-1].sin_angle <= 1e-8
+    assert res.record.rows[-1].relerr <= 1e-12
+    assert res.record.has_truth and not res.sketch_skipped and res.sketch_dim == 20
+
+
+def test_block_ascending(msvd, cuda):
+    """test_solver.cpp:167-187"""
+    import torch
+
+    a = torch.zeros((50, 6), dtype=torch.float64, device=cuda)
+    for j in range(6):
+        a[j, j] = 6.0 - j
+    res = gpu_solve(msvd, a, msvd.SolverOptions(block_size=2, seed=11))
+    assert res.status == "converged"
+    assert res.sigma[0] < res.sigma[1]
+    assert abs(res.sigma[0] - 1.0) <= 1e-10 and abs(res.sigma[1] - 2.0) <= 1e-10
+    assert np.sqrt(1 - min(1, res.v[5, 0] ** 2)) <= 1e-8
+    assert np.sqrt(1 - min(1, res.v[4, 1] ** 2)) <= 1e-8
+
+
+def _instance(port, m, n, sigma, seed):
+    a, vmin = port.assemble_svd(np.asarray(sigma, dtype=np.float64), m, seed)
+    return a, vmin
+
+
+def geometric_spectrum(n, last):
+    return np.power(last, np.arange(n) / (n - 1))
+
+
+def test_block_size_one_matches_single(msvd, cuda, port):
+    """test_solver.cpp:189-204: bit-identical record and vectors."""
+    a, vmin = _instance(port, 300, 30, geometric_spectrum(30, 1e-6), 21)
+    dev = to_device(a, cuda)
+    truth = msvd.GroundTruth(1e-6, vmin)
+    o = msvd.SolverOptions(seed=5, record_timing=False, max_iter=40)
+    single = gpu_solve(msvd, dev, o, truth, single=True)
+    block = gpu_solve(msvd, dev, msvd.SolverOptions(seed=5, record_timing=False, max_iter=40, block_size=1), truth)
+    assert single.record.to_csv() == block.record.to_csv()
+    assert single.sigma[0] == block.sigma[0]
+    assert np.array_equal(single.v, block.v)
+
+
+def test_easy_spectrum_accuracy_and_counts(msvd, cuda, port):
+    """test_solver.cpp:206-235"""
+    n, m = 100, 2000
+    spec = np.concatenate([np.power(10.0, -np.arange(n - 1) / (n - 2)), [1e-7]])
+    a, vmin = _instance(port, m, n, spec, 3)
+    dev = to_device(a, cuda)
+    truth = msvd.GroundTruth(spec[-1], vmin)
+    res = gpu_solve(msvd, dev, msvd.SolverOptions(seed=12), truth, single=True)
+    assert res.status == "converged" and res.iterations() <= 200
+    assert res.record.rows[-1].relerr <= 100 * 2.220446049250313e-16 * 1e7
+    eps = 2.220446049250313e-16
+    for j in range(1, len(res.record.rows)):
+        assert res.record.rows[j].theta <= res.record.rows[j - 1].theta + 4 * eps * res.sigma_max_estimate
+    for row in res.record.rows:
+        assert row.matvecs_a == 1 + row.iter and row.matvecs_at == 1 + row.iter
+
+
+def test_exact_counts_and_cache_verification(msvd, cuda, port):
+    """test_solver.cpp:237-265"""
+    a, _ = _instance(port, 120, 12, geometric_spectrum(12, 1e-5), 77)
+    dev = to_device(a, cuda)
+    o = msvd.SolverOptions(seed=3, max_iter=37, tol=0.0, record_timing=False)
+    plain = gpu_solve(msvd, dev, o, single=True)
+    assert plain.status == "max_iter_reached" and plain.iterations() == 37
+    assert plain.record.rows[-1].matvecs_a == 38 and plain.record.rows[-1].matvecs_at == 38
+    vo = msvd.SolverOptions(seed=3, max_iter=37, tol=0.0, record_timing=False, verify_cached_products=True)
+    ver = gpu_solve(msvd, dev, vo, single=True)
+    assert ver.verify_count == 1
+    assert ver.max_cache_drift <= 1e-10 * ver.sigma_max_estimate
+    assert ver.record.to_csv() == plain.record.to_csv()
+
+
+def test_trial_basis_orthonormal_and_optimal(msvd, cuda, port):
+    """test_solver.cpp:267-297"""
+    a, _ = _instance(port, 150, 15, geometric_spectrum(15, 1e-4), 9)
+    dev = to_device(a, cuda)
+    res = gpu_solve(msvd, dev, msvd.SolverOptions(seed=4, max_iter=30, tol=0.0, store_iterates=True), single=True)
+    assert len(res.trail_t) == 30
+    rng = np.random.default_rng(1234)
+    eps = 2.220446049250313e-16
+    for k, t in enumerate(res.trail_t):
+        assert np.abs(t.T @ t - np.eye(t.shape[1])).max() <= 1e-12
+        theta_next = res.record.rows[k + 1].theta
+        for _ in range(10):
+            y = t @ rng.standard_normal(t.shape[1])
+            y /= np.linalg.norm(y)
+            q = np.linalg.norm(a @ y)
+            assert theta_next <= q * (1 + 1e-10) + 4 * eps * res.sigma_max_estimate
+
+
+def test_sketch_skipped_exact_preconditioner(msvd, cuda, port):
+    """test_solver.cpp:343-357 (m <= 4n: direct SVD of A)"""
+    spec = geometric_spectrum(40, 1e-4)
+    a, vmin = _instance(port, 80, 40, spec, 13)
+    res = gpu_solve(msvd, to_device(a, cuda), msvd.SolverOptions(seed=2), msvd.GroundTruth(spec[-1], vmin),
+                    single=True)
+    assert res.sketch_skipped and res.sketch_dim == 0 and res.zeta == 0
+    assert res.status == "converged" and res.iterations() <= 30
+    assert res.record.rows[-1].relerr <= 1e-8 and res.record.rows[-1].sin_angle <= 1e-6
+
+
+def test_tolerance_only_stops_early(msvd, cuda, port):
+    """test_solver.cpp:359-368"""
+    a, _ = _instance(port, 80, 40, geometric_spectrum(40, 1e-4), 13)
+    res = gpu_solve(msvd, to_device(a, cuda), msvd.SolverOptions(seed=2, use_stagnation=False, tol=1e-8),
+                    single=True)
+    assert res.status == "converged" and res.iterations() <= 6
+
+
+def test_equal_singular_values_deterministic(msvd, cuda, port):
+    """test_solver.cpp:370-389: zero-residual branch replaces directions deterministically."""
+    q = port.haar_orthonormal(60, 12, 55)
+    dev = to_device(3.0 * q, cuda)
+    o = msvd.SolverOptions(seed=19, max_iter=15, tol=1e-12, record_timing=False)
+    r1 = gpu_solve(msvd, dev, o, single=True)
+    r2 = gpu_solve(msvd, dev, o, single=True)
+    assert r1.status == "converged"
+    assert abs(r1.sigma[0] - 3.0) <= 3e-12
+    assert r1.record.to_csv() == r2.record.to_csv()
+    assert np.array_equal(r1.v, r2.v)
+
+
+def test_record_format(msvd, cuda):
+    """test_solver.cpp:391-418"""
+    import torch
+
+    a = torch.zeros((30, 4), dtype=torch.float64, device=cuda)
+    for j in range(4):
+        a[j, j] = 4.0 - j
+    o = msvd.SolverOptions(seed=1, max_iter=3, tol=0.0, record_timing=False)
+    res = gpu_solve(msvd, a, o, single=True)
+    csv = res.record.to_csv()
+    assert csv.startswith("iter,matvecs_A,matvecs_At,wall_ms,theta,resid_norm,singval_relerr,sin_angle\n")
+    assert csv.count("\n") == 5 and ",,\n" in csv
+    assert csv.splitlines()[1].split(",")[3] == "0"
+    wt = gpu_solve(msvd, a, o, msvd.GroundTruth(1.0, np.array([0.0, 0.0, 0.0, 1.0])), single=True)
+    assert ",,\n" not in wt.record.to_csv()
+
+
+def test_max_iter_zero(msvd, cuda, port):
+    """test_solver.cpp:420-430"""
+    a, _ = _instance(port, 90, 9, geometric_spectrum(9, 1e-3), 41)
+    res = gpu_solve(msvd, to_device(a, cuda), msvd.SolverOptions(seed=6, max_iter=0), single=True)
+    assert res.status == "max_iter_reached" and len(res.record.rows) == 1
+    assert res.sigma[0] == res.record.rows[0].theta
+    assert abs(np.linalg.norm(res.v[:, 0]) - 1.0) <= 1e-13
+
+
+def test_sketch_rows_may_exceed_m(msvd, cuda, port):
+    """test_solver.cpp:432-444"""
+    spec = geometric_spectrum(20, 1e-2)
+    spec[19] = 1e-5
+    a, vmin = _instance(port, 60, 20, spec, 23)
+    res = gpu_solve(msvd, to_device(a, cuda), msvd.SolverOptions(seed=14, sketch_dim=128),
+                    msvd.GroundTruth(1e-5, vmin), single=True)
+    assert not res.sketch_skipped and res.sketch_dim == 128
+    assert res.record.rows[-1].relerr <= 1e-6
+
+
+def test_validation_errors(msvd, cuda, port):
+    """test_solver.cpp:446-477"""
+    import torch
+
+    wide = torch.zeros((3, 5), dtype=torch.float64, device=cuda)
+    with pytest.raises(msvd.DimensionError):
+        gpu_solve(msvd, wide, msvd.SolverOptions(), single=True)
+    a, _ = _instance(port, 40, 8, geometric_spectrum(8, 1e-2), 17)
+    dev = to_device(a, cuda)
+    with pytest.raises(msvd.DimensionError):
+        gpu_solve(msvd, dev, msvd.SolverOptions(block_size=3))
+    with pytest.raises(msvd.NumericalError):
+        gpu_solve(msvd, dev, msvd.SolverOptions(tol=1.5), single=True)
+    with pytest.raises(msvd.NumericalError):
+        gpu_solve(msvd, dev, msvd.SolverOptions(check_every=0), single=True)
+    with pytest.raises(msvd.DimensionError):
+        gpu_solve(msvd, dev, msvd.SolverOptions(sketch_dim=30), single=True)
+    with pytest.raises(msvd.DimensionError):
+        gpu_solve(msvd, dev, msvd.SolverOptions(sketch_dim=4), single=True)
+    with pytest.raises(msvd.DimensionError):
+        gpu_solve(msvd, dev, msvd.SolverOptions(), msvd.GroundTruth(1.0, np.zeros(3)), single=True)
+    bad = dev.clone()
+    bad[3, 2] = float("inf")
+    with pytest.raises(msvd.NumericalError):
+        gpu_solve(msvd, bad, msvd.SolverOptions(), single=True)
+
+
+def test_precond_kinds_none_and_diagonal(msvd, cuda, port):
+    """lobpcg_solve's other kinds (solver.cpp:58-70, 336-340) against the oracle."""
+    spec = geometric_spectrum(30, 1e-3)
+    a, _ = _instance(port, 600, 30, spec, 5)
+    dev = to_device(a, cuda)
+    for kind in (msvd.PrecondKind.none, msvd.PrecondKind.diagonal):
+        o = msvd.SolverOptions(seed=3, max_iter=60, tol=1e-10, use_stagnation=False, record_timing=False)
+        res = msvd.lobpcg_solve(msvd.DeviceDenseOperator(dev), kind, o)
+        ref = port.lobpcg_solve(a, o.to_abi(kind))
+        assert abs(res.iterations() - ref["iterations"]) <= 1
+        assert abs(res.sigma[0] - ref["sigma"][0]) <= SIGMA_TOL * ref["sigma_max_estimate"]
+
+
+def test_solve_host_end_to_end(msvd, cuda, port):
+    """msvd_solve_host: host buffer in, same answer as the device-resident path."""
+    cfg, sig, a, vmin = c1_problem(port)
+    opts = msvd.SolverOptions(seed=7, sketch_dim=cfg.d, tol=cfg.tol, use_stagnation=False, record_timing=False)
+    host = np.ascontiguousarray(a)
+    r1 = msvd.solve_host(host, opts)
+    r2 = gpu_solve(msvd, to_device(a, cuda), opts)
+    assert r1.record.to_csv() == r2.record.to_csv()
+    assert np.array_equal(r1.v, r2.v)
+
+
+def test_fake_group_two_ranks(msvd, cuda, port):
+    """Row-sharded solve over the in-process communicator (2 ranks, 1 GPU):
+    same answer as one rank within the parity gates."""
+    import threading
+
+    import torch
+
+    cfg, sig, a, vmin = c1_problem(port)
+    opts = msvd.SolverOptions(seed=7, sketch_dim=cfg.d, tol=cfg.tol, use_stagnation=False, record_timing=False)
+    dev = to_device(a, cuda)
+    one = gpu_solve(msvd, dev, opts)
+    for nr in (2, 3):
+        grp = msvd.FakeGroup(nr)
+        out = [None] * nr
+        errs = []
+
+        def run(r):
+            try:
+                torch.cuda.set_device(0)
+                ctx = grp.context(r)
+                r0, rows = msvd.shard_rows(cfg.m, nr, r)
+                op = msvd.DeviceDenseOperator(dev[r0:r0 + rows], ctx=ctx, row0=r0, m_global=cfg.m)
+                out[r] = msvd.rlobpcg_block(op, opts)
+            except Exception as e:  # pragma: no cover - reported below
+                errs.append(e)
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(nr)]
+        [t.start() for t in th]
+        [t.join() for t in th]
+        assert not errs, errs
+        for r in range(nr):
+            assert out[r].record.to_csv() == out[0].record.to_csv()
+            assert abs(out[r].iterations() - one.iterations()) <= 1
+            assert abs(out[r].sigma[0] - one.sigma[0]) <= SIGMA_TOL * one.sigma_max_estimate
+            assert subspace_sin(one.v, out[r].v) <= ANGLE_TOL
+        grp.close()
+
+
+@pytest.mark.slow
+def test_c2_full_size(msvd, cuda):
+    """Headline config at full size (8 GB): converges in the oracle's 21
+    iterations to the documented accuracy."""
+    import torch
+
+    cfg = problems.CONFIGS["c2"]
+    sig = cfg.spectrum()
+    a_dev, vmin = problems.make_problem_gpu(cfg.m, cfg.n, sig, device=cuda)
+    opts = msvd.SolverOptions(seed=7, sketch_dim=cfg.d, tol=cfg.tol, use_stagnation=False)
+    res = gpu_solve(msvd, a_dev, opts, msvd.GroundTruth(sig[-1], vmin), single=True)
+    assert res.status == "converged"
+    assert abs(res.iterations() - 21) <= 1
+    assert res.record.rows[-1].relerr <= 1e-8
+    del a_dev
+    torch.cuda.empty_cache()
