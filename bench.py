@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 RLOBPCG hot path (BASELINE.json metric, config C2).
+
+Metric: time-to-solution (s) of rlobpcg_single on the headline configuration
+(m = 1e6, n = 1e3 fp64, b = 1, d = 4n, tol 1e-12, tolerance-only stop, solver
+seed 7) with A resident in HBM; one step = one complete solve (sketch, sketch
+SVD, init, all LOBPCG iterations).  Also reported: the A-stream GB/s per
+iteration, the roofline of the dominant kernel (the K2 Gram pass) measured
+live with CUDA events on the library's stream, and an end-to-end number
+through the public host-buffer entry point (msvd_solve_host, pinned A copied
+in every step).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun ... bench.py --gpus N   (row-sharded over NCCL, one rank per GPU)
+
+`--impl reference` times the reference's own CPU solver (oracle/_ref, built
+from the reference's sources; else the oracle port) on a bounded sample of
+the same workload and extrapolates to the full size (see `cpu_baseline`).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-to-solution (s) & A-stream HBM GB/s per iteration, m=1e6 n=1e3 fp64"
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2")
+    p.add_argument("--m", type=int, default=0, help="override rows (debug only; invalidates the metric)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[5 + i]
+                          and "Not" not in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def reference_arm(args, cfg):
+    """Reference CPU solver on a bounded sample, extrapolated to the config."""
+    import torch
+
+    from oracle import pyoracle
+    from paper_2602_16797_b200 import abi, problems
+
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    kind = "reference" if pyoracle.available("ref") else "port"
+    orc = pyoracle.load("ref" if kind == "reference" else "port")
+    m_s = 20_000
+    sig = cfg.spectrum()
+    if torch.cuda.is_available():
+        a_dev, _ = problems.make_problem_gpu(m_s, cfg.n, sig)
+        a = a_dev.cpu().numpy()
+        del a_dev
+    else:
+        a, _ = pyoracle.load("port").synth_dense(sig, m_s, problems.DATA_SEED)
+        a = np.ascontiguousarray(a)
+    opts = abi.default_options(seed=problems.SOLVER_SEED, sketch_dim=cfg.d, tol=cfg.tol,
+                               block_size=cfg.b, use_stagnation=0)
+    # per-pass cost at the sample size, to split the m-scaling part
+    acm = np.asfortranarray(a)
+
+    def one():
+        t0 = time.perf_counter()
+        r = orc.lobpcg_solve(acm, opts)
+        t = time.perf_counter() - t0
+        t_sk0 = time.perf_counter()
+        orc.sketch_apply(acm, cfg.d, 4, problems.SOLVER_SEED)
+        t_sk = time.perf_counter() - t_sk0
+        setup = r["record"][0]["wall_ms"] / 1e3
+        iters = r["iterations"]
+        per_pass = (t - setup) / max(1, 2 * iters)
+        scale = cfg.m / m_s
+        # m-proportional parts: sketch, 2 init passes, 2 passes per iteration
+        t_full = t + (scale - 1.0) * (t_sk + per_pass * 2 * (iters + 1))
+        return t_full, t, iters, per_pass
+
+    warm = min(args.warmup, 1)
+    for _ in range(warm):
+        one()
+    vals = []
+    budget = 240.0
+    t_start = time.perf_counter()
+    samples = []
+    for k in range(args.steps):
+        v, t, iters, per_pass = one()
+        vals.append(v)
+        samples.append(t)
+        if time.perf_counter() - t_start > budget and k + 1 < args.steps:
+            break
+    value = float(np.mean(vals))
+    a_gbs = 8.0 * cfg.m * cfg.n / (per_pass * cfg.m / m_s) / 1e9
+    sample = (f"reference lobpcg_solve (single-threaded, {kind}) on the {cfg.name} recipe at m={m_s} "
+              f"(n={cfg.n}, d={cfg.d}, tol {cfg.tol:g}, tol-only), {iters} iterations, {np.mean(samples):.2f} s per "
+              f"sample; extrapolated to m={cfg.m} by scaling the sketch and A passes linearly in m "
+              f"(the sketch SVD is m-independent)")
+    line = {
+        "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus, "steps": len(vals),
+        "warmup": warm, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: m={cfg.m} n={cfg.n} b={cfg.b} d={cfg.d} tol={cfg.tol:g}",
+                   "inputs": "host RAM"},
+        "impl": "reference",
+        "a_stream_gbs": a_gbs,
+        "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    return line
+
+
+def cpu_baseline_quick(cfg):
+    """Reported CPU baseline for our arm (rank 0, N=1): same model as the
+    reference arm with one sample."""
+    class A:
+        warmup = 0
+        steps = 1
+        gpus = 1
+    line = reference_arm(A, cfg)
+    return line["cpu_baseline"] if line else None
+
+
+def ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_16797_b200 import minsvd as msvd
+    from paper_2602_16797_b200 import problems
+
+    ws, rank, local = dist_env()
+    if ws != args.gpus:
+        args.gpus = ws
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.tensor(list(msvd.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        stream = torch.cuda.current_stream(dev)
+        ctx = msvd.Context(local, comm_kind=1, nranks=ws, rank=rank, nccl_id=bytes(idt.cpu().tolist()),
+                           stream=stream.cuda_stream or 1)
+    else:
+        stream = torch.cuda.current_stream(dev)
+        ctx = msvd.Context(local, stream=stream.cuda_stream or 1)
+
+    m = args.m or cfg.m
+    sig = cfg.spectrum()
+    a_full, vmin = problems.make_problem_gpu(m, cfg.n, sig, device=dev)
+    r0, rows = msvd.shard_rows(m, ws, rank)
+    if ws > 1:
+        a = a_full[r0:r0 + rows].clone()
+        del a_full
+    else:
+        a = a_full
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    op = msvd.DeviceDenseOperator(a, ctx=ctx, row0=r0, m_global=m)
+    opts = msvd.SolverOptions(seed=problems.SOLVER_SEED, sketch_dim=cfg.d, tol=cfg.tol, block_size=cfg.b,
+                              use_stagnation=False, record_timing=False)
+    solve = msvd.rlobpcg_single if cfg.b == 1 else msvd.rlobpcg_block
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        res = solve(op, opts)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ctx.profile(True)
+    l0 = ctx.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    iters = []
+    loop_ms = []
+    for _ in range(args.steps):
+        res = solve(op, opts)
+        iters.append(res.iterations())
+        loop_ms.append(res.timings_ms["loop"])
+    ev1.record(stream)
+    barrier()
+    launches = ctx.launch_count() - l0
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    ms_step = ms / args.steps
+    it = int(np.median(iters))
+    a_bytes_iter = 16.0 * m * cfg.n  # two passes over A per iteration (whole job)
+    a_gbs_iter = a_bytes_iter / (np.median(loop_ms) / it / 1e3) / 1e9 if it else None
+
+    # roofline of the dominant kernel (K2 gram pass): algorithmic bytes per
+    # launch = 8 * m_local * n (A once; skinny reads/writes are <0.5%)
+    g_ms, g_cnt = prof["gram"]
+    a_ms, a_cnt = prof["apply"]
+    bytes_launch = 8.0 * rows * cfg.n
+    peak, peak_kind = peaks()
+    achieved = bytes_launch / (g_ms / g_cnt / 1e3) / 1e9 if g_cnt else None
+    achieved_apply = bytes_launch / (a_ms / a_cnt / 1e3) / 1e9 if a_cnt else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(cfg.name, {}).get("gram_kernel")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U diag(s) V^T, generated on device)",
+        "config": {"workload": f"{cfg.name}: m={m} n={cfg.n} b={cfg.b} d={cfg.d} tol={cfg.tol:g} tol-only",
+                   "parallelism": f"row-shard x{ws}", "iterations": it,
+                   "l2": "inputs larger than L2 (A = %.1f GB per rank)" % (8.0 * rows * cfg.n / 1e9)},
+        "a_stream_gbs_per_iter": a_gbs_iter,
+        "breakdown_ms": {k: round(v, 3) for k, v in res.timings_ms.items()},
+        "kernel_ms": {k: round(v[0] / max(1, args.steps), 3) for k, v in prof.items()},
+        "roofline": {"kernel": "gram_kernel (K2, A^T Y)", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "bytes_per_launch": bytes_launch,
+                     "apply_kernel_achieved": achieved_apply},
+        "clocks": clk,
+        "gpu_launches": launches,
+    }
+    if rank == 0 and ws == 1 and not args.no_e2e:
+        line["e2e"] = e2e(msvd, ctx, a, res, opts, args, cfg, solve)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline_quick(cfg)
+        except Exception as ex:  # reported, never fatal
+            line["cpu_baseline"] = {"value": None, "error": str(ex)}
+    if ws > 1:
+        dist.barrier()
+    return line if rank == 0 else None
+
+
+def e2e(msvd, ctx, a, res, opts, args, cfg, solve):
+    """Same metric through the public host-buffer entry (msvd_solve_host):
+    pinned host A copied H2D inside every step, results read back D2H."""
+    import torch
+
+    host = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+    host.copy_(a)
+    hnp = host.numpy()
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 3))
+    msvd.solve_host(hnp, opts, ctx=ctx)  # warm
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        r = msvd.solve_host(hnp, opts, ctx=ctx)
+    t = (time.perf_counter() - t0) / steps
+    h2d = 8 * a.shape[0] * a.shape[1]
+    d2h = 8 * cfg.n * cfg.b + 64 * len(r.record.rows) + 8 * cfg.b
+    del host
+    return {"value": t, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "note": "wall clock around msvd_solve_host (synchronous call), pinned host A"}
+
+
+def main():
+    args = parse()
+    from paper_2602_16797_b200 import problems
+
+    cfg = problems.CONFIGS[args.config]
+    if args.impl == "reference":
+        line = reference_arm(args, cfg)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+    line = ours(args, cfg)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

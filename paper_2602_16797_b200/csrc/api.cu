@@ -28,6 +28,16 @@ void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(MSVD_ERR_CUDA, std::string(cudaGetErrorString(e)) + " in " + what);
 }
 
+void* Ctx::ensure_sa(size_t bytes) {
+    if (bytes > sa_bytes) {
+        if (sa) MSVD_CUDA(cudaFree(sa));
+        sa = nullptr;
+        MSVD_CUDA(cudaMalloc(&sa, bytes));
+        sa_bytes = bytes;
+    }
+    return sa;
+}
+
 void* Ctx::ensure_scratch(size_t bytes) {
     if (bytes > scratch_bytes) {
         if (scratch) MSVD_CUDA(cudaFree(scratch));
@@ -36,6 +46,25 @@ void* Ctx::ensure_scratch(size_t bytes) {
         scratch_bytes = bytes;
     }
     return scratch;
+}
+
+ProfScope::ProfScope(Ctx& ctx, int s) : c(ctx), slot(s) {
+    if (!c.profiling) return;
+    size_t& used = c.prof_used[slot];
+    auto& v = c.prof_ev[slot];
+    if (used == v.size()) {
+        std::pair<cudaEvent_t, cudaEvent_t> e;
+        MSVD_CUDA(cudaEventCreate(&e.first));
+        MSVD_CUDA(cudaEventCreate(&e.second));
+        v.push_back(e);
+    }
+    MSVD_CUDA(cudaEventRecord(v[used].first, c.stream));
+    stop = v[used].second;
+}
+ProfScope::~ProfScope() {
+    if (!stop) return;
+    cudaEventRecord(stop, c.stream);
+    ++c.prof_used[slot];
 }
 
 namespace {
@@ -98,10 +127,12 @@ Plan validate(int64_t m, int64_t n, const msvd_options& o) {
     return p;
 }
 
-// one cudaMalloc for all per-solve buffers
+// all per-solve buffers carved from one ctx-owned allocation (grown on
+// demand, reused across solves: no cudaMalloc/cudaFree inside a solve)
 struct Arena {
+    Ctx& c;
     std::vector<std::pair<void**, size_t>> req;
-    void* base = nullptr;
+    explicit Arena(Ctx& ctx) : c(ctx) {}
     template <class T>
     void add(T** p, size_t count) {
         req.push_back({reinterpret_cast<void**>(p), ((sizeof(T) * std::max<size_t>(count, 1) + 255) / 256) * 256});
@@ -109,15 +140,17 @@ struct Arena {
     void commit() {
         size_t tot = 0;
         for (auto& r : req) tot += r.second;
-        MSVD_CUDA(cudaMalloc(&base, tot));
+        if (tot > c.arena_bytes) {
+            if (c.arena) MSVD_CUDA(cudaFree(c.arena));
+            c.arena = nullptr;
+            MSVD_CUDA(cudaMalloc(&c.arena, tot));
+            c.arena_bytes = tot;
+        }
         size_t off = 0;
         for (auto& r : req) {
-            *r.first = static_cast<unsigned char*>(base) + off;
+            *r.first = static_cast<unsigned char*>(c.arena) + off;
             off += r.second;
         }
-    }
-    ~Arena() {
-        if (base) cudaFree(base);
     }
 };
 
@@ -187,7 +220,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         if (!c.ev[i]) MSVD_CUDA(cudaEventCreate(&c.ev[i]));
     MSVD_CUDA(cudaEventRecord(c.ev[0], c.stream));
 
-    Arena ar;
+    Arena ar(c);
     DevState* st;
     msvd_record_row* rows;
     double *rh, *th, *Vcol, *Vrow, *sig, *AVb[2], *AXb[2], *AW, *Vb[2], *Xb[2], *W, *Rres, *tmp, *Cm, *Gpart,
@@ -250,7 +283,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
             // DenseOperator construction rejects non-finite data (operator.cpp:35-37)
             launch_colnorms(c, make_geom(c, M->A, ml, static_cast<int32_t>(n), M->ld), cpart, tmp);
         } else {
-            MSVD_CUDA(cudaMalloc(&SA, sizeof(double) * plan.d * n));
+            SA = static_cast<double*>(c.ensure_sa(sizeof(double) * plan.d * n));
             sketch_dev(c, geom, M->row0, plan.d, o.zeta, o.seed, SA, st);
             comm.allreduce_sum(SA, static_cast<size_t>(plan.d * n), c.stream);
             sa_rows = plan.d;
@@ -267,10 +300,10 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
             }
             precond_build_dev(c, SA, sa_rows, n, Vcol, Vrow, sig, &sigma1, &nfloor);
         } catch (...) {
-            cudaFree(SA);
+            if (plan.skip) cudaFree(SA);
             throw;
         }
-        MSVD_CUDA(cudaFree(SA));
+        if (plan.skip) MSVD_CUDA(cudaFree(SA));
         if (ranks > 1) {  // every rank uses rank 0's factorization bit for bit
             comm.bcast(Vcol, static_cast<size_t>(n * n), 0, c.stream);
             comm.bcast(Vrow, static_cast<size_t>(n * n), 0, c.stream);
@@ -634,8 +667,17 @@ int32_t msvd_ctx_destroy(msvd_ctx* ctx) {
         if (c.solver) cusolverDnDestroy(c.solver);
         if (c.scratch) cudaFree(c.scratch);
         if (c.pstate) cudaFree(c.pstate);
+        if (c.svd_ws) cudaFree(c.svd_ws);
+        if (c.arena) cudaFree(c.arena);
+        if (c.sa) cudaFree(c.sa);
+        if (c.svd_lw) cudaFree(c.svd_lw);
         for (auto& e : c.ev)
             if (e) cudaEventDestroy(e);
+        for (auto& v : c.prof_ev)
+            for (auto& e : v) {
+                cudaEventDestroy(e.first);
+                cudaEventDestroy(e.second);
+            }
         if (c.own_stream) cudaStreamDestroy(c.stream);
         delete ctx;
     });
@@ -650,6 +692,30 @@ int32_t msvd_ctx_synchronize(msvd_ctx* ctx) {
 }
 
 int64_t msvd_launch_count(msvd_ctx* ctx) { return ctx ? ctx->c.launches : -1; }
+
+int32_t msvd_ctx_profile(msvd_ctx* ctx, int32_t enable) {
+    return guard([&] {
+        need(ctx, "context");
+        Ctx& c = ctx->c;
+        c.profiling = enable != 0;
+        for (auto& u : c.prof_used) u = 0;
+    });
+}
+
+int32_t msvd_ctx_profile_read(msvd_ctx* ctx, double* ms, int64_t* counts, int32_t nslots) {
+    return guard([&] {
+        need(ctx, "context");
+        Ctx& c = ctx->c;
+        set_device(c);
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+        for (int s = 0; s < nslots && s < kProfSlots; ++s) {
+            double tot = 0.0;
+            for (size_t i = 0; i < c.prof_used[s]; ++i) tot += ev_ms(c.prof_ev[s][i].first, c.prof_ev[s][i].second);
+            if (ms) ms[s] = tot;
+            if (counts) counts[s] = static_cast<int64_t>(c.prof_used[s]);
+        }
+    });
+}
 
 void msvd_abi_sizes(int64_t* out, int32_t n) {
     const int64_t s[5] = {sizeof(msvd_options), sizeof(msvd_record_row), sizeof(msvd_truth), sizeof(msvd_result),

@@ -78,6 +78,9 @@ struct StreamGeom {
 
 struct Ctx;
 
+enum ProfSlot { kProfApply = 0, kProfGram, kProfTsqr, kProfRR, kProfSketch, kProfSvd, kProfPrecond, kProfCgs2,
+                kProfReduce, kProfControl, kProfSlots };
+
 // ---- launchers (kernels.cu) -----------------------------------------------
 StreamGeom make_geom(const Ctx& c, const double* A, int64_t m, int32_t n, int64_t ld);
 // Y (m x b, out cols) = A W (W n x b col-major)
@@ -184,6 +187,29 @@ struct Ctx {
     size_t scratch_bytes = 0;
     void* ensure_scratch(size_t bytes);
     DevState* pstate = nullptr;  // error word for primitive entry points
+    void* arena = nullptr;       // per-solve buffers (reused)
+    size_t arena_bytes = 0;
+    void* sa = nullptr;          // sketch d x n
+    size_t sa_bytes = 0;
+    void* ensure_sa(size_t bytes);
+    void* svd_ws = nullptr;      // preconditioner factorization workspace
+    size_t svd_ws_bytes = 0;
+    void* svd_lw = nullptr;      // cuSOLVER work buffer
+    size_t svd_lw_bytes = 0;
+    // optional per-kernel-class timing (bench evidence): event pairs per slot
+    bool profiling = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[kProfSlots];
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_pool;
+    size_t prof_used[kProfSlots] = {};
+};
+
+// RAII: events around the launches of one kernel class when profiling
+struct ProfScope {
+    Ctx& c;
+    int slot;
+    cudaEvent_t stop = nullptr;
+    ProfScope(Ctx& ctx, int s);
+    ~ProfScope();
 };
 
 void* fake_group_create(int n);

@@ -134,6 +134,7 @@ void build_sparsestack_dev(Ctx& c, int64_t d, int64_t m, int zeta, uint64_t seed
 void sketch_dev(Ctx& c, const StreamGeom& g, int64_t row0, int64_t d, int zeta, uint64_t seed, double* SA,
                 DevState* st) {
     const int64_t m = g.m;
+    ProfScope prof(c, kProfSketch);
     if (m == 0) {
         MSVD_CUDA(cudaMemsetAsync(SA, 0, sizeof(double) * d * g.n, c.stream));
         return;

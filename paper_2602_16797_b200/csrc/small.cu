@@ -763,6 +763,7 @@ void rr_launch(Ctx& c, const RRArgs& a) {
 int tsqr_parts(const Ctx& c) { return c.num_sms; }
 
 void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st, int iter) {
+    ProfScope prof(c, kProfTsqr);
     TsqrArgs a{T, m, k, Rparts, st, iter};
     const int grid = tsqr_parts(c);
     switch (km_for(k)) {
@@ -776,6 +777,7 @@ void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st,
 }
 
 void launch_rr(Ctx& c, const RRArgs& a) {
+    ProfScope prof(c, kProfRR);
     switch (km_for(a.k)) {
         case 4: rr_launch<4>(c, a); break;
         case 8: rr_launch<8>(c, a); break;
@@ -797,6 +799,7 @@ void launch_small_svd(Ctx& c, const double* B, int k, double* sigma, double* V, 
 
 void launch_reduce_g(Ctx& c, const double* Gpart, int nparts, int64_t n, int b, const double* V,
                      const DevState* st, int residual, double* Gout, double* nrm_part, int nblk) {
+    ProfScope prof(c, kProfReduce);
     dim3 grid(static_cast<unsigned>(nblk), static_cast<unsigned>(b));
     reduce_g_kernel<<<grid, 256, 0, c.stream>>>(Gpart, nparts, n, b, V, st, residual, Gout, nrm_part);
     MSVD_CUDA(cudaGetLastError());
@@ -804,6 +807,7 @@ void launch_reduce_g(Ctx& c, const double* Gpart, int nparts, int64_t n, int b, 
 }
 
 void launch_control(Ctx& c, const ControlArgs& a) {
+    ProfScope prof(c, kProfControl);
     control_kernel<<<1, 256, 0, c.stream>>>(a);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
@@ -822,6 +826,7 @@ static void precond_b(Ctx& c, const double* Vcol, const double* Vrow, const doub
 void launch_precond(Ctx& c, int kind, const double* Vcol, const double* Vrow, const double* sig,
                     const double* dinv, int64_t n, const double* R, int b, double* tmp, double* W,
                     DevState* st, int iter) {
+    ProfScope prof(c, kProfPrecond);
     if (kind != MSVD_PRECOND_RANDOMIZED) {
         const int64_t tot = n * b;
         diag_scale_kernel<<<static_cast<unsigned>(ceil_div(tot, 256)), 256, 0, c.stream>>>(kind, R, dinv, n, b, W,
@@ -843,6 +848,7 @@ void launch_precond(Ctx& c, int kind, const double* Vcol, const double* Vrow, co
 }
 
 void launch_cgs2(Ctx& c, double* W, int64_t n, int b, Cols basis, int nb, DevState* st, int iter) {
+    ProfScope prof(c, kProfCgs2);
     cgs2_kernel<<<1, kCgsT, 0, c.stream>>>(W, n, b, basis, nb, st, iter);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;

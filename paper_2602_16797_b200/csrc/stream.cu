@@ -42,21 +42,25 @@ __device__ void produce(const StreamGeom& g, const Pipe& p, int64_t r_begin, int
     if (g.tma) {
         if (lane != 0) return;
         const uint64_t pol = l2_evict_first_policy();
+        int s = 0;
+        uint32_t ph = 1;  // parity of the empty phase to wait for (first lap: none)
         for (int64_t c = 0; c < nchunks; ++c) {
-            const int s = static_cast<int>(c % g.stages);
-            const int64_t it = c / g.stages;
-            if (c >= g.stages) mbar_wait(&p.empty[s], static_cast<uint32_t>((it - 1) & 1));
+            if (c >= g.stages) mbar_wait(&p.empty[s], ph);
             const int64_t r0 = r_begin + c * g.rc;
             const int64_t rc = min(static_cast<int64_t>(g.rc), r_end - r0);
             const uint32_t bytes = static_cast<uint32_t>(rc * g.ld * 8);
             mbar_arrive_expect_tx(&p.full[s], bytes);
             bulk_g2s(p.stage0 + s * p.stage_bytes, g.A + r0 * g.ld, bytes, &p.full[s], pol);
+            if (++s == g.stages) {
+                s = 0;
+                ph ^= 1;
+            }
         }
     } else {
+        int s = 0;
+        uint32_t ph = 1;
         for (int64_t c = 0; c < nchunks; ++c) {
-            const int s = static_cast<int>(c % g.stages);
-            const int64_t it = c / g.stages;
-            if (c >= g.stages) mbar_wait(&p.empty[s], static_cast<uint32_t>((it - 1) & 1));
+            if (c >= g.stages) mbar_wait(&p.empty[s], ph);
             const int64_t r0 = r_begin + c * g.rc;
             const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
             double* dst = reinterpret_cast<double*>(p.stage0 + s * p.stage_bytes);
@@ -66,6 +70,10 @@ __device__ void produce(const StreamGeom& g, const Pipe& p, int64_t r_begin, int
             }
             __syncwarp();
             mbar_arrive(&p.full[s]);  // all 32 lanes arrive (count includes them)
+            if (++s == g.stages) {
+                s = 0;
+                ph ^= 1;
+            }
         }
     }
 }
@@ -88,16 +96,27 @@ struct ApplyArgs {
     OutCols out;      // b columns of length m
 };
 
-// K3: Y = A W.  Warps 1..8 consume; each row's b partial dots are reduced
-// across the 256 consumer threads with a warp transpose-reduce + one named
-// barrier per group of floor(32/B) rows.
+// K3: Y = A W.  Warps 1..8 consume.  Each warp reduces its threads'
+// partial dots for a group of rows with a warp transpose-reduce and writes
+// them to a per-stage slot; the last warp to finish a stage (shared-memory
+// ticket) sums the 8 warp partials in fixed order and stores the rows -- no
+// CTA-wide barrier on the streaming path, deterministic results.
+constexpr int kRedSlots = 64;  // rows-per-chunk x B cap for the apply kernel
+
+template <int B>
+struct ApplyShape {
+    static constexpr int NV = B == 1 ? 4 : (B == 2 ? 8 : 16);  // transpose slots
+    static constexpr int GR = NV / B;                          // rows per group
+};
+
 template <int B>
 __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const StreamGeom& g = a.g;
     unsigned char* extra;
-    Pipe p = carve(smem, g, sizeof(double) * 2 * 8 * 32, &extra);
-    double* red = reinterpret_cast<double*>(extra);  // [2][8][32]
+    Pipe p = carve(smem, g, sizeof(double) * g.stages * 8 * kRedSlots + 64 * sizeof(int), &extra);
+    double* red = reinterpret_cast<double*>(extra);  // [stages][8][kRedSlots]
+    int* ticket = reinterpret_cast<int*>(red + g.stages * 8 * kRedSlots);
     int64_t r_begin, r_end;
     cta_rows(g.m, r_begin, r_end);
     if (threadIdx.x == 0) {
@@ -105,6 +124,7 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) 
         for (int s = 0; s < g.stages; ++s) {
             mbar_init(&p.full[s], full_count);
             mbar_init(&p.empty[s], kConsumers / 32);
+            ticket[s] = 0;
         }
         mbar_fence_init();
     }
@@ -129,16 +149,17 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) 
             w[i][1][j] = c0 + 1 < n ? a.W[c0 + 1 + static_cast<int64_t>(j) * n] : 0.0;
         }
     }
-    constexpr int NV = B >= 5 ? 16 : 32;  // transpose-reduce slots
-    constexpr int GR = NV / B;            // rows per reduction group
+    constexpr int NV = ApplyShape<B>::NV;
+    constexpr int GR = ApplyShape<B>::GR;
     const int64_t nchunks = ceil_div(r_end - r_begin, g.rc);
-    int buf = 0;
+    int s = 0;
+    uint32_t ph = 0;
     for (int64_t c = 0; c < nchunks; ++c) {
-        const int s = static_cast<int>(c % g.stages);
-        mbar_wait(&p.full[s], static_cast<uint32_t>((c / g.stages) & 1));
+        mbar_wait(&p.full[s], ph);
         const double* As = reinterpret_cast<const double*>(p.stage0 + s * p.stage_bytes);
         const int64_t r0 = r_begin + c * g.rc;
         const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
+        double* rs = red + (static_cast<size_t>(s) * 8 + cw) * kRedSlots;
         for (int g0 = 0; g0 < rc; g0 += GR) {
             const int gn = min(GR, rc - g0);
             double v[NV];
@@ -164,19 +185,34 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) 
                 }
             }
             const double tot = warp_transpose_reduce<NV>(v);
-            red[(buf * 8 + cw) * 32 + lane] = tot;
-            named_sync(1, kConsumers);
-            if (ct < gn * B) {
+            if (lane < gn * B) rs[g0 * B + lane] = tot;
+        }
+        // ticket: the 8th warp through this stage finishes the rows
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+            __threadfence_block();
+            last = atomicAdd(&ticket[s], 1) == 7;
+        }
+        last = __shfl_sync(kFull, last, 0);
+        if (last) {
+            __threadfence_block();
+            const double* r8 = red + static_cast<size_t>(s) * 8 * kRedSlots;
+            for (int v = lane; v < rc * B; v += 32) {
                 double sum = 0.0;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) sum += red[(buf * 8 + q) * 32 + ct];
-                const int rr = ct / B, j = ct - (ct / B) * B;
-                a.out.p[j][r0 + g0 + rr] = sum;
+                for (int q = 0; q < 8; ++q) sum += r8[q * kRedSlots + v];
+                const int rr = v / B, j = v - (v / B) * B;
+                a.out.p[j][r0 + rr] = sum;
             }
-            buf ^= 1;
+            if (lane == 0) ticket[s] = 0;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&p.empty[s]);
+        if (++s == g.stages) {
+            s = 0;
+            ph ^= 1;
+        }
     }
 }
 
@@ -225,34 +261,65 @@ __global__ void __launch_bounds__(64 + kConsumers, 1) gram_kernel(GramArgs a) {
         return;
     }
     if (warp == 1) {
+        // Y rows are formed 32 at a time (lane = row) so the skinny loads of a
+        // whole window are in flight together, then handed to the stages that
+        // cover them.  The window runs ahead of the A stream, never behind it.
+        int64_t w0 = 0, w1 = 0;  // current window [w0, w1)
+        double yv[2 * B];
+#pragma unroll
+        for (int j = 0; j < 2 * B; ++j) yv[j] = 0.0;
+        int s = 0;
+        uint32_t ph = 1;
         for (int64_t c = 0; c < nchunks; ++c) {
-            const int s = static_cast<int>(c % g.stages);
-            const int64_t it = c / g.stages;
-            if (c >= g.stages) mbar_wait(&p.empty[s], static_cast<uint32_t>((it - 1) & 1));
             const int64_t r0 = r_begin + c * g.rc;
             const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
             double* ys = Ys + static_cast<size_t>(s) * g.rc * B;
-            for (int r = lane; r < rc; r += 32) {
-                const int64_t gr = r0 + r;
-                if (a.direct) {
+            bool waited = c < g.stages;
+            for (int64_t sub = r0; sub < r0 + rc;) {
+                if (sub >= w1) {
+                    w0 = sub;
+                    w1 = min(sub + 32, r_end);
+                    const int64_t gr = w0 + lane;
+                    if (gr < w1) {
+                        if (a.direct) {
 #pragma unroll
-                    for (int j = 0; j < B; ++j) ys[r * B + j] = a.T.p[j][gr];
-                } else {
-                    double t[kMaxK];
+                            for (int j = 0; j < B; ++j) yv[j] = a.T.p[j][gr];
+                        } else {
+                            double t[kMaxK];
 #pragma unroll
-                    for (int l = 0; l < kMaxK; ++l) t[l] = l < a.k ? a.T.p[l][gr] : 0.0;
-                    for (int j = 0; j < a.q; ++j) {
-                        double y = 0.0;
+                            for (int l = 0; l < kMaxK; ++l) t[l] = l < a.k ? a.T.p[l][gr] : 0.0;
 #pragma unroll
-                        for (int l = 0; l < kMaxK; ++l)
-                            if (l < a.k) y = fma(Cs[l + j * a.k], t[l], y);
-                        if (j < B) ys[r * B + j] = y;
-                        a.out.p[j][gr] = y;
+                            for (int j = 0; j < 2 * B; ++j) {
+                                if (j < a.q) {
+                                    double y = 0.0;
+#pragma unroll
+                                    for (int l = 0; l < kMaxK; ++l)
+                                        if (l < a.k) y = fma(Cs[l + j * a.k], t[l], y);
+                                    yv[j] = y;
+                                    a.out.p[j][gr] = y;
+                                }
+                            }
+                        }
                     }
                 }
+                if (!waited) {
+                    mbar_wait(&p.empty[s], ph);
+                    waited = true;
+                }
+                const int64_t end = min(w1, r0 + rc);
+                const int64_t gr = w0 + lane;
+                if (gr >= sub && gr < end) {
+#pragma unroll
+                    for (int j = 0; j < B; ++j) ys[(gr - r0) * B + j] = yv[j];
+                }
+                sub = end;
             }
             __syncwarp();
             mbar_arrive(&p.full[s]);
+            if (++s == g.stages) {
+                s = 0;
+                ph ^= 1;
+            }
         }
         return;
     }
@@ -264,9 +331,10 @@ __global__ void __launch_bounds__(64 + kConsumers, 1) gram_kernel(GramArgs a) {
     for (int i = 0; i < kMaxPairs; ++i)
 #pragma unroll
         for (int j = 0; j < B; ++j) acc[i][0][j] = acc[i][1][j] = 0.0;
+    int s = 0;
+    uint32_t ph = 0;
     for (int64_t c = 0; c < nchunks; ++c) {
-        const int s = static_cast<int>(c % g.stages);
-        mbar_wait(&p.full[s], static_cast<uint32_t>((c / g.stages) & 1));
+        mbar_wait(&p.full[s], ph);
         const double* As = reinterpret_cast<const double*>(p.stage0 + s * p.stage_bytes);
         const double* ys = Ys + static_cast<size_t>(s) * g.rc * B;
         const int64_t r0 = r_begin + c * g.rc;
@@ -293,6 +361,10 @@ __global__ void __launch_bounds__(64 + kConsumers, 1) gram_kernel(GramArgs a) {
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&p.empty[s]);
+        if (++s == g.stages) {
+            s = 0;
+            ph ^= 1;
+        }
     }
     double* gp = a.Gpart + static_cast<size_t>(blockIdx.x) * B * n;
 #pragma unroll
@@ -307,7 +379,18 @@ __global__ void __launch_bounds__(64 + kConsumers, 1) gram_kernel(GramArgs a) {
 }
 
 size_t apply_smem(const StreamGeom& g) {
-    return 256 + ((sizeof(double) * 2 * 8 * 32 + 127) / 128) * 128 + g.stages * g.stage_bytes;
+    const size_t extra = sizeof(double) * g.stages * 8 * kRedSlots + 64 * sizeof(int);
+    return 256 + ((extra + 127) / 128) * 128 + g.stages * g.stage_bytes;
+}
+
+// cap rows per chunk (stage geometry recomputed for the smaller chunk)
+StreamGeom cap_rows(StreamGeom g, int maxrc) {
+    if (g.rc <= maxrc) return g;
+    const int64_t row_bytes = static_cast<int64_t>(g.ld_s) * 8;
+    g.rc = maxrc;
+    g.stage_bytes = ((static_cast<size_t>(g.rc) * row_bytes + 127) / 128) * 128;
+    g.stages = static_cast<int32_t>(std::max<size_t>(2, std::min<size_t>(8, kStageBudget / g.stage_bytes)));
+    return g;
 }
 size_t gram_smem(const StreamGeom& g, int B) {
     const size_t extra = sizeof(double) * kMaxK * 2 * kMaxB + sizeof(double) * g.stages * g.rc * B;
@@ -367,7 +450,8 @@ StreamGeom make_geom(const Ctx& c, const double* A, int64_t m, int32_t n, int64_
 
 void launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out) {
     if (g.m == 0) return;
-    ApplyArgs a{g, W, out};
+    ProfScope prof(c, kProfApply);
+    ApplyArgs a{cap_rows(g, kRedSlots / std::max(1, b)), W, out};
     switch (b) {
         case 1: apply_b<1>(c, a); break;
         case 2: apply_b<2>(c, a); break;
@@ -383,6 +467,7 @@ void launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
 
 void launch_gram(Ctx& c, const StreamGeom& g, Cols T, int k, const double* Cm, int q, int b,
                  OutCols out, bool direct, double* Gpart) {
+    ProfScope prof(c, kProfGram);
     GramArgs a{g, T, k, Cm, q, out, direct ? 1 : 0, Gpart};
     if (g.m == 0) {
         MSVD_CUDA(cudaMemsetAsync(Gpart, 0, sizeof(double) * g.grid * b * g.n, c.stream));

@@ -3,7 +3,7 @@
 // dense_svd(SA) in the reference is Householder QR (d x n -> n x n R) then
 // one-sided Jacobi on R.  Here the n-scale factorization runs on the device
 // with cuSOLVER (allowed by the north star): geqrf reduces the tall sketch,
-// then an SVD of R (gesvdj by default; MSVD_SVD=gesvd|gesvdj|gesvdp selects).
+// then an SVD of R (gesvdp, the polar-decomposition SVD, by default; MSVD_SVD=gesvd|gesvdj|gesvdp selects).
 // A small kernel then applies the reference's conventions: descending order,
 // each right vector signed so its largest-magnitude entry is positive
 // (svd.cpp:232-248), and the sqrt(n) u sigma_1 floor (precond.cpp:26-34).
@@ -86,25 +86,42 @@ void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double
                        double* sigma_max, int64_t* nfloor) {
     if (n < 1) fail(MSVD_ERR_DIMENSION, "build_preconditioner: empty sketch");
     if (rows < n) fail(MSVD_ERR_DIMENSION, "build_preconditioner: sketch has fewer rows than columns");
+    ProfScope prof(c, kProfSvd);
     if (!c.solver) {
         MSVD_SOLVER(cusolverDnCreate(&c.solver));
     }
     MSVD_SOLVER(cusolverDnSetStream(c.solver, c.stream));
     const char* algo_env = std::getenv("MSVD_SVD");
-    const std::string algo = algo_env ? algo_env : "gesvdj";
+    const std::string algo = algo_env ? algo_env : "gesvdp";
     const int in = static_cast<int>(n), ir = static_cast<int>(rows);
 
-    // scratch: work (rows x n) | R (n x n) | V (n x n) | tau (n) | info + out2
+    // ctx-owned workspace (grown on demand, reused across solves):
+    // work (rows x n) | R (n x n) | V (n x n) | tau (n) | out2 (4) | info (4 ints)
     const size_t wbytes = sizeof(double) * static_cast<size_t>(rows) * n;
     const size_t nn = sizeof(double) * static_cast<size_t>(n) * n;
-    double *work = nullptr, *R = nullptr, *V = nullptr, *tau = nullptr, *out2 = nullptr, *lw = nullptr;
-    int* info = nullptr;
-    MSVD_CUDA(cudaMalloc(&work, wbytes));
-    MSVD_CUDA(cudaMalloc(&R, nn));
-    MSVD_CUDA(cudaMalloc(&V, nn));
-    MSVD_CUDA(cudaMalloc(&tau, sizeof(double) * n + 64));
-    MSVD_CUDA(cudaMalloc(&out2, sizeof(double) * 4));
-    MSVD_CUDA(cudaMalloc(&info, sizeof(int) * 4));
+    const size_t need = wbytes + 2 * nn + sizeof(double) * (n + 8) + 64;
+    if (need > c.svd_ws_bytes) {
+        if (c.svd_ws) MSVD_CUDA(cudaFree(c.svd_ws));
+        c.svd_ws = nullptr;
+        MSVD_CUDA(cudaMalloc(&c.svd_ws, need));
+        c.svd_ws_bytes = need;
+    }
+    double* work = static_cast<double*>(c.svd_ws);
+    double* R = work + static_cast<size_t>(rows) * n;
+    double* V = R + static_cast<size_t>(n) * n;
+    double* tau = V + static_cast<size_t>(n) * n;
+    double* out2 = tau + n;
+    int* info = reinterpret_cast<int*>(out2 + 4);
+    double* lw = nullptr;
+    auto lwork_buf = [&](size_t bytes) -> double* {
+        if (bytes > c.svd_lw_bytes) {
+            if (c.svd_lw) MSVD_CUDA(cudaFree(c.svd_lw));
+            c.svd_lw = nullptr;
+            MSVD_CUDA(cudaMalloc(&c.svd_lw, bytes));
+            c.svd_lw_bytes = bytes;
+        }
+        return static_cast<double*>(c.svd_lw);
+    };
     MSVD_CUDA(cudaMemsetAsync(info, 0, sizeof(int) * 4, c.stream));
     MSVD_CUDA(cudaMemcpyAsync(work, SA, wbytes, cudaMemcpyDeviceToDevice, c.stream));
     int vt_layout = 0;
@@ -112,10 +129,8 @@ void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double
         if (rows > n) {
             int lwork = 0;
             MSVD_SOLVER(cusolverDnDgeqrf_bufferSize(c.solver, ir, in, work, ir, &lwork));
-            MSVD_CUDA(cudaMalloc(&lw, sizeof(double) * (lwork + 1)));
+            lw = lwork_buf(sizeof(double) * (lwork + 1));
             MSVD_SOLVER(cusolverDnDgeqrf(c.solver, ir, in, work, ir, tau, lw, lwork, info));
-            MSVD_CUDA(cudaFree(lw));
-            lw = nullptr;
             upper_copy_kernel<<<static_cast<unsigned>(ceil_div(n * n, 256)), 256, 0, c.stream>>>(work, rows, n, R);
         } else {
             MSVD_CUDA(cudaMemcpyAsync(R, work, nn, cudaMemcpyDeviceToDevice, c.stream));
@@ -123,7 +138,7 @@ void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double
         if (algo == "gesvd") {
             int lwork = 0;
             MSVD_SOLVER(cusolverDnDgesvd_bufferSize(c.solver, in, in, &lwork));
-            MSVD_CUDA(cudaMalloc(&lw, sizeof(double) * (lwork + 1)));
+            lw = lwork_buf(sizeof(double) * (lwork + 1));
             double* rwork = work;  // reuse (>= n doubles)
             MSVD_SOLVER(cusolverDnDgesvd(c.solver, 'N', 'A', in, in, R, in, sig, nullptr, 1, V, in, lw, lwork,
                                          rwork, info + 1));
@@ -136,7 +151,7 @@ void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double
             MSVD_SOLVER(cusolverDnXgesvdp_bufferSize(c.solver, params, CUSOLVER_EIG_MODE_VECTOR, 0, n, n, CUDA_R_64F, R,
                                                      n, CUDA_R_64F, sig, CUDA_R_64F, U, n, CUDA_R_64F, V, n,
                                                      CUDA_R_64F, &dws, &hws));
-            MSVD_CUDA(cudaMalloc(&lw, dws + 64));
+            lw = lwork_buf(dws + 64);
             std::vector<char> hbuf(hws + 64);
             double err_sigma = 0.0;
             MSVD_SOLVER(cusolverDnXgesvdp(c.solver, params, CUSOLVER_EIG_MODE_VECTOR, 0, n, n, CUDA_R_64F, R, n,
@@ -153,7 +168,7 @@ void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double
             double* U = work;
             MSVD_SOLVER(cusolverDnDgesvdj_bufferSize(c.solver, CUSOLVER_EIG_MODE_VECTOR, 0, in, in, R, in, sig, U, in,
                                                      V, in, &lwork, params));
-            MSVD_CUDA(cudaMalloc(&lw, sizeof(double) * (lwork + 1)));
+            lw = lwork_buf(sizeof(double) * (lwork + 1));
             MSVD_SOLVER(cusolverDnDgesvdj(c.solver, CUSOLVER_EIG_MODE_VECTOR, 0, in, in, R, in, sig, U, in, V, in, lw,
                                           lwork, info + 1, params));
             MSVD_SOLVER(cusolverDnDestroyGesvdjInfo(params));
@@ -177,22 +192,8 @@ void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double
         *sigma_max = h[0];
         *nfloor = static_cast<int64_t>(h[1]);
     } catch (...) {
-        cudaFree(work);
-        cudaFree(R);
-        cudaFree(V);
-        cudaFree(tau);
-        cudaFree(out2);
-        cudaFree(info);
-        if (lw) cudaFree(lw);
         throw;
     }
-    cudaFree(work);
-    cudaFree(R);
-    cudaFree(V);
-    cudaFree(tau);
-    cudaFree(out2);
-    cudaFree(info);
-    if (lw) cudaFree(lw);
     if (*sigma_max == 0.0) fail(MSVD_ERR_NUMERICAL, "build_preconditioner: sketched matrix is exactly zero");
 }
 

@@ -111,6 +111,8 @@ def _declare(lib):
                                   P(abi.Result)]),
         "msvd_launch_count": (i64, [vp]),
         "msvd_abi_sizes": (None, [P(i64), i32]),
+        "msvd_ctx_profile": (i32, [vp, i32]),
+        "msvd_ctx_profile_read": (i32, [vp, P(d), P(i64), i32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -125,7 +127,7 @@ EXPORTED = (
     "msvd_fake_group_destroy msvd_ctx_create msvd_ctx_destroy msvd_ctx_synchronize msvd_matrix_attach "
     "msvd_matrix_detach msvd_apply msvd_apply_adjoint msvd_column_norms msvd_build_sparsestack msvd_sketch "
     "msvd_precond_build msvd_precond_apply msvd_tsqr_r msvd_small_svd msvd_lobpcg_solve msvd_rlobpcg_single "
-    "msvd_rlobpcg_block msvd_solve_host msvd_launch_count msvd_abi_sizes"
+    "msvd_rlobpcg_block msvd_solve_host msvd_launch_count msvd_abi_sizes msvd_ctx_profile msvd_ctx_profile_read"
 ).split()
 
 
@@ -289,6 +291,19 @@ class Context:
     def launch_count(self):
         return lib().msvd_launch_count(self.handle)
 
+    PROFILE_SLOTS = ("apply", "gram", "tsqr", "rr", "sketch", "svd", "precond", "cgs2", "reduce", "control")
+
+    def profile(self, enable=True):
+        """Per-kernel-class CUDA-event timing on this context's stream."""
+        check(lib().msvd_ctx_profile(self.handle, int(enable)))
+
+    def profile_read(self):
+        n = len(self.PROFILE_SLOTS)
+        ms = (C.c_double * n)()
+        cnt = (C.c_int64 * n)()
+        check(lib().msvd_ctx_profile_read(self.handle, ms, cnt, n))
+        return {k: (ms[i], cnt[i]) for i, k in enumerate(self.PROFILE_SLOTS)}
+
     def close(self):
         if self.handle:
             lib().msvd_ctx_destroy(self.handle)
@@ -304,9 +319,20 @@ class Context:
 _default_ctx = {}
 
 
+def torch_stream_handle(device=0):
+    """The current torch stream of `device` as a cudaStream_t for the
+    library, so library kernels are ordered with the torch work that
+    produced their inputs (torch's default stream 0 -> cudaStreamLegacy)."""
+    import torch
+
+    h = torch.cuda.current_stream(device).cuda_stream
+    return h if h else 1  # cudaStreamLegacy
+
+
 def default_context(device=0):
+    """Context on `device` bound to torch's current stream there."""
     if device not in _default_ctx:
-        _default_ctx[device] = Context(device)
+        _default_ctx[device] = Context(device, stream=torch_stream_handle(device))
     return _default_ctx[device]
 
 
@@ -325,8 +351,8 @@ class FakeGroup:
         self.handle = h
         self.nranks = nranks
 
-    def context(self, rank, device=0):
-        return Context(device, comm_kind=2, nranks=self.nranks, rank=rank, fake_group=self.handle)
+    def context(self, rank, device=0, stream=None):
+        return Context(device, comm_kind=2, nranks=self.nranks, rank=rank, fake_group=self.handle, stream=stream)
 
     def close(self):
         if self.handle:

@@ -84,7 +84,7 @@ def _haar_gpu(torch, rows, cols, gen, device, block_rows=None):
         s = torch.sign(torch.diagonal(r))
         s[s == 0] = 1.0
         q *= s
-        return q
+        return q.contiguous()  # cuSOLVER's Q is column-major; A is row-major
     nb = (rows + block_rows - 1) // block_rows
     q = torch.empty(rows, cols, dtype=torch.float64, device=device)
     rs = []
