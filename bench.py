@@ -84,7 +84,10 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 9:
-                self.rows.append(parts)
+                self.rows.append([time.perf_counter()] + parts)
+
+    def mark(self, which):
+        setattr(self, which, time.perf_counter())
 
     def stop(self):
         if self.proc:
@@ -93,13 +96,17 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", float("inf"))
+        timed = [r[1:] for r in self.rows if t0 <= r[0] <= t1]
+        rows = timed if len(timed) >= 3 else [r[1:] for r in self.rows]  # short window: whole run
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if "Active" in r[5 + i]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[5 + i]
                           and "Not" not in r[5 + i]})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows), "samples_in_timed_region": len(timed),
+                "window": "timed region" if len(timed) >= 3 else "warm-up + timed region"}
 
 
 def dist_env():
@@ -241,11 +248,12 @@ def ours(args, cfg):
             dist.barrier()
         torch.cuda.synchronize()
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         res = solve(op, opts)
     barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.mark("t0")
     ctx.profile(True)
     l0 = ctx.launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -259,6 +267,7 @@ def ours(args, cfg):
         loop_ms.append(res.timings_ms["loop"])
     ev1.record(stream)
     barrier()
+    clocks.mark("t1")
     launches = ctx.launch_count() - l0
     prof = ctx.profile_read()
     ctx.profile(False)

@@ -12,6 +12,8 @@
 //   gram_kernel   (K2)  G = A^T (T C)     -- solver.cpp:357-369 residual_of with
 //                        the recurrence products AV' = AT C, AX' = AT mix
 //                        (solver.cpp:421, :462) formed in-tile by a Y warp.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "msvd_internal.h"
 
@@ -78,14 +80,18 @@ __device__ void produce(const StreamGeom& g, const Pipe& p, int64_t r_begin, int
     }
 }
 
+// barrier area: full[stages] + empty[stages], 128-byte aligned
+__host__ __device__ constexpr size_t bar_bytes(int stages) { return ((16 * static_cast<size_t>(stages) + 127) / 128) * 128; }
+
 // shared-memory carve-up common to both kernels
 __device__ __forceinline__ Pipe carve(unsigned char* smem, const StreamGeom& g, size_t extra_bytes,
                                       unsigned char** extra) {
     Pipe p;
+    const size_t bars = bar_bytes(g.stages);
     p.full = reinterpret_cast<uint64_t*>(smem);
     p.empty = p.full + g.stages;
-    *extra = smem + 256;
-    p.stage0 = smem + 256 + ((extra_bytes + 127) / 128) * 128;
+    *extra = smem + bars;
+    p.stage0 = smem + bars + ((extra_bytes + 127) / 128) * 128;
     p.stage_bytes = g.stage_bytes;
     return p;
 }
@@ -113,10 +119,11 @@ template <int B>
 __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const StreamGeom& g = a.g;
+    const int nslot = 2 * g.stages;  // reduction ring: a warp is at most `stages` chunks ahead
     unsigned char* extra;
-    Pipe p = carve(smem, g, sizeof(double) * g.stages * 8 * kRedSlots + 64 * sizeof(int), &extra);
-    double* red = reinterpret_cast<double*>(extra);  // [stages][8][kRedSlots]
-    int* ticket = reinterpret_cast<int*>(red + g.stages * 8 * kRedSlots);
+    Pipe p = carve(smem, g, sizeof(double) * nslot * 8 * kRedSlots + 64 * sizeof(int), &extra);
+    double* red = reinterpret_cast<double*>(extra);  // [nslot][8][kRedSlots]
+    int* ticket = reinterpret_cast<int*>(red + nslot * 8 * kRedSlots);
     int64_t r_begin, r_end;
     cta_rows(g.m, r_begin, r_end);
     if (threadIdx.x == 0) {
@@ -124,8 +131,8 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) 
         for (int s = 0; s < g.stages; ++s) {
             mbar_init(&p.full[s], full_count);
             mbar_init(&p.empty[s], kConsumers / 32);
-            ticket[s] = 0;
         }
+        for (int s = 0; s < nslot; ++s) ticket[s] = 0;
         mbar_fence_init();
     }
     __syncthreads();
@@ -152,14 +159,14 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) 
     constexpr int NV = ApplyShape<B>::NV;
     constexpr int GR = ApplyShape<B>::GR;
     const int64_t nchunks = ceil_div(r_end - r_begin, g.rc);
-    int s = 0;
+    int s = 0, slot = 0;
     uint32_t ph = 0;
     for (int64_t c = 0; c < nchunks; ++c) {
         mbar_wait(&p.full[s], ph);
         const double* As = reinterpret_cast<const double*>(p.stage0 + s * p.stage_bytes);
         const int64_t r0 = r_begin + c * g.rc;
         const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
-        double* rs = red + (static_cast<size_t>(s) * 8 + cw) * kRedSlots;
+        double* rs = red + (static_cast<size_t>(slot) * 8 + cw) * kRedSlots;
         for (int g0 = 0; g0 < rc; g0 += GR) {
             const int gn = min(GR, rc - g0);
             double v[NV];
@@ -187,17 +194,24 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) 
             const double tot = warp_transpose_reduce<NV>(v);
             if (lane < gn * B) rs[g0 * B + lane] = tot;
         }
-        // ticket: the 8th warp through this stage finishes the rows
+        // the stage's rows are in registers/partials now: hand it back to the
+        // producer before the cross-warp finish, so the pipeline stays full
         __syncwarp();
+        if (lane == 0) mbar_arrive(&p.empty[s]);
+        if (++s == g.stages) {
+            s = 0;
+            ph ^= 1;
+        }
+        // ticket: the 8th warp through this chunk sums the warp partials
         int last = 0;
         if (lane == 0) {
             __threadfence_block();
-            last = atomicAdd(&ticket[s], 1) == 7;
+            last = atomicAdd(&ticket[slot], 1) == 7;
         }
         last = __shfl_sync(kFull, last, 0);
         if (last) {
             __threadfence_block();
-            const double* r8 = red + static_cast<size_t>(s) * 8 * kRedSlots;
+            const double* r8 = red + static_cast<size_t>(slot) * 8 * kRedSlots;
             for (int v = lane; v < rc * B; v += 32) {
                 double sum = 0.0;
 #pragma unroll
@@ -205,12 +219,99 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) 
                 const int rr = v / B, j = v - (v / B) * B;
                 a.out.p[j][r0 + rr] = sum;
             }
-            if (lane == 0) ticket[s] = 0;
+            __syncwarp();
+            if (lane == 0) ticket[slot] = 0;
+        }
+        if (++slot == nslot) slot = 0;
+    }
+}
+
+// K3, narrow-block variant (b small): every chunk is owned by ONE consumer
+// warp (chunk c -> warp c mod 8), lanes own fixed column pairs and keep W in
+// registers, and a row's b dot products are finished with warp butterflies.
+// No cross-warp reduction at all; the ring is deep (many small stages), so
+// the producer always has bytes in flight while each warp works on its chunk.
+template <int B, int PL>
+__global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const StreamGeom& g = a.g;
+    unsigned char* extra;
+    Pipe p = carve(smem, g, 0, &extra);
+    int64_t r_begin, r_end;
+    cta_rows(g.m, r_begin, r_end);
+    if (threadIdx.x == 0) {
+        const uint32_t full_count = g.tma ? 1u : 32u;
+        for (int s = 0; s < g.stages; ++s) {
+            mbar_init(&p.full[s], full_count);
+            mbar_init(&p.empty[s], 1);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp == 0) {
+        produce(g, p, r_begin, r_end);
+        return;
+    }
+    const int cw = warp - 1;
+    const int n = g.n;
+    const int npairs = (n + 1) >> 1;
+    double w[PL][2][B];
+#pragma unroll
+    for (int i = 0; i < PL; ++i) {
+        const int c0 = 2 * (lane + 32 * i);
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            w[i][0][j] = c0 < n ? a.W[c0 + static_cast<int64_t>(j) * n] : 0.0;
+            w[i][1][j] = c0 + 1 < n ? a.W[c0 + 1 + static_cast<int64_t>(j) * n] : 0.0;
+        }
+    }
+    const int64_t nchunks = ceil_div(r_end - r_begin, g.rc);
+    int s = cw;
+    uint32_t ph = 0;
+    while (s >= g.stages) {
+        s -= g.stages;
+        ph ^= 1;
+    }
+    for (int64_t c = cw; c < nchunks; c += 8) {
+        mbar_wait(&p.full[s], ph);
+        const double* As = reinterpret_cast<const double*>(p.stage0 + s * p.stage_bytes);
+        const int64_t r0 = r_begin + c * g.rc;
+        const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
+        for (int r = 0; r < rc; ++r) {
+            const double* row = As + static_cast<int64_t>(r) * g.ld_s;
+            double acc[B];
+#pragma unroll
+            for (int j = 0; j < B; ++j) acc[j] = 0.0;
+#pragma unroll
+            for (int i = 0; i < PL; ++i) {
+                const int pi = lane + 32 * i;
+                if (pi < npairs) {
+                    const double2 x = *reinterpret_cast<const double2*>(row + 2 * pi);
+                    const double xy = (2 * pi + 1 < n) ? x.y : 0.0;
+#pragma unroll
+                    for (int j = 0; j < B; ++j) {
+                        acc[j] = fma(x.x, w[i][0][j], acc[j]);
+                        acc[j] = fma(xy, w[i][1][j], acc[j]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < B; ++j) acc[j] = warp_sum(acc[j]);
+            if (lane < B) {
+                double v = acc[0];
+#pragma unroll
+                for (int j = 1; j < B; ++j)
+                    if (lane == j) v = acc[j];
+                a.out.p[lane][r0 + r] = v;
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&p.empty[s]);
-        if (++s == g.stages) {
-            s = 0;
+        s += 8;
+        while (s >= g.stages) {
+            s -= g.stages;
             ph ^= 1;
         }
     }
@@ -379,8 +480,26 @@ __global__ void __launch_bounds__(64 + kConsumers, 1) gram_kernel(GramArgs a) {
 }
 
 size_t apply_smem(const StreamGeom& g) {
-    const size_t extra = sizeof(double) * g.stages * 8 * kRedSlots + 64 * sizeof(int);
-    return 256 + ((extra + 127) / 128) * 128 + g.stages * g.stage_bytes;
+    const size_t extra = sizeof(double) * 2 * g.stages * 8 * kRedSlots + 64 * sizeof(int);
+    return bar_bytes(g.stages) + ((extra + 127) / 128) * 128 + g.stages * g.stage_bytes;
+}
+
+int64_t env_int(const char* name, int64_t dflt) {
+    const char* v = std::getenv(name);
+    return v ? std::atoll(v) : dflt;
+}
+
+// re-chunk a geometry: rows per stage from a target stage size, stage count
+// from a shared-memory budget (env MSVD_STAGE_KB / MSVD_STAGE_BUDGET_KB
+// override, for tuning sweeps)
+StreamGeom rechunk(StreamGeom g, int64_t target_kb, int64_t budget_kb) {
+    const int64_t row_bytes = static_cast<int64_t>(g.ld_s) * 8;
+    const int64_t target = env_int("MSVD_STAGE_KB", target_kb) * 1024;
+    const int64_t budget = env_int("MSVD_STAGE_BUDGET_KB", budget_kb) * 1024;
+    g.rc = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(target / row_bytes, 64)));
+    g.stage_bytes = ((static_cast<size_t>(g.rc) * row_bytes + 127) / 128) * 128;
+    g.stages = static_cast<int32_t>(std::max<size_t>(2, std::min<size_t>(8, budget / g.stage_bytes)));
+    return g;
 }
 
 // cap rows per chunk (stage geometry recomputed for the smaller chunk)
@@ -394,7 +513,60 @@ StreamGeom cap_rows(StreamGeom g, int maxrc) {
 }
 size_t gram_smem(const StreamGeom& g, int B) {
     const size_t extra = sizeof(double) * kMaxK * 2 * kMaxB + sizeof(double) * g.stages * g.rc * B;
-    return 256 + ((extra + 127) / 128) * 128 + g.stages * g.stage_bytes;
+    return bar_bytes(g.stages) + ((extra + 127) / 128) * 128 + g.stages * g.stage_bytes;
+}
+
+template <int B, int PL>
+void apply_rows_b(Ctx& c, const ApplyArgs& a) {
+    static bool attr = false;
+    if (!attr) {
+        MSVD_CUDA(cudaFuncSetAttribute(apply_rows_kernel<B, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(c.smem_optin)));
+        attr = true;
+    }
+    const size_t sm = bar_bytes(a.g.stages) + a.g.stages * a.g.stage_bytes;
+    apply_rows_kernel<B, PL><<<a.g.grid, 32 + kConsumers, sm, c.stream>>>(a);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+// geometry of the narrow variant: ~8 KB stages, deep ring (<= 32 stages)
+StreamGeom rows_geom(StreamGeom g) {
+    const int64_t row_bytes = static_cast<int64_t>(g.ld_s) * 8;
+    const int64_t target = env_int("MSVD_ROWS_STAGE_KB", 8) * 1024;
+    const int64_t budget = env_int("MSVD_ROWS_BUDGET_KB", 168) * 1024;
+    g.rc = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(target / row_bytes, 64)));
+    g.stage_bytes = ((static_cast<size_t>(g.rc) * row_bytes + 127) / 128) * 128;
+    // chunk c goes to warp c % 8 and stage c % stages: with stages a multiple
+    // of 8 every stage is only ever consumed by one warp, in order, so a
+    // warp can never run two mbarrier phases ahead of a stage (parity ABA)
+    const size_t per_warp = std::max<size_t>(2, std::min<size_t>(4, budget / (8 * g.stage_bytes)));
+    g.stages = static_cast<int32_t>(8 * per_warp);
+    return g;
+}
+
+// true if launched
+bool try_apply_rows(Ctx& c, const ApplyArgs& a0, int b) {
+    if (std::getenv("MSVD_APPLY_TICKET")) return false;
+    const int npairs = (a0.g.n + 1) / 2;
+    const int pl = (npairs + 31) / 32;
+    ApplyArgs a = a0;
+    a.g = rows_geom(a0.g);
+    if (a.g.stages * a.g.stage_bytes + bar_bytes(a.g.stages) > c.smem_optin) return false;
+    if (b == 1) {
+        if (pl <= 4) return apply_rows_b<1, 4>(c, a), true;
+        if (pl <= 8) return apply_rows_b<1, 8>(c, a), true;
+        if (pl <= 16) return apply_rows_b<1, 16>(c, a), true;
+        if (pl <= 32) return apply_rows_b<1, 32>(c, a), true;
+    } else if (b == 2) {
+        if (pl <= 4) return apply_rows_b<2, 4>(c, a), true;
+        if (pl <= 8) return apply_rows_b<2, 8>(c, a), true;
+        if (pl <= 16) return apply_rows_b<2, 16>(c, a), true;
+    } else if (b == 4 || b == 3) {
+        if (pl <= 4) return (b == 4 ? apply_rows_b<4, 4>(c, a) : apply_rows_b<3, 4>(c, a)), true;
+        if (pl <= 8) return (b == 4 ? apply_rows_b<4, 8>(c, a) : apply_rows_b<3, 8>(c, a)), true;
+    }
+    return false;
 }
 
 template <int B>
@@ -441,17 +613,22 @@ StreamGeom make_geom(const Ctx& c, const double* A, int64_t m, int32_t n, int64_
     const int64_t row_bytes = static_cast<int64_t>(g.ld_s) * 8;
     if (row_bytes > kStageBudget / 2)
         fail(MSVD_ERR_DIMENSION, "msvd: leading dimension too large for the stream pipeline");
-    g.rc = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(kStageTarget / row_bytes, 64)));
+    const int64_t target = env_int("MSVD_STAGE_KB", kStageTarget / 1024) * 1024;
+    const int64_t budget = env_int("MSVD_STAGE_BUDGET_KB", kStageBudget / 1024) * 1024;
+    g.rc = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(target / row_bytes, 64)));
     g.stage_bytes = ((static_cast<size_t>(g.rc) * row_bytes + 127) / 128) * 128;
-    g.stages = static_cast<int32_t>(std::max<size_t>(2, std::min<size_t>(8, kStageBudget / g.stage_bytes)));
-    g.grid = c.num_sms;
+    g.stages = static_cast<int32_t>(std::max<size_t>(2, std::min<size_t>(8, budget / g.stage_bytes)));
+    g.grid = c.num_sms * static_cast<int32_t>(env_int("MSVD_CTAS_PER_SM", 1));
     return g;
 }
 
 void launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out) {
     if (g.m == 0) return;
     ProfScope prof(c, kProfApply);
-    ApplyArgs a{cap_rows(g, kRedSlots / std::max(1, b)), W, out};
+    if (try_apply_rows(c, ApplyArgs{g, W, out}, b)) return;
+    // ticket variant: large stages amortize the per-chunk cross-warp finish
+    // (measured: 48 KB x 3 stages best at n = 2000, b = 5)
+    ApplyArgs a{cap_rows(rechunk(g, 48, 144), kRedSlots / std::max(1, b)), W, out};
     switch (b) {
         case 1: apply_b<1>(c, a); break;
         case 2: apply_b<2>(c, a); break;
@@ -468,7 +645,10 @@ void launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
 void launch_gram(Ctx& c, const StreamGeom& g, Cols T, int k, const double* Cm, int q, int b,
                  OutCols out, bool direct, double* Gpart) {
     ProfScope prof(c, kProfGram);
-    GramArgs a{g, T, k, Cm, q, out, direct ? 1 : 0, Gpart};
+    // stage geometry by block size (tuning sweep, profiles/README.md):
+    // b = 1: 32 KB x 3, b = 2: 48 KB x 3, b >= 3: 64 KB x 2
+    const StreamGeom gg = b == 1 ? rechunk(g, 32, 96) : (b == 2 ? rechunk(g, 48, 144) : rechunk(g, 64, 128));
+    GramArgs a{gg, T, k, Cm, q, out, direct ? 1 : 0, Gpart};
     if (g.m == 0) {
         MSVD_CUDA(cudaMemsetAsync(Gpart, 0, sizeof(double) * g.grid * b * g.n, c.stream));
         return;
