@@ -28,6 +28,16 @@ void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) fail(MSVD_ERR_CUDA, std::string(cudaGetErrorString(e)) + " in " + what);
 }
 
+void* Ctx::ensure_sar(size_t bytes) {
+    if (bytes > sar_bytes) {
+        if (sar) MSVD_CUDA(cudaFree(sar));
+        sar = nullptr;
+        MSVD_CUDA(cudaMalloc(&sar, bytes));
+        sar_bytes = bytes;
+    }
+    return sar;
+}
+
 void* Ctx::ensure_sa(size_t bytes) {
     if (bytes > sa_bytes) {
         if (sa) MSVD_CUDA(cudaFree(sa));
@@ -199,7 +209,15 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 // ---------------------------------------------------------------------------
 // lobpcg_solve on a device (row-sharded) dense operator
 // ---------------------------------------------------------------------------
-void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_result* res) {
+// optional host source of A: the H2D copy is chunked on a side stream and
+// each chunk is sketched as soon as it lands (msvd_solve_host)
+struct HostSource {
+    const double* hA;
+    int64_t ld;
+};
+
+void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_result* res,
+           const HostSource* hs = nullptr) {
     Ctx& c = M->ctx->c;
     set_device(c);
     Comm& comm = *c.comm;
@@ -265,6 +283,10 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     {
         double* SA = nullptr;
         int64_t sa_rows = 0;
+        if (hs && plan.skip && ml > 0)
+            MSVD_CUDA(cudaMemcpy2DAsync(const_cast<double*>(M->A), sizeof(double) * M->ld, hs->hA,
+                                        sizeof(double) * hs->ld, sizeof(double) * n, ml, cudaMemcpyHostToDevice,
+                                        c.stream));
         if (plan.skip) {
             // m <= 4n: P from a direct SVD of A (solver.cpp:132-134).  Assemble the
             // global A (exact: other ranks contribute zeros) and transpose it.
@@ -284,7 +306,29 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
             launch_colnorms(c, make_geom(c, M->A, ml, static_cast<int32_t>(n), M->ld), cpart, tmp);
         } else {
             SA = static_cast<double*>(c.ensure_sa(sizeof(double) * plan.d * n));
-            sketch_dev(c, geom, M->row0, plan.d, o.zeta, o.seed, SA, st);
+            if (!hs) {
+                sketch_dev(c, geom, M->row0, plan.d, o.zeta, o.seed, SA, st);
+            } else {
+                // overlap: chunk i is copied on the side stream while chunk i-1 is sketched
+                ProfScope prof(c, kProfSketch);
+                if (!c.copy_stream) MSVD_CUDA(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+                if (!c.copy_ev) MSVD_CUDA(cudaEventCreateWithFlags(&c.copy_ev, cudaEventDisableTiming));
+                MSVD_CUDA(cudaEventRecord(c.copy_ev, c.stream));  // device buffer free to overwrite
+                MSVD_CUDA(cudaStreamWaitEvent(c.copy_stream, c.copy_ev, 0));
+                double* SAr = sketch_begin(c, plan.d, n);
+                const int64_t step = sketch_chunk_rows(M->ld);
+                const SketchLists L = sketch_prepare(c, ml, M->row0, plan.d, o.zeta, o.seed, step);
+                for (int64_t r = 0; r < ml; r += step) {
+                    const int64_t rows = std::min(ml - r, step);
+                    MSVD_CUDA(cudaMemcpy2DAsync(const_cast<double*>(M->A) + r * M->ld, sizeof(double) * M->ld,
+                                                hs->hA + r * hs->ld, sizeof(double) * hs->ld, sizeof(double) * n,
+                                                rows, cudaMemcpyHostToDevice, c.copy_stream));
+                    MSVD_CUDA(cudaEventRecord(c.copy_ev, c.copy_stream));
+                    MSVD_CUDA(cudaStreamWaitEvent(c.stream, c.copy_ev, 0));
+                    sketch_rows(c, L, M->A, M->ld, static_cast<int>(n), geom.tma, r / step, SAr, st);
+                }
+                sketch_finish(c, SAr, plan.d, n, SA);
+            }
             comm.allreduce_sum(SA, static_cast<size_t>(plan.d * n), c.stream);
             sa_rows = plan.d;
         }
@@ -498,7 +542,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         }
     }
     MSVD_CUDA(cudaEventRecord(c.ev[4], c.stream));
-    const DevState hs = read_state(c, st);
+    const DevState fin = read_state(c, st);
 
     // ---- results (solver.cpp:469-476): ascending from the smallest ----
     std::vector<double> V(static_cast<size_t>(n) * b);
@@ -513,7 +557,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     MSVD_CUDA(cudaEventRecord(c.ev[5], c.stream));
     MSVD_CUDA(cudaStreamSynchronize(c.stream));
     for (int j = 0; j < b; ++j) {
-        res->sigma[j] = hs.theta[b - 1 - j];
+        res->sigma[j] = fin.theta[b - 1 - j];
         std::memcpy(res->v + static_cast<size_t>(j) * n, V.data() + static_cast<size_t>(b - 1 - j) * n,
                     sizeof(double) * n);
     }
@@ -528,8 +572,8 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     res->sketch_dim = plan.skip ? 0 : plan.d;
     res->zeta = plan.skip ? 0 : o.zeta;
     res->verify_count = verify_count;
-    res->max_cache_drift = hs.max_drift;
-    res->degenerate_replacements = hs.replacements;
+    res->max_cache_drift = fin.max_drift;
+    res->degenerate_replacements = fin.replacements;
     res->t_sketch_ms = ev_ms(c.ev[0], c.ev[1]);
     res->t_svd_ms = ev_ms(c.ev[1], c.ev[2]);
     res->t_init_ms = ev_ms(c.ev[2], c.ev[3]);
@@ -669,7 +713,11 @@ int32_t msvd_ctx_destroy(msvd_ctx* ctx) {
         if (c.pstate) cudaFree(c.pstate);
         if (c.svd_ws) cudaFree(c.svd_ws);
         if (c.arena) cudaFree(c.arena);
+        if (c.hostA) cudaFree(c.hostA);
+        if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
+        if (c.copy_ev) cudaEventDestroy(c.copy_ev);
         if (c.sa) cudaFree(c.sa);
+        if (c.sar) cudaFree(c.sar);
         if (c.svd_lw) cudaFree(c.svd_lw);
         for (auto& e : c.ev)
             if (e) cudaEventDestroy(e);
@@ -945,20 +993,18 @@ int32_t msvd_solve_host(msvd_ctx* ctx, const double* hA, int64_t m_local, int64_
         set_device(c);
         if (m_local > 0) need(hA, "host matrix");
         if (ld < n) fail(MSVD_ERR_DIMENSION, "msvd: leading dimension below column count");
+        if (m_local < 0 || n < 0) fail(MSVD_ERR_DIMENSION, "DenseMatrix: negative dimension");
         const int64_t ldd = (n % 2 == 0) ? n : n + 1;  // even pitch keeps the TMA path
-        double* dA = nullptr;
-        MSVD_CUDA(cudaMalloc(&dA, sizeof(double) * std::max<int64_t>(m_local * ldd, 1)));
-        try {
-            if (m_local > 0)
-                MSVD_CUDA(cudaMemcpy2DAsync(dA, sizeof(double) * ldd, hA, sizeof(double) * ld, sizeof(double) * n,
-                                            m_local, cudaMemcpyHostToDevice, c.stream));
-            msvd_matrix M{ctx, dA, m_local, n, ldd, row0, m_global};
-            solve(&M, *opts, truth, res);
-        } catch (...) {
-            cudaFree(dA);
-            throw;
+        const size_t bytes = sizeof(double) * static_cast<size_t>(std::max<int64_t>(m_local * ldd, 1));
+        if (bytes > c.hostA_bytes) {  // device copy of A, reused across calls
+            if (c.hostA) MSVD_CUDA(cudaFree(c.hostA));
+            c.hostA = nullptr;
+            MSVD_CUDA(cudaMalloc(&c.hostA, bytes));
+            c.hostA_bytes = bytes;
         }
-        cudaFree(dA);
+        msvd_matrix M{ctx, static_cast<double*>(c.hostA), m_local, n, ldd, row0, m_global};
+        HostSource hs{hA, ld};
+        solve(&M, *opts, truth, res, &hs);
     });
 }
 

@@ -154,6 +154,22 @@ void build_sparsestack_dev(Ctx& c, int64_t d, int64_t m, int zeta, uint64_t seed
                            int8_t* sgn);
 void sketch_dev(Ctx& c, const StreamGeom& g, int64_t row0, int64_t d, int zeta, uint64_t seed,
                 double* SA, DevState* st);
+// chunked form: sort the (sketch row, source row) lists once, then add row
+// chunks in order (bit-identical to one pass); used to overlap H2D copies
+struct SketchLists {
+    int64_t d = 0, m = 0;
+    double val = 0.0;
+    const int64_t* offs = nullptr;
+    const uint32_t* vals = nullptr;
+    const int64_t* bounds = nullptr;  // [chunk][sketch row] segment starts
+    int64_t step = 0;                 // source rows per chunk
+};
+SketchLists sketch_prepare(Ctx& c, int64_t m, int64_t row0, int64_t d, int zeta, uint64_t seed, int64_t step);
+void sketch_rows(Ctx& c, const SketchLists& L, const double* A, int64_t ld, int n, int vec, int64_t chunk,
+                 double* SA, DevState* st);
+int64_t sketch_chunk_rows(int64_t ld);
+double* sketch_begin(Ctx& c, int64_t d, int64_t n);  // zeroed row-major running sums
+void sketch_finish(Ctx& c, const double* SAr, int64_t d, int64_t n, double* SA);
 
 // ---- preconditioner factorization (svd.cu) --------------------------------
 void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double* Vcol,
@@ -189,9 +205,16 @@ struct Ctx {
     DevState* pstate = nullptr;  // error word for primitive entry points
     void* arena = nullptr;       // per-solve buffers (reused)
     size_t arena_bytes = 0;
+    void* hostA = nullptr;       // device copy of A for msvd_solve_host
+    size_t hostA_bytes = 0;
+    cudaStream_t copy_stream = nullptr;  // H2D chunks overlapped with the sketch
+    cudaEvent_t copy_ev = nullptr;
     void* sa = nullptr;          // sketch d x n
     size_t sa_bytes = 0;
     void* ensure_sa(size_t bytes);
+    void* sar = nullptr;         // row-major sketch accumulator
+    size_t sar_bytes = 0;
+    void* ensure_sar(size_t bytes);
     void* svd_ws = nullptr;      // preconditioner factorization workspace
     size_t svd_ws_bytes = 0;
     void* svd_lw = nullptr;      // cuSOLVER work buffer
