@@ -192,12 +192,9 @@ struct FakeComm final : Comm {
 }  // namespace
 
 Comm* make_comm(const msvd_ctx_desc& desc, cudaStream_t) {
-    if (desc.comm_kind == 0 || desc.nranks <= 1) {
-        if (desc.comm_kind == 2 && desc.fake_group && desc.nranks == 1)
-            return new FakeComm(static_cast<FakeGroup*>(desc.fake_group), 0);
-        return new NoComm();
-    }
-    if (desc.rank < 0 || desc.rank >= desc.nranks) fail(MSVD_ERR_INVALID, "msvd: rank outside [0, nranks)");
+    if (desc.comm_kind == 0) return new NoComm();
+    if (desc.nranks < 1 || desc.rank < 0 || desc.rank >= desc.nranks)
+        fail(MSVD_ERR_INVALID, "msvd: rank outside [0, nranks)");
     if (desc.comm_kind == 1) return new NcclComm(desc);
     if (desc.comm_kind == 2) {
         if (!desc.fake_group) fail(MSVD_ERR_INVALID, "msvd: fake communicator needs a group");

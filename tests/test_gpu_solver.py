@@ -365,6 +365,38 @@ def test_solve_host_end_to_end(msvd, cuda, port):
     assert np.array_equal(r1.v, r2.v)
 
 
+def test_solve_host_chunked_sketch_bit_identical(msvd, cuda, port, monkeypatch):
+    """The host-input path sketches A in row chunks as they land (overlapped
+    with the H2D copy); the chunked running sums equal the one-pass sketch bit
+    for bit, so the whole record is identical."""
+    cfg, sig, a, vmin = c1_problem(port)
+    opts = msvd.SolverOptions(seed=7, sketch_dim=cfg.d, tol=cfg.tol, use_stagnation=False, record_timing=False)
+    ref = gpu_solve(msvd, to_device(a, cuda), opts)
+    for mb in ("1", "3"):
+        monkeypatch.setenv("MSVD_SKETCH_CHUNK_MB", mb)  # C1: 8 and 3 chunks
+        r = msvd.solve_host(np.ascontiguousarray(a), opts, want_precond=True)
+        assert r.record.to_csv() == ref.record.to_csv()
+        assert np.array_equal(r.v, ref.v)
+
+
+def test_nccl_single_rank(msvd, cuda, port):
+    """The NCCL communicator (dlopen'ed libnccl) on one rank: every collective
+    of the sharded path runs and the answer equals the no-comm solve."""
+    import torch
+
+    cfg, sig, a, vmin = c1_problem(port)
+    opts = msvd.SolverOptions(seed=7, sketch_dim=cfg.d, tol=cfg.tol, use_stagnation=False, record_timing=False)
+    dev = to_device(a, cuda)
+    plain = gpu_solve(msvd, dev, opts)
+    ctx = msvd.Context(0, comm_kind=1, nranks=1, rank=0, nccl_id=msvd.nccl_unique_id(),
+                       stream=msvd.torch_stream_handle(0))
+    r = msvd.rlobpcg_block(msvd.DeviceDenseOperator(dev, ctx=ctx), opts)
+    assert r.record.to_csv() == plain.record.to_csv()
+    assert np.array_equal(r.v, plain.v)
+    ctx.close()
+    torch.cuda.synchronize()
+
+
 def test_fake_group_two_ranks(msvd, cuda, port):
     """Row-sharded solve over the in-process communicator (2 ranks, 1 GPU):
     same answer as one rank within the parity gates."""
