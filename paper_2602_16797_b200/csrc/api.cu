@@ -9,6 +9,7 @@
 // on the GPU; there is no CPU fallback.
 #include <algorithm>
 #include <cstddef>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -264,8 +265,9 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     ar.add(&Gpart, static_cast<size_t>(geom.grid) * b * n);
     ar.add(&Gout, n * b);
     ar.add(&nrm, static_cast<size_t>(b) * nblk);
-    ar.add(&Rparts, static_cast<size_t>(nparts) * kmax * kmax);
-    ar.add(&Rall, static_cast<size_t>(ranks) * nparts * kmax * kmax);
+    const int nparts_max = std::max(nparts, geom.grid);
+    ar.add(&Rparts, static_cast<size_t>(nparts_max) * kmax * kmax);
+    ar.add(&Rall, static_cast<size_t>(ranks) * nparts_max * kmax * kmax);
     ar.add(&tv, n);
     ar.add(&dinv, n);
     ar.add(&cpart, static_cast<size_t>(c.num_sms) * n);
@@ -389,11 +391,26 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
             for (int j = 0; j < pr.second; ++j) t.p[at++] = pr.first + static_cast<int64_t>(j) * n;
         return t;
     };
-    auto tsqr_all = [&](Cols T, int k, int iter) -> std::pair<const double*, int> {
-        launch_tsqr(c, T, ml, k, Rparts, st, iter);
-        if (ranks == 1) return {Rparts, nparts};
-        comm.allgather(Rparts, Rall, static_cast<size_t>(nparts) * k * k, c.stream);
-        return {Rall, nparts * ranks};
+    // A*W pass with the TSQR fused into it when the kernel supports it;
+    // otherwise a separate TSQR pass over the trial block.  Per-rank R factors
+    // are then gathered in rank order.
+    auto apply_tsqr = [&](Cols Tlead, int nlead, OutCols aw, Cols Tall, int k, int iter) -> std::pair<const double*, int> {
+        TsqrFuse fz{};
+        fz.T = Tlead;
+        fz.k = k;
+        fz.Rparts = Rparts;
+        fz.st = st;
+        fz.iter = iter;
+        (void)nlead;
+        int np = nparts;
+        if (launch_apply(c, geom, W, b, aw, std::getenv("MSVD_NO_FUSED_TSQR") ? nullptr : &fz)) {
+            np = geom.grid;
+        } else {
+            launch_tsqr(c, Tall, ml, k, Rparts, st, iter);
+        }
+        if (ranks == 1) return {Rparts, np};
+        comm.allgather(Rparts, Rall, static_cast<size_t>(np) * k * k, c.stream);
+        return {Rall, np * ranks};
     };
     auto residual = [&](const double* V) {  // G = A^T Y summed over ranks; R = G - theta^2 V
         if (ranks == 1) {
@@ -443,9 +460,8 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     launch_copy_cols(c, Vcol, n, n - b, n, b, W);  // sketch_and_solve_init: last b columns
     OutCols out{};
     for (int j = 0; j < b; ++j) out.p[j] = AW + static_cast<int64_t>(j) * ml;
-    launch_apply(c, geom, W, b, out);
     {
-        auto parts = tsqr_all(cols_m({{AW, b}}), b, -1);
+        auto parts = apply_tsqr(Cols{}, 0, out, cols_m({{AW, b}}), b, -1);
         RRArgs ra{};
         ra.Rparts = parts.first;
         ra.nparts = parts.second;
@@ -485,9 +501,8 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         launch_precond(c, kind, Vcol, Vrow, sig, dinv, n, Rres, b, tmp, W, st, i);
         launch_cgs2(c, W, n, b, cols_n({{Vb[cur], b}, {Xb[cur], nx}}), b + nx, st, i);
         for (int j = 0; j < b; ++j) out.p[j] = AW + static_cast<int64_t>(j) * ml;
-        launch_apply(c, geom, W, b, out);
         const Cols Tm = cols_m({{AVb[cur], b}, {AXb[cur], nx}, {AW, b}});
-        auto parts = tsqr_all(Tm, k, i);
+        auto parts = apply_tsqr(cols_m({{AVb[cur], b}, {AXb[cur], nx}}), b + nx, out, Tm, k, i);
         RRArgs ra{};
         ra.Rparts = parts.first;
         ra.nparts = parts.second;

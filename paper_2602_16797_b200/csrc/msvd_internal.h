@@ -58,6 +58,14 @@ struct DevState {
 struct Cols {
     const double* p[kMaxK];
 };
+struct DevState;
+struct TsqrFuse {
+    Cols T;           // the k - b leading trial columns (AV, AX), length m
+    int k;            // trial width; the A*W output supplies the last b columns
+    double* Rparts;   // [grid][k][k]
+    DevState* st;
+    int iter;
+};
 struct OutCols {
     double* p[2 * kMaxB];
 };
@@ -83,8 +91,12 @@ enum ProfSlot { kProfApply = 0, kProfGram, kProfTsqr, kProfRR, kProfSketch, kPro
 
 // ---- launchers (kernels.cu) -----------------------------------------------
 StreamGeom make_geom(const Ctx& c, const double* A, int64_t m, int32_t n, int64_t ld);
-// Y (m x b, out cols) = A W (W n x b col-major)
-void launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out);
+// Y (m x b, out cols) = A W (W n x b col-major).  With `fuse`, the pass may
+// also fold [T | Y] into per-CTA R factors (returns true if it did; the
+// caller then skips launch_tsqr)
+struct TsqrFuse;
+bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out,
+                  const TsqrFuse* fuse = nullptr);
 // Gpart[grid][b][n]: A^T Y with Y = T C (gram mode, writes Y cols + extra cols)
 // or Y = T (direct mode, q == b, no writes)
 void launch_gram(Ctx& c, const StreamGeom& g, Cols T, int k, const double* Cm, int q, int b,

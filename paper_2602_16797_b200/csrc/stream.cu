@@ -15,6 +15,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "fold.cuh"
 #include "msvd_internal.h"
 
 namespace msvd {
@@ -96,10 +97,16 @@ __device__ __forceinline__ Pipe carve(unsigned char* smem, const StreamGeom& g, 
     return p;
 }
 
+// TsqrFuse (msvd_internal.h): fused TSQR epilogue of the A*W pass (north-star
+// item 3) -- the rows of the trial block [AV AX | AW] are folded into per-CTA
+// Householder R factors while the pass streams, so the m x k block is never
+// re-read.
+
 struct ApplyArgs {
     StreamGeom g;
     const double* W;  // n x b col-major
     OutCols out;      // b columns of length m
+    TsqrFuse ts;      // ts.Rparts == nullptr: no fused TSQR
 };
 
 // K3: Y = A W.  Warps 1..8 consume.  Each warp reduces its threads'
@@ -231,12 +238,14 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) 
 // registers, and a row's b dot products are finished with warp butterflies.
 // No cross-warp reduction at all; the ring is deep (many small stages), so
 // the producer always has bytes in flight while each warp works on its chunk.
-template <int B, int PL>
+template <int B, int PL, int KM>
 __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const StreamGeom& g = a.g;
+    // KM > 0: fused TSQR; per consumer warp an R factor and a 32-row tile
+    constexpr size_t kTsqrBytes = KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM) : 0;
     unsigned char* extra;
-    Pipe p = carve(smem, g, 0, &extra);
+    Pipe p = carve(smem, g, kTsqrBytes, &extra);
     int64_t r_begin, r_end;
     cta_rows(g.m, r_begin, r_end);
     if (threadIdx.x == 0) {
@@ -247,6 +256,9 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArg
         }
         mbar_fence_init();
     }
+    if (KM > 0)
+        for (size_t i = threadIdx.x; i < kTsqrBytes / sizeof(double); i += blockDim.x)
+            reinterpret_cast<double*>(extra)[i] = 0.0;
     __syncthreads();
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -255,6 +267,11 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArg
         return;
     }
     const int cw = warp - 1;
+    double* Rw = KM > 0 ? reinterpret_cast<double*>(extra) + cw * KM * KM : nullptr;
+    double* tile = KM > 0 ? reinterpret_cast<double*>(extra) + 8 * KM * KM + cw * 32 * KM : nullptr;
+    const int kt = KM > 0 ? a.ts.k - B : 0;  // leading (cached) columns of the trial block
+    int ntile = 0;
+    bool finite = true;
     const int n = g.n;
     const int npairs = (n + 1) >> 1;
     double w[PL][2][B];
@@ -280,6 +297,9 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArg
         const int64_t r0 = r_begin + c * g.rc;
         const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
         for (int r = 0; r < rc; ++r) {
+            // cached trial columns of this row (independent of the dots: in flight meanwhile)
+            double tv = 0.0;
+            if (KM > 0 && lane < kt) tv = a.ts.T.p[lane][r0 + r];
             const double* row = As + static_cast<int64_t>(r) * g.ld_s;
             double acc[B];
 #pragma unroll
@@ -305,6 +325,22 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArg
                 for (int j = 1; j < B; ++j)
                     if (lane == j) v = acc[j];
                 a.out.p[lane][r0 + r] = v;
+                if (KM > 0) tile[ntile * KM + kt + lane] = v;
+            }
+            if (KM > 0) {
+                if (lane < kt) tile[ntile * KM + lane] = tv;
+                if (++ntile == 32) {
+                    __syncwarp();
+                    double x[KM > 0 ? KM : 1];
+#pragma unroll
+                    for (int l = 0; l < (KM > 0 ? KM : 1); ++l) {
+                        x[l] = l < a.ts.k ? tile[lane * KM + l] : 0.0;
+                        finite = finite && isfinite(x[l]);
+                    }
+                    __syncwarp();
+                    if constexpr (KM > 0) fold_rows<KM>(Rw, x, a.ts.k);
+                    ntile = 0;
+                }
             }
         }
         __syncwarp();
@@ -313,6 +349,39 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArg
         while (s >= g.stages) {
             s -= g.stages;
             ph ^= 1;
+        }
+    }
+    if constexpr (KM > 0) {
+        // remaining rows of the warp's tile, then an 8 -> 1 tree over the CTA
+        __syncwarp();
+        if (ntile > 0) {
+            double x[KM];
+#pragma unroll
+            for (int l = 0; l < KM; ++l) {
+                x[l] = (lane < ntile && l < a.ts.k) ? tile[lane * KM + l] : 0.0;
+                finite = finite && isfinite(x[l]);
+            }
+            __syncwarp();
+            fold_rows<KM>(Rw, x, a.ts.k);
+        }
+        if (!__all_sync(kFull, finite) && lane == 0 && a.ts.st)
+            if (atomicCAS(&a.ts.st->err_code, 0, kErrNonfiniteAT) == 0) a.ts.st->err_iter = a.ts.iter;
+        named_sync(2, kConsumers);
+        double* R0 = reinterpret_cast<double*>(extra);
+#pragma unroll
+        for (int st = 1; st < 8; st <<= 1) {
+            if ((cw % (2 * st)) == 0) {
+                double x[KM];
+                rows_of<KM>(R0 + (cw + st) * KM * KM, a.ts.k, x);
+                fold_rows<KM>(Rw, x, a.ts.k);
+            }
+            named_sync(3, kConsumers);
+        }
+        const int k = a.ts.k;
+        double* out = a.ts.Rparts + static_cast<size_t>(blockIdx.x) * k * k;
+        for (int i = threadIdx.x - 32; i < k * k; i += kConsumers) {
+            const int r = i % k, cc = i / k;
+            out[i] = r <= cc ? R0[r + cc * KM] : 0.0;
         }
     }
 }
@@ -516,18 +585,28 @@ size_t gram_smem(const StreamGeom& g, int B) {
     return bar_bytes(g.stages) + ((extra + 127) / 128) * 128 + g.stages * g.stage_bytes;
 }
 
-template <int B, int PL>
+template <int B, int PL, int KM>
 void apply_rows_b(Ctx& c, const ApplyArgs& a) {
     static bool attr = false;
     if (!attr) {
-        MSVD_CUDA(cudaFuncSetAttribute(apply_rows_kernel<B, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MSVD_CUDA(cudaFuncSetAttribute(apply_rows_kernel<B, PL, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(c.smem_optin)));
         attr = true;
     }
-    const size_t sm = bar_bytes(a.g.stages) + a.g.stages * a.g.stage_bytes;
-    apply_rows_kernel<B, PL><<<a.g.grid, 32 + kConsumers, sm, c.stream>>>(a);
+    const size_t tsqr = KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM) : 0;
+    const size_t sm = bar_bytes(a.g.stages) + ((tsqr + 127) / 128) * 128 + a.g.stages * a.g.stage_bytes;
+    apply_rows_kernel<B, PL, KM><<<a.g.grid, 32 + kConsumers, sm, c.stream>>>(a);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
+}
+
+// dispatch on the fused-TSQR width (KM = k rounded up to 4/8/16)
+template <int B, int PL>
+void apply_rows_km(Ctx& c, const ApplyArgs& a) {
+    if (!a.ts.Rparts) return apply_rows_b<B, PL, 0>(c, a);
+    if (a.ts.k <= 4) return apply_rows_b<B, PL, 4>(c, a);
+    if (a.ts.k <= 8) return apply_rows_b<B, PL, 8>(c, a);
+    return apply_rows_b<B, PL, 16>(c, a);
 }
 
 // geometry of the narrow variant: ~8 KB stages, deep ring (<= 32 stages)
@@ -545,26 +624,28 @@ StreamGeom rows_geom(StreamGeom g) {
     return g;
 }
 
-// true if launched
+// true if launched (the fused TSQR, when requested, was then done too)
 bool try_apply_rows(Ctx& c, const ApplyArgs& a0, int b) {
     if (std::getenv("MSVD_APPLY_TICKET")) return false;
     const int npairs = (a0.g.n + 1) / 2;
     const int pl = (npairs + 31) / 32;
+    if (a0.ts.Rparts && (a0.ts.k > 16 || a0.ts.k < b)) return false;
     ApplyArgs a = a0;
     a.g = rows_geom(a0.g);
-    if (a.g.stages * a.g.stage_bytes + bar_bytes(a.g.stages) > c.smem_optin) return false;
+    const size_t tsqr = a0.ts.Rparts ? sizeof(double) * 8 * (16 * 16 + 32 * 16) : 0;
+    if (a.g.stages * a.g.stage_bytes + bar_bytes(a.g.stages) + tsqr > c.smem_optin) return false;
     if (b == 1) {
-        if (pl <= 4) return apply_rows_b<1, 4>(c, a), true;
-        if (pl <= 8) return apply_rows_b<1, 8>(c, a), true;
-        if (pl <= 16) return apply_rows_b<1, 16>(c, a), true;
-        if (pl <= 32) return apply_rows_b<1, 32>(c, a), true;
+        if (pl <= 4) return apply_rows_km<1, 4>(c, a), true;
+        if (pl <= 8) return apply_rows_km<1, 8>(c, a), true;
+        if (pl <= 16) return apply_rows_km<1, 16>(c, a), true;
+        if (pl <= 32) return apply_rows_km<1, 32>(c, a), true;
     } else if (b == 2) {
-        if (pl <= 4) return apply_rows_b<2, 4>(c, a), true;
-        if (pl <= 8) return apply_rows_b<2, 8>(c, a), true;
-        if (pl <= 16) return apply_rows_b<2, 16>(c, a), true;
+        if (pl <= 4) return apply_rows_km<2, 4>(c, a), true;
+        if (pl <= 8) return apply_rows_km<2, 8>(c, a), true;
+        if (pl <= 16) return apply_rows_km<2, 16>(c, a), true;
     } else if (b == 4 || b == 3) {
-        if (pl <= 4) return (b == 4 ? apply_rows_b<4, 4>(c, a) : apply_rows_b<3, 4>(c, a)), true;
-        if (pl <= 8) return (b == 4 ? apply_rows_b<4, 8>(c, a) : apply_rows_b<3, 8>(c, a)), true;
+        if (pl <= 4) return (b == 4 ? apply_rows_km<4, 4>(c, a) : apply_rows_km<3, 4>(c, a)), true;
+        if (pl <= 8) return (b == 4 ? apply_rows_km<4, 8>(c, a) : apply_rows_km<3, 8>(c, a)), true;
     }
     return false;
 }
@@ -622,13 +703,14 @@ StreamGeom make_geom(const Ctx& c, const double* A, int64_t m, int32_t n, int64_
     return g;
 }
 
-void launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out) {
-    if (g.m == 0) return;
+bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out, const TsqrFuse* fuse) {
+    if (g.m == 0) return false;
     ProfScope prof(c, kProfApply);
-    if (try_apply_rows(c, ApplyArgs{g, W, out}, b)) return;
+    TsqrFuse none{};
+    if (try_apply_rows(c, ApplyArgs{g, W, out, fuse ? *fuse : none}, b)) return fuse != nullptr;
     // ticket variant: large stages amortize the per-chunk cross-warp finish
     // (measured: 48 KB x 3 stages best at n = 2000, b = 5)
-    ApplyArgs a{cap_rows(rechunk(g, 48, 144), kRedSlots / std::max(1, b)), W, out};
+    ApplyArgs a{cap_rows(rechunk(g, 48, 144), kRedSlots / std::max(1, b)), W, out, none};
     switch (b) {
         case 1: apply_b<1>(c, a); break;
         case 2: apply_b<2>(c, a); break;
@@ -640,6 +722,7 @@ void launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
         case 8: apply_b<8>(c, a); break;
         default: fail(MSVD_ERR_DIMENSION, "msvd: block size above 8 is not supported");
     }
+    return false;
 }
 
 void launch_gram(Ctx& c, const StreamGeom& g, Cols T, int k, const double* Cm, int q, int b,
