@@ -92,7 +92,7 @@ void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double
     }
     MSVD_SOLVER(cusolverDnSetStream(c.solver, c.stream));
     const char* algo_env = std::getenv("MSVD_SVD");
-    const std::string algo = algo_env ? algo_env : "gesvdp";
+    const std::string algo = algo_env ? algo_env : "gesvd";
     const int in = static_cast<int>(n), ir = static_cast<int>(rows);
 
     // ctx-owned workspace (grown on demand, reused across solves):
