@@ -344,7 +344,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
                 for (double v : h)
                     if (!std::isfinite(v)) fail(MSVD_ERR_NUMERICAL, "DenseOperator: non-finite entry");
             }
-            precond_build_dev(c, SA, sa_rows, n, Vcol, Vrow, sig, &sigma1, &nfloor);
+            precond_build_dev(c, SA, sa_rows, n, Vcol, Vrow, sig, &sigma1, &nfloor, b + 8);
         } catch (...) {
             if (plan.skip) cudaFree(SA);
             throw;

@@ -184,8 +184,10 @@ double* sketch_begin(Ctx& c, int64_t d, int64_t n);  // zeroed row-major running
 void sketch_finish(Ctx& c, const double* SAr, int64_t d, int64_t n, double* SA);
 
 // ---- preconditioner factorization (svd.cu) --------------------------------
+// tail_hint: number of smallest singular triplets refined to Jacobi accuracy
+// when the fast polar SVD is used (the solver passes b + 8)
 void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double* Vcol,
-                       double* Vrow, double* sig, double* sigma_max, int64_t* nfloor);
+                       double* Vrow, double* sig, double* sigma_max, int64_t* nfloor, int tail_hint = 8);
 
 // ---- communicator (comm.cu) ----------------------------------------------
 struct Comm {

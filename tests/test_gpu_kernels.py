@@ -211,12 +211,13 @@ def test_precond_build_and_apply(msvd, cuda, port, rows, n):
     assert np.allclose(w.cpu().numpy().T, want, rtol=1e-9, atol=1e-9 * np.abs(want).max())
 
 
-@pytest.mark.parametrize("algo", ["gesvdj", "gesvdp"])
+@pytest.mark.parametrize("algo", ["gesvdj", "gesvd", "polar", "gesvdp"])
 def test_precond_floor_and_zero(msvd, cuda, algo, monkeypatch):
     """The floor (precond.cpp:26-34).  An exactly rank-deficient sketch is
-    floored by the Jacobi SVD (relative accuracy, like the reference's); the
-    polar SVD (default, faster) resolves tiny values only to ~u sigma_1, so
-    there the check is that every value sits at or above the floor."""
+    floored by the Jacobi / QR-iteration SVDs and by the default polar SVD
+    with its tail refinement; the raw polar SVD resolves tiny values only to
+    ~u sigma_1, so there the check is that every value sits at or above the
+    floor."""
     import torch
 
     monkeypatch.setenv("MSVD_SVD", algo)
@@ -231,7 +232,7 @@ def test_precond_floor_and_zero(msvd, cuda, algo, monkeypatch):
     smax, nf = C.c_double(), C.c_int64()
     msvd.check(msvd.lib().msvd_precond_build(ctx.handle, _ptr(dsa), 10, 4, _ptr(vt), _ptr(sig), C.byref(smax),
                                              C.byref(nf)))
-    if algo == "gesvdj":
+    if algo != "gesvdp":  # raw polar SVD: tiny values only to ~u sigma_1
         assert nf.value >= 1
     assert sig.min().item() >= 2.0 * 2.220446049250313e-16 * smax.value * (1 - 1e-12)
     zero = torch.zeros((3, 6), dtype=torch.float64, device=cuda)
