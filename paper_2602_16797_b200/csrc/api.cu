@@ -403,7 +403,10 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         fz.iter = iter;
         (void)nlead;
         int np = nparts;
-        if (launch_apply(c, geom, W, b, aw, std::getenv("MSVD_NO_FUSED_TSQR") ? nullptr : &fz)) {
+        // fused only for b = 1 (k <= 3): measured, the fold's registers slow the
+        // wider A*W kernels more than a separate TSQR pass costs
+        const bool fuse = b == 1 && !std::getenv("MSVD_NO_FUSED_TSQR");
+        if (launch_apply(c, geom, W, b, aw, fuse ? &fz : nullptr)) {
             np = geom.grid;
         } else {
             launch_tsqr(c, Tall, ml, k, Rparts, st, iter);

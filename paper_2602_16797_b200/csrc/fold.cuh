@@ -67,3 +67,78 @@ __device__ __forceinline__ void rows_of(const double* R2, int k, double (&x)[KM]
 }
 
 }  // namespace msvd
+
+namespace msvd {
+
+// Shared-memory form of the same Householder fold, for wide trial blocks:
+// lane l owns column l of the stacked [R; X] block, so each reflector costs
+// plain FMAs over shared memory instead of k butterfly reductions.
+//   Rs: k x k upper triangular, column-major, leading dimension KM
+//   Xs: 32 x k rows, row-major, leading dimension XLD (= KM + 1: no conflicts)
+// Same reflector convention as fold_rows (svd.cpp:37).
+template <int KM>
+__device__ void fold_smem(double* Rs, double* Xs, int k) {
+    constexpr int XLD = KM + 1;
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    for (int j = 0; j < k; ++j) {
+        double beta = 0.0, inv = 0.0;
+        int skip = 0;
+        if (lane == j) {
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                const double a0 = Xs[i * XLD + j], a1 = Xs[(i + 1) * XLD + j];
+                const double a2 = Xs[(i + 2) * XLD + j], a3 = Xs[(i + 3) * XLD + j];
+                s0 = fma(a0, a0, s0);
+                s1 = fma(a1, a1, s1);
+                s2 = fma(a2, a2, s2);
+                s3 = fma(a3, a3, s3);
+            }
+            const double rjj = Rs[j + j * KM];
+            const double nrm2 = rjj * rjj + ((s0 + s1) + (s2 + s3));
+            if (nrm2 == 0.0) {
+                skip = 1;  // svd.cpp:33-36
+            } else {
+                const double xnorm = sqrt(nrm2);
+                const double alpha = rjj >= 0.0 ? -xnorm : xnorm;
+                const double v0 = rjj - alpha;
+                beta = -v0 / alpha;
+                inv = 1.0 / v0;
+                Rs[j + j * KM] = alpha;
+            }
+        }
+        skip = __shfl_sync(kFull, skip, j);
+        if (skip) continue;
+        beta = __shfl_sync(kFull, beta, j);
+        inv = __shfl_sync(kFull, inv, j);
+        if (lane > j && lane < k) {
+            double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                d0 = fma(Xs[i * XLD + j], Xs[i * XLD + lane], d0);
+                d1 = fma(Xs[(i + 1) * XLD + j], Xs[(i + 1) * XLD + lane], d1);
+                d2 = fma(Xs[(i + 2) * XLD + j], Xs[(i + 2) * XLD + lane], d2);
+                d3 = fma(Xs[(i + 3) * XLD + j], Xs[(i + 3) * XLD + lane], d3);
+            }
+            const double rjl = Rs[j + lane * KM];
+            const double s = (rjl + inv * ((d0 + d1) + (d2 + d3))) * beta;
+            Rs[j + lane * KM] = rjl - s;
+            const double si = s * inv;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) Xs[i * XLD + lane] -= si * Xs[i * XLD + j];
+        }
+        __syncwarp();
+    }
+}
+
+// the rows of an upper-triangular R2 (ld KM) as the X block of fold_smem
+template <int KM>
+__device__ __forceinline__ void load_rows_smem(const double* R2, int k, double* Xs) {
+    constexpr int XLD = KM + 1;
+    const int lane = threadIdx.x & 31;
+    for (int l = 0; l < k; ++l) Xs[lane * XLD + l] = (lane < k && l >= lane) ? R2[lane + l * KM] : 0.0;
+    __syncwarp();
+}
+
+}  // namespace msvd

@@ -64,6 +64,51 @@ __global__ void __launch_bounds__(256) tsqr_kernel(TsqrArgs a) {
     }
 }
 
+// Wide trial blocks: 16 warps per CTA, shared-memory folds (fold_smem)
+template <int KM>
+__global__ void __launch_bounds__(512) tsqr_smem_kernel(TsqrArgs a) {
+    extern __shared__ __align__(16) double tsm[];
+    constexpr int XLD = KM + 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
+    double* Rw = tsm + warp * KM * KM;
+    double* Xs = tsm + nw * KM * KM + warp * 32 * XLD;
+    for (int i = lane; i < KM * KM; i += 32) Rw[i] = 0.0;
+    const int64_t r0 = (a.m * blockIdx.x) / gridDim.x;
+    const int64_t r1 = (a.m * (blockIdx.x + 1)) / gridDim.x;
+    const int64_t ntiles = ceil_div(r1 - r0, 32);
+    bool finite = true;
+    for (int64_t t = warp; t < ntiles; t += nw) {
+        const int64_t row = r0 + t * 32 + lane;
+        double v[KM];  // all loads in flight before the first shared store
+#pragma unroll
+        for (int l = 0; l < KM; ++l) v[l] = (l < a.k && row < r1) ? a.T.p[l][row] : 0.0;
+#pragma unroll
+        for (int l = 0; l < KM; ++l)
+            if (l < a.k) {
+                finite = finite && isfinite(v[l]);
+                Xs[lane * XLD + l] = v[l];
+            }
+        fold_smem<KM>(Rw, Xs, a.k);
+    }
+    if (!__all_sync(kFull, finite) && lane == 0 && a.st) {
+        if (atomicCAS(&a.st->err_code, 0, kErrNonfiniteAT) == 0) a.st->err_iter = a.iter;
+    }
+    __syncthreads();
+    for (int s = 1; s < nw; s <<= 1) {
+        if ((warp % (2 * s)) == 0 && warp + s < nw) {
+            load_rows_smem<KM>(tsm + (warp + s) * KM * KM, a.k, Xs);
+            fold_smem<KM>(Rw, Xs, a.k);
+        }
+        __syncthreads();
+    }
+    double* out = a.Rparts + static_cast<size_t>(blockIdx.x) * a.k * a.k;
+    for (int i = threadIdx.x; i < a.k * a.k; i += blockDim.x) {
+        const int r = i % a.k, cc = i / a.k;
+        out[i] = r <= cc ? tsm[r + cc * KM] : 0.0;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // One-sided Jacobi SVD of a k x k (k <= 24) matrix in shared memory with a
 // round-robin parallel pair order (one warp per pair, lanes over rows); the
@@ -172,6 +217,13 @@ __device__ bool jacobi_svd(double* Bm, double* V, int k, double* sig, double* Vs
 // ---------------------------------------------------------------------------
 // Rayleigh-Ritz (solver.cpp:352-355 init, :417-421 and :453-462 iteration)
 // ---------------------------------------------------------------------------
+// the rr kernel's fold scratch lives after its other shared arrays
+template <int KM>
+__device__ __forceinline__ double* rr_scratch(double* sh) {
+    return sh + (16 * KM * KM + 3 * KM * KM + KM + 2 * KM * kMaxB + 2) + (KM + 1) / 2 + 2;
+}
+#define ord_end_scratch(sh, KM) rr_scratch<KM>(sh)
+
 template <int KM>
 __global__ void __launch_bounds__(512) rr_kernel(RRArgs a) {
     extern __shared__ __align__(16) double sh[];
@@ -187,23 +239,39 @@ __global__ void __launch_bounds__(512) rr_kernel(RRArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k = a.k, b = a.b;
 
-    // 1. merge the partial R factors: warp w folds parts w, w+32, ...; then a tree
+    // 1. merge the partial R factors: warp w folds parts w, w+16, ...; then a tree
     for (int i = lane; i < KM * KM; i += 32) Rw[warp * KM * KM + i] = 0.0;
     __syncwarp();
     const int nw = blockDim.x >> 5;
+    double* Xs = ord_end_scratch(sh, KM) + warp * 32 * (KM + 1);
     for (int pi = warp; pi < a.nparts; pi += nw) {
-        double x[KM];
         const double* R2 = a.Rparts + static_cast<size_t>(pi) * k * k;
+        if constexpr (KM >= 8) {
+            double v[KM];
 #pragma unroll
-        for (int l = 0; l < KM; ++l) x[l] = (lane < k && l >= lane && l < k) ? R2[lane + l * k] : 0.0;
-        fold_rows<KM>(Rw + warp * KM * KM, x, k);
+            for (int l = 0; l < KM; ++l) v[l] = (lane < k && l >= lane && l < k) ? R2[lane + l * k] : 0.0;
+#pragma unroll
+            for (int l = 0; l < KM; ++l)
+                if (l < k) Xs[lane * (KM + 1) + l] = v[l];
+            fold_smem<KM>(Rw + warp * KM * KM, Xs, k);
+        } else {
+            double x[KM];
+#pragma unroll
+            for (int l = 0; l < KM; ++l) x[l] = (lane < k && l >= lane && l < k) ? R2[lane + l * k] : 0.0;
+            fold_rows<KM>(Rw + warp * KM * KM, x, k);
+        }
     }
     __syncthreads();
     for (int s = 1; s < nw; s <<= 1) {
         if ((warp % (2 * s)) == 0 && warp + s < nw) {
-            double x[KM];
-            rows_of<KM>(Rw + (warp + s) * KM * KM, k, x);
-            fold_rows<KM>(Rw + warp * KM * KM, x, k);
+            if constexpr (KM >= 8) {
+                load_rows_smem<KM>(Rw + (warp + s) * KM * KM, k, Xs);
+                fold_smem<KM>(Rw + warp * KM * KM, Xs, k);
+            } else {
+                double x[KM];
+                rows_of<KM>(Rw + (warp + s) * KM * KM, k, x);
+                fold_rows<KM>(Rw + warp * KM * KM, x, k);
+            }
         }
         __syncthreads();
     }
@@ -680,7 +748,8 @@ __global__ void __launch_bounds__(512) small_svd_kernel(const double* B, int k, 
 
 template <int KM>
 size_t rr_smem() {
-    return sizeof(double) * (16 * KM * KM + 3 * KM * KM + KM + 2 * KM * kMaxB + 2) + sizeof(int) * KM + 64;
+    return sizeof(double) * ((16 * KM * KM + 3 * KM * KM + KM + 2 * KM * kMaxB + 2) + (KM + 1) / 2 + 2 +
+                             16 * 32 * (KM + 1)) + 64;
 }
 
 int km_for(int k) {
@@ -708,11 +777,16 @@ void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st,
     ProfScope prof(c, kProfTsqr);
     TsqrArgs a{T, m, k, Rparts, st, iter};
     const int grid = tsqr_parts(c);
+    auto smem_launch = [&](auto kernel, int km) {
+        const size_t sm = sizeof(double) * 16 * (km * km + 32 * (km + 1));
+        MSVD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+        kernel<<<grid, 512, sm, c.stream>>>(a);
+    };
     switch (km_for(k)) {
         case 4: tsqr_kernel<4><<<grid, 256, 0, c.stream>>>(a); break;
-        case 8: tsqr_kernel<8><<<grid, 256, 0, c.stream>>>(a); break;
-        case 16: tsqr_kernel<16><<<grid, 256, 0, c.stream>>>(a); break;
-        default: tsqr_kernel<24><<<grid, 256, 0, c.stream>>>(a); break;
+        case 8: smem_launch(tsqr_smem_kernel<8>, 8); break;
+        case 16: smem_launch(tsqr_smem_kernel<16>, 16); break;
+        default: smem_launch(tsqr_smem_kernel<24>, 24); break;
     }
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;

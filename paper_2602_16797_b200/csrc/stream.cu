@@ -238,12 +238,14 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) 
 // registers, and a row's b dot products are finished with warp butterflies.
 // No cross-warp reduction at all; the ring is deep (many small stages), so
 // the producer always has bytes in flight while each warp works on its chunk.
+constexpr int kRowsFused = 4;  // rows per chunk supported by the fused TSQR prefetch
+
 template <int B, int PL, int KM>
 __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const StreamGeom& g = a.g;
     // KM > 0: fused TSQR; per consumer warp an R factor and a 32-row tile
-    constexpr size_t kTsqrBytes = KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM) : 0;
+    constexpr size_t kTsqrBytes = KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM + 2 * kRowsFused * KM) : 0;
     unsigned char* extra;
     Pipe p = carve(smem, g, kTsqrBytes, &extra);
     int64_t r_begin, r_end;
@@ -269,6 +271,9 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArg
     const int cw = warp - 1;
     double* Rw = KM > 0 ? reinterpret_cast<double*>(extra) + cw * KM * KM : nullptr;
     double* tile = KM > 0 ? reinterpret_cast<double*>(extra) + 8 * KM * KM + cw * 32 * KM : nullptr;
+    // cached trial-column values of the next chunk, prefetched with cp.async
+    double* tbuf = KM > 0 ? reinterpret_cast<double*>(extra) + 8 * (KM * KM + 32 * KM) + cw * 2 * kRowsFused * KM
+                          : nullptr;
     const int kt = KM > 0 ? a.ts.k - B : 0;  // leading (cached) columns of the trial block
     int ntile = 0;
     bool finite = true;
@@ -291,15 +296,30 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArg
         s -= g.stages;
         ph ^= 1;
     }
+    auto prefetch = [&](int64_t cc, int buf) {
+        if (KM > 0 && cc < nchunks && lane < kt) {
+            const int64_t rr0 = r_begin + cc * g.rc;
+            const int rcc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - rr0));
+            const double* src = a.ts.T.p[lane];
+            for (int r = 0; r < rcc; ++r) cp_async8(tbuf + (buf * kRowsFused + r) * KM + lane, src + rr0 + r);
+        }
+        cp_async_commit();
+    };
+    int tb = 0;
+    if (KM > 0) prefetch(cw, 0);
     for (int64_t c = cw; c < nchunks; c += 8) {
+        if (KM > 0) {
+            prefetch(c + 8, tb ^ 1);  // next chunk of this warp, in flight while this one runs
+            cp_async_wait<1>();       // this chunk's values have landed
+            __syncwarp();
+        }
         mbar_wait(&p.full[s], ph);
         const double* As = reinterpret_cast<const double*>(p.stage0 + s * p.stage_bytes);
         const int64_t r0 = r_begin + c * g.rc;
         const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
         for (int r = 0; r < rc; ++r) {
-            // cached trial columns of this row (independent of the dots: in flight meanwhile)
             double tv = 0.0;
-            if (KM > 0 && lane < kt) tv = a.ts.T.p[lane][r0 + r];
+            if (KM > 0 && lane < kt) tv = tbuf[(tb * kRowsFused + r) * KM + lane];
             const double* row = As + static_cast<int64_t>(r) * g.ld_s;
             double acc[B];
 #pragma unroll
@@ -350,8 +370,10 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArg
             s -= g.stages;
             ph ^= 1;
         }
+        tb ^= 1;
     }
     if constexpr (KM > 0) {
+        cp_async_wait<0>();
         // remaining rows of the warp's tile, then an 8 -> 1 tree over the CTA
         __syncwarp();
         if (ntile > 0) {
@@ -593,7 +615,7 @@ void apply_rows_b(Ctx& c, const ApplyArgs& a) {
                                        static_cast<int>(c.smem_optin)));
         attr = true;
     }
-    const size_t tsqr = KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM) : 0;
+    const size_t tsqr = KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM + 2 * kRowsFused * KM) : 0;
     const size_t sm = bar_bytes(a.g.stages) + ((tsqr + 127) / 128) * 128 + a.g.stages * a.g.stage_bytes;
     apply_rows_kernel<B, PL, KM><<<a.g.grid, 32 + kConsumers, sm, c.stream>>>(a);
     MSVD_CUDA(cudaGetLastError());
@@ -632,7 +654,8 @@ bool try_apply_rows(Ctx& c, const ApplyArgs& a0, int b) {
     if (a0.ts.Rparts && (a0.ts.k > 16 || a0.ts.k < b)) return false;
     ApplyArgs a = a0;
     a.g = rows_geom(a0.g);
-    const size_t tsqr = a0.ts.Rparts ? sizeof(double) * 8 * (16 * 16 + 32 * 16) : 0;
+    if (a0.ts.Rparts && a.g.rc > kRowsFused) return false;  // tiny n: separate TSQR pass
+    const size_t tsqr = a0.ts.Rparts ? sizeof(double) * 8 * (16 * 16 + 32 * 16 + 2 * kRowsFused * 16) : 0;
     if (a.g.stages * a.g.stage_bytes + bar_bytes(a.g.stages) + tsqr > c.smem_optin) return false;
     if (b == 1) {
         if (pl <= 4) return apply_rows_km<1, 4>(c, a), true;
