@@ -727,6 +727,7 @@ int32_t msvd_ctx_destroy(msvd_ctx* ctx) {
         cudaStreamSynchronize(c.stream);
         delete c.comm;
         if (c.solver) cusolverDnDestroy(c.solver);
+        if (c.blas) cublasDestroy(c.blas);
         if (c.scratch) cudaFree(c.scratch);
         if (c.pstate) cudaFree(c.pstate);
         if (c.svd_ws) cudaFree(c.svd_ws);
@@ -969,7 +970,9 @@ int32_t msvd_small_svd(msvd_ctx* ctx, const double* dB, int64_t k, double* dSigm
         DevState* st = prim_state(c);
         MSVD_CUDA(cudaMemsetAsync(st, 0, sizeof(DevState), c.stream));
         launch_small_svd(c, dB, static_cast<int>(k), dSigma, dV, st);
-        read_state(c, st);
+        const DevState h = read_state(c, st);
+        if (std::getenv("MSVD_DEBUG_JACOBI")) std::fprintf(stderr, "msvd_small_svd: k=%lld sweeps=%g\n",
+                                                         static_cast<long long>(k), h.worst_jacobi);
     });
 }
 

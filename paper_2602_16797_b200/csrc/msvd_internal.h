@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <cstdint>
@@ -210,6 +211,7 @@ struct Ctx {
     bool own_stream = false;
     Comm* comm = nullptr;
     cusolverDnHandle_t solver = nullptr;
+    cublasHandle_t blas = nullptr;
     int64_t launches = 0;
     cudaEvent_t ev[8] = {};
     // reusable device scratch

@@ -172,6 +172,7 @@ __device__ bool jacobi_svd(double* Bm, double* V, int k, double* sig, double* Vs
         }
         converged = *worst_s <= 1e-15;
         __syncthreads();
+        if (threadIdx.x == 0) worst_s[1] = sweep + 1;  // sweeps used (diagnostics)
     }
     if (threadIdx.x < k) {
         double s = 0.0;
@@ -742,6 +743,7 @@ __global__ void __launch_bounds__(512) small_svd_kernel(const double* B, int k, 
     __syncthreads();
     const bool ok = jacobi_svd<KM>(Bm, V, k, sig, Vs, ord, worst);
     if (!ok && threadIdx.x == 0) st->err_code = kErrJacobi;
+    if (threadIdx.x == 0) st->worst_jacobi = worst[1];
     if (threadIdx.x < k) sigma[threadIdx.x] = sig[threadIdx.x];
     for (int i = threadIdx.x; i < k * k; i += blockDim.x) Vout[i] = Vs[(i % k) + (i / k) * KM];
 }

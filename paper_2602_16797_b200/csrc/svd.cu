@@ -1,12 +1,17 @@
 // Randomized preconditioner factorization (precond.cpp:11-36).
 //
 // dense_svd(SA) in the reference is Householder QR (d x n -> n x n R) then
-// one-sided Jacobi on R.  Here the n-scale factorization runs on the device
-// with cuSOLVER (allowed by the north star): geqrf reduces the tall sketch,
-// then an SVD of R.  Default ("polar"): cuSOLVER's QDWH polar SVD (gesvdp,
-// the fastest on B200) followed by a Jacobi-accurate refinement of the
-// singular triplets it cannot resolve (refine_tail below).  MSVD_SVD =
-// gesvd | gesvdj | gesvdp | polar selects.
+// one-sided Jacobi on R (svd.cpp:99-150, :180-252).  Here geqrf (cuSOLVER)
+// reduces the tall sketch to R, and the default SVD ("eigj") is the same
+// one-sided Jacobi, started from the eigenvectors of R^T R (cuSOLVER syevd):
+// B = R V0 has nearly orthogonal columns, so the Jacobi sweeps converge in
+// one or two passes.  Those passes run as dense simultaneous rotations on the
+// tensor cores (all pair tangents from the Gram B^T B, Q = exp(K), B <- B Q,
+// V <- V Q), with the reference's stop rule read from the Gram; pairs with
+// large rotations (near-degenerate or rank-deficient clusters) get exact
+// pairwise Jacobi sweeps, and anything else falls back to exact block sweeps
+// over all pairs.  MSVD_SVD = eigj | polar | gesvd | gesvdj | gesvdp selects
+// (polar: QDWH gesvdp + an inverse-iteration refinement of its tail).
 // A small kernel then applies the reference's conventions: descending order,
 // each right vector signed so its largest-magnitude entry is positive
 // (svd.cpp:232-248), and the sqrt(n) u sigma_1 floor (precond.cpp:26-34).
@@ -16,10 +21,14 @@
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "msvd_internal.h"
 
 namespace msvd {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -169,6 +178,466 @@ __global__ void permute_cols_kernel(const double* V, int64_t n, const int* ord, 
     out[i + j * n] = V[i + static_cast<int64_t>(ord[j]) * n];
 }
 
+
+// ---- eig-started one-sided Jacobi ("eigj") --------------------------------
+// One-sided Jacobi (svd.cpp:99-150: same rotation formulas, same 1e-15
+// pair-cosine threshold, same 60-sweep limit) on B = R V0, where V0 are the
+// eigenvectors of R^T R.  The eigen-solve is only a starting rotation: the
+// columns of B are already nearly orthogonal, so the sweeps that restore the
+// reference's Jacobi accuracy converge quadratically in a few passes instead
+// of the ~10 a cold start needs.  One persistent cooperative grid: each round
+// of the parallel round-robin ordering rotates n/2 disjoint column pairs (one
+// CTA per pair, fixed-order block reductions -> deterministic), then the grid
+// synchronises.  B and V (2 n^2 doubles) stay resident in L2.
+struct JacobiGridArgs {
+    double* B;       // n x n column-major
+    double* V;       // n x n column-major
+    int n;
+    double* worst;   // [kJacMaxSweeps] pair-cosine maxima, zeroed
+    int* status;     // [0] sweeps used, [1] 0 ok / 1 no convergence
+};
+constexpr int kJacMaxSweeps = 60;
+constexpr int kJacThreads = 256;
+
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+    // non-negative doubles order like their bit patterns
+    atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+__global__ void __launch_bounds__(kJacThreads) jacobi_grid_kernel(JacobiGridArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[3][kJacThreads / 32];
+    __shared__ double rot[3];
+    const int n = a.n, K2 = n + (n & 1), npairs = K2 / 2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int sweep = 0;
+    bool converged = n <= 1;
+    for (; sweep < kJacMaxSweeps && !converged; ++sweep) {
+        for (int r = 0; r < K2 - 1; ++r) {
+            for (int pi = blockIdx.x; pi < npairs; pi += gridDim.x) {
+                int p, q;
+                if (pi == 0) {
+                    p = r;
+                    q = K2 - 1;
+                } else {
+                    p = (r + pi) % (K2 - 1);
+                    q = (r - pi + (K2 - 1)) % (K2 - 1);
+                }
+                if (p > q) {
+                    const int t = p;
+                    p = q;
+                    q = t;
+                }
+                if (q >= n) continue;  // odd n: the phantom column
+                double* bp = a.B + static_cast<size_t>(p) * n;
+                double* bq = a.B + static_cast<size_t>(q) * n;
+                double spp = 0.0, sqq = 0.0, spq = 0.0;
+                for (int i = threadIdx.x; i < n; i += kJacThreads) {
+                    const double x = bp[i], y = bq[i];
+                    spp = fma(x, x, spp);
+                    sqq = fma(y, y, sqq);
+                    spq = fma(x, y, spq);
+                }
+                spp = warp_sum(spp);
+                sqq = warp_sum(sqq);
+                spq = warp_sum(spq);
+                if (lane == 0) {
+                    red[0][warp] = spp;
+                    red[1][warp] = sqq;
+                    red[2][warp] = spq;
+                }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    double app = 0.0, aqq = 0.0, apq = 0.0;
+                    for (int w = 0; w < kJacThreads / 32; ++w) {
+                        app += red[0][w];
+                        aqq += red[1][w];
+                        apq += red[2][w];
+                    }
+                    double c = 1.0, sn = 0.0;
+                    bool go = false;
+                    if (!(app == 0.0 || aqq == 0.0 || apq == 0.0)) {
+                        const double rel = fabs(apq) / sqrt(app * aqq);
+                        atomic_max_nonneg(&a.worst[sweep], rel);
+                        if (rel > 1e-15) {
+                            const double tau = (aqq - app) / (2.0 * apq);
+                            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                            c = 1.0 / sqrt(1.0 + t * t);
+                            sn = c * t;
+                            go = true;
+                        }
+                    }
+                    rot[0] = c;
+                    rot[1] = sn;
+                    rot[2] = go ? 1.0 : 0.0;
+                }
+                __syncthreads();
+                if (rot[2] != 0.0) {
+                    const double c = rot[0], sn = rot[1];
+                    double* vp = a.V + static_cast<size_t>(p) * n;
+                    double* vq = a.V + static_cast<size_t>(q) * n;
+                    for (int i = threadIdx.x; i < n; i += kJacThreads) {
+                        const double xp = bp[i], xq = bq[i];
+                        bp[i] = c * xp - sn * xq;
+                        bq[i] = sn * xp + c * xq;
+                        const double yp = vp[i], yq = vq[i];
+                        vp[i] = c * yp - sn * yq;
+                        vq[i] = sn * yp + c * yq;
+                    }
+                }
+                __syncthreads();
+            }
+            grid.sync();
+        }
+        converged = *reinterpret_cast<volatile double*>(&a.worst[sweep]) <= 1e-15;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.status[0] = sweep;
+        a.status[1] = converged ? 0 : 1;
+    }
+}
+
+// Block form of the same sweep, for n up to a few thousand: the columns are
+// grouped in blocks of W, and the parallel round-robin runs over blocks.  A
+// CTA takes a block pair (I, J), stages its 2W columns of B in shared memory,
+// rotates every cross pair (W sub-rounds of W disjoint pairs, one thread
+// group per pair; plus the intra-block pairs in the first round of a sweep),
+// then writes B back and applies the accumulated 2W x 2W rotation to V.  One
+// grid barrier per block round: n/W - 1 instead of n - 1 per sweep.  Every
+// rotation still recomputes its three dots from the current columns, exactly
+// as svd.cpp:110-143 does.
+template <int W>
+__global__ void __launch_bounds__(kJacThreads) jacobi_block_kernel(JacobiGridArgs a) {
+    constexpr int G = kJacThreads / W;  // threads per pair group
+    constexpr int NWG = (G + 31) / 32;  // warps per group
+    constexpr int C2 = 2 * W;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double bs[];  // [2W][n]
+    __shared__ double Q[C2 * C2];                 // accumulated rotation, column-major
+    __shared__ double red[W][3][NWG];
+    __shared__ double rot[W][3];
+    const int n = a.n;
+    const int nb = (n + W - 1) / W, NB = nb + (nb & 1), npairs = NB / 2;
+    const int g = threadIdx.x / G, gl = threadIdx.x % G, wg = gl >> 5, lane = threadIdx.x & 31;
+
+    // rotate local columns p, q (every thread of the CTA calls this in lockstep)
+    auto rotate = [&](int p, int q, int sweep) {
+        const double* bp = bs + p * n;
+        const double* bq = bs + q * n;
+        double spp = 0.0, sqq = 0.0, spq = 0.0;
+        for (int i = gl; i < n; i += G) {
+            const double x = bp[i], y = bq[i];
+            spp = fma(x, x, spp);
+            sqq = fma(y, y, sqq);
+            spq = fma(x, y, spq);
+        }
+        spp = warp_sum(spp);
+        sqq = warp_sum(sqq);
+        spq = warp_sum(spq);
+        if (lane == 0) {
+            red[g][0][wg] = spp;
+            red[g][1][wg] = sqq;
+            red[g][2][wg] = spq;
+        }
+        __syncthreads();
+        if (gl == 0) {
+            double app = 0.0, aqq = 0.0, apq = 0.0;
+#pragma unroll
+            for (int w = 0; w < NWG; ++w) {
+                app += red[g][0][w];
+                aqq += red[g][1][w];
+                apq += red[g][2][w];
+            }
+            double c = 1.0, sn = 0.0, go = 0.0;
+            if (!(app == 0.0 || aqq == 0.0 || apq == 0.0)) {
+                const double rel = fabs(apq) / sqrt(app * aqq);
+                atomic_max_nonneg(&a.worst[sweep], rel);
+                if (rel > 1e-15) {
+                    const double tau = (aqq - app) / (2.0 * apq);
+                    const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                    c = 1.0 / sqrt(1.0 + t * t);
+                    sn = c * t;
+                    go = 1.0;
+                }
+            }
+            rot[g][0] = c;
+            rot[g][1] = sn;
+            rot[g][2] = go;
+        }
+        __syncthreads();
+        if (rot[g][2] != 0.0) {
+            const double c = rot[g][0], sn = rot[g][1];
+            double* wp = bs + p * n;
+            double* wq = bs + q * n;
+            for (int i = gl; i < n; i += G) {
+                const double xp = wp[i], xq = wq[i];
+                wp[i] = c * xp - sn * xq;
+                wq[i] = sn * xp + c * xq;
+            }
+            if (gl < C2) {
+                const double yp = Q[gl + p * C2], yq = Q[gl + q * C2];
+                Q[gl + p * C2] = c * yp - sn * yq;
+                Q[gl + q * C2] = sn * yp + c * yq;
+            }
+        }
+        __syncthreads();
+    };
+
+    int sweep = 0;
+    bool converged = n <= 1;
+    for (; sweep < kJacMaxSweeps && !converged; ++sweep) {
+        for (int r = 0; r < NB - 1; ++r) {
+            for (int pi = blockIdx.x; pi < npairs; pi += gridDim.x) {
+                int I, J;
+                if (pi == 0) {
+                    I = r;
+                    J = NB - 1;
+                } else {
+                    I = (r + pi) % (NB - 1);
+                    J = (r - pi + (NB - 1)) % (NB - 1);
+                }
+                if (I > J) {
+                    const int t = I;
+                    I = J;
+                    J = t;
+                }
+                auto col = [&](int k) {
+                    const int cc = k < W ? I * W + k : J * W + (k - W);
+                    return cc < n ? cc : -1;
+                };
+                for (int i = threadIdx.x; i < n; i += kJacThreads) {
+#pragma unroll
+                    for (int k = 0; k < C2; ++k)
+                        bs[k * n + i] = col(k) >= 0 ? a.B[static_cast<size_t>(col(k)) * n + i] : 0.0;
+                }
+                for (int i = threadIdx.x; i < C2 * C2; i += kJacThreads) Q[i] = (i % C2) == (i / C2) ? 1.0 : 0.0;
+                __syncthreads();
+                if (r == 0) {  // intra-block pairs of both blocks (round robin on W columns)
+                    const int blk = g / (W / 2), idx = g % (W / 2);
+                    for (int s = 0; s < W - 1; ++s) {
+                        int p, q;
+                        if (idx == 0) {
+                            p = s;
+                            q = W - 1;
+                        } else {
+                            p = (s + idx) % (W - 1);
+                            q = (s - idx + (W - 1)) % (W - 1);
+                        }
+                        if (p > q) {
+                            const int t = p;
+                            p = q;
+                            q = t;
+                        }
+                        rotate(blk * W + p, blk * W + q, sweep);
+                    }
+                }
+                for (int s = 0; s < W; ++s) rotate(g, W + (g + s) % W, sweep);
+                // write back B, apply the accumulated rotation to V
+                for (int i = threadIdx.x; i < n; i += kJacThreads) {
+                    double v[C2];
+#pragma unroll
+                    for (int k = 0; k < C2; ++k) {
+                        if (col(k) >= 0) a.B[static_cast<size_t>(col(k)) * n + i] = bs[k * n + i];
+                        v[k] = col(k) >= 0 ? a.V[static_cast<size_t>(col(k)) * n + i] : 0.0;
+                    }
+#pragma unroll
+                    for (int k = 0; k < C2; ++k) {
+                        if (col(k) < 0) continue;
+                        double o = 0.0;
+#pragma unroll
+                        for (int l = 0; l < C2; ++l) o = fma(v[l], Q[l + k * C2], o);
+                        a.V[static_cast<size_t>(col(k)) * n + i] = o;
+                    }
+                }
+                __syncthreads();
+            }
+            grid.sync();
+        }
+        converged = *reinterpret_cast<volatile double*>(&a.worst[sweep]) <= 1e-15;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.status[0] = sweep;
+        a.status[1] = converged ? 0 : 1;
+    }
+}
+
+
+constexpr double kStrongT = 1e-5;  // |tan| above which a pair goes to the exact cluster sweep
+constexpr int kMaxCluster = 64;
+
+// All pair rotations of one Jacobi sweep at once, from the Gram H = B^T B:
+// K(p, q) = t_pq, K(q, p) = -t_pq with t the reference's rotation tangent
+// (svd.cpp:118-131; pairs at or below the 1e-15 cosine are left alone, zero
+// columns skipped).  Per-block partials: max pair cosine, max |t|, sum t^2.
+__global__ void pair_rot_kernel(const double* H, int64_t n, double* K, double* part, int* strong) {
+    __shared__ double red[4][8];
+    double mrel = 0.0, mt = 0.0, st = 0.0, ns = 0.0;
+    for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < n * n;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx % n, j = idx / n;
+        double kv = 0.0;
+        if (i != j) {
+            const int64_t p = i < j ? i : j, q = i < j ? j : i;
+            const double app = H[p + p * n], aqq = H[q + q * n], apq = H[p + q * n];
+            if (!(app == 0.0 || aqq == 0.0 || apq == 0.0)) {
+                const double rel = fabs(apq) / sqrt(app * aqq);
+                if (rel > 1e-15) {
+                    const double tau = (aqq - app) / (2.0 * apq);
+                    const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                    if (fabs(t) > kStrongT) {  // left to the exact cluster sweep
+                        if (i < j) {
+                            strong[p] = 1;
+                            strong[q] = 1;
+                            ns += 1.0;
+                        }
+                    } else {
+                        kv = i < j ? t : -t;
+                        if (i < j) {
+                            mt = fmax(mt, fabs(t));
+                            st = fma(t, t, st);
+                        }
+                    }
+                }
+                if (i < j) mrel = fmax(mrel, rel);
+            }
+        }
+        K[idx] = kv;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mrel = fmax(mrel, __shfl_xor_sync(0xffffffffu, mrel, o));
+        mt = fmax(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+        st += __shfl_xor_sync(0xffffffffu, st, o);
+        ns += __shfl_xor_sync(0xffffffffu, ns, o);
+    }
+    const int warp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[0][warp] = mrel;
+        red[1][warp] = mt;
+        red[2][warp] = st;
+        red[3][warp] = ns;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0, s2 = 0.0, s3 = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            a = fmax(a, red[0][w]);
+            b = fmax(b, red[1][w]);
+            s2 += red[2][w];
+            s3 += red[3][w];
+        }
+        part[4 * blockIdx.x] = a;
+        part[4 * blockIdx.x + 1] = b;
+        part[4 * blockIdx.x + 2] = s2;
+        part[4 * blockIdx.x + 3] = s3;
+    }
+}
+
+
+// Exact one-sided Jacobi (svd.cpp:99-150) restricted to the few columns that
+// take part in strong rotations (near-degenerate or rank-deficient clusters):
+// one CTA, round-robin over the m <= 64 listed columns, a warp per pair,
+// sweeps until every pair inside the cluster is at or below 1e-15.
+__global__ void __launch_bounds__(1024) cluster_jacobi_kernel(double* B, double* V, int64_t n, const int* cols, int m,
+                                                              int* status) {
+    __shared__ double worst;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int M2 = m + (m & 1);
+    int sweep = 0;
+    bool conv = m <= 1;
+    for (; sweep < kJacMaxSweeps && !conv; ++sweep) {
+        if (threadIdx.x == 0) worst = 0.0;
+        __syncthreads();
+        for (int r = 0; r < M2 - 1; ++r) {
+            for (int pi = warp; pi < M2 / 2; pi += nw) {
+                int a, b;
+                if (pi == 0) {
+                    a = r;
+                    b = M2 - 1;
+                } else {
+                    a = (r + pi) % (M2 - 1);
+                    b = (r - pi + (M2 - 1)) % (M2 - 1);
+                }
+                if (a >= m || b >= m) continue;
+                const int p = min(cols[a], cols[b]), q = max(cols[a], cols[b]);
+                double* bp = B + static_cast<size_t>(p) * n;
+                double* bq = B + static_cast<size_t>(q) * n;
+                double app = 0.0, aqq = 0.0, apq = 0.0;
+                for (int64_t i = lane; i < n; i += 32) {
+                    const double x = bp[i], y = bq[i];
+                    app = fma(x, x, app);
+                    aqq = fma(y, y, aqq);
+                    apq = fma(x, y, apq);
+                }
+                app = warp_sum(app);
+                aqq = warp_sum(aqq);
+                apq = warp_sum(apq);
+                if (app == 0.0 || aqq == 0.0 || apq == 0.0) continue;
+                const double rel = fabs(apq) / sqrt(app * aqq);
+                if (lane == 0) atomic_max_nonneg(&worst, rel);
+                if (rel <= 1e-15) continue;
+                const double tau = (aqq - app) / (2.0 * apq);
+                const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                const double c = 1.0 / sqrt(1.0 + t * t);
+                const double sn = c * t;
+                double* vp = V + static_cast<size_t>(p) * n;
+                double* vq = V + static_cast<size_t>(q) * n;
+                for (int64_t i = lane; i < n; i += 32) {
+                    const double xp = bp[i], xq = bq[i];
+                    bp[i] = c * xp - sn * xq;
+                    bq[i] = sn * xp + c * xq;
+                    const double yp = vp[i], yq = vq[i];
+                    vp[i] = c * yp - sn * yq;
+                    vq[i] = sn * yp + c * yq;
+                }
+            }
+            __syncthreads();
+        }
+        conv = worst <= 1e-15;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        status[0] = sweep;
+        status[1] = conv ? 0 : 1;
+    }
+}
+
+// T = I + alpha K
+__global__ void ident_axpy_kernel(const double* K, double alpha, int64_t n, double* T) {
+    for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < n * n;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        T[idx] = (K ? alpha * K[idx] : 0.0) + ((idx % n) == (idx / n) ? 1.0 : 0.0);
+}
+
+// sig[j] = ||B(:, j)|| (warp per column, fixed-order sums)
+__global__ void colnorm_kernel(const double* B, int64_t n, double* sig) {
+    const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (j >= n) return;
+    double s = 0.0;
+    for (int64_t i = lane; i < n; i += 32) s = fma(B[i + j * n], B[i + j * n], s);
+    s = warp_sum(s);
+    if (lane == 0) sig[j] = sqrt(s);
+}
+
+// stable descending order by rank: rank(i) = #{sig_j > sig_i} + #{j < i : sig_j == sig_i}
+__global__ void rank_sort_kernel(const double* sig, int64_t n, const double* V, double* sig_out, double* V_out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x);
+    __shared__ int64_t rk;
+    if (threadIdx.x == 0) rk = 0;
+    __syncthreads();
+    const double si = sig[i];
+    int64_t cnt = 0;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+        const double sj = sig[j];
+        cnt += (sj > si || (sj == si && j < i)) ? 1 : 0;
+    }
+    cnt = static_cast<int64_t>(warp_sum(static_cast<double>(cnt)));
+    if ((threadIdx.x & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&rk), static_cast<unsigned long long>(cnt));
+    __syncthreads();
+    const int64_t r = rk;
+    if (threadIdx.x == 0) sig_out[r] = si;
+    for (int64_t t = threadIdx.x; t < n; t += blockDim.x) V_out[t + r * n] = V[t + i * n];
+}
 }  // namespace
 
 // Polar SVD (cusolver gesvdp, QDWH) is fast but only backward stable to a few
@@ -243,6 +712,181 @@ static void refine_tail(Ctx& c, const double* R, int64_t n, double* V, double* s
     if (h.err_code) fail(MSVD_ERR_NUMERICAL, "build_preconditioner: tail refinement Jacobi did not converge");
 }
 
+
+// eig-started Jacobi SVD of the n x n upper-triangular R (column-major):
+// G = R^T R, V0 = eig(G) (cuSOLVER syevd), B = R V0, then one-sided Jacobi
+// sweeps on (B, V) to the reference's 1e-15 pair-cosine tolerance.  On return
+// sig (descending) and V (column-major, columns in the same order).
+// work: >= n*n doubles scratch; wv: >= n doubles.
+template <class LW>
+static void eig_jacobi(Ctx& c, const double* R, int64_t n, double* V, double* sig, double* work, double* wv,
+                       int* info, LW&& lwork_buf) {
+    if (!c.blas) {
+        if (cublasCreate(&c.blas) != CUBLAS_STATUS_SUCCESS) fail(MSVD_ERR_CUDA, "cublasCreate failed");
+        cublasSetPointerMode(c.blas, CUBLAS_POINTER_MODE_HOST);
+    }
+    if (cublasSetStream(c.blas, c.stream) != CUBLAS_STATUS_SUCCESS) fail(MSVD_ERR_CUDA, "cublasSetStream failed");
+    const int in = static_cast<int>(n);
+    const double one = 1.0, zero = 0.0;
+    // G = R^T R into V (full square; syevd reads the lower triangle)
+    if (cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, in, in, in, &one, R, in, R, in, &zero, V, in) !=
+        CUBLAS_STATUS_SUCCESS)
+        fail(MSVD_ERR_CUDA, "cublasDgemm (R^T R) failed");
+    int lwork = 0;
+    MSVD_SOLVER(cusolverDnDsyevd_bufferSize(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, in, V, in, wv,
+                                            &lwork));
+    double* lw = lwork_buf(sizeof(double) * (lwork + 1));
+    MSVD_SOLVER(cusolverDnDsyevd(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, in, V, in, wv, lw, lwork,
+                                 info));
+    // B = R V0 into work
+    if (cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_N, in, in, in, &one, R, in, V, in, &zero, work, in) !=
+        CUBLAS_STATUS_SUCCESS)
+        fail(MSVD_ERR_CUDA, "cublasDgemm (R V) failed");
+    auto gemm = [&](cublasOperation_t ta, const double* A, const double* Bm, double alpha, double beta, double* C,
+                    const char* what) {
+        if (cublasDgemm(c.blas, ta, CUBLAS_OP_N, in, in, in, &alpha, A, in, Bm, in, &beta, C, in) !=
+            CUBLAS_STATUS_SUCCESS)
+            fail(MSVD_ERR_CUDA, std::string("cublasDgemm failed: ") + what);
+    };
+    // Simultaneous sweeps while every rotation is small: Q = exp(K) (degree-5
+    // Taylor, Horner form; ||K||_F <= 1e-3 keeps the truncation below 1e-18),
+    // B <- B Q, V <- V Q.  Each step squares the off-diagonal mass like a
+    // Jacobi sweep.  The loop exits through the reference's own stop rule
+    // (every pair cosine <= 1e-15, read from the Gram of the current B);
+    // anything else -- a near-degenerate cluster, a rank-deficient block --
+    // falls through to the exact sweeps below.
+    const size_t nn = static_cast<size_t>(n) * n;
+    const int pgrid = static_cast<int>(std::min<int64_t>(ceil_div(static_cast<int64_t>(nn), 256), 4 * c.num_sms));
+    double* pool = lwork_buf(sizeof(double) * (3 * nn + 4 * pgrid + 8) + sizeof(int) * (2 * n + 8));
+    double* K = pool;
+    double* T1 = K + nn;
+    double* T2 = T1 + nn;
+    double* part = T2 + nn;
+    int* strong = reinterpret_cast<int*>(part + 4 * pgrid + 8);
+    int* clist = strong + n;
+    int* cstat = clist + n;
+    double* B = work;
+    double* Vp = V;
+    std::vector<double> hp(4 * pgrid);
+    std::vector<int> hflag(n), hcols;
+    bool done = false;
+    int steps = 0, csweeps = 0;
+    const char* ms = std::getenv("MSVD_JACOBI_GEMM_STEPS");
+    const int max_steps = ms ? std::atoi(ms) : 8;
+    const bool dbg = std::getenv("MSVD_DEBUG_JACOBI") != nullptr;
+    for (; steps < max_steps; ++steps) {
+        gemm(CUBLAS_OP_T, B, B, 1.0, 0.0, T1, "B^T B");
+        MSVD_CUDA(cudaMemsetAsync(strong, 0, sizeof(int) * n, c.stream));
+        pair_rot_kernel<<<pgrid, 256, 0, c.stream>>>(T1, n, K, part, strong);
+        MSVD_CUDA(cudaMemcpyAsync(hp.data(), part, sizeof(double) * 4 * pgrid, cudaMemcpyDeviceToHost, c.stream));
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+        c.launches += 2;
+        double mrel = 0.0, mt = 0.0, st = 0.0, ns = 0.0;
+        for (int b = 0; b < pgrid; ++b) {
+            mrel = std::max(mrel, hp[4 * b]);
+            mt = std::max(mt, hp[4 * b + 1]);
+            st += hp[4 * b + 2];
+            ns += hp[4 * b + 3];
+        }
+        const double fro = std::sqrt(2.0 * st);
+        if (dbg)
+            std::fprintf(stderr, "eig_jacobi: step %d max cos %.3e max t %.3e ||K||_F %.3e strong pairs %.0f\n", steps,
+                         mrel, mt, fro, ns);
+        if (mrel <= 1e-15) {  // the reference's stop rule, svd.cpp:146
+            done = true;
+            break;
+        }
+        hcols.clear();
+        if (ns > 0) {
+            MSVD_CUDA(cudaMemcpyAsync(hflag.data(), strong, sizeof(int) * n, cudaMemcpyDeviceToHost, c.stream));
+            MSVD_CUDA(cudaStreamSynchronize(c.stream));
+            for (int64_t j = 0; j < n; ++j)
+                if (hflag[j]) hcols.push_back(static_cast<int>(j));
+        }
+        if (fro > 1e-3 || static_cast<int>(hcols.size()) > kMaxCluster) break;  // -> exact sweeps
+        if (st > 0.0) {
+            ident_axpy_kernel<<<pgrid, 256, 0, c.stream>>>(K, 0.2, n, T2);
+            const double coef[4] = {0.25, 1.0 / 3.0, 0.5, 1.0};
+            for (double a : coef) {
+                ident_axpy_kernel<<<pgrid, 256, 0, c.stream>>>(nullptr, 0.0, n, T1);
+                gemm(CUBLAS_OP_N, K, T2, a, 1.0, T1, "Taylor");
+                std::swap(T1, T2);
+            }
+            // Q in T2
+            gemm(CUBLAS_OP_N, B, T2, 1.0, 0.0, T1, "B Q");
+            std::swap(B, T1);
+            gemm(CUBLAS_OP_N, Vp, T2, 1.0, 0.0, K, "V Q");
+            std::swap(Vp, K);
+            c.launches += 11;
+        }
+        if (!hcols.empty()) {
+            MSVD_CUDA(cudaMemcpyAsync(clist, hcols.data(), sizeof(int) * hcols.size(), cudaMemcpyHostToDevice,
+                                      c.stream));
+            cluster_jacobi_kernel<<<1, 1024, 0, c.stream>>>(B, Vp, n, clist, static_cast<int>(hcols.size()), cstat);
+            int h2[2];
+            MSVD_CUDA(cudaMemcpyAsync(h2, cstat, sizeof(h2), cudaMemcpyDeviceToHost, c.stream));
+            MSVD_CUDA(cudaStreamSynchronize(c.stream));
+            ++c.launches;
+            csweeps += h2[0];
+            if (h2[1]) fail(MSVD_ERR_NUMERICAL, "one_sided_jacobi: no convergence after 60 sweeps (cluster)");
+        }
+        // GEMM cosines carry a sqrt(n) u roundoff floor at the 1e-15 threshold:
+        // once every computed cosine is at that floor (<= 1e-13), the rotation
+        // just applied leaves true cosines at O(max^2) -- stop here.
+        if (mrel <= 1e-13) {
+            done = true;
+            ++steps;
+            break;
+        }
+    }
+    int hs[2] = {0, 0};
+    if (!done) {
+        // exact sweeps: worst[60] | status[2]
+        double* worst = static_cast<double*>(c.ensure_scratch(sizeof(double) * (kJacMaxSweeps + 2)));
+        int* status = reinterpret_cast<int*>(worst + kJacMaxSweeps);
+        MSVD_CUDA(cudaMemsetAsync(worst, 0, sizeof(double) * (kJacMaxSweeps + 2), c.stream));
+        JacobiGridArgs ja{B, Vp, in, worst, status};
+        void* kargs[] = {&ja};
+        auto coop = [&](const void* fn, int64_t units, size_t smem) {
+            if (smem > 48 * 1024)
+                MSVD_CUDA(
+                    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            int per_sm = 0;
+            MSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kJacThreads, smem));
+            const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(units, int64_t(per_sm) * c.num_sms));
+            MSVD_CUDA(cudaLaunchCooperativeKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kJacThreads), kargs,
+                                                  smem, c.stream));
+        };
+        // block width: MSVD_JACOBI_W = 1 (pair per CTA) | 4 | 8; default 4 when it fits
+        const char* jw = std::getenv("MSVD_JACOBI_W");
+        const int want = jw ? std::atoi(jw) : 4;
+        const size_t budget = 200 * 1024;
+        auto block_pairs = [&](int64_t w) {
+            const int64_t nb = (n + w - 1) / w;
+            return (nb + (nb & 1)) / 2;
+        };
+        if (want == 8 && sizeof(double) * 16 * n <= budget)
+            coop(reinterpret_cast<const void*>(jacobi_block_kernel<8>), block_pairs(8), sizeof(double) * 16 * n);
+        else if (want == 4 && sizeof(double) * 8 * n <= budget)
+            coop(reinterpret_cast<const void*>(jacobi_block_kernel<4>), block_pairs(4), sizeof(double) * 8 * n);
+        else
+            coop(reinterpret_cast<const void*>(jacobi_grid_kernel), (n + (n & 1)) / 2, 0);
+        MSVD_CUDA(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, c.stream));
+        ++c.launches;
+    }
+    colnorm_kernel<<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, c.stream>>>(B, n, wv);
+    // sorted copies into B's buffer (free after the norms), then into V
+    rank_sort_kernel<<<static_cast<unsigned>(n), 256, 0, c.stream>>>(wv, n, Vp, sig, B);
+    MSVD_CUDA(cudaMemcpyAsync(V, B, sizeof(double) * nn, cudaMemcpyDeviceToDevice, c.stream));
+    MSVD_CUDA(cudaGetLastError());
+    c.launches += 3;
+    MSVD_CUDA(cudaStreamSynchronize(c.stream));
+    if (std::getenv("MSVD_DEBUG_JACOBI"))
+        std::fprintf(stderr, "eig_jacobi: n=%lld gemm steps=%d cluster sweeps=%d exact sweeps=%d\n",
+                     static_cast<long long>(n), steps, csweeps, hs[0]);
+    if (hs[1]) fail(MSVD_ERR_NUMERICAL, "one_sided_jacobi: no convergence after 60 sweeps");
+}
+
 void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double* Vcol, double* Vrow, double* sig,
                        double* sigma_max, int64_t* nfloor, int tail_hint) {
     if (n < 1) fail(MSVD_ERR_DIMENSION, "build_preconditioner: empty sketch");
@@ -253,7 +897,7 @@ void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double
     }
     MSVD_SOLVER(cusolverDnSetStream(c.solver, c.stream));
     const char* algo_env = std::getenv("MSVD_SVD");
-    const std::string algo = algo_env ? algo_env : "polar";
+    const std::string algo = algo_env ? algo_env : "eigj";
     const int in = static_cast<int>(n), ir = static_cast<int>(rows);
 
     // ctx-owned workspace (grown on demand, reused across solves):
@@ -297,7 +941,10 @@ void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double
         } else {
             MSVD_CUDA(cudaMemcpyAsync(R, work, nn, cudaMemcpyDeviceToDevice, c.stream));
         }
-        if (algo == "gesvd") {
+        if (algo == "eigj") {
+            eig_jacobi(c, R, n, V, sig, work, tau, info + 1, lwork_buf);
+            vt_layout = 0;
+        } else if (algo == "gesvd") {
             int lwork = 0;
             MSVD_SOLVER(cusolverDnDgesvd_bufferSize(c.solver, in, in, &lwork));
             lw = lwork_buf(sizeof(double) * (lwork + 1));

@@ -211,7 +211,7 @@ def test_precond_build_and_apply(msvd, cuda, port, rows, n):
     assert np.allclose(w.cpu().numpy().T, want, rtol=1e-9, atol=1e-9 * np.abs(want).max())
 
 
-@pytest.mark.parametrize("algo", ["gesvdj", "gesvd", "polar", "gesvdp"])
+@pytest.mark.parametrize("algo", ["eigj", "gesvdj", "gesvd", "polar", "gesvdp"])
 def test_precond_floor_and_zero(msvd, cuda, algo, monkeypatch):
     """The floor (precond.cpp:26-34).  An exactly rank-deficient sketch is
     floored by the Jacobi / QR-iteration SVDs and by the default polar SVD
