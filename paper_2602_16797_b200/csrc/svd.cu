@@ -190,8 +190,9 @@ __global__ void permute_cols_kernel(const double* V, int64_t n, const int* ord, 
 // CTA per pair, fixed-order block reductions -> deterministic), then the grid
 // synchronises.  B and V (2 n^2 doubles) stay resident in L2.
 struct JacobiGridArgs {
-    double* B;       // n x n column-major
+    double* B;       // rows x n column-major
     double* V;       // n x n column-major
+    int rows;
     int n;
     double* worst;   // [kJacMaxSweeps] pair-cosine maxima, zeroed
     int* status;     // [0] sweeps used, [1] 0 ok / 1 no convergence
@@ -229,10 +230,10 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_grid_kernel(JacobiGridArgs
                     q = t;
                 }
                 if (q >= n) continue;  // odd n: the phantom column
-                double* bp = a.B + static_cast<size_t>(p) * n;
-                double* bq = a.B + static_cast<size_t>(q) * n;
+                double* bp = a.B + static_cast<size_t>(p) * a.rows;
+                double* bq = a.B + static_cast<size_t>(q) * a.rows;
                 double spp = 0.0, sqq = 0.0, spq = 0.0;
-                for (int i = threadIdx.x; i < n; i += kJacThreads) {
+                for (int i = threadIdx.x; i < a.rows; i += kJacThreads) {
                     const double x = bp[i], y = bq[i];
                     spp = fma(x, x, spp);
                     sqq = fma(y, y, sqq);
@@ -276,10 +277,12 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_grid_kernel(JacobiGridArgs
                     const double c = rot[0], sn = rot[1];
                     double* vp = a.V + static_cast<size_t>(p) * n;
                     double* vq = a.V + static_cast<size_t>(q) * n;
-                    for (int i = threadIdx.x; i < n; i += kJacThreads) {
+                    for (int i = threadIdx.x; i < a.rows; i += kJacThreads) {
                         const double xp = bp[i], xq = bq[i];
                         bp[i] = c * xp - sn * xq;
                         bq[i] = sn * xp + c * xq;
+                    }
+                    for (int i = threadIdx.x; i < n; i += kJacThreads) {
                         const double yp = vp[i], yq = vq[i];
                         vp[i] = c * yp - sn * yq;
                         vq[i] = sn * yp + c * yq;
@@ -297,172 +300,7 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_grid_kernel(JacobiGridArgs
     }
 }
 
-// Block form of the same sweep, for n up to a few thousand: the columns are
-// grouped in blocks of W, and the parallel round-robin runs over blocks.  A
-// CTA takes a block pair (I, J), stages its 2W columns of B in shared memory,
-// rotates every cross pair (W sub-rounds of W disjoint pairs, one thread
-// group per pair; plus the intra-block pairs in the first round of a sweep),
-// then writes B back and applies the accumulated 2W x 2W rotation to V.  One
-// grid barrier per block round: n/W - 1 instead of n - 1 per sweep.  Every
-// rotation still recomputes its three dots from the current columns, exactly
-// as svd.cpp:110-143 does.
-template <int W>
-__global__ void __launch_bounds__(kJacThreads) jacobi_block_kernel(JacobiGridArgs a) {
-    constexpr int G = kJacThreads / W;  // threads per pair group
-    constexpr int NWG = (G + 31) / 32;  // warps per group
-    constexpr int C2 = 2 * W;
-    cg::grid_group grid = cg::this_grid();
-    extern __shared__ __align__(16) double bs[];  // [2W][n]
-    __shared__ double Q[C2 * C2];                 // accumulated rotation, column-major
-    __shared__ double red[W][3][NWG];
-    __shared__ double rot[W][3];
-    const int n = a.n;
-    const int nb = (n + W - 1) / W, NB = nb + (nb & 1), npairs = NB / 2;
-    const int g = threadIdx.x / G, gl = threadIdx.x % G, wg = gl >> 5, lane = threadIdx.x & 31;
-
-    // rotate local columns p, q (every thread of the CTA calls this in lockstep)
-    auto rotate = [&](int p, int q, int sweep) {
-        const double* bp = bs + p * n;
-        const double* bq = bs + q * n;
-        double spp = 0.0, sqq = 0.0, spq = 0.0;
-        for (int i = gl; i < n; i += G) {
-            const double x = bp[i], y = bq[i];
-            spp = fma(x, x, spp);
-            sqq = fma(y, y, sqq);
-            spq = fma(x, y, spq);
-        }
-        spp = warp_sum(spp);
-        sqq = warp_sum(sqq);
-        spq = warp_sum(spq);
-        if (lane == 0) {
-            red[g][0][wg] = spp;
-            red[g][1][wg] = sqq;
-            red[g][2][wg] = spq;
-        }
-        __syncthreads();
-        if (gl == 0) {
-            double app = 0.0, aqq = 0.0, apq = 0.0;
-#pragma unroll
-            for (int w = 0; w < NWG; ++w) {
-                app += red[g][0][w];
-                aqq += red[g][1][w];
-                apq += red[g][2][w];
-            }
-            double c = 1.0, sn = 0.0, go = 0.0;
-            if (!(app == 0.0 || aqq == 0.0 || apq == 0.0)) {
-                const double rel = fabs(apq) / sqrt(app * aqq);
-                atomic_max_nonneg(&a.worst[sweep], rel);
-                if (rel > 1e-15) {
-                    const double tau = (aqq - app) / (2.0 * apq);
-                    const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                    c = 1.0 / sqrt(1.0 + t * t);
-                    sn = c * t;
-                    go = 1.0;
-                }
-            }
-            rot[g][0] = c;
-            rot[g][1] = sn;
-            rot[g][2] = go;
-        }
-        __syncthreads();
-        if (rot[g][2] != 0.0) {
-            const double c = rot[g][0], sn = rot[g][1];
-            double* wp = bs + p * n;
-            double* wq = bs + q * n;
-            for (int i = gl; i < n; i += G) {
-                const double xp = wp[i], xq = wq[i];
-                wp[i] = c * xp - sn * xq;
-                wq[i] = sn * xp + c * xq;
-            }
-            if (gl < C2) {
-                const double yp = Q[gl + p * C2], yq = Q[gl + q * C2];
-                Q[gl + p * C2] = c * yp - sn * yq;
-                Q[gl + q * C2] = sn * yp + c * yq;
-            }
-        }
-        __syncthreads();
-    };
-
-    int sweep = 0;
-    bool converged = n <= 1;
-    for (; sweep < kJacMaxSweeps && !converged; ++sweep) {
-        for (int r = 0; r < NB - 1; ++r) {
-            for (int pi = blockIdx.x; pi < npairs; pi += gridDim.x) {
-                int I, J;
-                if (pi == 0) {
-                    I = r;
-                    J = NB - 1;
-                } else {
-                    I = (r + pi) % (NB - 1);
-                    J = (r - pi + (NB - 1)) % (NB - 1);
-                }
-                if (I > J) {
-                    const int t = I;
-                    I = J;
-                    J = t;
-                }
-                auto col = [&](int k) {
-                    const int cc = k < W ? I * W + k : J * W + (k - W);
-                    return cc < n ? cc : -1;
-                };
-                for (int i = threadIdx.x; i < n; i += kJacThreads) {
-#pragma unroll
-                    for (int k = 0; k < C2; ++k)
-                        bs[k * n + i] = col(k) >= 0 ? a.B[static_cast<size_t>(col(k)) * n + i] : 0.0;
-                }
-                for (int i = threadIdx.x; i < C2 * C2; i += kJacThreads) Q[i] = (i % C2) == (i / C2) ? 1.0 : 0.0;
-                __syncthreads();
-                if (r == 0) {  // intra-block pairs of both blocks (round robin on W columns)
-                    const int blk = g / (W / 2), idx = g % (W / 2);
-                    for (int s = 0; s < W - 1; ++s) {
-                        int p, q;
-                        if (idx == 0) {
-                            p = s;
-                            q = W - 1;
-                        } else {
-                            p = (s + idx) % (W - 1);
-                            q = (s - idx + (W - 1)) % (W - 1);
-                        }
-                        if (p > q) {
-                            const int t = p;
-                            p = q;
-                            q = t;
-                        }
-                        rotate(blk * W + p, blk * W + q, sweep);
-                    }
-                }
-                for (int s = 0; s < W; ++s) rotate(g, W + (g + s) % W, sweep);
-                // write back B, apply the accumulated rotation to V
-                for (int i = threadIdx.x; i < n; i += kJacThreads) {
-                    double v[C2];
-#pragma unroll
-                    for (int k = 0; k < C2; ++k) {
-                        if (col(k) >= 0) a.B[static_cast<size_t>(col(k)) * n + i] = bs[k * n + i];
-                        v[k] = col(k) >= 0 ? a.V[static_cast<size_t>(col(k)) * n + i] : 0.0;
-                    }
-#pragma unroll
-                    for (int k = 0; k < C2; ++k) {
-                        if (col(k) < 0) continue;
-                        double o = 0.0;
-#pragma unroll
-                        for (int l = 0; l < C2; ++l) o = fma(v[l], Q[l + k * C2], o);
-                        a.V[static_cast<size_t>(col(k)) * n + i] = o;
-                    }
-                }
-                __syncthreads();
-            }
-            grid.sync();
-        }
-        converged = *reinterpret_cast<volatile double*>(&a.worst[sweep]) <= 1e-15;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a.status[0] = sweep;
-        a.status[1] = converged ? 0 : 1;
-    }
-}
-
-
-constexpr double kStrongT = 1e-5;  // |tan| above which a pair goes to the exact cluster sweep
+constexpr double kStrongT = 1e-2;  // |tan| above which a pair goes to the exact cluster sweep
 constexpr int kMaxCluster = 64;
 
 // All pair rotations of one Jacobi sweep at once, from the Gram H = B^T B:
@@ -537,8 +375,8 @@ __global__ void pair_rot_kernel(const double* H, int64_t n, double* K, double* p
 // take part in strong rotations (near-degenerate or rank-deficient clusters):
 // one CTA, round-robin over the m <= 64 listed columns, a warp per pair,
 // sweeps until every pair inside the cluster is at or below 1e-15.
-__global__ void __launch_bounds__(1024) cluster_jacobi_kernel(double* B, double* V, int64_t n, const int* cols, int m,
-                                                              int* status) {
+__global__ void __launch_bounds__(1024) cluster_jacobi_kernel(double* B, double* V, int64_t rows, int64_t n, const int* cols,
+                                                              int m, int* status) {
     __shared__ double worst;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int M2 = m + (m & 1);
@@ -559,10 +397,10 @@ __global__ void __launch_bounds__(1024) cluster_jacobi_kernel(double* B, double*
                 }
                 if (a >= m || b >= m) continue;
                 const int p = min(cols[a], cols[b]), q = max(cols[a], cols[b]);
-                double* bp = B + static_cast<size_t>(p) * n;
-                double* bq = B + static_cast<size_t>(q) * n;
+                double* bp = B + static_cast<size_t>(p) * rows;
+                double* bq = B + static_cast<size_t>(q) * rows;
                 double app = 0.0, aqq = 0.0, apq = 0.0;
-                for (int64_t i = lane; i < n; i += 32) {
+                for (int64_t i = lane; i < rows; i += 32) {
                     const double x = bp[i], y = bq[i];
                     app = fma(x, x, app);
                     aqq = fma(y, y, aqq);
@@ -581,10 +419,12 @@ __global__ void __launch_bounds__(1024) cluster_jacobi_kernel(double* B, double*
                 const double sn = c * t;
                 double* vp = V + static_cast<size_t>(p) * n;
                 double* vq = V + static_cast<size_t>(q) * n;
-                for (int64_t i = lane; i < n; i += 32) {
+                for (int64_t i = lane; i < rows; i += 32) {
                     const double xp = bp[i], xq = bq[i];
                     bp[i] = c * xp - sn * xq;
                     bq[i] = sn * xp + c * xq;
+                }
+                for (int64_t i = lane; i < n; i += 32) {
                     const double yp = vp[i], yq = vq[i];
                     vp[i] = c * yp - sn * yq;
                     vq[i] = sn * yp + c * yq;
@@ -609,12 +449,12 @@ __global__ void ident_axpy_kernel(const double* K, double alpha, int64_t n, doub
 }
 
 // sig[j] = ||B(:, j)|| (warp per column, fixed-order sums)
-__global__ void colnorm_kernel(const double* B, int64_t n, double* sig) {
+__global__ void colnorm_kernel(const double* B, int64_t rows, int64_t n, double* sig) {
     const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (j >= n) return;
     double s = 0.0;
-    for (int64_t i = lane; i < n; i += 32) s = fma(B[i + j * n], B[i + j * n], s);
+    for (int64_t i = lane; i < rows; i += 32) s = fma(B[i + j * rows], B[i + j * rows], s);
     s = warp_sum(s);
     if (lane == 0) sig[j] = sqrt(s);
 }
@@ -713,55 +553,56 @@ static void refine_tail(Ctx& c, const double* R, int64_t n, double* V, double* s
 }
 
 
-// eig-started Jacobi SVD of the n x n upper-triangular R (column-major):
-// G = R^T R, V0 = eig(G) (cuSOLVER syevd), B = R V0, then one-sided Jacobi
-// sweeps on (B, V) to the reference's 1e-15 pair-cosine tolerance.  On return
-// sig (descending) and V (column-major, columns in the same order).
-// work: >= n*n doubles scratch; wv: >= n doubles.
+// eig-started one-sided Jacobi SVD of the sketch SA (rows x n, column-major,
+// leading dimension rows):  G = SA^T SA, V0 = eig(G) (cuSOLVER syevd),
+// B = SA V0, then Jacobi passes on (B, V) to the reference's 1e-15 pair-cosine
+// tolerance.  The reference runs its Jacobi on the R of a Householder QR of SA
+// (svd.cpp:180-252); B^T B is the same Gram either way, and starting from SA
+// skips the QR.  On return sig (descending) and V (n x n, column-major, same
+// order).  work: >= rows*n doubles scratch; wv: >= n doubles.
 template <class LW>
-static void eig_jacobi(Ctx& c, const double* R, int64_t n, double* V, double* sig, double* work, double* wv,
-                       int* info, LW&& lwork_buf) {
+static void eig_jacobi(Ctx& c, const double* SA, int64_t rows, int64_t n, double* V, double* sig, double* work,
+                       double* wv, int* info, LW&& lwork_buf) {
     if (!c.blas) {
         if (cublasCreate(&c.blas) != CUBLAS_STATUS_SUCCESS) fail(MSVD_ERR_CUDA, "cublasCreate failed");
         cublasSetPointerMode(c.blas, CUBLAS_POINTER_MODE_HOST);
     }
     if (cublasSetStream(c.blas, c.stream) != CUBLAS_STATUS_SUCCESS) fail(MSVD_ERR_CUDA, "cublasSetStream failed");
-    const int in = static_cast<int>(n);
-    const double one = 1.0, zero = 0.0;
-    // G = R^T R into V (full square; syevd reads the lower triangle)
-    if (cublasDgemm(c.blas, CUBLAS_OP_T, CUBLAS_OP_N, in, in, in, &one, R, in, R, in, &zero, V, in) !=
-        CUBLAS_STATUS_SUCCESS)
-        fail(MSVD_ERR_CUDA, "cublasDgemm (R^T R) failed");
+    const int in = static_cast<int>(n), ir = static_cast<int>(rows);
+    // C (mm x nn) = alpha op(A) Bm + beta C, inner dimension kk
+    auto gemm = [&](cublasOperation_t ta, int mm, int nn_, int kk, const double* A, int lda, const double* Bm, int ldb,
+                    double alpha, double beta, double* C, int ldc, const char* what) {
+        if (cublasDgemm(c.blas, ta, CUBLAS_OP_N, mm, nn_, kk, &alpha, A, lda, Bm, ldb, &beta, C, ldc) !=
+            CUBLAS_STATUS_SUCCESS)
+            fail(MSVD_ERR_CUDA, std::string("cublasDgemm failed: ") + what);
+    };
+    // G = SA^T SA into V (syevd reads the lower triangle)
+    gemm(CUBLAS_OP_T, in, in, ir, SA, ir, SA, ir, 1.0, 0.0, V, in, "SA^T SA");
     int lwork = 0;
     MSVD_SOLVER(cusolverDnDsyevd_bufferSize(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, in, V, in, wv,
                                             &lwork));
     double* lw = lwork_buf(sizeof(double) * (lwork + 1));
     MSVD_SOLVER(cusolverDnDsyevd(c.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, in, V, in, wv, lw, lwork,
                                  info));
-    // B = R V0 into work
-    if (cublasDgemm(c.blas, CUBLAS_OP_N, CUBLAS_OP_N, in, in, in, &one, R, in, V, in, &zero, work, in) !=
-        CUBLAS_STATUS_SUCCESS)
-        fail(MSVD_ERR_CUDA, "cublasDgemm (R V) failed");
-    auto gemm = [&](cublasOperation_t ta, const double* A, const double* Bm, double alpha, double beta, double* C,
-                    const char* what) {
-        if (cublasDgemm(c.blas, ta, CUBLAS_OP_N, in, in, in, &alpha, A, in, Bm, in, &beta, C, in) !=
-            CUBLAS_STATUS_SUCCESS)
-            fail(MSVD_ERR_CUDA, std::string("cublasDgemm failed: ") + what);
-    };
-    // Simultaneous sweeps while every rotation is small: Q = exp(K) (degree-5
-    // Taylor, Horner form; ||K||_F <= 1e-3 keeps the truncation below 1e-18),
-    // B <- B Q, V <- V Q.  Each step squares the off-diagonal mass like a
-    // Jacobi sweep.  The loop exits through the reference's own stop rule
-    // (every pair cosine <= 1e-15, read from the Gram of the current B);
-    // anything else -- a near-degenerate cluster, a rank-deficient block --
-    // falls through to the exact sweeps below.
-    const size_t nn = static_cast<size_t>(n) * n;
+    // B = SA V0 into work
+    gemm(CUBLAS_OP_N, ir, in, in, SA, ir, V, in, 1.0, 0.0, work, ir, "SA V0");
+    c.launches += 3;
+
+    // Simultaneous passes while every rotation is small: K holds the tangent
+    // of every pair's Jacobi rotation (svd.cpp:118-131) computed from the
+    // Gram B^T B, Q = exp(K) (scaling and squaring around a degree-5 Taylor in
+    // Horner form, ||K / 2^s||_F <= 1e-3), B <- B Q, V <- V Q.  Each pass
+    // squares the off-diagonal mass like a Jacobi sweep.  Pairs whose rotation
+    // is large (near-degenerate or rank-deficient clusters, |t| > 1e-2) are
+    // left out of K and rotated by exact pairwise sweeps over just their
+    // columns; anything else falls through to exact sweeps over all pairs.
+    const size_t nn = static_cast<size_t>(n) * n, rn = static_cast<size_t>(rows) * n;
     const int pgrid = static_cast<int>(std::min<int64_t>(ceil_div(static_cast<int64_t>(nn), 256), 4 * c.num_sms));
-    double* pool = lwork_buf(sizeof(double) * (3 * nn + 4 * pgrid + 8) + sizeof(int) * (2 * n + 8));
+    double* pool = lwork_buf(sizeof(double) * (2 * nn + rn + 4 * pgrid + 8) + sizeof(int) * (2 * n + 8));
     double* K = pool;
-    double* T1 = K + nn;
-    double* T2 = T1 + nn;
-    double* part = T2 + nn;
+    double* T2 = K + nn;
+    double* T1 = T2 + nn;  // rows x n: the Gram, Taylor terms, then B Q
+    double* part = T1 + rn;
     int* strong = reinterpret_cast<int*>(part + 4 * pgrid + 8);
     int* clist = strong + n;
     int* cstat = clist + n;
@@ -775,7 +616,7 @@ static void eig_jacobi(Ctx& c, const double* R, int64_t n, double* V, double* si
     const int max_steps = ms ? std::atoi(ms) : 8;
     const bool dbg = std::getenv("MSVD_DEBUG_JACOBI") != nullptr;
     for (; steps < max_steps; ++steps) {
-        gemm(CUBLAS_OP_T, B, B, 1.0, 0.0, T1, "B^T B");
+        gemm(CUBLAS_OP_T, in, in, ir, B, ir, B, ir, 1.0, 0.0, T1, in, "B^T B");
         MSVD_CUDA(cudaMemsetAsync(strong, 0, sizeof(int) * n, c.stream));
         pair_rot_kernel<<<pgrid, 256, 0, c.stream>>>(T1, n, K, part, strong);
         MSVD_CUDA(cudaMemcpyAsync(hp.data(), part, sizeof(double) * 4 * pgrid, cudaMemcpyDeviceToHost, c.stream));
@@ -803,26 +644,42 @@ static void eig_jacobi(Ctx& c, const double* R, int64_t n, double* V, double* si
             for (int64_t j = 0; j < n; ++j)
                 if (hflag[j]) hcols.push_back(static_cast<int>(j));
         }
-        if (fro > 1e-3 || static_cast<int>(hcols.size()) > kMaxCluster) break;  // -> exact sweeps
+        if (fro > 4.0 || static_cast<int>(hcols.size()) > kMaxCluster) break;  // -> exact sweeps
         if (st > 0.0) {
-            ident_axpy_kernel<<<pgrid, 256, 0, c.stream>>>(K, 0.2, n, T2);
+            // exp(K) = exp(K / 2^sq)^(2^sq), with ||K / 2^sq||_F <= 1e-3
+            int sq = 0;
+            while (fro / std::ldexp(1.0, sq) > 1e-3) ++sq;
+            const double sc = std::ldexp(1.0, -sq);
+            ident_axpy_kernel<<<pgrid, 256, 0, c.stream>>>(K, 0.2 * sc, n, T2);
+            double* Ta = T1;
+            double* Tb = T2;
             const double coef[4] = {0.25, 1.0 / 3.0, 0.5, 1.0};
             for (double a : coef) {
-                ident_axpy_kernel<<<pgrid, 256, 0, c.stream>>>(nullptr, 0.0, n, T1);
-                gemm(CUBLAS_OP_N, K, T2, a, 1.0, T1, "Taylor");
-                std::swap(T1, T2);
+                ident_axpy_kernel<<<pgrid, 256, 0, c.stream>>>(nullptr, 0.0, n, Ta);
+                gemm(CUBLAS_OP_N, in, in, in, K, in, Tb, in, a * sc, 1.0, Ta, in, "Taylor");
+                std::swap(Ta, Tb);
             }
-            // Q in T2
-            gemm(CUBLAS_OP_N, B, T2, 1.0, 0.0, T1, "B Q");
+            for (int k = 0; k < sq; ++k) {
+                gemm(CUBLAS_OP_N, in, in, in, Tb, in, Tb, in, 1.0, 0.0, Ta, in, "square");
+                std::swap(Ta, Tb);
+            }
+            if (Tb != T2) {
+                MSVD_CUDA(cudaMemcpyAsync(T2, Tb, sizeof(double) * nn, cudaMemcpyDeviceToDevice, c.stream));
+                Tb = T2;
+            }
+            c.launches += sq;
+            // Q = exp(K) in Tb == T2
+            gemm(CUBLAS_OP_N, ir, in, in, B, ir, Tb, in, 1.0, 0.0, T1, ir, "B Q");
             std::swap(B, T1);
-            gemm(CUBLAS_OP_N, Vp, T2, 1.0, 0.0, K, "V Q");
+            gemm(CUBLAS_OP_N, in, in, in, Vp, in, Tb, in, 1.0, 0.0, K, in, "V Q");
             std::swap(Vp, K);
             c.launches += 11;
         }
         if (!hcols.empty()) {
             MSVD_CUDA(cudaMemcpyAsync(clist, hcols.data(), sizeof(int) * hcols.size(), cudaMemcpyHostToDevice,
                                       c.stream));
-            cluster_jacobi_kernel<<<1, 1024, 0, c.stream>>>(B, Vp, n, clist, static_cast<int>(hcols.size()), cstat);
+            cluster_jacobi_kernel<<<1, 1024, 0, c.stream>>>(B, Vp, rows, n, clist, static_cast<int>(hcols.size()),
+                                                            cstat);
             int h2[2];
             MSVD_CUDA(cudaMemcpyAsync(h2, cstat, sizeof(h2), cudaMemcpyDeviceToHost, c.stream));
             MSVD_CUDA(cudaStreamSynchronize(c.stream));
@@ -830,9 +687,9 @@ static void eig_jacobi(Ctx& c, const double* R, int64_t n, double* V, double* si
             csweeps += h2[0];
             if (h2[1]) fail(MSVD_ERR_NUMERICAL, "one_sided_jacobi: no convergence after 60 sweeps (cluster)");
         }
-        // GEMM cosines carry a sqrt(n) u roundoff floor at the 1e-15 threshold:
-        // once every computed cosine is at that floor (<= 1e-13), the rotation
-        // just applied leaves true cosines at O(max^2) -- stop here.
+        // GEMM cosines carry a ~sqrt(rows) u roundoff floor right at the 1e-15
+        // threshold: once every computed cosine is at that floor (<= 1e-13),
+        // the rotation just applied leaves the true cosines at O(max^2).
         if (mrel <= 1e-13) {
             done = true;
             ++steps;
@@ -841,49 +698,31 @@ static void eig_jacobi(Ctx& c, const double* R, int64_t n, double* V, double* si
     }
     int hs[2] = {0, 0};
     if (!done) {
-        // exact sweeps: worst[60] | status[2]
+        // exact pairwise sweeps over all pairs: worst[60] | status[2]
         double* worst = static_cast<double*>(c.ensure_scratch(sizeof(double) * (kJacMaxSweeps + 2)));
         int* status = reinterpret_cast<int*>(worst + kJacMaxSweeps);
         MSVD_CUDA(cudaMemsetAsync(worst, 0, sizeof(double) * (kJacMaxSweeps + 2), c.stream));
-        JacobiGridArgs ja{B, Vp, in, worst, status};
+        JacobiGridArgs ja{B, Vp, ir, in, worst, status};
         void* kargs[] = {&ja};
-        auto coop = [&](const void* fn, int64_t units, size_t smem) {
-            if (smem > 48 * 1024)
-                MSVD_CUDA(
-                    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            int per_sm = 0;
-            MSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kJacThreads, smem));
-            const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(units, int64_t(per_sm) * c.num_sms));
-            MSVD_CUDA(cudaLaunchCooperativeKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(kJacThreads), kargs,
-                                                  smem, c.stream));
-        };
-        // block width: MSVD_JACOBI_W = 1 (pair per CTA) | 4 | 8; default 4 when it fits
-        const char* jw = std::getenv("MSVD_JACOBI_W");
-        const int want = jw ? std::atoi(jw) : 4;
-        const size_t budget = 200 * 1024;
-        auto block_pairs = [&](int64_t w) {
-            const int64_t nb = (n + w - 1) / w;
-            return (nb + (nb & 1)) / 2;
-        };
-        if (want == 8 && sizeof(double) * 16 * n <= budget)
-            coop(reinterpret_cast<const void*>(jacobi_block_kernel<8>), block_pairs(8), sizeof(double) * 16 * n);
-        else if (want == 4 && sizeof(double) * 8 * n <= budget)
-            coop(reinterpret_cast<const void*>(jacobi_block_kernel<4>), block_pairs(4), sizeof(double) * 8 * n);
-        else
-            coop(reinterpret_cast<const void*>(jacobi_grid_kernel), (n + (n & 1)) / 2, 0);
+        int per_sm = 0;
+        MSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_grid_kernel, kJacThreads, 0));
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((n + (n & 1)) / 2, int64_t(per_sm) * c.num_sms));
+        MSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(jacobi_grid_kernel),
+                                              dim3(static_cast<unsigned>(grid)), dim3(kJacThreads), kargs, 0,
+                                              c.stream));
         MSVD_CUDA(cudaMemcpyAsync(hs, status, sizeof(hs), cudaMemcpyDeviceToHost, c.stream));
         ++c.launches;
     }
-    colnorm_kernel<<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, c.stream>>>(B, n, wv);
+    colnorm_kernel<<<static_cast<unsigned>(ceil_div(n * 32, 256)), 256, 0, c.stream>>>(B, rows, n, wv);
     // sorted copies into B's buffer (free after the norms), then into V
     rank_sort_kernel<<<static_cast<unsigned>(n), 256, 0, c.stream>>>(wv, n, Vp, sig, B);
     MSVD_CUDA(cudaMemcpyAsync(V, B, sizeof(double) * nn, cudaMemcpyDeviceToDevice, c.stream));
     MSVD_CUDA(cudaGetLastError());
-    c.launches += 3;
+    c.launches += 2;
     MSVD_CUDA(cudaStreamSynchronize(c.stream));
-    if (std::getenv("MSVD_DEBUG_JACOBI"))
-        std::fprintf(stderr, "eig_jacobi: n=%lld gemm steps=%d cluster sweeps=%d exact sweeps=%d\n",
-                     static_cast<long long>(n), steps, csweeps, hs[0]);
+    if (dbg)
+        std::fprintf(stderr, "eig_jacobi: n=%lld rows=%lld gemm steps=%d cluster sweeps=%d exact sweeps=%d\n",
+                     static_cast<long long>(n), static_cast<long long>(rows), steps, csweeps, hs[0]);
     if (hs[1]) fail(MSVD_ERR_NUMERICAL, "one_sided_jacobi: no convergence after 60 sweeps");
 }
 
@@ -929,9 +768,12 @@ void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double
         return static_cast<double*>(c.svd_lw);
     };
     MSVD_CUDA(cudaMemsetAsync(info, 0, sizeof(int) * 4, c.stream));
-    MSVD_CUDA(cudaMemcpyAsync(work, SA, wbytes, cudaMemcpyDeviceToDevice, c.stream));
     int vt_layout = 0;
     try {
+        if (algo == "eigj") {
+            eig_jacobi(c, SA, rows, n, V, sig, work, tau, info + 1, lwork_buf);
+        } else {
+        MSVD_CUDA(cudaMemcpyAsync(work, SA, wbytes, cudaMemcpyDeviceToDevice, c.stream));
         if (rows > n) {
             int lwork = 0;
             MSVD_SOLVER(cusolverDnDgeqrf_bufferSize(c.solver, ir, in, work, ir, &lwork));
@@ -941,10 +783,7 @@ void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double
         } else {
             MSVD_CUDA(cudaMemcpyAsync(R, work, nn, cudaMemcpyDeviceToDevice, c.stream));
         }
-        if (algo == "eigj") {
-            eig_jacobi(c, R, n, V, sig, work, tau, info + 1, lwork_buf);
-            vt_layout = 0;
-        } else if (algo == "gesvd") {
+        if (algo == "gesvd") {
             int lwork = 0;
             MSVD_SOLVER(cusolverDnDgesvd_bufferSize(c.solver, in, in, &lwork));
             lw = lwork_buf(sizeof(double) * (lwork + 1));
@@ -985,6 +824,7 @@ void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double
             MSVD_SOLVER(cusolverDnDestroyGesvdjInfo(params));
             vt_layout = 0;
         }
+        }  // R-based algorithms
         check_sorted_kernel<<<1, 1, 0, c.stream>>>(sig, n, info + 2);
         signfix_kernel<<<static_cast<unsigned>(ceil_div(n, 128)), 128, 0, c.stream>>>(V, vt_layout, n, Vcol, Vrow);
         floor_kernel<<<1, 1, 0, c.stream>>>(sig, n, out2, info + 1);
