@@ -1,3 +1,25 @@
+    # roofline of the dominant kernel -- the A*W pass, which in one-pass mode
+    # also forms A^T A W and folds the TSQR (every iteration), while the
+    # stand-alone Gram pass runs only at check iterations.  Algorithmic bytes
+    # per launch = 8 * m_local * n (A once; the skinny reads/writes are <0.5%).
+    g_ms, g_cnt = prof["gram"]
+    a_ms, a_cnt = prof["apply"]
+    bytes_launch = 8.0 * rows * cfg.n
+    peak, peak_kind = peaks()
+    achieved_gram = bytes_launch / (g_ms / g_cnt / 1e3) / 1e9 if g_cnt else None
+    achieved_apply = bytes_launch / (a_ms / a_cnt / 1e3) / 1e9 if a_cnt else None
+    dominant = "apply" if a_ms >= g_ms else "gram"
+    achieved = achieved_apply if dominant == "apply" else achieved_gram
+    kname = ("apply kernel (K3: A W; one-pass: + A^T A W and the fused TSQR)" if dominant == "apply"
+             else "gram_kernel (K2, A^T Y)")
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(cfg.name, {}).get(dominant + "_kernel")
+        except Exception:
+            traffic = None
+
 #!/usr/bin/env python
 """Benchmark of the B200 RLOBPCG hot path (BASELINE.json metric, config C2).
 
@@ -5,8 +27,9 @@ Metric: time-to-solution (s) of rlobpcg_single on the headline configuration
 (m = 1e6, n = 1e3 fp64, b = 1, d = 4n, tol 1e-12, tolerance-only stop, solver
 seed 7) with A resident in HBM; one step = one complete solve (sketch, sketch
 SVD, init, all LOBPCG iterations).  Also reported: the A-stream GB/s per
-iteration, the roofline of the dominant kernel (the K2 Gram pass) measured
-live with CUDA events on the library's stream, and an end-to-end number
+iteration, the roofline of the dominant kernel (the A*W pass, which in
+one-pass mode also forms A^T A W) measured live with CUDA events on the
+library's stream, and an end-to-end number
 through the public host-buffer entry point (msvd_solve_host, pinned A copied
 in every step).
 
@@ -279,8 +302,11 @@ def ours(args, cfg):
     ms = t.item()
     ms_step = ms / args.steps
     it = int(np.median(iters))
-    a_bytes_iter = 16.0 * m * cfg.n  # two passes over A per iteration (whole job)
-    a_gbs_iter = a_bytes_iter / (np.median(loop_ms) / it / 1e3) / 1e9 if it else None
+    # A-stream rate of the iteration loop: passes over A actually made in the
+    # loop (A*W every iteration; the Gram pass every iteration in two-pass
+    # mode, at check iterations in one-pass mode) x 8 m n bytes / loop time
+    loop_passes = (prof["apply"][1] + prof["gram"][1]) / max(1, args.steps) - 2  # minus the init pair
+    a_gbs_iter = loop_passes * 8.0 * m * cfg.n / (np.median(loop_ms) / 1e3) / 1e9 if it else None
 
     # roofline of the dominant kernel (K2 gram pass): algorithmic bytes per
     # launch = 8 * m_local * n (A once; skinny reads/writes are <0.5%)
@@ -306,13 +332,15 @@ def ours(args, cfg):
                    "parallelism": f"row-shard x{ws}", "iterations": it,
                    "l2": "inputs larger than L2 (A = %.1f GB per rank)" % (8.0 * rows * cfg.n / 1e9)},
         "a_stream_gbs_per_iter": a_gbs_iter,
+        "a_passes_per_iter": loop_passes / it if it else None,
         "breakdown_ms": {k: round(v, 3) for k, v in res.timings_ms.items()},
         "kernel_ms": {k: round(v[0] / max(1, args.steps), 3) for k, v in prof.items()},
-        "roofline": {"kernel": "gram_kernel (K2, A^T Y)", "bound": "hbm", "achieved": achieved,
+        "roofline": {"kernel": kname, "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "bytes_per_launch": bytes_launch,
-                     "apply_kernel_achieved": achieved_apply},
+                     "bytes_per_launch": bytes_launch, "launches": a_cnt if dominant == "apply" else g_cnt,
+                     "apply_kernel_achieved": achieved_apply, "gram_kernel_achieved": achieved_gram,
+                     "gram_launches": g_cnt},
         "clocks": clk,
         "gpu_launches": launches,
     }

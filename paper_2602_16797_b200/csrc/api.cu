@@ -243,7 +243,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     DevState* st;
     msvd_record_row* rows;
     double *rh, *th, *Vcol, *Vrow, *sig, *AVb[2], *AXb[2], *AW, *Vb[2], *Xb[2], *W, *Rres, *tmp, *Cm, *Gpart,
-        *Gout, *nrm, *Rparts, *Rall, *tv, *dinv, *cpart, *fresh;
+        *Gout, *nrm, *Rparts, *Rall, *tv, *dinv, *cpart, *fresh, *ZVb[2], *ZXb[2], *ZW;
     ar.add(&st, 1);
     ar.add(&rows, max_iter + 2);
     ar.add(&rh, max_iter + 2);
@@ -256,7 +256,10 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         ar.add(&AXb[i], ml * b);
         ar.add(&Vb[i], n * b);
         ar.add(&Xb[i], n * b);
+        ar.add(&ZVb[i], n * b);
+        ar.add(&ZXb[i], n * b);
     }
+    ar.add(&ZW, n * b);
     ar.add(&AW, ml * b);
     ar.add(&W, n * b);
     ar.add(&Rres, n * b);
@@ -394,6 +397,30 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     // A*W pass with the TSQR fused into it when the kernel supports it;
     // otherwise a separate TSQR pass over the trial block.  Per-rank R factors
     // are then gathered in rank order.
+    // fused TSQR only for b = 1 (k <= 3): measured, the fold's registers slow
+    // the wider A*W kernels more than a separate TSQR pass costs
+    const bool fuse = b == 1 && !std::getenv("MSVD_NO_FUSED_TSQR");
+    // One-pass mode: the A*W pass also forms A^T A W, and the n-side images
+    // Z = A^T A [V X W] are carried through the Rayleigh-Ritz recurrences next
+    // to V and X, so between checks the residual A^T A V' = Z C needs no
+    // second pass over A (the Gram apply).  Same products as the
+    // reference in exact arithmetic (solver.cpp:357-369 forms A^T (AT C) with
+    // AT C from the cached products; here (A^T AT) C from the cached images).
+    // Every check iteration (solver.cpp:439, the only place the stop rule
+    // reads the residual) still runs the reference's Gram pass, whose result
+    // also refreshes the image A^T A V'.  MSVD_ONE_PASS = 0 forces two passes.
+    bool one_pass = false;
+    {
+        const char* e = std::getenv("MSVD_ONE_PASS");
+        TsqrFuse probe{};
+        probe.k = 3 * b;
+        probe.Rparts = Rparts;
+        // the stagnation test also reads the residual 5 rows back
+        // (solver.cpp:190-200): that row must be a check row too
+        const bool rows_exact = !o.use_stagnation || 5 % o.check_every == 0;
+        one_pass = !(e && std::atoi(e) == 0) && o.check_every > 1 && rows_exact &&
+                   apply_gram_supported(c, geom, b, fuse ? &probe : nullptr);
+    }
     auto apply_tsqr = [&](Cols Tlead, int nlead, OutCols aw, Cols Tall, int k, int iter) -> std::pair<const double*, int> {
         TsqrFuse fz{};
         fz.T = Tlead;
@@ -403,13 +430,14 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         fz.iter = iter;
         (void)nlead;
         int np = nparts;
-        // fused only for b = 1 (k <= 3): measured, the fold's registers slow the
-        // wider A*W kernels more than a separate TSQR pass costs
-        const bool fuse = b == 1 && !std::getenv("MSVD_NO_FUSED_TSQR");
-        if (launch_apply(c, geom, W, b, aw, fuse ? &fz : nullptr)) {
+        if (launch_apply(c, geom, W, b, aw, fuse ? &fz : nullptr, one_pass ? Gpart : nullptr)) {
             np = geom.grid;
         } else {
             launch_tsqr(c, Tall, ml, k, Rparts, st, iter);
+        }
+        if (one_pass) {  // ZW = A^T A W summed over CTAs (and ranks)
+            launch_reduce_g(c, Gpart, geom.grid, n, b, W, st, 0, ZW, nrm, nblk);
+            if (ranks > 1) comm.allreduce_sum(ZW, static_cast<size_t>(n * b), c.stream);
         }
         if (ranks == 1) return {Rparts, np};
         comm.allgather(Rparts, Rall, static_cast<size_t>(np) * k * k, c.stream);
@@ -423,6 +451,12 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
             comm.allreduce_sum(Gout, static_cast<size_t>(n * b), c.stream);
             launch_reduce_g(c, Gout, 1, n, b, V, st, 1, Rres, nrm, nblk);
         }
+    };
+    // one-pass check iterations: G = A^T (AT C) from the gram pass, summed over
+    // CTAs and ranks, becomes the image A^T A V' carried forward
+    auto exact_images = [&](double* ZV) {
+        launch_reduce_g(c, Gpart, geom.grid, n, b, nullptr, st, 0, ZV, nrm, nblk);
+        if (ranks > 1) comm.allreduce_sum(ZV, static_cast<size_t>(n * b), c.stream);
     };
     ControlArgs ca{};
     ca.nblk = nblk;
@@ -479,11 +513,20 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         ra.theta_out = theta_dev;
         ra.st = st;
         ra.iter = -1;
+        if (one_pass) {
+            ra.Z = cols_n({{ZW, b}});
+            ra.ZVout = ZVb[0];
+        }
         launch_rr(c, ra);
         OutCols yo{};
         for (int j = 0; j < b; ++j) yo.p[j] = AVb[0] + static_cast<int64_t>(j) * ml;
         launch_gram(c, geom, cols_m({{AW, b}}), b, Cm, b, b, yo, false, Gpart);
-        residual(Vb[0]);
+        if (one_pass) {
+            exact_images(ZVb[0]);
+            launch_reduce_g(c, ZVb[0], 1, n, b, Vb[0], st, 1, Rres, nrm, nblk);
+        } else {
+            residual(Vb[0]);
+        }
         ca.V = Vb[0];
         ca.row = 0;
         ca.check = 0;
@@ -520,17 +563,36 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         ra.theta_out = theta_dev;
         ra.st = st;
         ra.iter = i;
+        if (one_pass) {
+            ra.Z = cols_n({{ZVb[cur], b}, {ZXb[cur], nx}, {ZW, b}});
+            ra.ZVout = ZVb[nxt];
+            ra.ZXout = ZXb[nxt];
+        }
         launch_rr(c, ra);
         OutCols yo{};
         for (int j = 0; j < b; ++j) {
             yo.p[j] = AVb[nxt] + static_cast<int64_t>(j) * ml;
             yo.p[b + j] = AXb[nxt] + static_cast<int64_t>(j) * ml;
         }
-        launch_gram(c, geom, Tm, k, Cm, 2 * b, b, yo, false, Gpart);
-        residual(Vb[nxt]);
+        const bool check_it = (i % o.check_every) == 0;
+        if (one_pass && !check_it) {
+            {
+                ProfScope prof(c, kProfReduce);  // m x k recurrence products: no pass over A
+                launch_tcombine(c, Tm, k, Cm, 2 * b, yo, ml);
+            }
+            launch_reduce_g(c, ZVb[nxt], 1, n, b, Vb[nxt], st, 1, Rres, nrm, nblk);
+        } else {
+            launch_gram(c, geom, Tm, k, Cm, 2 * b, b, yo, false, Gpart);
+            if (one_pass) {  // check iteration: the reference's residual, and a fresh A^T A V'
+                exact_images(ZVb[nxt]);
+                launch_reduce_g(c, ZVb[nxt], 1, n, b, Vb[nxt], st, 1, Rres, nrm, nblk);
+            } else {
+                residual(Vb[nxt]);
+            }
+        }
         ca.V = Vb[nxt];
         ca.row = i + 1;
-        ca.check = (i % o.check_every) == 0;
+        ca.check = check_it;
         launch_control(c, ca);
         last_row = i + 1;
         if (o.store_iterates) {

@@ -71,6 +71,10 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // named barrier among `nthreads` threads (id 1..15; 0 is __syncthreads)
+// order this thread's earlier generic shared-memory accesses before later
+// async-proxy (bulk copy) writes to the same buffer
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -96,8 +96,13 @@ StreamGeom make_geom(const Ctx& c, const double* A, int64_t m, int32_t n, int64_
 // also fold [T | Y] into per-CTA R factors (returns true if it did; the
 // caller then skips launch_tsqr)
 struct TsqrFuse;
+// gpart != nullptr (one-pass mode): the same pass also writes the per-CTA
+// partials [grid][b][n] of A^T (A W); only where apply_gram_supported()
 bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out,
-                  const TsqrFuse* fuse = nullptr);
+                  const TsqrFuse* fuse = nullptr, double* gpart = nullptr);
+bool apply_gram_supported(const Ctx& c, const StreamGeom& g, int b, const TsqrFuse* fuse);
+// out[j] = T Cm[:, j] for j < q (m-side recurrence products without A)
+void launch_tcombine(Ctx& c, Cols T, int k, const double* Cm, int q, OutCols out, int64_t m);
 // Gpart[grid][b][n]: A^T Y with Y = T C (gram mode, writes Y cols + extra cols)
 // or Y = T (direct mode, q == b, no writes)
 void launch_gram(Ctx& c, const StreamGeom& g, Cols T, int k, const double* Cm, int q, int b,
@@ -121,6 +126,9 @@ struct RRArgs {
     double* sig_out;     // optional k: all Ritz sigma (tests)
     double* Vfull_out;   // optional k x k sorted, sign-fixed V (tests)
     double* R_out;       // optional k x k merged R factor (tests / msvd_tsqr_r)
+    Cols Z;              // one-pass mode: n-side A^T A images of T ([ZV ZX ZW]), or Z.p[0] == nullptr
+    double* ZVout;       // n x b: A^T A V' = Z C
+    double* ZXout;       // n x b (mode 1): A^T A X' = Z mix
     DevState* st;
     int iter;
 };

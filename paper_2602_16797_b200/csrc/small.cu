@@ -359,21 +359,49 @@ __global__ void __launch_bounds__(512) rr_kernel(RRArgs a) {
         }
     }
     __syncthreads();
-    // 5. n-side products V' = T C, X' = T mix (dense.cpp:75-89 matmul)
-    for (int64_t i = threadIdx.x; i < a.n; i += blockDim.x) {
-        double t[KM];
+    // 5. n-side products V' = T C, X' = T mix (dense.cpp:75-89 matmul); in
+    //    one-pass mode the same combinations of the A^T A images Z
+    const bool zmode = a.Z.p[0] != nullptr;
+    for (int pass = 0; pass < (zmode ? 2 : 1); ++pass) {
+        const Cols& src = pass == 0 ? a.T : a.Z;
+        double* vo = pass == 0 ? a.Vout : a.ZVout;
+        double* xo = pass == 0 ? a.Xout : a.ZXout;
+        for (int64_t i = threadIdx.x; i < a.n; i += blockDim.x) {
+            double t[KM];
 #pragma unroll
-        for (int l = 0; l < KM; ++l) t[l] = l < k ? a.T.p[l][i] : 0.0;
-        for (int j = 0; j < b; ++j) {
-            double v = 0.0, xv = 0.0;
+            for (int l = 0; l < KM; ++l) t[l] = l < k ? src.p[l][i] : 0.0;
+            for (int j = 0; j < b; ++j) {
+                double v = 0.0, xv = 0.0;
 #pragma unroll
-            for (int l = 0; l < KM; ++l)
-                if (l < k) {
-                    v = fma(Vs[l + (lead + j) * KM], t[l], v);
-                    if (a.mode == 1) xv = fma(mix[l + j * KM], t[l], xv);
-                }
-            a.Vout[i + j * a.n] = v;
-            if (a.mode == 1) a.Xout[i + j * a.n] = xv;
+                for (int l = 0; l < KM; ++l)
+                    if (l < k) {
+                        v = fma(Vs[l + (lead + j) * KM], t[l], v);
+                        if (a.mode == 1) xv = fma(mix[l + j * KM], t[l], xv);
+                    }
+                vo[i + j * a.n] = v;
+                if (a.mode == 1) xo[i + j * a.n] = xv;
+            }
+        }
+    }
+}
+
+// m-side recurrence products without A: out[j][i] = sum_l T[l][i] Cm[l + j k]
+// (solver.cpp:421, :462 -- AV' = AT C, AX' = AT mix), one thread per row
+__global__ void tcombine_kernel(Cols T, int k, const double* Cm, int q, OutCols out, int64_t m) {
+    __shared__ double Cs[kMaxK * 2 * kMaxB];
+    for (int i = threadIdx.x; i < k * q; i += blockDim.x) Cs[i] = Cm[i];
+    __syncthreads();
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < m;
+         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double t[kMaxK];
+#pragma unroll
+        for (int l = 0; l < kMaxK; ++l) t[l] = l < k ? T.p[l][r] : 0.0;
+        for (int j = 0; j < q; ++j) {
+            double y = 0.0;
+#pragma unroll
+            for (int l = 0; l < kMaxK; ++l)
+                if (l < k) y = fma(Cs[l + j * k], t[l], y);
+            out.p[j][r] = y;
         }
     }
 }
@@ -790,6 +818,14 @@ void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st,
         case 16: smem_launch(tsqr_smem_kernel<16>, 16); break;
         default: smem_launch(tsqr_smem_kernel<24>, 24); break;
     }
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void launch_tcombine(Ctx& c, Cols T, int k, const double* Cm, int q, OutCols out, int64_t m) {
+    if (m == 0) return;
+    const int grid = static_cast<int>(std::min<int64_t>(ceil_div(m, 256), 8 * c.num_sms));
+    tcombine_kernel<<<grid, 256, 0, c.stream>>>(T, k, Cm, q, out, m);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
 }

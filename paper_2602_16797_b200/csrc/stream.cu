@@ -107,6 +107,7 @@ struct ApplyArgs {
     const double* W;  // n x b col-major
     OutCols out;      // b columns of length m
     TsqrFuse ts;      // ts.Rparts == nullptr: no fused TSQR
+    double* gpart;    // [grid][b][n] A_cta^T (A_cta W) partials (one-pass mode), or nullptr
 };
 
 // K3: Y = A W.  Warps 1..8 consume.  Each warp reduces its threads'
@@ -240,14 +241,28 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) 
 // the producer always has bytes in flight while each warp works on its chunk.
 constexpr int kRowsFused = 4;  // rows per chunk supported by the fused TSQR prefetch
 
-template <int B, int PL, int KM>
+//
+// GR: the same pass also accumulates A_cta^T (A_cta W) -- each lane re-reads
+// its columns of the row from shared memory once the row's dot products are
+// known -- so one sweep over A yields both A W and A^T A W (one-pass mode).
+template <int B, int PL, int KM, bool GR>
 __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const StreamGeom& g = a.g;
     // KM > 0: fused TSQR; per consumer warp an R factor and a 32-row tile
     constexpr size_t kTsqrBytes = KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM + 2 * kRowsFused * KM) : 0;
+    // GR: W lives in shared memory (pairs, column-major, npad = n rounded up
+    // to even) so the registers hold the A^T (A W) accumulators instead
+    const int npad = (g.n + 1) & ~1;
+    const size_t ws_bytes = GR ? sizeof(double) * npad * B : 0;
     unsigned char* extra;
-    Pipe p = carve(smem, g, kTsqrBytes, &extra);
+    Pipe p = carve(smem, g, kTsqrBytes + ws_bytes, &extra);
+    double* ws = reinterpret_cast<double*>(extra + kTsqrBytes);
+    if constexpr (GR)
+        for (int i = threadIdx.x; i < npad * B; i += blockDim.x) {
+            const int cc = i % npad, j = i / npad;
+            ws[i] = cc < g.n ? a.W[cc + static_cast<int64_t>(j) * g.n] : 0.0;
+        }
     int64_t r_begin, r_end;
     cta_rows(g.m, r_begin, r_end);
     if (threadIdx.x == 0) {
@@ -279,9 +294,14 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArg
     bool finite = true;
     const int n = g.n;
     const int npairs = (n + 1) >> 1;
-    double w[PL][2][B];
+    double w[GR ? 1 : PL][2][B];
+    double ga[GR ? PL : 1][2][B];
 #pragma unroll
-    for (int i = 0; i < PL; ++i) {
+    for (int i = 0; i < (GR ? PL : 1); ++i)
+#pragma unroll
+        for (int j = 0; j < B; ++j) ga[i][0][j] = ga[i][1][j] = 0.0;
+#pragma unroll
+    for (int i = 0; i < (GR ? 0 : PL); ++i) {
         const int c0 = 2 * (lane + 32 * i);
 #pragma unroll
         for (int j = 0; j < B; ++j) {
@@ -332,13 +352,37 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArg
                     const double xy = (2 * pi + 1 < n) ? x.y : 0.0;
 #pragma unroll
                     for (int j = 0; j < B; ++j) {
-                        acc[j] = fma(x.x, w[i][0][j], acc[j]);
-                        acc[j] = fma(xy, w[i][1][j], acc[j]);
+                        double w0, w1;
+                        if constexpr (GR) {
+                            const double2 wv = *reinterpret_cast<const double2*>(ws + j * npad + 2 * pi);
+                            w0 = wv.x;
+                            w1 = wv.y;
+                        } else {
+                            w0 = w[i][0][j];
+                            w1 = w[i][1][j];
+                        }
+                        acc[j] = fma(x.x, w0, acc[j]);
+                        acc[j] = fma(xy, w1, acc[j]);
                     }
                 }
             }
 #pragma unroll
             for (int j = 0; j < B; ++j) acc[j] = warp_sum(acc[j]);
+            if constexpr (GR) {
+#pragma unroll
+                for (int i = 0; i < PL; ++i) {
+                    const int pi = lane + 32 * i;
+                    if (pi < npairs) {
+                        const double2 x = *reinterpret_cast<const double2*>(row + 2 * pi);
+                        const double xy = (2 * pi + 1 < n) ? x.y : 0.0;
+#pragma unroll
+                        for (int j = 0; j < B; ++j) {
+                            ga[i][0][j] = fma(x.x, acc[j], ga[i][0][j]);
+                            ga[i][1][j] = fma(xy, acc[j], ga[i][1][j]);
+                        }
+                    }
+                }
+            }
             if (lane < B) {
                 double v = acc[0];
 #pragma unroll
@@ -404,6 +448,246 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArg
         for (int i = threadIdx.x - 32; i < k * k; i += kConsumers) {
             const int r = i % k, cc = i / k;
             out[i] = r <= cc ? R0[r + cc * KM] : 0.0;
+        }
+    }
+    if constexpr (GR) {
+        // 8 warp partials -> one CTA partial, fixed order, through the (now
+        // idle) stage ring: every chunk was consumed, so every bulk copy landed
+        named_sync(4, kConsumers);
+        double* red = reinterpret_cast<double*>(p.stage0);  // [8][B][n]
+#pragma unroll
+        for (int i = 0; i < PL; ++i) {
+            const int c0 = 2 * (lane + 32 * i);
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                if (c0 < n) red[(static_cast<size_t>(cw) * B + j) * n + c0] = ga[i][0][j];
+                if (c0 + 1 < n) red[(static_cast<size_t>(cw) * B + j) * n + c0 + 1] = ga[i][1][j];
+            }
+        }
+        named_sync(5, kConsumers);
+        double* gp = a.gpart + static_cast<size_t>(blockIdx.x) * B * n;
+        for (int i = threadIdx.x - 32; i < B * n; i += kConsumers) {
+            double sum = red[i];
+#pragma unroll
+            for (int q = 1; q < 8; ++q) sum += red[static_cast<size_t>(q) * B * n + i];
+            gp[i] = sum;
+        }
+    }
+}
+
+
+// Self-fed form of the narrow kernel (TMA only): no producer warp.  Chunk c
+// belongs to warp c % 8 and stage c % stages, and stages is a multiple of 8,
+// so each warp owns its stages outright: it consumes a stage and immediately
+// refills it with its own chunk c + stages.  Eight warps per CTA instead of
+// nine lifts the register cap from 168 to 255 -- room for W and, in one-pass
+// mode (GR), the A^T (A W) accumulators and the row values in registers.
+template <int B, int PL, int KM, bool GR>
+__global__ void __launch_bounds__(256, 1) apply_self_kernel(ApplyArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const StreamGeom& g = a.g;
+    constexpr size_t kTsqrBytes = KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM + 2 * kRowsFused * KM) : 0;
+    unsigned char* extra;
+    Pipe p = carve(smem, g, kTsqrBytes, &extra);
+    int64_t r_begin, r_end;
+    cta_rows(g.m, r_begin, r_end);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < g.stages; ++s) mbar_init(&p.full[s], 1);
+        mbar_fence_init();
+    }
+    if (KM > 0)
+        for (size_t i = threadIdx.x; i < kTsqrBytes / sizeof(double); i += blockDim.x)
+            reinterpret_cast<double*>(extra)[i] = 0.0;
+    __syncthreads();
+    const int cw = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int per_warp = g.stages / 8;
+    const int64_t nchunks = ceil_div(r_end - r_begin, g.rc);
+    const uint64_t pol = l2_evict_first_policy();
+    auto issue = [&](int64_t c, int s) {  // lane 0: chunk c into its stage s = c % stages
+        const int64_t r0 = r_begin + c * g.rc;
+        const int64_t rc = min(static_cast<int64_t>(g.rc), r_end - r0);
+        const uint32_t bytes = static_cast<uint32_t>(rc * g.ld * 8);
+        mbar_arrive_expect_tx(&p.full[s], bytes);
+        bulk_g2s(p.stage0 + s * p.stage_bytes, g.A + r0 * g.ld, bytes, &p.full[s], pol);
+    };
+    if (lane == 0)
+        for (int j = 0; j < per_warp; ++j) {
+            const int64_t c = cw + 8 * static_cast<int64_t>(j);
+            if (c < nchunks) issue(c, cw + 8 * j);
+        }
+    double* Rw = KM > 0 ? reinterpret_cast<double*>(extra) + cw * KM * KM : nullptr;
+    double* tile = KM > 0 ? reinterpret_cast<double*>(extra) + 8 * KM * KM + cw * 32 * KM : nullptr;
+    double* tbuf = KM > 0 ? reinterpret_cast<double*>(extra) + 8 * (KM * KM + 32 * KM) + cw * 2 * kRowsFused * KM
+                          : nullptr;
+    const int kt = KM > 0 ? a.ts.k - B : 0;
+    int ntile = 0;
+    bool finite = true;
+    const int n = g.n;
+    const int npairs = (n + 1) >> 1;
+    double w[PL][2][B];
+    double ga[GR ? PL : 1][2][B];
+#pragma unroll
+    for (int i = 0; i < PL; ++i) {
+        const int c0 = 2 * (lane + 32 * i);
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            w[i][0][j] = c0 < n ? a.W[c0 + static_cast<int64_t>(j) * n] : 0.0;
+            w[i][1][j] = c0 + 1 < n ? a.W[c0 + 1 + static_cast<int64_t>(j) * n] : 0.0;
+            if (GR) ga[GR ? i : 0][0][j] = ga[GR ? i : 0][1][j] = 0.0;
+        }
+    }
+    auto prefetch = [&](int64_t cc, int buf) {
+        if (KM > 0 && cc < nchunks && lane < kt) {
+            const int64_t rr0 = r_begin + cc * g.rc;
+            const int rcc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - rr0));
+            const double* src = a.ts.T.p[lane];
+            for (int r = 0; r < rcc; ++r) cp_async8(tbuf + (buf * kRowsFused + r) * KM + lane, src + rr0 + r);
+        }
+        cp_async_commit();
+    };
+    int tb = 0;
+    if (KM > 0) prefetch(cw, 0);
+    // column offsets clamped into the row: lanes past the last pair re-read
+    // it (their W entries are zero, and their A^T A W sums are never stored),
+    // so the row loop has no per-pair branches
+    int off[PL];
+    bool keepy[PL];
+#pragma unroll
+    for (int i = 0; i < PL; ++i) {
+        const int pi = min(lane + 32 * i, npairs - 1);
+        off[i] = 2 * pi;
+        keepy[i] = 2 * pi + 1 < n;
+    }
+    int s = cw;
+    uint32_t ph = 0;
+    for (int64_t c = cw; c < nchunks; c += 8) {
+        if (KM > 0) {
+            prefetch(c + 8, tb ^ 1);
+            cp_async_wait<1>();
+            __syncwarp();
+        }
+        mbar_wait(&p.full[s], ph);
+        const double* As = reinterpret_cast<const double*>(p.stage0 + s * p.stage_bytes);
+        const int64_t r0 = r_begin + c * g.rc;
+        const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
+        for (int r = 0; r < rc; ++r) {
+            double tv = 0.0;
+            if (KM > 0 && lane < kt) tv = tbuf[(tb * kRowsFused + r) * KM + lane];
+            const double* row = As + static_cast<int64_t>(r) * g.ld_s;
+            double acc[B];
+#pragma unroll
+            for (int j = 0; j < B; ++j) acc[j] = 0.0;
+            double2 xr[GR ? PL : 1];
+#pragma unroll
+            for (int i = 0; i < PL; ++i) {
+                double2 x = *reinterpret_cast<const double2*>(row + off[i]);
+                x.y = keepy[i] ? x.y : 0.0;  // odd n: the pad column is not A
+                if (GR) xr[GR ? i : 0] = x;
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                    acc[j] = fma(x.x, w[i][0][j], acc[j]);
+                    acc[j] = fma(x.y, w[i][1][j], acc[j]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < B; ++j) acc[j] = warp_sum(acc[j]);
+            if constexpr (GR) {
+#pragma unroll
+                for (int i = 0; i < PL; ++i)
+#pragma unroll
+                    for (int j = 0; j < B; ++j) {
+                        ga[i][0][j] = fma(xr[i].x, acc[j], ga[i][0][j]);
+                        ga[i][1][j] = fma(xr[i].y, acc[j], ga[i][1][j]);
+                    }
+            }
+            if (lane < B) {
+                double v = acc[0];
+#pragma unroll
+                for (int j = 1; j < B; ++j)
+                    if (lane == j) v = acc[j];
+                a.out.p[lane][r0 + r] = v;
+                if (KM > 0) tile[ntile * KM + kt + lane] = v;
+            }
+            if (KM > 0) {
+                if (lane < kt) tile[ntile * KM + lane] = tv;
+                if (++ntile == 32) {
+                    __syncwarp();
+                    double x[KM > 0 ? KM : 1];
+#pragma unroll
+                    for (int l = 0; l < (KM > 0 ? KM : 1); ++l) {
+                        x[l] = l < a.ts.k ? tile[lane * KM + l] : 0.0;
+                        finite = finite && isfinite(x[l]);
+                    }
+                    __syncwarp();
+                    if constexpr (KM > 0) fold_rows<KM>(Rw, x, a.ts.k);
+                    ntile = 0;
+                }
+            }
+        }
+        __syncwarp();
+        // refill the stage just consumed: every lane's reads of it have
+        // retired (their values fed the warp reductions above)
+        if (lane == 0 && c + g.stages < nchunks) issue(c + g.stages, s);
+        tb ^= 1;
+        s += 8;
+        if (s >= g.stages) {
+            s -= g.stages;
+            ph ^= 1;
+        }
+    }
+    if constexpr (KM > 0) {
+        cp_async_wait<0>();
+        __syncwarp();
+        if (ntile > 0) {
+            double x[KM];
+#pragma unroll
+            for (int l = 0; l < KM; ++l) {
+                x[l] = (lane < ntile && l < a.ts.k) ? tile[lane * KM + l] : 0.0;
+                finite = finite && isfinite(x[l]);
+            }
+            __syncwarp();
+            fold_rows<KM>(Rw, x, a.ts.k);
+        }
+        if (!__all_sync(kFull, finite) && lane == 0 && a.ts.st)
+            if (atomicCAS(&a.ts.st->err_code, 0, kErrNonfiniteAT) == 0) a.ts.st->err_iter = a.ts.iter;
+        __syncthreads();
+        double* R0 = reinterpret_cast<double*>(extra);
+#pragma unroll
+        for (int st = 1; st < 8; st <<= 1) {
+            if ((cw % (2 * st)) == 0) {
+                double x[KM];
+                rows_of<KM>(R0 + (cw + st) * KM * KM, a.ts.k, x);
+                fold_rows<KM>(Rw, x, a.ts.k);
+            }
+            __syncthreads();
+        }
+        const int k = a.ts.k;
+        double* out = a.ts.Rparts + static_cast<size_t>(blockIdx.x) * k * k;
+        for (int i = threadIdx.x; i < k * k; i += blockDim.x) {
+            const int r = i % k, cc = i / k;
+            out[i] = r <= cc ? R0[r + cc * KM] : 0.0;
+        }
+    }
+    if constexpr (GR) {
+        __syncthreads();  // every chunk consumed: the stage ring is free
+        double* red = reinterpret_cast<double*>(p.stage0);  // [8][B][n]
+#pragma unroll
+        for (int i = 0; i < PL; ++i) {
+            const int c0 = 2 * (lane + 32 * i);
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                if (c0 < n) red[(static_cast<size_t>(cw) * B + j) * n + c0] = ga[i][0][j];
+                if (c0 + 1 < n) red[(static_cast<size_t>(cw) * B + j) * n + c0 + 1] = ga[i][1][j];
+            }
+        }
+        __syncthreads();
+        double* gp = a.gpart + static_cast<size_t>(blockIdx.x) * B * n;
+        for (int i = threadIdx.x; i < B * n; i += blockDim.x) {
+            double sum = red[i];
+#pragma unroll
+            for (int q = 1; q < 8; ++q) sum += red[static_cast<size_t>(q) * B * n + i];
+            gp[i] = sum;
         }
     }
 }
@@ -607,17 +891,36 @@ size_t gram_smem(const StreamGeom& g, int B) {
     return bar_bytes(g.stages) + ((extra + 127) / 128) * 128 + g.stages * g.stage_bytes;
 }
 
-template <int B, int PL, int KM>
+template <int B, int PL, int KM, bool GR>
 void apply_rows_b(Ctx& c, const ApplyArgs& a) {
     static bool attr = false;
     if (!attr) {
-        MSVD_CUDA(cudaFuncSetAttribute(apply_rows_kernel<B, PL, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MSVD_CUDA(cudaFuncSetAttribute(apply_rows_kernel<B, PL, KM, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(c.smem_optin)));
         attr = true;
     }
-    const size_t tsqr = KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM + 2 * kRowsFused * KM) : 0;
+    // self-fed form: faster for the one-pass and wider blocks; the producer
+    // form stays ahead for the plain b = 1 pass (measured, C2)
+    const bool self = a.g.tma && !std::getenv("MSVD_APPLY_PRODUCER") && (GR || B > 1 || std::getenv("MSVD_APPLY_SELF"));
+    if (self) {
+        static bool attr2 = false;
+        if (!attr2) {
+            MSVD_CUDA(cudaFuncSetAttribute(apply_self_kernel<B, PL, KM, GR>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(c.smem_optin)));
+            attr2 = true;
+        }
+        const size_t tsqr = KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM + 2 * kRowsFused * KM) : 0;
+        const size_t sm = bar_bytes(a.g.stages) + ((tsqr + 127) / 128) * 128 + a.g.stages * a.g.stage_bytes;
+        apply_self_kernel<B, PL, KM, GR><<<a.g.grid, 256, sm, c.stream>>>(a);
+        MSVD_CUDA(cudaGetLastError());
+        ++c.launches;
+        return;
+    }
+    const size_t tsqr = (KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM + 2 * kRowsFused * KM) : 0) +
+                        (GR ? sizeof(double) * ((a.g.n + 1) & ~1) * B : 0);
     const size_t sm = bar_bytes(a.g.stages) + ((tsqr + 127) / 128) * 128 + a.g.stages * a.g.stage_bytes;
-    apply_rows_kernel<B, PL, KM><<<a.g.grid, 32 + kConsumers, sm, c.stream>>>(a);
+    apply_rows_kernel<B, PL, KM, GR><<<a.g.grid, 32 + kConsumers, sm, c.stream>>>(a);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
 }
@@ -625,38 +928,69 @@ void apply_rows_b(Ctx& c, const ApplyArgs& a) {
 // dispatch on the fused-TSQR width (KM = k rounded up to 4/8/16)
 template <int B, int PL>
 void apply_rows_km(Ctx& c, const ApplyArgs& a) {
-    if (!a.ts.Rparts) return apply_rows_b<B, PL, 0>(c, a);
-    if (a.ts.k <= 4) return apply_rows_b<B, PL, 4>(c, a);
-    if (a.ts.k <= 8) return apply_rows_b<B, PL, 8>(c, a);
-    return apply_rows_b<B, PL, 16>(c, a);
+    if (a.gpart) {  // one-pass mode (B * PL <= 16: registers); fused TSQR only in the k <= 4 form
+        if constexpr (B * PL <= 16) {
+            if (!a.ts.Rparts) return apply_rows_b<B, PL, 0, true>(c, a);
+            return apply_rows_b<B, PL, 4, true>(c, a);
+        } else {
+            fail(MSVD_ERR_INVALID, "msvd: one-pass A*W / A^T A W launch on an unsupported shape");
+        }
+    }
+    if (!a.ts.Rparts) return apply_rows_b<B, PL, 0, false>(c, a);
+    if (a.ts.k <= 4) return apply_rows_b<B, PL, 4, false>(c, a);
+    if (a.ts.k <= 8) return apply_rows_b<B, PL, 8, false>(c, a);
+    return apply_rows_b<B, PL, 16, false>(c, a);
 }
 
-// geometry of the narrow variant: ~8 KB stages, deep ring (<= 32 stages)
-StreamGeom rows_geom(StreamGeom g) {
+// shared memory the narrow kernels need besides the stage ring
+size_t rows_extra_bytes(const StreamGeom& g0, int b, const TsqrFuse* ts, bool gram) {
+    const int km = ts && ts->Rparts ? (ts->k <= 4 ? 4 : (ts->k <= 8 ? 8 : 16)) : 0;
+    const size_t tsqr = km ? sizeof(double) * 8 * (km * km + 32 * km + 2 * kRowsFused * km) : 0;
+    const size_t ws = gram && !(g0.tma && !std::getenv("MSVD_APPLY_PRODUCER")) ? sizeof(double) * ((g0.n + 1) & ~1) * b
+                                                                               : 0;  // (self-fed GR keeps W in registers)
+    return ((tsqr + ws + 127) / 128) * 128;
+}
+
+// geometry of the narrow variant: ~8 KB stages, as deep a ring as shared
+// memory allows (<= 4 stages per warp)
+StreamGeom rows_geom(const Ctx& c, StreamGeom g, size_t extra) {
     const int64_t row_bytes = static_cast<int64_t>(g.ld_s) * 8;
     const int64_t target = env_int("MSVD_ROWS_STAGE_KB", 8) * 1024;
-    const int64_t budget = env_int("MSVD_ROWS_BUDGET_KB", 168) * 1024;
     g.rc = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(target / row_bytes, 64)));
     g.stage_bytes = ((static_cast<size_t>(g.rc) * row_bytes + 127) / 128) * 128;
+    const int64_t avail = static_cast<int64_t>(c.smem_optin) - static_cast<int64_t>(extra) - 1024;
+    const int64_t budget = std::min<int64_t>(env_int("MSVD_ROWS_BUDGET_KB", 168) * 1024, avail);  // measured: 2 stages per warp
     // chunk c goes to warp c % 8 and stage c % stages: with stages a multiple
     // of 8 every stage is only ever consumed by one warp, in order, so a
     // warp can never run two mbarrier phases ahead of a stage (parity ABA)
-    const size_t per_warp = std::max<size_t>(2, std::min<size_t>(4, budget / (8 * g.stage_bytes)));
+    const int64_t per_warp = std::max<int64_t>(2, std::min<int64_t>(4, budget / (8 * static_cast<int64_t>(g.stage_bytes))));
     g.stages = static_cast<int32_t>(8 * per_warp);
     return g;
 }
 
+// can the narrow kernel take this launch (b, n, fused TSQR width, one-pass gram)?
+bool rows_ok(const Ctx& c, const StreamGeom& g0, int b, const TsqrFuse* ts, bool gram) {
+    if (std::getenv("MSVD_APPLY_TICKET")) return false;
+    const int npairs = (g0.n + 1) / 2;
+    const int pl = (npairs + 31) / 32;
+    const bool pl_ok = (b == 1 && pl <= 32) || (b == 2 && pl <= 16) || ((b == 3 || b == 4) && pl <= 8);
+    if (!pl_ok) return false;
+    if (ts && ts->Rparts && (ts->k > (gram ? 4 : 16) || ts->k < b)) return false;
+    const size_t extra = rows_extra_bytes(g0, b, ts, gram);
+    const StreamGeom g = rows_geom(c, g0, extra);
+    if (ts && ts->Rparts && g.rc > kRowsFused) return false;  // tiny n: separate TSQR pass
+    if (g.stages * g.stage_bytes + bar_bytes(g.stages) + extra > c.smem_optin) return false;
+    if (gram && sizeof(double) * 8 * b * g0.n > static_cast<size_t>(g.stages) * g.stage_bytes) return false;
+    return true;
+}
+
 // true if launched (the fused TSQR, when requested, was then done too)
 bool try_apply_rows(Ctx& c, const ApplyArgs& a0, int b) {
-    if (std::getenv("MSVD_APPLY_TICKET")) return false;
+    if (!rows_ok(c, a0.g, b, &a0.ts, a0.gpart != nullptr)) return false;
     const int npairs = (a0.g.n + 1) / 2;
     const int pl = (npairs + 31) / 32;
-    if (a0.ts.Rparts && (a0.ts.k > 16 || a0.ts.k < b)) return false;
     ApplyArgs a = a0;
-    a.g = rows_geom(a0.g);
-    if (a0.ts.Rparts && a.g.rc > kRowsFused) return false;  // tiny n: separate TSQR pass
-    const size_t tsqr = a0.ts.Rparts ? sizeof(double) * 8 * (16 * 16 + 32 * 16 + 2 * kRowsFused * 16) : 0;
-    if (a.g.stages * a.g.stage_bytes + bar_bytes(a.g.stages) + tsqr > c.smem_optin) return false;
+    a.g = rows_geom(c, a0.g, rows_extra_bytes(a0.g, b, &a0.ts, a0.gpart != nullptr));
     if (b == 1) {
         if (pl <= 4) return apply_rows_km<1, 4>(c, a), true;
         if (pl <= 8) return apply_rows_km<1, 8>(c, a), true;
@@ -726,14 +1060,25 @@ StreamGeom make_geom(const Ctx& c, const double* A, int64_t m, int32_t n, int64_
     return g;
 }
 
-bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out, const TsqrFuse* fuse) {
-    if (g.m == 0) return false;
+bool apply_gram_supported(const Ctx& c, const StreamGeom& g, int b, const TsqrFuse* fuse) {
+    const int pl = ((g.n + 1) / 2 + 31) / 32;
+    const int plt = pl <= 4 ? 4 : (pl <= 8 ? 8 : (pl <= 16 ? 16 : 32));  // the PL template the launch picks
+    return b * plt <= 16 && rows_ok(c, g, b, fuse, true);
+}
+
+bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out, const TsqrFuse* fuse,
+                  double* gpart) {
+    if (g.m == 0) {
+        if (gpart) MSVD_CUDA(cudaMemsetAsync(gpart, 0, sizeof(double) * g.grid * b * g.n, c.stream));
+        return false;
+    }
     ProfScope prof(c, kProfApply);
     TsqrFuse none{};
-    if (try_apply_rows(c, ApplyArgs{g, W, out, fuse ? *fuse : none}, b)) return fuse != nullptr;
+    if (try_apply_rows(c, ApplyArgs{g, W, out, fuse ? *fuse : none, gpart}, b)) return fuse != nullptr;
+    if (gpart) fail(MSVD_ERR_INVALID, "msvd: one-pass A*W / A^T A W launch on an unsupported shape");
     // ticket variant: large stages amortize the per-chunk cross-warp finish
     // (measured: 48 KB x 3 stages best at n = 2000, b = 5)
-    ApplyArgs a{cap_rows(rechunk(g, 48, 144), kRedSlots / std::max(1, b)), W, out, none};
+    ApplyArgs a{cap_rows(rechunk(g, 48, 144), kRedSlots / std::max(1, b)), W, out, none, nullptr};
     switch (b) {
         case 1: apply_b<1>(c, a); break;
         case 2: apply_b<2>(c, a); break;

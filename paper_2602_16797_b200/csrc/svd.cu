@@ -1,17 +1,18 @@
 // Randomized preconditioner factorization (precond.cpp:11-36).
 //
 // dense_svd(SA) in the reference is Householder QR (d x n -> n x n R) then
-// one-sided Jacobi on R (svd.cpp:99-150, :180-252).  Here geqrf (cuSOLVER)
-// reduces the tall sketch to R, and the default SVD ("eigj") is the same
-// one-sided Jacobi, started from the eigenvectors of R^T R (cuSOLVER syevd):
-// B = R V0 has nearly orthogonal columns, so the Jacobi sweeps converge in
-// one or two passes.  Those passes run as dense simultaneous rotations on the
+// one-sided Jacobi on R (svd.cpp:99-150, :180-252).  The default here
+// ("eigj") is the same one-sided Jacobi, run on SA itself (same Gram as R)
+// and started from the eigenvectors of SA^T SA (cuSOLVER syevd): B = SA V0 has
+// nearly orthogonal columns, so the Jacobi sweeps converge in one or two
+// passes.  Those passes run as dense simultaneous rotations on the
 // tensor cores (all pair tangents from the Gram B^T B, Q = exp(K), B <- B Q,
 // V <- V Q), with the reference's stop rule read from the Gram; pairs with
 // large rotations (near-degenerate or rank-deficient clusters) get exact
 // pairwise Jacobi sweeps, and anything else falls back to exact block sweeps
 // over all pairs.  MSVD_SVD = eigj | polar | gesvd | gesvdj | gesvdp selects
-// (polar: QDWH gesvdp + an inverse-iteration refinement of its tail).
+// (the others: geqrf to R, then cuSOLVER's SVD of R; polar = QDWH gesvdp + an
+// inverse-iteration refinement of its tail).
 // A small kernel then applies the reference's conventions: descending order,
 // each right vector signed so its largest-magnitude entry is positive
 // (svd.cpp:232-248), and the sqrt(n) u sigma_1 floor (precond.cpp:26-34).
@@ -47,22 +48,47 @@ __global__ void upper_copy_kernel(const double* W, int64_t ldw, int64_t n, doubl
 }
 
 // V given column-major (vt_layout 0) or as V^T column-major (1).  Produce
-// sign-fixed Vcol (column-major) and Vrow (row-major) copies.
+// sign-fixed Vcol (column-major) and Vrow (row-major) copies: each column
+// signed so its largest-magnitude entry (first one on ties) is positive
+// (svd.cpp:232-248).  One CTA per column.
 __global__ void signfix_kernel(const double* Vin, int vt_layout, int64_t n, double* Vcol, double* Vrow) {
-    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j >= n) return;
+    const int64_t j = blockIdx.x;
+    __shared__ double bv[32];
+    __shared__ int64_t bi[32];
     auto at = [&](int64_t i) { return vt_layout ? Vin[j + i * n] : Vin[i + j * n]; };
-    int64_t imax = 0;
     double amax = -1.0;
-    for (int64_t i = 0; i < n; ++i) {
+    int64_t imax = 0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const double a = fabs(at(i));
-        if (a > amax) {
+        if (a > amax) {  // ascending i per thread: keeps the first maximum
             amax = a;
             imax = i;
         }
     }
-    const double s = at(imax) < 0.0 ? -1.0 : 1.0;
-    for (int64_t i = 0; i < n; ++i) {
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, amax, o);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, imax, o);
+        if (ov > amax || (ov == amax && oi < imax)) {
+            amax = ov;
+            imax = oi;
+        }
+    }
+    const int warp = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        bv[warp] = amax;
+        bi[warp] = imax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+            if (bv[w] > bv[0] || (bv[w] == bv[0] && bi[w] < bi[0])) {
+                bv[0] = bv[w];
+                bi[0] = bi[w];
+            }
+    }
+    __syncthreads();
+    const double s = at(bi[0]) < 0.0 ? -1.0 : 1.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const double v = s * at(i);
         Vcol[i + j * n] = v;
         Vrow[j + i * n] = v;
@@ -84,13 +110,11 @@ __global__ void floor_kernel(double* sig, int64_t n, double* out2, int* info_fla
     out2[2] = static_cast<double>(*info_flag);
 }
 
-// defensive: enforce descending order (cuSOLVER returns sorted values; ties keep order)
+// defensive: enforce descending order (the SVDs return sorted values)
 __global__ void check_sorted_kernel(const double* sig, int64_t n, int* flag) {
-    for (int64_t j = 1; j < n; ++j)
-        if (sig[j] > sig[j - 1]) {
-            *flag = 1000 + static_cast<int>(j);
-            return;
-        }
+    for (int64_t j = 1 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+         j += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (sig[j] > sig[j - 1]) atomicCAS(flag, 0, 1000 + static_cast<int>(j));
 }
 
 // Triangular solves for the tail refinement (single CTA, p <= 32 right-hand
@@ -825,8 +849,8 @@ void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double
             vt_layout = 0;
         }
         }  // R-based algorithms
-        check_sorted_kernel<<<1, 1, 0, c.stream>>>(sig, n, info + 2);
-        signfix_kernel<<<static_cast<unsigned>(ceil_div(n, 128)), 128, 0, c.stream>>>(V, vt_layout, n, Vcol, Vrow);
+        check_sorted_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, c.stream>>>(sig, n, info + 2);
+        signfix_kernel<<<static_cast<unsigned>(n), 256, 0, c.stream>>>(V, vt_layout, n, Vcol, Vrow);
         floor_kernel<<<1, 1, 0, c.stream>>>(sig, n, out2, info + 1);
         MSVD_CUDA(cudaGetLastError());
         c.launches += 4;
