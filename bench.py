@@ -1,25 +1,3 @@
-    # roofline of the dominant kernel -- the A*W pass, which in one-pass mode
-    # also forms A^T A W and folds the TSQR (every iteration), while the
-    # stand-alone Gram pass runs only at check iterations.  Algorithmic bytes
-    # per launch = 8 * m_local * n (A once; the skinny reads/writes are <0.5%).
-    g_ms, g_cnt = prof["gram"]
-    a_ms, a_cnt = prof["apply"]
-    bytes_launch = 8.0 * rows * cfg.n
-    peak, peak_kind = peaks()
-    achieved_gram = bytes_launch / (g_ms / g_cnt / 1e3) / 1e9 if g_cnt else None
-    achieved_apply = bytes_launch / (a_ms / a_cnt / 1e3) / 1e9 if a_cnt else None
-    dominant = "apply" if a_ms >= g_ms else "gram"
-    achieved = achieved_apply if dominant == "apply" else achieved_gram
-    kname = ("apply kernel (K3: A W; one-pass: + A^T A W and the fused TSQR)" if dominant == "apply"
-             else "gram_kernel (K2, A^T Y)")
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(cfg.name, {}).get(dominant + "_kernel")
-        except Exception:
-            traffic = None
-
 #!/usr/bin/env python
 """Benchmark of the B200 RLOBPCG hot path (BASELINE.json metric, config C2).
 
@@ -308,21 +286,28 @@ def ours(args, cfg):
     loop_passes = (prof["apply"][1] + prof["gram"][1]) / max(1, args.steps) - 2  # minus the init pair
     a_gbs_iter = loop_passes * 8.0 * m * cfg.n / (np.median(loop_ms) / 1e3) / 1e9 if it else None
 
-    # roofline of the dominant kernel (K2 gram pass): algorithmic bytes per
-    # launch = 8 * m_local * n (A once; skinny reads/writes are <0.5%)
+    # roofline of the dominant kernel -- the A*W pass, which in one-pass mode
+    # also forms A^T A W and folds the TSQR (every iteration), while the
+    # stand-alone Gram pass runs only at check iterations.  Algorithmic bytes
+    # per launch = 8 * m_local * n (A once; the skinny reads/writes are <0.5%).
     g_ms, g_cnt = prof["gram"]
     a_ms, a_cnt = prof["apply"]
     bytes_launch = 8.0 * rows * cfg.n
     peak, peak_kind = peaks()
-    achieved = bytes_launch / (g_ms / g_cnt / 1e3) / 1e9 if g_cnt else None
+    achieved_gram = bytes_launch / (g_ms / g_cnt / 1e3) / 1e9 if g_cnt else None
     achieved_apply = bytes_launch / (a_ms / a_cnt / 1e3) / 1e9 if a_cnt else None
+    dominant = "apply" if a_ms >= g_ms else "gram"
+    achieved = achieved_apply if dominant == "apply" else achieved_gram
+    kname = ("apply kernel (K3: A W; one-pass: + A^T A W and the fused TSQR)" if dominant == "apply"
+             else "gram_kernel (K2, A^T Y)")
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(cfg.name, {}).get("gram_kernel")
+            traffic = json.load(open(tpath)).get(cfg.name, {}).get(dominant + "_kernel")
         except Exception:
             traffic = None
+
 
     line = {
         "metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,

@@ -38,7 +38,11 @@ def launches(path):
 
 
 def full(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # a .ncu-rep (read through ncu -i) or its `--page raw --csv` export
+    if path.endswith(".csv"):
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     ci = {h: i for i, h in enumerate(hdr)}
@@ -73,7 +77,7 @@ def main():
     tag, lpath, fpath = sys.argv[1:4]
     agg = launches(lpath)
     tot = sum(a[1] for a in agg.values())
-    lines = [f"# {tag}: per-kernel device time of one `python bench.py --steps 1 --warmup 1` process",
+    lines = [f"# {tag}: per-kernel device time of one `python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline` process",
              "# (ncu --metrics gpu__time_duration.sum --clock-control none; cold-cache, serialised:",
              "#  compare SHARES, not absolutes).  Includes input generation (torch/cuSOLVER QR) and",
              "#  the warm-up + timed solve.", f"# total {tot:.1f} ms", "",
@@ -88,7 +92,7 @@ def main():
     open(os.path.join(HERE, f"{tag}_launches.txt"), "w").write("\n".join(lines) + "\n")
 
     res = full(fpath)
-    lines = [f"# {tag}: ncu --set full --clock-control none on the C2 bench (m=1e6, n=1e3, b=1)", ""]
+    lines = [f"# {tag}: ncu --set full --clock-control none on the C2 bench (m=1e6, n=1e3, b=1), first launch of each", ""]
     traffic = {}
     for d in res:
         lines.append(d["kernel"])
@@ -100,9 +104,9 @@ def main():
             rb = to_bytes(d["dram__bytes_read.sum"])
             wb = to_bytes(d["dram__bytes_write.sum"])
             lines.append(f"    => DRAM traffic {(rb + wb) / 1e9:.4f} GB in {ms:.3f} ms = {(rb + wb) / ms / 1e6:.0f} GB/s")
-            if "gram_kernel" in d["kernel"]:
+            if "gram_kernel" in d["kernel"] and "gram_kernel" not in traffic:
                 traffic["gram_kernel"] = rb + wb
-            if "apply" in d["kernel"]:
+            if "apply" in d["kernel"] and "apply_kernel" not in traffic:
                 traffic["apply_kernel"] = rb + wb
         lines.append("")
     open(os.path.join(HERE, f"{tag}_full.txt"), "w").write("\n".join(lines) + "\n")
