@@ -91,7 +91,11 @@ def main():
         lines.append(f"{ms:10.3f} {100 * ms / ot:6.2f}% {cnt:8d}  {name[:110]}")
     open(os.path.join(HERE, f"{tag}_launches.txt"), "w").write("\n".join(lines) + "\n")
 
-    res = full(fpath)
+    res, seen = [], set()
+    for d in full(fpath):  # first launch of each kernel
+        if d["kernel"] not in seen:
+            seen.add(d["kernel"])
+            res.append(d)
     lines = [f"# {tag}: ncu --set full --clock-control none on the C2 bench (m=1e6, n=1e3, b=1), first launch of each", ""]
     traffic = {}
     for d in res:
