@@ -458,6 +458,14 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         launch_reduce_g(c, Gpart, geom.grid, n, b, nullptr, st, 0, ZV, nrm, nblk);
         if (ranks > 1) comm.allreduce_sum(ZV, static_cast<size_t>(n * b), c.stream);
     };
+    // gated checks (opt-in, MSVD_CHECK_GATE = 1; tolerance-only stop, one rank).
+    // Off by default: skipping the refresh of A^T A V' far from convergence
+    // moves where a run that sits at the roundoff floor happens to dip below
+    // tol (C5 shape: 91 iterations instead of the reference's 100).
+    const bool gate_checks = one_pass && !o.use_stagnation && ranks == 1 && std::getenv("MSVD_CHECK_GATE") &&
+                             std::atoi(std::getenv("MSVD_CHECK_GATE")) != 0;
+    const int* skip_flag = reinterpret_cast<const int*>(reinterpret_cast<unsigned char*>(st) +
+                                                         offsetof(DevState, skip_exact));
     ControlArgs ca{};
     ca.nblk = nblk;
     ca.nrm_part = nrm;
@@ -581,6 +589,21 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
                 launch_tcombine(c, Tm, k, Cm, 2 * b, yo, ml);
             }
             launch_reduce_g(c, ZVb[nxt], 1, n, b, Vb[nxt], st, 1, Rres, nrm, nblk);
+        } else if (one_pass && gate_checks) {
+            // check iteration, tolerance-only stop: the images' residual first;
+            // if it is more than 4x above the stop threshold the reference's
+            // test cannot pass (the two residuals agree far above the roundoff
+            // floor), and the Gram pass, the refresh and the exact residual
+            // all exit at once (device flag, no host round trip)
+            {
+                ProfScope prof(c, kProfReduce);
+                launch_tcombine(c, Tm, k, Cm, 2 * b, yo, ml);
+            }
+            launch_reduce_g(c, ZVb[nxt], 1, n, b, Vb[nxt], st, 1, Rres, nrm, nblk);
+            launch_gate(c, nrm, nblk, b, st, 4.0 * sigma1 * sigma1 * plan.tol);
+            launch_gram(c, geom, Tm, k, Cm, 2 * b, b, yo, false, Gpart, skip_flag);
+            launch_reduce_g(c, Gpart, geom.grid, n, b, nullptr, st, 0, ZVb[nxt], nrm, nblk, skip_flag);
+            launch_reduce_g(c, ZVb[nxt], 1, n, b, Vb[nxt], st, 1, Rres, nrm, nblk, skip_flag);
         } else {
             launch_gram(c, geom, Tm, k, Cm, 2 * b, b, yo, false, Gpart);
             if (one_pass) {  // check iteration: the reference's residual, and a fresh A^T A V'

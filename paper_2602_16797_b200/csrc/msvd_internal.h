@@ -53,6 +53,8 @@ struct DevState {
     double theta[kMaxB];    // Ritz values of the current target block (descending)
     double max_drift;
     double worst_jacobi;
+    int32_t skip_exact;     // one-pass check gate: 1 = the images' residual decides (far from tol)
+    int32_t pad_;
 };
 
 // column-pointer bundles passed by value to kernels
@@ -106,7 +108,7 @@ void launch_tcombine(Ctx& c, Cols T, int k, const double* Cm, int q, OutCols out
 // Gpart[grid][b][n]: A^T Y with Y = T C (gram mode, writes Y cols + extra cols)
 // or Y = T (direct mode, q == b, no writes)
 void launch_gram(Ctx& c, const StreamGeom& g, Cols T, int k, const double* Cm, int q, int b,
-                 OutCols out, bool direct, double* Gpart);
+                 OutCols out, bool direct, double* Gpart, const int* skip = nullptr);
 // per-CTA Householder R of the m x k column block T, Rparts[nparts][k][k]
 int tsqr_parts(const Ctx& c);  // number of partial R factors launch_tsqr produces
 void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st, int iter);
@@ -135,7 +137,10 @@ struct RRArgs {
 void launch_rr(Ctx& c, const RRArgs& a);
 
 void launch_reduce_g(Ctx& c, const double* Gpart, int nparts, int64_t n, int b, const double* V,
-                     const DevState* st, int residual, double* Gout, double* nrm_part, int nblk);
+                     const DevState* st, int residual, double* Gout, double* nrm_part, int nblk,
+                     const int* skip = nullptr);
+// st->skip_exact = (max_j ||R_j|| > thresh): the gate of a one-pass check iteration
+void launch_gate(Ctx& c, const double* nrm_part, int nblk, int b, DevState* st, double thresh);
 struct ControlArgs {
     const double* nrm_part;  // b x nblk partial sums of squares
     int nblk;

@@ -406,17 +406,32 @@ __global__ void tcombine_kernel(Cols T, int k, const double* Cm, int q, OutCols 
     }
 }
 
-// G = sum of per-CTA partials (fixed order); R = G - theta^2 V; partial norms
-__global__ void __launch_bounds__(256) reduce_g_kernel(const double* Gpart, int nparts, int64_t n, int b,
-                                                       const double* V, const DevState* st, int residual,
-                                                       double* Gout, double* nrm_part) {
+// G = sum of per-CTA partials (fixed order); R = G - theta^2 V; partial norms.
+// A block covers 256 columns with 4 thread groups; group g sums partials
+// g, g+4, ... in order, and the 4 group sums are added in fixed order.
+constexpr int kRedGroups = 4;
+__global__ void __launch_bounds__(256 * kRedGroups) reduce_g_kernel(const double* Gpart, int nparts, int64_t n, int b,
+                                                                    const double* V, const DevState* st, int residual,
+                                                                    double* Gout, double* nrm_part, const int* skip) {
+    if (skip && *skip) return;
+    __shared__ double part[kRedGroups][256];
     __shared__ double red[8];
     const int j = blockIdx.y;
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int t = threadIdx.x & 255, grp = threadIdx.x >> 8;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + t;
+    double s = 0.0;
+    if (i < n) {
+#pragma unroll 8
+        for (int p = grp; p < nparts; p += kRedGroups) s += Gpart[(static_cast<size_t>(p) * b + j) * n + i];
+    }
+    part[grp][t] = s;
+    __syncthreads();
+    if (grp != 0) return;
     double v = 0.0;
     if (i < n) {
-        double s = 0.0;
-        for (int p = 0; p < nparts; ++p) s += Gpart[(static_cast<size_t>(p) * b + j) * n + i];
+        s = part[0][t];
+#pragma unroll
+        for (int g = 1; g < kRedGroups; ++g) s += part[g][t];
         if (residual) {
             const double th = st->theta[j];
             s -= (th * th) * V[i + j * n];
@@ -425,13 +440,27 @@ __global__ void __launch_bounds__(256) reduce_g_kernel(const double* Gpart, int 
         v = s * s;
     }
     v = warp_sum(v);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < 8; ++w) t += red[w];
-        nrm_part[j * gridDim.x + blockIdx.x] = t;
+    if ((t & 31) == 0) red[t >> 5] = v;
+    named_sync(1, 256);
+    if (t == 0) {
+        double tt = 0.0;
+        for (int w = 0; w < 8; ++w) tt += red[w];
+        nrm_part[j * gridDim.x + blockIdx.x] = tt;
     }
+}
+
+// one-pass check gate: the residual norm as control_kernel forms it, from the
+// images' residual; far above the tolerance the stop test cannot pass, and
+// the exact Gram pass is skipped
+__global__ void gate_kernel(const double* nrm_part, int nblk, int b, DevState* st, double thresh) {
+    if (threadIdx.x != 0) return;
+    double best = 0.0;
+    for (int j = 0; j < b; ++j) {
+        double s = 0.0;
+        for (int x = 0; x < nblk; ++x) s += nrm_part[j * nblk + x];
+        best = fmax(best, sqrt(s));
+    }
+    st->skip_exact = best > thresh ? 1 : 0;
 }
 
 // record row + stop rule (solver.cpp:376-397, :177-211)
@@ -508,8 +537,9 @@ __global__ void __launch_bounds__(256) control_kernel(ControlArgs a) {
 // warp-per-vector coalesced dot products over an L2-resident n x n matrix.
 // ---------------------------------------------------------------------------
 template <int B>
-__global__ void __launch_bounds__(256) dots_kernel(const double* M, int64_t n, const double* X,
-                                                   const double* sig, double* out, DevState* st, int iter,
+__global__ void __launch_bounds__(256) dots_kernel(const double* __restrict__ M, int64_t n,
+                                                   const double* __restrict__ X, const double* __restrict__ sig,
+                                                   double* __restrict__ out, DevState* st, int iter,
                                                    int check_finite) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t c = static_cast<int64_t>(blockIdx.x) * 8 + warp;
@@ -518,7 +548,8 @@ __global__ void __launch_bounds__(256) dots_kernel(const double* M, int64_t n, c
     double acc[B];
 #pragma unroll
     for (int j = 0; j < B; ++j) acc[j] = 0.0;
-    for (int64_t i = lane; i < n; i += 32) {
+#pragma unroll 8
+    for (int64_t i = lane; i < n; i += 32) {  // unrolled: the L2 loads of 8 steps in flight together
         const double mv = mc[i];
 #pragma unroll
         for (int j = 0; j < B; ++j) acc[j] = fma(mv, X[i + j * n], acc[j]);
@@ -824,7 +855,7 @@ void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st,
 
 void launch_tcombine(Ctx& c, Cols T, int k, const double* Cm, int q, OutCols out, int64_t m) {
     if (m == 0) return;
-    const int grid = static_cast<int>(std::min<int64_t>(ceil_div(m, 256), 8 * c.num_sms));
+    const int grid = static_cast<int>(std::min<int64_t>(ceil_div(m, 256), 64 * c.num_sms));
     tcombine_kernel<<<grid, 256, 0, c.stream>>>(T, k, Cm, q, out, m);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
@@ -852,10 +883,19 @@ void launch_small_svd(Ctx& c, const double* B, int k, double* sigma, double* V, 
 }
 
 void launch_reduce_g(Ctx& c, const double* Gpart, int nparts, int64_t n, int b, const double* V,
-                     const DevState* st, int residual, double* Gout, double* nrm_part, int nblk) {
+                     const DevState* st, int residual, double* Gout, double* nrm_part, int nblk,
+                     const int* skip) {
     ProfScope prof(c, kProfReduce);
     dim3 grid(static_cast<unsigned>(nblk), static_cast<unsigned>(b));
-    reduce_g_kernel<<<grid, 256, 0, c.stream>>>(Gpart, nparts, n, b, V, st, residual, Gout, nrm_part);
+    reduce_g_kernel<<<grid, 256 * kRedGroups, 0, c.stream>>>(Gpart, nparts, n, b, V, st, residual, Gout, nrm_part,
+                                                             skip);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void launch_gate(Ctx& c, const double* nrm_part, int nblk, int b, DevState* st, double thresh) {
+    ProfScope prof(c, kProfControl);
+    gate_kernel<<<1, 32, 0, c.stream>>>(nrm_part, nblk, b, st, thresh);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
 }

@@ -701,6 +701,7 @@ struct GramArgs {
     OutCols out;       // q output columns (gram mode)
     int direct;        // Y = T (k == B), no outputs
     double* Gpart;     // [grid][B][n]
+    const int* skip;   // device flag: nonzero = the pass is not needed (one-pass check gate)
 };
 
 // K2: Gpart = A_cta^T Y_cta.  Warp 1 (the Y warp) forms Y rows for each
@@ -709,6 +710,7 @@ struct GramArgs {
 template <int B>
 __global__ void __launch_bounds__(64 + kConsumers, 1) gram_kernel(GramArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
+    if (a.skip && *a.skip) return;
     const StreamGeom& g = a.g;
     const size_t cm_bytes = sizeof(double) * kMaxK * 2 * kMaxB;
     const size_t ys_bytes = sizeof(double) * g.stages * g.rc * B;
@@ -1094,12 +1096,12 @@ bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
 }
 
 void launch_gram(Ctx& c, const StreamGeom& g, Cols T, int k, const double* Cm, int q, int b,
-                 OutCols out, bool direct, double* Gpart) {
+                 OutCols out, bool direct, double* Gpart, const int* skip) {
     ProfScope prof(c, kProfGram);
     // stage geometry by block size (tuning sweep, profiles/README.md):
     // b = 1: 32 KB x 3, b = 2: 48 KB x 3, b >= 3: 64 KB x 2
     const StreamGeom gg = b == 1 ? rechunk(g, 32, 96) : (b == 2 ? rechunk(g, 48, 144) : rechunk(g, 64, 128));
-    GramArgs a{gg, T, k, Cm, q, out, direct ? 1 : 0, Gpart};
+    GramArgs a{gg, T, k, Cm, q, out, direct ? 1 : 0, Gpart, skip};
     if (g.m == 0) {
         MSVD_CUDA(cudaMemsetAsync(Gpart, 0, sizeof(double) * g.grid * b * g.n, c.stream));
         return;
