@@ -528,12 +528,22 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         launch_rr(c, ra);
         OutCols yo{};
         for (int j = 0; j < b; ++j) yo.p[j] = AVb[0] + static_cast<int64_t>(j) * ml;
-        launch_gram(c, geom, cols_m({{AW, b}}), b, Cm, b, b, yo, false, Gpart);
-        if (one_pass) {
-            exact_images(ZVb[0]);
+        if (one_pass && !std::getenv("MSVD_INIT_GRAM")) {
+            // row 0 is not a check row: A^T A V0 = (A^T A W) C from the images
+            // the A*W pass just formed -- fresh, nothing carried yet
+            {
+                ProfScope prof(c, kProfReduce);
+                launch_tcombine(c, cols_m({{AW, b}}), b, Cm, b, yo, ml);
+            }
             launch_reduce_g(c, ZVb[0], 1, n, b, Vb[0], st, 1, Rres, nrm, nblk);
         } else {
-            residual(Vb[0]);
+            launch_gram(c, geom, cols_m({{AW, b}}), b, Cm, b, b, yo, false, Gpart);
+            if (one_pass) {
+                exact_images(ZVb[0]);
+                launch_reduce_g(c, ZVb[0], 1, n, b, Vb[0], st, 1, Rres, nrm, nblk);
+            } else {
+                residual(Vb[0]);
+            }
         }
         ca.V = Vb[0];
         ca.row = 0;
