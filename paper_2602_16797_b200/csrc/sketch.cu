@@ -203,6 +203,75 @@ __global__ void __launch_bounds__(kGatherT) gather_kernel(const double* A, int64
     if (!finite && st) atomicCAS(&st->err_code, 0, kErrNonfiniteA);
 }
 
+
+// Column-slice form of the one-shot gather: A is read in slices of 32*CPL
+// columns, one launch per slice, one warp per sketch row.  All d warps of a
+// slice are resident together and walk their (ascending) source lists at the
+// same pace, so the zeta readers of each A row-slice meet it in L2 within a
+// short window: A comes from HBM once instead of zeta times.  Same per-column
+// sequential __dmul_rn/__dadd_rn sums as gather_kernel -> the same bits.
+template <int kSliceCPL, int kSliceU>
+__global__ void __launch_bounds__(256, 4) gather_slice_kernel(const double* __restrict__ A, int64_t ld, int n,
+                                                           int64_t d, const int64_t* __restrict__ offs,
+                                                           const uint32_t* __restrict__ vals, double val,
+                                                           double* __restrict__ SA, DevState* st, int c0) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t s = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    if (s >= d) return;
+    const int64_t e0 = offs[s], e1 = offs[s + 1];
+    int col[kSliceCPL];
+    bool in[kSliceCPL];
+#pragma unroll
+    for (int q = 0; q < kSliceCPL; ++q) {
+        col[q] = c0 + lane + 32 * q;
+        in[q] = col[q] < n;
+        if (!in[q]) col[q] = n - 1;  // clamped load, result dropped
+    }
+    double acc[kSliceCPL];
+#pragma unroll
+    for (int q = 0; q < kSliceCPL; ++q) acc[q] = 0.0;
+    bool finite = true;
+    int64_t e = e0;
+    for (; e + kSliceU <= e1; e += kSliceU) {
+        // lane u < U fetches entry e+u; the row indices are then broadcast
+        const uint32_t mine = lane < kSliceU ? vals[e + lane] : 0u;
+        double x[kSliceU][kSliceCPL];
+        double sv[kSliceU];
+#pragma unroll
+        for (int u = 0; u < kSliceU; ++u) {
+            const uint32_t v = __shfl_sync(0xffffffffu, mine, u);
+            const int64_t r = v & 0x7fffffffu;
+            sv[u] = (v >> 31) ? -val : val;
+            const double* row = A + r * ld;
+#pragma unroll
+            for (int q = 0; q < kSliceCPL; ++q) x[u][q] = row[col[q]];
+        }
+#pragma unroll
+        for (int u = 0; u < kSliceU; ++u)
+#pragma unroll
+            for (int q = 0; q < kSliceCPL; ++q) {
+                acc[q] = __dadd_rn(acc[q], __dmul_rn(sv[u], x[u][q]));
+                finite = finite && isfinite(x[u][q]);
+            }
+    }
+    for (; e < e1; ++e) {
+        const uint32_t v = vals[e];
+        const int64_t r = v & 0x7fffffffu;
+        const double svv = (v >> 31) ? -val : val;
+        const double* row = A + r * ld;
+#pragma unroll
+        for (int q = 0; q < kSliceCPL; ++q) {
+            const double xv = row[col[q]];
+            acc[q] = __dadd_rn(acc[q], __dmul_rn(svv, xv));
+            finite = finite && isfinite(xv);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kSliceCPL; ++q)
+        if (in[q]) SA[s + static_cast<int64_t>(col[q]) * d] = acc[q];
+    if (!__all_sync(0xffffffffu, finite) && lane == 0 && st) atomicCAS(&st->err_code, 0, kErrNonfiniteA);
+}
+
 }  // namespace
 
 void build_sparsestack_dev(Ctx& c, int64_t d, int64_t m, int zeta, uint64_t seed, uint32_t* pos, int8_t* sgn) {
@@ -282,9 +351,10 @@ void sketch_finish(Ctx& c, const double* SAr, int64_t d, int64_t n, double* SA) 
     launch_transpose_rm_to_cm(c, SAr, d, n, n, SA);  // row-major running sums -> column-major SA
 }
 
-// A resident in HBM: one launch, one CTA per sketch row over its whole source
-// list (reads A zeta times, at full bandwidth).  The chunked form above is
-// used when A arrives from the host, where it hides under the H2D copy.
+// A resident in HBM: column slices, one warp per sketch row (gather_slice_kernel;
+// MSVD_SKETCH_GATHER = 1 selects the one-launch gather that reads A zeta
+// times).  The chunked form above is used when A arrives from the host, where
+// it hides under the H2D copy.
 void sketch_dev(Ctx& c, const StreamGeom& g, int64_t row0, int64_t d, int zeta, uint64_t seed, double* SA,
                 DevState* st) {
     ProfScope prof(c, kProfSketch);
@@ -293,10 +363,25 @@ void sketch_dev(Ctx& c, const StreamGeom& g, int64_t row0, int64_t d, int zeta, 
         return;
     }
     const SketchLists L = sketch_prepare(c, g.m, row0, d, zeta, seed, g.m);  // one chunk
-    gather_kernel<<<static_cast<unsigned>(d), kGatherT, 0, c.stream>>>(g.A, g.ld, g.n, d, L.offs, L.vals, L.val, SA,
-                                                                       st, g.tma);
-    MSVD_CUDA(cudaGetLastError());
-    ++c.launches;
+    if (std::getenv("MSVD_SKETCH_GATHER")) {  // one launch, A read zeta times
+        gather_kernel<<<static_cast<unsigned>(d), kGatherT, 0, c.stream>>>(g.A, g.ld, g.n, d, L.offs, L.vals, L.val,
+                                                                           SA, st, g.tma);
+        MSVD_CUDA(cudaGetLastError());
+        ++c.launches;
+        return;
+    }
+    const char* ce = std::getenv("MSVD_SKETCH_CPL");
+    const int cpl = ce ? std::atoi(ce) : 2;  // measured (C2): 32*2 columns x 8 entries in flight per warp
+    const int slice = 32 * cpl;
+    const unsigned grid = static_cast<unsigned>(ceil_div(d, 8));
+    for (int c0 = 0; c0 < g.n; c0 += slice) {
+        if (cpl == 1) gather_slice_kernel<1, 16><<<grid, 256, 0, c.stream>>>(g.A, g.ld, g.n, d, L.offs, L.vals, L.val, SA, st, c0);
+        else if (cpl == 2) gather_slice_kernel<2, 8><<<grid, 256, 0, c.stream>>>(g.A, g.ld, g.n, d, L.offs, L.vals, L.val, SA, st, c0);
+        else if (cpl == 8) gather_slice_kernel<8, 2><<<grid, 256, 0, c.stream>>>(g.A, g.ld, g.n, d, L.offs, L.vals, L.val, SA, st, c0);
+        else gather_slice_kernel<4, 4><<<grid, 256, 0, c.stream>>>(g.A, g.ld, g.n, d, L.offs, L.vals, L.val, SA, st, c0);
+        MSVD_CUDA(cudaGetLastError());
+        ++c.launches;
+    }
 }
 
 }  // namespace msvd

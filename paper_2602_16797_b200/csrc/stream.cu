@@ -575,9 +575,14 @@ __global__ void __launch_bounds__(256, 1) apply_self_kernel(ApplyArgs a) {
             double tv = 0.0;
             if (KM > 0 && lane < kt) tv = tbuf[(tb * kRowsFused + r) * KM + lane];
             const double* row = As + static_cast<int64_t>(r) * g.ld_s;
-            double acc[B];
+            // NA independent partial sums per right-hand side (pairs i mod NA),
+            // combined in fixed order: a DFMA chain of 2 PL / NA, not 2 PL
+            constexpr int NA = PL >= 8 ? 4 : (PL >= 4 ? 2 : 1);
+            double part[NA][B];
 #pragma unroll
-            for (int j = 0; j < B; ++j) acc[j] = 0.0;
+            for (int q = 0; q < NA; ++q)
+#pragma unroll
+                for (int j = 0; j < B; ++j) part[q][j] = 0.0;
             double2 xr[GR ? PL : 1];
 #pragma unroll
             for (int i = 0; i < PL; ++i) {
@@ -586,9 +591,16 @@ __global__ void __launch_bounds__(256, 1) apply_self_kernel(ApplyArgs a) {
                 if (GR) xr[GR ? i : 0] = x;
 #pragma unroll
                 for (int j = 0; j < B; ++j) {
-                    acc[j] = fma(x.x, w[i][0][j], acc[j]);
-                    acc[j] = fma(x.y, w[i][1][j], acc[j]);
+                    part[i % NA][j] = fma(x.x, w[i][0][j], part[i % NA][j]);
+                    part[i % NA][j] = fma(x.y, w[i][1][j], part[i % NA][j]);
                 }
+            }
+            double acc[B];
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                acc[j] = part[0][j];
+#pragma unroll
+                for (int q = 1; q < NA; ++q) acc[j] += part[q][j];
             }
 #pragma unroll
             for (int j = 0; j < B; ++j) acc[j] = warp_sum(acc[j]);
