@@ -182,6 +182,19 @@ public:
         check(msvd_apply_adjoint(mat_, dY, b, dX));
     }
     void column_norms(double* dNorms) const { check(msvd_column_norms(mat_, dNorms)); }
+    // the iteration's two passes as primitives: K2 Y = T C and
+    // G = A^T Y[:, :b]; K3 A W with the TSQR R of [lead | A W]; the one-pass
+    // A W plus A^T A W
+    void gram_apply(const double* dT, index_t k, const double* dC, index_t q, index_t b, double* dG,
+                    double* dY) const {
+        check(msvd_gram_apply(mat_, dT, k, dC, q, b, dG, dY));
+    }
+    void aw_tsqr(const double* dW, index_t b, const double* dLead, index_t kl, double* dAW, double* dR) const {
+        check(msvd_aw_tsqr(mat_, dW, b, dLead, kl, dAW, dR));
+    }
+    void aw_gram(const double* dW, index_t b, double* dAW, double* dZ) const {
+        check(msvd_aw_gram(mat_, dW, b, dAW, dZ));
+    }
     msvd_matrix* get() const { return mat_; }
 
 private:

@@ -193,6 +193,26 @@ int32_t msvd_precond_apply(msvd_ctx* ctx, const double* dVt, const double* dSig,
  * reference's only up to +-1 (R^T R identical).                             */
 int32_t msvd_tsqr_r(msvd_ctx* ctx, const double* dT, int64_t rows, int64_t k,
                     double* dR);
+/* The two passes of an iteration as primitives.
+ * msvd_gram_apply -- residual_of solver.cpp:357-369 with the recurrence
+ *   products :421/:462 (kernel K2): dY (m_local x q) = dT (m_local x k,
+ *   col-major) dC (k x q, col-major) and dG (n x b) = A^T dY[:, 0:b], summed
+ *   over ranks; b <= q <= 2b.  dC == NULL: Y = T (q == k == b), dY unused.  */
+int32_t msvd_gram_apply(msvd_matrix* mat, const double* dT, int64_t k,
+                        const double* dC, int64_t q, int64_t b, double* dG,
+                        double* dY);
+/* msvd_aw_tsqr -- solver.cpp:412-416 (kernel K3): dAW (m_local x b) = A dW,
+ *   and dR (k x k, k = kl + b, upper) = the Householder R factor of the trial
+ *   block [dLead (m_local x kl) | AW] (svd.cpp:21-55, row signs up to +-1),
+ *   merged over CTAs and ranks.  kl = 0: dLead unused.                      */
+int32_t msvd_aw_tsqr(msvd_matrix* mat, const double* dW, int64_t b,
+                     const double* dLead, int64_t kl, double* dAW, double* dR);
+/* msvd_aw_gram -- the one-pass primitive: dAW (m_local x b) = A dW and
+ *   dZ (n x b) = A^T (A dW), summed over ranks, from ONE pass over A.  Where
+ *   the register-resident kernel does not fit (b * ceil(n/64) > 16 lanes'
+ *   worth) it makes the two passes instead.                                 */
+int32_t msvd_aw_gram(msvd_matrix* mat, const double* dW, int64_t b, double* dAW,
+                     double* dZ);
 /* svd.cpp:180-252 dense_svd(B, false) of a small square dB (k x k, k<=32)
  * already reduced to R: sigma descending, V sign-fixed.                     */
 int32_t msvd_small_svd(msvd_ctx* ctx, const double* dB, int64_t k,

@@ -1056,6 +1056,120 @@ int32_t msvd_tsqr_r(msvd_ctx* ctx, const double* dT, int64_t rows, int64_t k, do
     });
 }
 
+int32_t msvd_gram_apply(msvd_matrix* M, const double* dT, int64_t k, const double* dC, int64_t q, int64_t b,
+                        double* dG, double* dY) {
+    return guard([&] {
+        need(M, "matrix");
+        Ctx& c = M->ctx->c;
+        set_device(c);
+        if (b < 1 || b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size must lie in [1, 8]");
+        if (k < 1 || k > kMaxK) fail(MSVD_ERR_DIMENSION, "msvd: trial width must lie in [1, 24]");
+        const bool direct = dC == nullptr;
+        if (direct && (k != b || q != b)) fail(MSVD_ERR_DIMENSION, "msvd_gram_apply: Y = T needs q == k == b");
+        if (!direct && (q < b || q > 2 * b)) fail(MSVD_ERR_DIMENSION, "msvd_gram_apply: q must lie in [b, 2b]");
+        if (!direct && !dY) fail(MSVD_ERR_INVALID, "msvd_gram_apply: dY missing");
+        const int64_t n = M->n, ml = M->m_local;
+        const StreamGeom g = make_geom(c, M->A, ml, static_cast<int32_t>(n), M->ld);
+        const int nblk = static_cast<int>(ceil_div(n, 256));
+        const size_t gp = static_cast<size_t>(g.grid) * b * n;
+        double* s = static_cast<double*>(c.ensure_scratch(sizeof(double) * (gp + static_cast<size_t>(b) * nblk +
+                                                                            kMaxK * 2 * kMaxB)));
+        double* Cs = s + gp + static_cast<size_t>(b) * nblk;
+        Cols T{};
+        for (int l = 0; l < k; ++l) T.p[l] = dT + l * ml;
+        OutCols out{};
+        if (!direct) {
+            for (int j = 0; j < q; ++j) out.p[j] = dY + j * ml;
+            MSVD_CUDA(cudaMemcpyAsync(Cs, dC, sizeof(double) * k * q, cudaMemcpyDeviceToDevice, c.stream));
+        }
+        launch_gram(c, g, T, static_cast<int>(k), direct ? nullptr : Cs, static_cast<int>(q), static_cast<int>(b), out,
+                    direct, s);
+        launch_reduce_g(c, s, g.grid, n, static_cast<int>(b), nullptr, nullptr, 0, dG, s + gp, nblk);
+        c.comm->allreduce_sum(dG, static_cast<size_t>(n * b), c.stream);
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int32_t msvd_aw_tsqr(msvd_matrix* M, const double* dW, int64_t b, const double* dLead, int64_t kl, double* dAW,
+                     double* dR) {
+    return guard([&] {
+        need(M, "matrix");
+        Ctx& c = M->ctx->c;
+        set_device(c);
+        if (b < 1 || b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size must lie in [1, 8]");
+        const int64_t k = kl + b, ml = M->m_local, n = M->n;
+        if (kl < 0 || k > kMaxK) fail(MSVD_ERR_DIMENSION, "msvd: trial width must lie in [1, 24]");
+        if (M->m_global < k) fail(MSVD_ERR_DIMENSION, "householder_qr: requires rows >= cols");
+        const StreamGeom g = make_geom(c, M->A, ml, static_cast<int32_t>(n), M->ld);
+        const int np_max = std::max(tsqr_parts(c), g.grid);
+        const int ranks = c.comm->nranks();
+        const size_t pk = static_cast<size_t>(np_max) * k * k;
+        double* parts = static_cast<double*>(c.ensure_scratch(sizeof(double) * pk * (1 + ranks)));
+        double* all = parts + pk;
+        DevState* st = prim_state(c);
+        MSVD_CUDA(cudaMemsetAsync(st, 0, sizeof(DevState), c.stream));
+        OutCols out{};
+        for (int j = 0; j < b; ++j) out.p[j] = dAW + j * ml;
+        TsqrFuse fz{};
+        for (int l = 0; l < kl; ++l) fz.T.p[l] = dLead + l * ml;
+        fz.k = static_cast<int>(k);
+        fz.Rparts = parts;
+        fz.st = st;
+        int np = tsqr_parts(c);
+        if (launch_apply(c, g, dW, static_cast<int>(b), out, &fz)) {
+            np = g.grid;
+        } else {
+            Cols T{};
+            for (int l = 0; l < kl; ++l) T.p[l] = dLead + l * ml;
+            for (int j = 0; j < b; ++j) T.p[kl + j] = dAW + j * ml;
+            launch_tsqr(c, T, ml, static_cast<int>(k), parts, st, 0);
+        }
+        const double* src = parts;
+        if (ranks > 1) {
+            c.comm->allgather(parts, all, static_cast<size_t>(np) * k * k, c.stream);
+            src = all;
+        }
+        RRArgs ra{};
+        ra.Rparts = src;
+        ra.nparts = np * ranks;
+        ra.k = static_cast<int>(k);
+        ra.b = 1;
+        ra.mode = 2;
+        ra.R_out = dR;
+        ra.st = st;
+        launch_rr(c, ra);
+        read_state(c, st);
+    });
+}
+
+int32_t msvd_aw_gram(msvd_matrix* M, const double* dW, int64_t b, double* dAW, double* dZ) {
+    return guard([&] {
+        need(M, "matrix");
+        Ctx& c = M->ctx->c;
+        set_device(c);
+        if (b < 1 || b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size must lie in [1, 8]");
+        const int64_t n = M->n, ml = M->m_local;
+        const StreamGeom g = make_geom(c, M->A, ml, static_cast<int32_t>(n), M->ld);
+        const int nblk = static_cast<int>(ceil_div(n, 256));
+        const size_t gp = static_cast<size_t>(g.grid) * b * n;
+        double* s = static_cast<double*>(c.ensure_scratch(sizeof(double) * (gp + static_cast<size_t>(b) * nblk)));
+        OutCols out{};
+        for (int j = 0; j < b; ++j) out.p[j] = dAW + j * ml;
+        if (apply_gram_supported(c, g, static_cast<int>(b), nullptr)) {
+            launch_apply(c, g, dW, static_cast<int>(b), out, nullptr, s);
+        } else {  // two passes
+            launch_apply(c, g, dW, static_cast<int>(b), out);
+            Cols T{};
+            for (int j = 0; j < b; ++j) T.p[j] = dAW + j * ml;
+            launch_gram(c, g, T, static_cast<int>(b), nullptr, static_cast<int>(b), static_cast<int>(b), OutCols{},
+                        true, s);
+        }
+        launch_reduce_g(c, s, g.grid, n, static_cast<int>(b), nullptr, nullptr, 0, dZ, s + gp, nblk);
+        c.comm->allreduce_sum(dZ, static_cast<size_t>(n * b), c.stream);
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
 int32_t msvd_small_svd(msvd_ctx* ctx, const double* dB, int64_t k, double* dSigma, double* dV) {
     return guard([&] {
         need(ctx, "context");

@@ -103,6 +103,9 @@ def _declare(lib):
         "msvd_precond_build": (i32, [vp, vp, i64, i64, vp, vp, P(d), P(i64)]),
         "msvd_precond_apply": (i32, [vp, vp, vp, i64, vp, i64, vp]),
         "msvd_tsqr_r": (i32, [vp, vp, i64, i64, vp]),
+        "msvd_gram_apply": (i32, [vp, vp, i64, vp, i64, i64, vp, vp]),
+        "msvd_aw_tsqr": (i32, [vp, vp, i64, vp, i64, vp, vp]),
+        "msvd_aw_gram": (i32, [vp, vp, i64, vp, vp]),
         "msvd_small_svd": (i32, [vp, vp, i64, vp, vp]),
         "msvd_lobpcg_solve": (i32, [vp, P(abi.Options), P(abi.Truth), P(abi.Result)]),
         "msvd_rlobpcg_single": (i32, [vp, P(abi.Options), P(abi.Truth), P(abi.Result)]),
@@ -126,7 +129,8 @@ EXPORTED = (
     "msvd_validate_options msvd_shard_rows msvd_get_nccl_unique_id msvd_fake_group_create "
     "msvd_fake_group_destroy msvd_ctx_create msvd_ctx_destroy msvd_ctx_synchronize msvd_matrix_attach "
     "msvd_matrix_detach msvd_apply msvd_apply_adjoint msvd_column_norms msvd_build_sparsestack msvd_sketch "
-    "msvd_precond_build msvd_precond_apply msvd_tsqr_r msvd_small_svd msvd_lobpcg_solve msvd_rlobpcg_single "
+    "msvd_precond_build msvd_precond_apply msvd_tsqr_r msvd_gram_apply msvd_aw_tsqr msvd_aw_gram msvd_small_svd "
+    "msvd_lobpcg_solve msvd_rlobpcg_single "
     "msvd_rlobpcg_block msvd_solve_host msvd_launch_count msvd_abi_sizes msvd_ctx_profile msvd_ctx_profile_read"
 ).split()
 
@@ -433,6 +437,52 @@ class DeviceDenseOperator:
         x = torch.empty((b, self.n), dtype=torch.float64, device=self.a.device)
         check(lib().msvd_apply_adjoint(self.handle, C.c_void_p(yt.data_ptr()), b, C.c_void_p(x.data_ptr())))
         return x.t()
+
+    def gram_apply(self, t, c=None, b=None):
+        """K2 (solver.cpp:357-369, :421): Y = T C, G = A^T Y[:, :b]; c=None: G = A^T T."""
+        torch = _torch()
+        tt, k = self._cm(t, self.m_local)
+        if c is None:
+            b = k
+            q = k
+            ct = None
+        else:
+            c = torch.as_tensor(c, dtype=torch.float64, device=self.a.device)
+            q = c.shape[1]
+            b = q if b is None else b
+            ct = c.t().contiguous()  # column-major k x q
+        g = torch.empty((b, self.n), dtype=torch.float64, device=self.a.device)
+        y = torch.empty((q, self.m_local), dtype=torch.float64, device=self.a.device) if ct is not None else None
+        check(lib().msvd_gram_apply(self.handle, C.c_void_p(tt.data_ptr()), k,
+                                    C.c_void_p(ct.data_ptr()) if ct is not None else None, q, b,
+                                    C.c_void_p(g.data_ptr()), C.c_void_p(y.data_ptr()) if y is not None else None))
+        return g.t(), (y.t() if y is not None else None)
+
+    def aw_tsqr(self, w, lead=None):
+        """K3 (solver.cpp:412-416): AW = A W and the R factor of [lead | AW]."""
+        torch = _torch()
+        wt, b = self._cm(w, self.n)
+        if lead is not None:
+            lt, kl = self._cm(lead, self.m_local)
+        else:
+            lt, kl = None, 0
+        k = kl + b
+        aw = torch.empty((b, self.m_local), dtype=torch.float64, device=self.a.device)
+        r = torch.empty((k, k), dtype=torch.float64, device=self.a.device)
+        check(lib().msvd_aw_tsqr(self.handle, C.c_void_p(wt.data_ptr()), b,
+                                 C.c_void_p(lt.data_ptr()) if lt is not None else None, kl,
+                                 C.c_void_p(aw.data_ptr()), C.c_void_p(r.data_ptr())))
+        return aw.t(), r.t()
+
+    def aw_gram(self, w):
+        """One pass: AW = A W and Z = A^T A W."""
+        torch = _torch()
+        wt, b = self._cm(w, self.n)
+        aw = torch.empty((b, self.m_local), dtype=torch.float64, device=self.a.device)
+        z = torch.empty((b, self.n), dtype=torch.float64, device=self.a.device)
+        check(lib().msvd_aw_gram(self.handle, C.c_void_p(wt.data_ptr()), b, C.c_void_p(aw.data_ptr()),
+                                 C.c_void_p(z.data_ptr())))
+        return aw.t(), z.t()
 
     def apply(self, x):
         return self.apply_block(x)[:, 0]

@@ -97,6 +97,45 @@ def test_apply_and_adjoint(msvd, cuda, m, n, b):
     assert (aty - ref_aty).abs().max().item() <= tol_aty
 
 
+@pytest.mark.parametrize("m,n,b,kl", [(5000, 100, 1, 2), (20_000, 1000, 1, 2), (20_000, 1000, 2, 4), (9_999, 500, 4, 8),
+                                      (4096, 2000, 5, 10), (3000, 64, 1, 0), (100, 7, 2, 0)])
+def test_pass_primitives(msvd, cuda, m, n, b, kl):
+    """msvd_gram_apply (K2), msvd_aw_tsqr (K3 + TSQR) and msvd_aw_gram (one pass)
+    against torch fp64: solver.cpp:357-369/:421 and :412-416."""
+    import torch
+
+    g = torch.Generator(device=cuda).manual_seed(m + 7 * n + b)
+    a = torch.randn(m, n, dtype=torch.float64, device=cuda, generator=g)
+    w = torch.randn(n, b, dtype=torch.float64, device=cuda, generator=g)
+    lead = torch.randn(m, kl, dtype=torch.float64, device=cuda, generator=g) if kl else None
+    op = msvd.DeviceDenseOperator(a)
+    aw_ref = a @ w
+    tol_aw = 64 * np.sqrt(n) * 2.2e-16 * (a.abs() @ w.abs()).max().item()
+    # K3 + TSQR: AW and the R of [lead | AW] (R^T R is sign-free)
+    aw, r = op.aw_tsqr(w, lead)
+    assert (aw - aw_ref).abs().max().item() <= tol_aw
+    t = torch.cat([lead, aw_ref], dim=1) if kl else aw_ref
+    assert torch.allclose(torch.triu(r), r)
+    gram = t.t() @ t
+    assert (r.t() @ r - gram).abs().max().item() <= 1e-12 * gram.abs().max().item()
+    # one pass: AW and A^T A W
+    aw2, z = op.aw_gram(w)
+    assert (aw2 - aw_ref).abs().max().item() <= tol_aw
+    z_ref = a.t() @ aw_ref
+    assert (z - z_ref).abs().max().item() <= 64 * np.sqrt(m) * 2.2e-16 * (a.abs().t() @ aw_ref.abs()).max().item()
+    # K2: Y = T C, G = A^T Y[:, :b]
+    k = kl + b
+    cmat = torch.randn(k, 2 * b, dtype=torch.float64, device=cuda, generator=g)
+    gg, y = op.gram_apply(t, cmat, b)
+    y_ref = t @ cmat
+    assert (y - y_ref).abs().max().item() <= 64 * np.sqrt(k) * 2.2e-16 * (t.abs() @ cmat.abs()).max().item()
+    g_ref = a.t() @ y_ref[:, :b]
+    assert (gg - g_ref).abs().max().item() <= 64 * np.sqrt(m) * 2.2e-16 * (a.abs().t() @ y_ref[:, :b].abs()).max().item()
+    gd, none = op.gram_apply(aw_ref)  # direct: G = A^T T
+    assert none is None
+    assert (gd - z_ref).abs().max().item() <= 64 * np.sqrt(m) * 2.2e-16 * (a.abs().t() @ aw_ref.abs()).max().item()
+
+
 @pytest.mark.parametrize("pad", [1, 2, 3])
 def test_apply_unaligned_rows(msvd, cuda, pad):
     """Odd leading dimensions take the LDG producer path; results are the same."""
