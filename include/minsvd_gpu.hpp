@@ -269,5 +269,64 @@ inline SolveResult rlobpcg_block(const DeviceDenseOperator& a, const SolverOptio
     return detail::run(&msvd_rlobpcg_block, a, PrecondKind::randomized, opts, truth, false);
 }
 
+// ---- baselines.hpp:12-42 ---------------------------------------------------
+inline SolveResult lobpcg_generic(const DeviceDenseOperator& a, PrecondKind kind, const SolverOptions& opts,
+                                  const GroundTruth* truth = nullptr) {
+    return lobpcg_solve(a, kind, opts, truth);
+}
+
+enum class LanczosStatus { completed, invariant_subspace };
+
+struct LanczosResult {
+    double sigma_min = 0.0;
+    Vector v;
+    ConvergenceRecord record;
+    LanczosStatus status = LanczosStatus::completed;
+    int steps = 0;
+    std::vector<double> v_basis;  // n x steps, column-major
+    std::vector<double> u_basis;  // m_local x steps, column-major
+};
+
+// baselines.cpp:51-166 on the device (msvd_lanczos_gk)
+inline LanczosResult lanczos_gk(const DeviceDenseOperator& a, int iters, const Vector& v0,
+                                const GroundTruth* truth = nullptr, bool record_timing = true,
+                                index_t m_local = -1) {
+    if (static_cast<index_t>(v0.size()) != a.cols())
+        throw DimensionError("lanczos_gk: starting vector length mismatch");
+    if (truth && static_cast<index_t>(truth->v_min.size()) != a.cols())
+        throw DimensionError("lanczos_gk: ground-truth vector length mismatch");
+    const index_t ml = m_local < 0 ? a.rows() : m_local;
+    LanczosResult out;
+    out.v.assign(static_cast<size_t>(a.cols()), 0.0);
+    const size_t cap = static_cast<size_t>(iters > 0 ? iters : 1);
+    std::vector<msvd_record_row> rows(cap);
+    out.v_basis.assign(static_cast<size_t>(a.cols()) * cap, 0.0);
+    out.u_basis.assign(static_cast<size_t>(ml) * cap, 0.0);
+    msvd_lanczos_result r{};
+    r.v = out.v.data();
+    r.rows = rows.data();
+    r.rows_capacity = static_cast<int32_t>(cap);
+    r.v_basis = out.v_basis.data();
+    r.u_basis = out.u_basis.data();
+    msvd_truth t{};
+    if (truth) {
+        t.sigma_min = truth->sigma_min;
+        t.v_min = truth->v_min.data();
+    }
+    check(msvd_lanczos_gk(a.get(), iters, v0.data(), truth ? &t : nullptr, record_timing ? 1 : 0, &r));
+    out.sigma_min = r.sigma_min;
+    out.status = r.status == MSVD_LANCZOS_COMPLETED ? LanczosStatus::completed : LanczosStatus::invariant_subspace;
+    out.steps = r.steps;
+    out.record.has_truth = truth != nullptr;
+    for (int i = 0; i < r.rows_count && i < r.rows_capacity; ++i) {
+        const msvd_record_row& s = rows[static_cast<size_t>(i)];
+        out.record.rows.push_back(RecordRow{s.iter, static_cast<long>(s.matvecs_a), static_cast<long>(s.matvecs_at),
+                                            s.wall_ms, s.theta, s.resid, s.relerr, s.sin_angle});
+    }
+    out.v_basis.resize(static_cast<size_t>(a.cols()) * r.steps);
+    out.u_basis.resize(static_cast<size_t>(ml) * r.steps);
+    return out;
+}
+
 }  // namespace gpu
 }  // namespace minsvd

@@ -218,6 +218,37 @@ int32_t msvd_aw_gram(msvd_matrix* mat, const double* dW, int64_t b, double* dAW,
 int32_t msvd_small_svd(msvd_ctx* ctx, const double* dB, int64_t k,
                        double* dSigma, double* dV);
 
+/* ---- Krylov baseline (baselines.cpp:51-166 lanczos_gk) ----------------- */
+/* baselines.hpp:20-23 LanczosStatus */
+typedef enum msvd_lanczos_status {
+    MSVD_LANCZOS_COMPLETED = 0,
+    MSVD_LANCZOS_INVARIANT_SUBSPACE = 1
+} msvd_lanczos_status;
+
+/* baselines.hpp:25-33 LanczosResult.  Arrays are caller-owned HOST buffers;
+ * the bases are optional (NULL skips the copy).                             */
+typedef struct msvd_lanczos_result {
+    double sigma_min;           /* out: smallest Ritz value of the final section */
+    double* v;                  /* [n] matching right Ritz vector, unit norm     */
+    msvd_record_row* rows;      /* [rows_capacity], one row per step             */
+    int32_t rows_capacity;      /* >= iters to receive every row                 */
+    int32_t rows_count;         /* out */
+    int32_t status;             /* out: msvd_lanczos_status                      */
+    int32_t steps;              /* out: sections evaluated                       */
+    double* v_basis;            /* optional [n * iters], first `steps` columns   */
+    double* u_basis;            /* optional [m_local * iters], first `steps` cols */
+} msvd_lanczos_result;
+
+/* baselines.cpp:51-166 lanczos_gk(a, iters, v0, truth, record_timing):
+ * Golub-Kahan bidiagonalization from v0 (HOST, length n) with two-pass
+ * reorthogonalization of both Krylov bases, on the device; the smallest
+ * singular triplet of each bidiagonal section is found by bisection on its
+ * Golub-Kahan tridiagonal plus inverse iteration (LAPACK dbdsvdx's route)
+ * instead of the reference's dense Jacobi SVD of the section.              */
+int32_t msvd_lanczos_gk(msvd_matrix* mat, int32_t iters, const double* v0,
+                        const msvd_truth* truth, int32_t record_timing,
+                        msvd_lanczos_result* res);
+
 /* ---- full solve (solver.cpp:301-477, 479-489) ------------------------- */
 int32_t msvd_lobpcg_solve(msvd_matrix* mat, const msvd_options* opts,
                           const msvd_truth* truth, msvd_result* res);
@@ -235,7 +266,8 @@ int32_t msvd_solve_host(msvd_ctx* ctx, const double* hA, int64_t m_local,
                         msvd_result* res);
 
 /* sizeof of {msvd_options, msvd_record_row, msvd_truth, msvd_result,
- * msvd_ctx_desc} into out[0..n) (binding self-check; host only). */
+ * msvd_ctx_desc, msvd_lanczos_result} into out[0..n) (binding self-check;
+ * host only). */
 void msvd_abi_sizes(int64_t* out, int32_t n);
 
 /* Number of library kernels launched since ctx creation (bench evidence). */

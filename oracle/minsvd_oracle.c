@@ -754,7 +754,137 @@ static void solve_dense(mat a, const msvd_options *o, const msvd_truth *truth, m
     res->iterations = (int32_t)R.nrow - 1;
 }
 
+/* ------------------------------------------ lanczos_gk (baselines.cpp) */
+
+/* two full MGS passes against the first `used` columns (baselines.cpp:19-31) */
+static void reorth_mgs(double *w, int64_t len, mat basis, int64_t used) {
+    for (int pass = 0; pass < 2; ++pass)
+        for (int64_t l = 0; l < used; ++l) {
+            const double *c = col(basis, l);
+            double proj = 0.0;
+            for (int64_t i = 0; i < len; ++i) proj += c[i] * w[i];
+            for (int64_t i = 0; i < len; ++i) w[i] -= proj * c[i];
+        }
+}
+
+/* lanczos_gk (baselines.cpp:51-166) on a dense column-major A */
+static void lanczos_dense(mat a, int iters, const double *v0, const msvd_truth *truth, int timing,
+                          msvd_lanczos_result *res) {
+    const int64_t m = a.r, n = a.c;
+    if (m < n) raise_err(MSVD_ERR_DIMENSION, "lanczos_gk: matrix must be tall");
+    if (iters < 1 || iters > n) raise_err(MSVD_ERR_DIMENSION, "lanczos_gk: step count must lie in [1, cols]");
+    const double v0n = vnorm(v0, n);
+    if (v0n == 0.0) raise_err(MSVD_ERR_NUMERICAL, "lanczos_gk: starting vector is zero");
+    if (truth && !truth->v_min) raise_err(MSVD_ERR_DIMENSION, "lanczos_gk: ground-truth vector length mismatch");
+    const double t0 = now_ms();
+
+    mat vb = mnew(n, iters + 1), ub = mnew(m, iters);
+    double *alpha = (double *)zalloc(sizeof(double) * (size_t)iters);
+    double *beta = (double *)zalloc(sizeof(double) * (size_t)iters);
+    double *v = (double *)zalloc(sizeof(double) * (size_t)n);
+    memcpy(v, v0, sizeof(double) * (size_t)n);
+    vscale(v, n, 1.0 / v0n);
+    memcpy(col(vb, 0), v, sizeof(double) * (size_t)n);
+
+    double *u = (double *)zalloc(sizeof(double) * (size_t)m);
+    matvec(a, v, u);
+    long mva = 1, mvat = 0;
+    const double a1 = vnorm(u, m);
+    res->rows_count = 0;
+    res->steps = 0;
+    res->status = MSVD_LANCZOS_COMPLETED;
+    if (a1 == 0.0) { /* v0 is an exact null vector of A */
+        res->sigma_min = 0.0;
+        memcpy(res->v, v, sizeof(double) * (size_t)n);
+        res->status = MSVD_LANCZOS_INVARIANT_SUBSPACE;
+        return;
+    }
+    alpha[0] = a1;
+    vscale(u, m, 1.0 / a1);
+    memcpy(col(ub, 0), u, sizeof(double) * (size_t)m);
+    double coeff = a1;
+
+    double *w = (double *)zalloc(sizeof(double) * (size_t)n);
+    double *vest = (double *)zalloc(sizeof(double) * (size_t)n);
+    double *un = (double *)zalloc(sizeof(double) * (size_t)m);
+    for (int j = 1; j <= iters; ++j) {
+        matvec_t(a, col(ub, j - 1), w);
+        ++mvat;
+        const double *vp = col(vb, j - 1);
+        for (int64_t i = 0; i < n; ++i) w[i] += -alpha[j - 1] * vp[i];
+        reorth_mgs(w, n, vb, j);
+        const double bj = vnorm(w, n);
+        if (bj > coeff) coeff = bj;
+        beta[j - 1] = bj;
+
+        mat sec = mnew(j, j); /* bidiagonal_section (baselines.cpp:33-40) */
+        for (int i = 0; i < j; ++i) {
+            AT(sec, i, i) = alpha[i];
+            if (i + 1 < j) AT(sec, i, i + 1) = beta[i];
+        }
+        svdres s = svd_values_right(sec);
+        const double theta = s.sigma[j - 1];
+        const double *y = col(s.v, j - 1);
+        memset(vest, 0, sizeof(double) * (size_t)n);
+        for (int l = 0; l < j; ++l) {
+            const double *c = col(vb, l);
+            for (int64_t i = 0; i < n; ++i) vest[i] += y[l] * c[i];
+        }
+        const double resid = alpha[j - 1] * bj * fabs(y[j - 1]);
+
+        msvd_record_row row;
+        memset(&row, 0, sizeof row);
+        row.iter = j;
+        row.matvecs_a = mva;
+        row.matvecs_at = mvat;
+        row.wall_ms = timing ? now_ms() - t0 : 0.0;
+        row.theta = theta;
+        row.resid = resid;
+        row.relerr = -1.0;
+        row.sin_angle = -1.0;
+        if (truth) {
+            const double sn = truth->sigma_min;
+            row.relerr = sn > 0.0 ? fabs(theta - sn) / sn : fabs(theta);
+            double c = vdot(vest, truth->v_min, n);
+            c = c < -1.0 ? -1.0 : (c > 1.0 ? 1.0 : c);
+            const double s2 = 1.0 - c * c;
+            row.sin_angle = sqrt(s2 > 0.0 ? s2 : 0.0);
+        }
+        if (res->rows_count < res->rows_capacity) res->rows[res->rows_count] = row;
+        res->rows_count++;
+        res->sigma_min = theta;
+        memcpy(res->v, vest, sizeof(double) * (size_t)n);
+        res->steps = j;
+
+        if (bj <= 64.0 * EPS * coeff) { res->status = MSVD_LANCZOS_INVARIANT_SUBSPACE; break; }
+        if (j == iters) break;
+
+        vscale(w, n, 1.0 / bj);
+        memcpy(col(vb, j), w, sizeof(double) * (size_t)n);
+        matvec(a, w, un);
+        ++mva;
+        const double *up = col(ub, j - 1);
+        for (int64_t i = 0; i < m; ++i) un[i] += -bj * up[i];
+        reorth_mgs(un, m, ub, j);
+        const double aj = vnorm(un, m);
+        if (aj > coeff) coeff = aj;
+        if (aj <= 64.0 * EPS * coeff) { res->status = MSVD_LANCZOS_INVARIANT_SUBSPACE; break; }
+        alpha[j] = aj;
+        vscale(un, m, 1.0 / aj);
+        memcpy(col(ub, j), un, sizeof(double) * (size_t)m);
+    }
+    if (res->v_basis) memcpy(res->v_basis, vb.p, sizeof(double) * (size_t)(n * res->steps));
+    if (res->u_basis) memcpy(res->u_basis, ub.p, sizeof(double) * (size_t)(m * res->steps));
+}
+
 /* ---------------------------------------------------------------- exports */
+
+int orc_lanczos_gk(const double *a_colmajor, int64_t m, int64_t n, int iters, const double *v0,
+                   const msvd_truth *truth, int record_timing, msvd_lanczos_result *res) {
+    ENTER();
+    lanczos_dense(mview((double *)a_colmajor, m, n), iters, v0, truth, record_timing, res);
+    LEAVE();
+}
 
 void orc_splitmix_draws(uint64_t seed, uint64_t key, int keyed, int kind, int64_t count, double *out_f,
                         uint64_t *out_u, uint64_t bound) {

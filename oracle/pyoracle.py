@@ -132,6 +132,9 @@ class Oracle:
         self._cc = g("check_convergence")
         self._cc.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64, C.c_int,
                              C.c_double, C.c_double, C.c_double, C.c_int, C.POINTER(C.c_int)]
+        self._lz = g("lanczos_gk")
+        self._lz.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_int64, C.c_int, C.POINTER(C.c_double),
+                             C.POINTER(abi.Truth), C.c_int, C.POINTER(abi.LanczosResult)]
         self._cgs2 = g("cgs2")
         self._cgs2.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_int64, C.POINTER(C.c_double),
                                C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]
@@ -283,6 +286,51 @@ class Oracle:
             tr = abi.Truth(float(truth[0]), _p(vmin))
         self._check(self._solve(_p(a), m, n, C.byref(o), C.byref(tr) if tr else None, C.byref(res)))
         return _result_dict(res, rows, sigma, v, vt, sig, trail, has_truth=truth is not None)
+
+    # -- Krylov baseline ----------------------------------------------------
+    def lanczos_gk(self, a, iters, v0, truth=None, record_timing=False, want_bases=False):
+        """baselines.cpp:51-166 on a dense A; returns a dict shaped like
+        LanczosResult."""
+        a = _colmajor(a)
+        m, n = a.shape
+        v0 = _f64(v0)
+        res, rows, v, vb, ub = _lanczos_buffers(m, n, iters, want_bases)
+        tr = None
+        if truth is not None:
+            vmin = _f64(truth[1])
+            tr = abi.Truth(float(truth[0]), _p(vmin))
+        self._check(self._lz(_p(a), m, n, int(iters), _p(v0), C.byref(tr) if tr else None, int(record_timing),
+                             C.byref(res)))
+        return lanczos_dict(res, rows, v, vb, ub)
+
+
+def _lanczos_buffers(m, n, iters, want_bases):
+    cap = max(int(iters), 1)
+    rows = (abi.RecordRow * cap)()
+    v = np.zeros(n)
+    res = abi.LanczosResult()
+    res.v = _p(v)
+    res.rows = rows
+    res.rows_capacity = cap
+    vb = ub = None
+    if want_bases:
+        vb = np.zeros((n, cap), order="F")
+        ub = np.zeros((m, cap), order="F")
+        res.v_basis = _p(vb)
+        res.u_basis = _p(ub)
+    return res, rows, v, vb, ub
+
+
+def lanczos_dict(res, rows, v, vb, ub):
+    cnt = res.rows_count
+    rec = [dict(iter=r.iter, matvecs_a=r.matvecs_a, matvecs_at=r.matvecs_at, wall_ms=r.wall_ms,
+                theta=r.theta, resid=r.resid, relerr=r.relerr, sin_angle=r.sin_angle)
+           for r in rows[:min(cnt, res.rows_capacity)]]
+    steps = res.steps
+    return dict(sigma_min=res.sigma_min, v=v.copy(), record=rec, steps=steps,
+                status="completed" if res.status == abi.LANCZOS_COMPLETED else "invariant_subspace",
+                v_basis=None if vb is None else vb[:, :steps].copy(order="F"),
+                u_basis=None if ub is None else ub[:, :steps].copy(order="F"))
 
 
 def _result_dict(res, rows, sigma, v, vt, sig, trail, has_truth):

@@ -10,6 +10,7 @@
 #include <exception>
 #include <string>
 
+#include "minsvd/baselines.hpp"
 #include "minsvd/errors.hpp"
 #include "minsvd/matgen.hpp"
 #include "minsvd/operator.hpp"
@@ -277,6 +278,47 @@ int ref_lobpcg_solve(const double* a, int64_t m, int64_t n, const msvd_options* 
                 res->iterate_cb(res->iterate_user, 1, static_cast<int32_t>(i), r.trail_v[i].data(),
                                 r.trail_v[i].rows(), r.trail_v[i].cols());
         }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// baselines.cpp:51-166 lanczos_gk on a DenseOperator (A column-major m x n).
+int ref_lanczos_gk(const double* a, int64_t m, int64_t n, int iters, const double* v0,
+                   const msvd_truth* truth, int record_timing, msvd_lanczos_result* res) {
+    try {
+        DenseOperator op(wrap(a, m, n));
+        GroundTruth gt;
+        const GroundTruth* gtp = nullptr;
+        if (truth) {
+            gt.sigma_min = truth->sigma_min;
+            gt.v_min.assign(truth->v_min, truth->v_min + n);
+            gtp = &gt;
+        }
+        Vector v(v0, v0 + n);
+        LanczosResult r = lanczos_gk(op, iters, v, gtp, record_timing != 0);
+        res->sigma_min = r.sigma_min;
+        std::memcpy(res->v, r.v.data(), sizeof(double) * r.v.size());
+        res->rows_count = static_cast<int32_t>(r.record.rows.size());
+        for (size_t i = 0; i < r.record.rows.size() && static_cast<int32_t>(i) < res->rows_capacity;
+             ++i) {
+            const RecordRow& src = r.record.rows[i];
+            msvd_record_row& dst = res->rows[i];
+            dst.iter = src.iter;
+            dst.matvecs_a = src.matvecs_a;
+            dst.matvecs_at = src.matvecs_at;
+            dst.wall_ms = src.wall_ms;
+            dst.theta = src.theta;
+            dst.resid = src.resid;
+            dst.relerr = src.relerr;
+            dst.sin_angle = src.sin_angle;
+        }
+        res->status = r.status == LanczosStatus::completed ? MSVD_LANCZOS_COMPLETED
+                                                           : MSVD_LANCZOS_INVARIANT_SUBSPACE;
+        res->steps = r.steps;
+        if (res->v_basis) unwrap(r.v_basis, res->v_basis);
+        if (res->u_basis) unwrap(r.u_basis, res->u_basis);
         return 0;
     } catch (const std::exception& e) {
         return fail(e);

@@ -97,6 +97,27 @@ class Result(C.Structure):
     ]
 
 
+LANCZOS_COMPLETED = 0
+LANCZOS_INVARIANT_SUBSPACE = 1
+
+
+class LanczosResult(C.Structure):
+    """baselines.hpp:25-33 LanczosResult (msvd_lanczos_result); arrays are
+    caller-owned."""
+
+    _fields_ = [
+        ("sigma_min", C.c_double),
+        ("v", C.POINTER(C.c_double)),
+        ("rows", C.POINTER(RecordRow)),
+        ("rows_capacity", C.c_int32),
+        ("rows_count", C.c_int32),
+        ("status", C.c_int32),
+        ("steps", C.c_int32),
+        ("v_basis", C.POINTER(C.c_double)),
+        ("u_basis", C.POINTER(C.c_double)),
+    ]
+
+
 class CtxDesc(C.Structure):
     _fields_ = [
         ("device", C.c_int32),

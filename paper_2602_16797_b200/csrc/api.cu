@@ -880,9 +880,9 @@ int32_t msvd_ctx_profile_read(msvd_ctx* ctx, double* ms, int64_t* counts, int32_
 }
 
 void msvd_abi_sizes(int64_t* out, int32_t n) {
-    const int64_t s[5] = {sizeof(msvd_options), sizeof(msvd_record_row), sizeof(msvd_truth), sizeof(msvd_result),
-                          sizeof(msvd_ctx_desc)};
-    for (int i = 0; i < n && i < 5; ++i) out[i] = s[i];
+    const int64_t s[6] = {sizeof(msvd_options), sizeof(msvd_record_row), sizeof(msvd_truth), sizeof(msvd_result),
+                          sizeof(msvd_ctx_desc), sizeof(msvd_lanczos_result)};
+    for (int i = 0; i < n && i < 6; ++i) out[i] = s[i];
 }
 
 int32_t msvd_matrix_attach(msvd_ctx* ctx, const double* dA, int64_t m_local, int64_t n, int64_t ld, int64_t row0,
@@ -1182,6 +1182,19 @@ int32_t msvd_small_svd(msvd_ctx* ctx, const double* dB, int64_t k, double* dSigm
         const DevState h = read_state(c, st);
         if (std::getenv("MSVD_DEBUG_JACOBI")) std::fprintf(stderr, "msvd_small_svd: k=%lld sweeps=%g\n",
                                                          static_cast<long long>(k), h.worst_jacobi);
+    });
+}
+
+int32_t msvd_lanczos_gk(msvd_matrix* mat, int32_t iters, const double* v0, const msvd_truth* truth,
+                        int32_t record_timing, msvd_lanczos_result* res) {
+    return guard([&] {
+        need(mat, "matrix");
+        need(v0, "starting vector");
+        need(res, "result");
+        need(res->v, "result vector");
+        Ctx& c = mat->ctx->c;
+        set_device(c);
+        lanczos_run(c, *mat, iters, v0, truth, record_timing != 0, res);
     });
 }
 

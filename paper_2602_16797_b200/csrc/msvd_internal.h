@@ -203,6 +203,10 @@ void sketch_finish(Ctx& c, const double* SAr, int64_t d, int64_t n, double* SA);
 void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double* Vcol,
                        double* Vrow, double* sig, double* sigma_max, int64_t* nfloor, int tail_hint = 8);
 
+// ---- Golub-Kahan-Lanczos baseline (lanczos.cu) ---------------------------
+void lanczos_run(Ctx& c, const msvd_matrix& M, int iters, const double* v0h, const msvd_truth* truth, bool timing,
+                 msvd_lanczos_result* res);
+
 // ---- communicator (comm.cu) ----------------------------------------------
 struct Comm {
     virtual ~Comm() = default;

@@ -107,6 +107,7 @@ def _declare(lib):
         "msvd_aw_tsqr": (i32, [vp, vp, i64, vp, i64, vp, vp]),
         "msvd_aw_gram": (i32, [vp, vp, i64, vp, vp]),
         "msvd_small_svd": (i32, [vp, vp, i64, vp, vp]),
+        "msvd_lanczos_gk": (i32, [vp, i32, vp, P(abi.Truth), i32, P(abi.LanczosResult)]),
         "msvd_lobpcg_solve": (i32, [vp, P(abi.Options), P(abi.Truth), P(abi.Result)]),
         "msvd_rlobpcg_single": (i32, [vp, P(abi.Options), P(abi.Truth), P(abi.Result)]),
         "msvd_rlobpcg_block": (i32, [vp, P(abi.Options), P(abi.Truth), P(abi.Result)]),
@@ -130,7 +131,7 @@ EXPORTED = (
     "msvd_fake_group_destroy msvd_ctx_create msvd_ctx_destroy msvd_ctx_synchronize msvd_matrix_attach "
     "msvd_matrix_detach msvd_apply msvd_apply_adjoint msvd_column_norms msvd_build_sparsestack msvd_sketch "
     "msvd_precond_build msvd_precond_apply msvd_tsqr_r msvd_gram_apply msvd_aw_tsqr msvd_aw_gram msvd_small_svd "
-    "msvd_lobpcg_solve msvd_rlobpcg_single "
+    "msvd_lanczos_gk msvd_lobpcg_solve msvd_rlobpcg_single "
     "msvd_rlobpcg_block msvd_solve_host msvd_launch_count msvd_abi_sizes msvd_ctx_profile msvd_ctx_profile_read"
 ).split()
 
@@ -595,6 +596,77 @@ def rlobpcg_single(a, opts=None, truth=None, want_precond=False):
 def rlobpcg_block(a, opts=None, truth=None, want_precond=False):
     """solver.hpp:180-181"""
     return _run("msvd_rlobpcg_block", a, abi.PRECOND_RANDOMIZED, opts, truth, want_precond)
+
+
+# ------------------------------------------------ baselines.hpp:12-42
+def lobpcg_generic(a, kind=PrecondKind.randomized, opts=None, truth=None, want_precond=False):
+    """baselines.hpp:12-14: LOBPCG with a selectable preconditioner kind."""
+    return lobpcg_solve(a, kind, opts, truth, want_precond)
+
+
+def sketch_and_solve_init(precond, b):
+    """precond.cpp:50-57: the last b columns of V-tilde."""
+    vt = precond.vtilde
+    if vt is None:
+        raise DimensionError("sketch_and_solve_init: preconditioner factors were not requested")
+    n = vt.shape[0]
+    if b < 1 or b > n:
+        raise DimensionError("sketch_and_solve_init: block size out of range")
+    return vt[:, n - b:].copy()
+
+
+class LanczosStatus:
+    completed = "completed"
+    invariant_subspace = "invariant_subspace"
+
+
+@dataclass
+class LanczosResult:
+    """baselines.hpp:25-33"""
+
+    sigma_min: float
+    v: np.ndarray
+    record: ConvergenceRecord
+    status: str
+    steps: int
+    v_basis: Optional[np.ndarray] = None
+    u_basis: Optional[np.ndarray] = None
+
+
+def lanczos_gk(a, iters, v0, truth=None, record_timing=True, want_bases=False):
+    """baselines.cpp:51-166 on the device (msvd_lanczos_gk)."""
+    if not isinstance(a, DeviceDenseOperator):
+        raise DimensionError("msvd: lanczos_gk accepts a DeviceDenseOperator only (no CPU fallback)")
+    v0 = np.ascontiguousarray(np.asarray(v0, dtype=np.float64).reshape(-1))
+    if v0.size != a.n:
+        raise DimensionError("lanczos_gk: starting vector length mismatch")
+    t, keep = _truth(truth, a.n) if truth is not None else (None, None)
+    if truth is not None and keep.size != a.n:
+        raise DimensionError("lanczos_gk: ground-truth vector length mismatch")
+    cap = max(int(iters), 1)
+    rows = (abi.RecordRow * cap)()
+    v = np.zeros(a.n)
+    r = abi.LanczosResult()
+    r.v = v.ctypes.data_as(C.POINTER(C.c_double))
+    r.rows = rows
+    r.rows_capacity = cap
+    vb = ub = None
+    if want_bases:
+        vb = np.zeros((a.n, cap), order="F")
+        ub = np.zeros((a.m_local, cap), order="F")
+        r.v_basis = vb.ctypes.data_as(C.POINTER(C.c_double))
+        r.u_basis = ub.ctypes.data_as(C.POINTER(C.c_double))
+    check(lib().msvd_lanczos_gk(a.handle, int(iters), v0.ctypes.data_as(C.c_void_p),
+                                C.byref(t) if t is not None else None, int(bool(record_timing)), C.byref(r)))
+    del keep
+    recs = [RecordRow(x.iter, x.matvecs_a, x.matvecs_at, x.wall_ms, x.theta, x.resid, x.relerr, x.sin_angle)
+            for x in rows[:min(r.rows_count, cap)]]
+    steps = r.steps
+    return LanczosResult(sigma_min=r.sigma_min, v=v, record=ConvergenceRecord(recs, truth is not None),
+                         status=(LanczosStatus.completed if r.status == abi.LANCZOS_COMPLETED
+                                 else LanczosStatus.invariant_subspace), steps=steps,
+                         v_basis=None if vb is None else vb[:, :steps].copy(order="F"),
+                         u_basis=None if ub is None else ub[:, :steps].copy(order="F"))
 
 
 def solve_host(a_host, opts=None, truth=None, ctx=None, row0=0, m_global=None, kind=abi.PRECOND_RANDOMIZED,

@@ -33,10 +33,10 @@ def test_library_exports_every_declared_symbol(msvd):
 
 
 def test_abi_struct_sizes_match_ctypes(msvd):
-    sizes = (C.c_int64 * 5)()
-    msvd.lib().msvd_abi_sizes(sizes, 5)
+    sizes = (C.c_int64 * 6)()
+    msvd.lib().msvd_abi_sizes(sizes, 6)
     assert list(sizes) == [C.sizeof(abi.Options), C.sizeof(abi.RecordRow), C.sizeof(abi.Truth),
-                           C.sizeof(abi.Result), C.sizeof(abi.CtxDesc)]
+                           C.sizeof(abi.Result), C.sizeof(abi.CtxDesc), C.sizeof(abi.LanczosResult)]
 
 
 def test_defaults_match_solver_options(msvd):

@@ -232,3 +232,61 @@ def test_port_validation_errors(port, ref):
         with pytest.raises(OracleError) as e:
             o.lobpcg_solve(nan, abi.default_options())
         assert e.value.code == abi.MSVD_ERR_NUMERICAL
+
+
+# ------------------------------------------------- lanczos_gk (baselines)
+def lanczos_rows(r):
+    return [[x["iter"], x["matvecs_a"], x["matvecs_at"], float(x["theta"]).hex(), float(x["resid"]).hex(),
+             float(x["relerr"]).hex(), float(x["sin_angle"]).hex()] for x in r["record"]]
+
+
+@pytest.mark.parametrize("name", sorted(GOLDEN["lanczos"]))
+def test_port_reproduces_lanczos_golden(port, name):
+    case = GOLDEN["lanczos"][name]
+    sig, a, vmin = matrix(port, case)
+    assert sha(a) == case["a_sha256"], "input regeneration drifted"
+    r = port.lanczos_gk(a, case["iters"], unhex(case["v0"]), truth=(sig[-1], vmin))
+    assert r["steps"] == case["steps"] and r["status"] == case["status"]
+    assert float(r["sigma_min"]).hex() == case["sigma_min"]
+    assert np.array_equal(r["v"], unhex(case["v"]))
+    assert lanczos_rows(r) == case["record"]
+
+
+def test_lanczos_port_equals_reference(port, ref):
+    """Step counts, early exits and both bases, bit for bit."""
+    rng = np.random.default_rng(5)
+    q = np.linalg.qr(rng.standard_normal((200, 24)))[0]
+    a = q @ np.diag(np.logspace(0, -5, 24)) @ np.linalg.qr(rng.standard_normal((24, 24)))[0].T
+    v0 = rng.standard_normal(24)
+    for iters in (1, 2, 7, 24):
+        r1 = port.lanczos_gk(a, iters, v0, want_bases=True)
+        r2 = ref.lanczos_gk(a, iters, v0, want_bases=True)
+        for key in ("steps", "status", "record"):
+            assert r1[key] == r2[key], (iters, key)
+        for key in ("v", "v_basis", "u_basis"):
+            assert np.array_equal(r1[key], r2[key]), (iters, key)
+        assert r1["sigma_min"] == r2["sigma_min"]
+    # exact null start: A v0 = 0 -> invariant subspace before any step
+    z = a.copy()
+    z[:, 3] = 0.0
+    e = np.zeros(24)
+    e[3] = 1.0
+    for o in (port, ref):
+        r = o.lanczos_gk(z, 5, e)
+        assert r["status"] == "invariant_subspace" and r["steps"] == 0 and r["sigma_min"] == 0.0
+        assert np.array_equal(r["v"], e)
+
+
+def test_lanczos_validation_errors(port, ref):
+    """baselines.cpp:53-61 error classes."""
+    from oracle.pyoracle import OracleError
+
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((30, 6))
+    cases = [(a, 0, np.ones(6), abi.MSVD_ERR_DIMENSION), (a, 7, np.ones(6), abi.MSVD_ERR_DIMENSION),
+             (a, 3, np.zeros(6), abi.MSVD_ERR_NUMERICAL), (a[:4], 2, np.ones(6), abi.MSVD_ERR_DIMENSION)]
+    for o in (port, ref):
+        for mat, iters, v0, code in cases:
+            with pytest.raises(OracleError) as e:
+                o.lanczos_gk(mat, iters, v0)
+            assert e.value.code == code, (iters, e.value)
