@@ -160,22 +160,17 @@ private:
     msvd_ctx* ctx_ = nullptr;
 };
 
-class DeviceDenseOperator {
+// Common handle of the device operators: the products and passes of one
+// LinearOperator (operator.hpp:15-39) over device memory.
+class DeviceOperator {
 public:
-    // borrowed device pointer: rows [row0, row0 + m_local) of an m_global x n
-    // row-major matrix with leading dimension ld
-    DeviceDenseOperator(const Context& ctx, const double* dA, index_t m_local, index_t n, index_t ld,
-                        index_t row0 = 0, index_t m_global = -1)
-        : m_(m_global < 0 ? m_local : m_global), n_(n) {
-        check(msvd_matrix_attach(ctx.get(), dA, m_local, n, ld, row0, m_, &mat_));
-    }
-    ~DeviceDenseOperator() { msvd_matrix_detach(mat_); }
-    DeviceDenseOperator(const DeviceDenseOperator&) = delete;
-    DeviceDenseOperator& operator=(const DeviceDenseOperator&) = delete;
+    virtual ~DeviceOperator() { msvd_matrix_detach(mat_); }
+    DeviceOperator(const DeviceOperator&) = delete;
+    DeviceOperator& operator=(const DeviceOperator&) = delete;
 
     index_t rows() const { return m_; }
     index_t cols() const { return n_; }
-    index_t nnz() const { return m_ * n_; }
+    virtual index_t nnz() const = 0;
     // device-to-device block products (column-major blocks)
     void apply_block(const double* dX, index_t b, double* dY) const { check(msvd_apply(mat_, dX, b, dY)); }
     void apply_adjoint_block(const double* dY, index_t b, double* dX) const {
@@ -197,9 +192,40 @@ public:
     }
     msvd_matrix* get() const { return mat_; }
 
-private:
+protected:
+    DeviceOperator(index_t m, index_t n) : m_(m), n_(n) {}
     msvd_matrix* mat_ = nullptr;
     index_t m_, n_;
+};
+
+// operator.hpp:41-56 DenseOperator: borrowed device pointer, rows
+// [row0, row0 + m_local) of an m_global x n row-major matrix (leading dim ld)
+class DeviceDenseOperator final : public DeviceOperator {
+public:
+    DeviceDenseOperator(const Context& ctx, const double* dA, index_t m_local, index_t n, index_t ld,
+                        index_t row0 = 0, index_t m_global = -1)
+        : DeviceOperator(m_global < 0 ? m_local : m_global, n) {
+        check(msvd_matrix_attach(ctx.get(), dA, m_local, n, ld, row0, m_, &mat_));
+    }
+    index_t nnz() const override { return m_ * n_; }
+};
+
+// operator.hpp:58-74 CsrOperator: borrowed device CSR arrays of the local
+// rows (row offsets int64, column indices of index_bytes = 4 or 8, values);
+// validated like CsrMatrix::validate at construction
+class DeviceCsrOperator final : public DeviceOperator {
+public:
+    DeviceCsrOperator(const Context& ctx, const int64_t* dRowOffsets, const void* dColIndices, int index_bytes,
+                      const double* dValues, index_t m_local, index_t n, index_t nnz, index_t row0 = 0,
+                      index_t m_global = -1)
+        : DeviceOperator(m_global < 0 ? m_local : m_global, n), nnz_(nnz) {
+        check(msvd_csr_attach(ctx.get(), dRowOffsets, dColIndices, index_bytes, dValues, m_local, n, nnz, row0, m_,
+                              &mat_));
+    }
+    index_t nnz() const override { return nnz_; }
+
+private:
+    index_t nnz_;
 };
 
 namespace detail {
@@ -209,7 +235,7 @@ inline void iterate_sink(void* user, int32_t kind, int32_t, const double* data, 
 }
 
 inline SolveResult run(int32_t (*fn)(msvd_matrix*, const msvd_options*, const msvd_truth*, msvd_result*),
-                       const DeviceDenseOperator& a, PrecondKind kind, const SolverOptions& opts,
+                       const DeviceOperator& a, PrecondKind kind, const SolverOptions& opts,
                        const GroundTruth* truth, bool force_single) {
     msvd_options o = opts.to_abi(kind);
     if (force_single) o.block_size = 1;
@@ -256,21 +282,21 @@ inline SolveResult run(int32_t (*fn)(msvd_matrix*, const msvd_options*, const ms
 }  // namespace detail
 
 // solver.hpp:172-181
-inline SolveResult lobpcg_solve(const DeviceDenseOperator& a, PrecondKind kind, const SolverOptions& opts,
+inline SolveResult lobpcg_solve(const DeviceOperator& a, PrecondKind kind, const SolverOptions& opts,
                                 const GroundTruth* truth = nullptr) {
     return detail::run(&msvd_lobpcg_solve, a, kind, opts, truth, false);
 }
-inline SolveResult rlobpcg_single(const DeviceDenseOperator& a, const SolverOptions& opts,
+inline SolveResult rlobpcg_single(const DeviceOperator& a, const SolverOptions& opts,
                                   const GroundTruth* truth = nullptr) {
     return detail::run(&msvd_rlobpcg_single, a, PrecondKind::randomized, opts, truth, true);
 }
-inline SolveResult rlobpcg_block(const DeviceDenseOperator& a, const SolverOptions& opts,
+inline SolveResult rlobpcg_block(const DeviceOperator& a, const SolverOptions& opts,
                                  const GroundTruth* truth = nullptr) {
     return detail::run(&msvd_rlobpcg_block, a, PrecondKind::randomized, opts, truth, false);
 }
 
 // ---- baselines.hpp:12-42 ---------------------------------------------------
-inline SolveResult lobpcg_generic(const DeviceDenseOperator& a, PrecondKind kind, const SolverOptions& opts,
+inline SolveResult lobpcg_generic(const DeviceOperator& a, PrecondKind kind, const SolverOptions& opts,
                                   const GroundTruth* truth = nullptr) {
     return lobpcg_solve(a, kind, opts, truth);
 }
@@ -288,7 +314,7 @@ struct LanczosResult {
 };
 
 // baselines.cpp:51-166 on the device (msvd_lanczos_gk)
-inline LanczosResult lanczos_gk(const DeviceDenseOperator& a, int iters, const Vector& v0,
+inline LanczosResult lanczos_gk(const DeviceOperator& a, int iters, const Vector& v0,
                                 const GroundTruth* truth = nullptr, bool record_timing = true,
                                 index_t m_local = -1) {
     if (static_cast<index_t>(v0.size()) != a.cols())

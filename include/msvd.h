@@ -162,6 +162,21 @@ int32_t msvd_matrix_attach(msvd_ctx* ctx, const double* dA, int64_t m_local,
                            int64_t n, int64_t ld, int64_t row0,
                            int64_t m_global, msvd_matrix** out);
 int32_t msvd_matrix_detach(msvd_matrix* mat);
+/* operator.hpp:58-74 CsrOperator over device memory (csr.hpp:10-25
+ * CsrMatrix): borrowed row offsets (int64, m_local + 1), column indices
+ * (index_bytes = 4 or 8, sorted and unique per row) and values (nnz), local
+ * rows [row0, row0 + m_local) of an m_global x n operator.  Validated like
+ * CsrMatrix::validate (csr.cpp:9-31: DimensionError / NumericalError with
+ * the reference's messages); the transpose is built once here so adjoint
+ * products are deterministic gathers.  Every entry point taking an
+ * msvd_matrix (products, sketch, solves, lanczos) accepts it; the handle
+ * must be released with msvd_matrix_detach.  Limits: < 2^31 local rows,
+ * < 2^32 local nonzeros.                                                    */
+int32_t msvd_csr_attach(msvd_ctx* ctx, const int64_t* dRowOffsets,
+                        const void* dColIndices, int32_t index_bytes,
+                        const double* dValues, int64_t m_local, int64_t n,
+                        int64_t nnz, int64_t row0, int64_t m_global,
+                        msvd_matrix** out);
 /* operator.cpp:7-12 apply_block: dY (m_local x b) = A dX (n x b)           */
 int32_t msvd_apply(msvd_matrix* mat, const double* dX, int64_t b, double* dY);
 /* operator.cpp:14-19 apply_adjoint_block: dX (n x b) = A^T dY (m_local x b),

@@ -386,6 +386,99 @@ static mat sstack_apply(sstack s, mat a) {
     return out;
 }
 
+/* ------------------------------------------------------- CSR (csr.cpp) */
+
+typedef struct { int64_t rows, cols; const int64_t *rp, *ci; const double *v; } csr;
+
+static int64_t csr_nnz(csr a) { return a.rp[a.rows]; }
+
+/* CsrMatrix::validate (csr.cpp:9-31), same checks in the same order */
+static void csr_validate(csr a, int64_t nnz) {
+    if (a.rows < 0 || a.cols < 0) raise_err(MSVD_ERR_DIMENSION, "CsrMatrix: negative dimension");
+    if (a.rp[0] != 0 || a.rp[a.rows] != nnz)
+        raise_err(MSVD_ERR_DIMENSION, "CsrMatrix: row_offsets endpoints inconsistent with nnz");
+    for (int64_t i = 0; i < a.rows; ++i) {
+        if (a.rp[i] > a.rp[i + 1])
+            raise_err(MSVD_ERR_DIMENSION, "CsrMatrix: row_offsets not nondecreasing at row %lld", (long long)i);
+        for (int64_t k = a.rp[i]; k < a.rp[i + 1]; ++k) {
+            const int64_t j = a.ci[k];
+            if (j < 0 || j >= a.cols)
+                raise_err(MSVD_ERR_DIMENSION, "CsrMatrix: column index out of range in row %lld", (long long)i);
+            if (k > a.rp[i] && a.ci[k - 1] >= j)
+                raise_err(MSVD_ERR_DIMENSION, "CsrMatrix: column indices not strictly increasing in row %lld",
+                          (long long)i);
+        }
+    }
+    for (int64_t k = 0; k < nnz; ++k)
+        if (!isfinite(a.v[k])) raise_err(MSVD_ERR_NUMERICAL, "CsrMatrix: non-finite value");
+}
+/* CsrMatrix::matvec (csr.cpp:33-44) */
+static void csr_matvec(csr a, const double *x, double *y) {
+    for (int64_t i = 0; i < a.rows; ++i) {
+        double s = 0.0;
+        for (int64_t k = a.rp[i]; k < a.rp[i + 1]; ++k) s += a.v[k] * x[a.ci[k]];
+        y[i] = s;
+    }
+}
+/* CsrMatrix::matvec_adjoint (csr.cpp:46-57): scatter, zero y_i skipped */
+static void csr_matvec_t(csr a, const double *y, double *x) {
+    for (int64_t j = 0; j < a.cols; ++j) x[j] = 0.0;
+    for (int64_t i = 0; i < a.rows; ++i) {
+        const double yi = y[i];
+        if (yi == 0.0) continue;
+        for (int64_t k = a.rp[i]; k < a.rp[i + 1]; ++k) x[a.ci[k]] += a.v[k] * yi;
+    }
+}
+/* CsrMatrix::to_dense (csr.cpp:59-65) */
+static mat csr_dense(csr a) {
+    mat d = mnew(a.rows, a.cols);
+    for (int64_t i = 0; i < a.rows; ++i)
+        for (int64_t k = a.rp[i]; k < a.rp[i + 1]; ++k) AT(d, i, a.ci[k]) = a.v[k];
+    return d;
+}
+/* sketch_apply(S, CsrMatrix) (sketch.cpp:97-118): rows outer, x = v * val */
+static mat sstack_apply_csr(sstack s, csr a) {
+    if (a.rows != s.m)
+        raise_err(MSVD_ERR_DIMENSION, "sketch_apply: operand has %lld rows, embedding expects %lld",
+                  (long long)a.rows, (long long)s.m);
+    mat out = mnew(s.d, a.cols);
+    const double val = 1.0 / sqrt((double)s.zeta);
+    const int64_t blk_rows = s.d / s.zeta;
+    for (int64_t r = 0; r < a.rows; ++r)
+        for (int64_t p = a.rp[r]; p < a.rp[r + 1]; ++p) {
+            const double x = a.v[p] * val;
+            double *oj = col(out, a.ci[p]);
+            for (int k = 0; k < s.zeta; ++k)
+                oj[blk_rows * k + s.pos[r * s.zeta + k]] += (double)s.sgn[r * s.zeta + k] * x;
+        }
+    return out;
+}
+
+/* ------------------------------------- LinearOperator (operator.hpp:15-39) */
+
+typedef struct { int is_csr; mat d; csr s; } op;
+
+static int64_t op_rows(op a) { return a.is_csr ? a.s.rows : a.d.r; }
+static int64_t op_cols(op a) { return a.is_csr ? a.s.cols : a.d.c; }
+static void op_apply(op a, const double *x, double *y) { if (a.is_csr) csr_matvec(a.s, x, y); else matvec(a.d, x, y); }
+static void op_adjoint(op a, const double *y, double *x) {
+    if (a.is_csr) csr_matvec_t(a.s, y, x); else matvec_t(a.d, y, x);
+}
+static mat op_dense(op a) { return a.is_csr ? csr_dense(a.s) : a.d; }
+static mat op_sketch(sstack s, op a) { return a.is_csr ? sstack_apply_csr(s, a.s) : sstack_apply(s, a.d); }
+/* column_norms: DenseOperator (operator.cpp:39-48), CsrOperator (:98-104) */
+static void op_colnorms(op a, double *out) {
+    const int64_t n = op_cols(a);
+    if (!a.is_csr) {
+        for (int64_t j = 0; j < n; ++j) out[j] = colnorm_from(a.d, j, 0);
+        return;
+    }
+    for (int64_t j = 0; j < n; ++j) out[j] = 0.0;
+    const int64_t nnz = csr_nnz(a.s);
+    for (int64_t k = 0; k < nnz; ++k) out[a.s.ci[k]] += a.s.v[k] * a.s.v[k];
+    for (int64_t j = 0; j < n; ++j) out[j] = sqrt(out[j]);
+}
+
 /* -------------------------------------------------- preconditioner (precond.cpp) */
 
 typedef struct { mat vt; double *sig; double smax; int floored; int64_t nfloor; } pcond;
@@ -527,9 +620,9 @@ static mat hcat3(mat a, mat b, mat c) {
     if (c.c) memcpy(col(o, at), c.p, sizeof(double) * (size_t)(a.r * c.c));
     return o;
 }
-static mat apply_cols(mat a, mat x) { /* operator.cpp:7-12 via DenseOperator::apply */
-    mat y = mnew(a.r, x.c);
-    for (int64_t j = 0; j < x.c; ++j) matvec(a, col(x, j), col(y, j));
+static mat apply_cols(op a, mat x) { /* operator.cpp:7-12 apply_block, column by column */
+    mat y = mnew(op_rows(a), x.c);
+    for (int64_t j = 0; j < x.c; ++j) op_apply(a, col(x, j), col(y, j));
     return y;
 }
 
@@ -578,11 +671,11 @@ static void record_row(recorder *R, int iter, mat vcur, const double *theta, dou
 }
 
 /* R = A^T AV - theta^2 V per column (:357-369) */
-static mat residual_block(mat a, mat v, mat av, const double *th, long *mvat) {
+static mat residual_block(op a, mat v, mat av, const double *th, long *mvat) {
     mat r = mnew(v.r, v.c);
     for (int64_t j = 0; j < v.c; ++j) {
         double *rc = col(r, j);
-        matvec_t(a, col(av, j), rc);
+        op_adjoint(a, col(av, j), rc);
         ++*mvat;
         const double t2 = th[j] * th[j];
         const double *vc = col(v, j);
@@ -596,9 +689,8 @@ static void emit(msvd_result *res, int kind, int iter, mat m) {
 }
 
 /* lobpcg_solve (solver.cpp:301-477) on a dense column-major A */
-static void solve_dense(mat a, const msvd_options *o, const msvd_truth *truth, msvd_result *res) {
-    const int64_t m = a.r, n = a.c, b = o->block_size;
-    if (!finite_all(a.p, m * n)) raise_err(MSVD_ERR_NUMERICAL, "DenseOperator: non-finite entry");
+static void solve_op(op a, const msvd_options *o, const msvd_truth *truth, msvd_result *res) {
+    const int64_t m = op_rows(a), n = op_cols(a), b = o->block_size;
     if (m < n) raise_err(MSVD_ERR_DIMENSION, "solver: matrix must have at least as many rows as columns");
     if (b < 1) raise_err(MSVD_ERR_DIMENSION, "solver: block size must be positive");
     if (n < 3 * b) raise_err(MSVD_ERR_DIMENSION, "solver: need at least 3x block size columns");
@@ -626,7 +718,7 @@ static void solve_dense(mat a, const msvd_options *o, const msvd_truth *truth, m
     int skipped = 0;
     if (o->sketch_dim < 0 && m <= 4 * n) {
         skipped = 1;
-        P = pcond_build(a);
+        P = pcond_build(op_dense(a));
     } else {
         if (o->sketch_dim < 0 && o->zeta <= 0)
             raise_err(MSVD_ERR_DIMENSION, "round_up_to_multiple: zeta must be positive");
@@ -634,7 +726,7 @@ static void solve_dense(mat a, const msvd_options *o, const msvd_truth *truth, m
                                       : o->sketch_dim;
         if (d < n) raise_err(MSVD_ERR_DIMENSION, "solver: sketch dimension below column count");
         sstack s = sstack_build(d, m, o->zeta, o->seed);
-        P = pcond_build(sstack_apply(s, a));
+        P = pcond_build(op_sketch(s, a));
         dim = d;
     }
     if (b > n) raise_err(MSVD_ERR_DIMENSION, "sketch_and_solve_init: block size out of range");
@@ -657,8 +749,9 @@ static void solve_dense(mat a, const msvd_options *o, const msvd_truth *truth, m
     double *dinv = NULL;
     if (o->precond_kind == MSVD_PRECOND_DIAGONAL) {
         dinv = (double *)zalloc(sizeof(double) * (size_t)n);
+        op_colnorms(a, dinv);
         for (int64_t j = 0; j < n; ++j) {
-            const double c = colnorm_from(a, j, 0);
+            const double c = dinv[j];
             dinv[j] = c > 0.0 ? 1.0 / (c * c) : 1.0;
         }
     }
@@ -768,9 +861,9 @@ static void reorth_mgs(double *w, int64_t len, mat basis, int64_t used) {
 }
 
 /* lanczos_gk (baselines.cpp:51-166) on a dense column-major A */
-static void lanczos_dense(mat a, int iters, const double *v0, const msvd_truth *truth, int timing,
-                          msvd_lanczos_result *res) {
-    const int64_t m = a.r, n = a.c;
+static void lanczos_op(op a, int iters, const double *v0, const msvd_truth *truth, int timing,
+                       msvd_lanczos_result *res) {
+    const int64_t m = op_rows(a), n = op_cols(a);
     if (m < n) raise_err(MSVD_ERR_DIMENSION, "lanczos_gk: matrix must be tall");
     if (iters < 1 || iters > n) raise_err(MSVD_ERR_DIMENSION, "lanczos_gk: step count must lie in [1, cols]");
     const double v0n = vnorm(v0, n);
@@ -787,7 +880,7 @@ static void lanczos_dense(mat a, int iters, const double *v0, const msvd_truth *
     memcpy(col(vb, 0), v, sizeof(double) * (size_t)n);
 
     double *u = (double *)zalloc(sizeof(double) * (size_t)m);
-    matvec(a, v, u);
+    op_apply(a, v, u);
     long mva = 1, mvat = 0;
     const double a1 = vnorm(u, m);
     res->rows_count = 0;
@@ -808,7 +901,7 @@ static void lanczos_dense(mat a, int iters, const double *v0, const msvd_truth *
     double *vest = (double *)zalloc(sizeof(double) * (size_t)n);
     double *un = (double *)zalloc(sizeof(double) * (size_t)m);
     for (int j = 1; j <= iters; ++j) {
-        matvec_t(a, col(ub, j - 1), w);
+        op_adjoint(a, col(ub, j - 1), w);
         ++mvat;
         const double *vp = col(vb, j - 1);
         for (int64_t i = 0; i < n; ++i) w[i] += -alpha[j - 1] * vp[i];
@@ -861,7 +954,7 @@ static void lanczos_dense(mat a, int iters, const double *v0, const msvd_truth *
 
         vscale(w, n, 1.0 / bj);
         memcpy(col(vb, j), w, sizeof(double) * (size_t)n);
-        matvec(a, w, un);
+        op_apply(a, w, un);
         ++mva;
         const double *up = col(ub, j - 1);
         for (int64_t i = 0; i < m; ++i) un[i] += -bj * up[i];
@@ -882,7 +975,53 @@ static void lanczos_dense(mat a, int iters, const double *v0, const msvd_truth *
 int orc_lanczos_gk(const double *a_colmajor, int64_t m, int64_t n, int iters, const double *v0,
                    const msvd_truth *truth, int record_timing, msvd_lanczos_result *res) {
     ENTER();
-    lanczos_dense(mview((double *)a_colmajor, m, n), iters, v0, truth, record_timing, res);
+    op a = {0, mview((double *)a_colmajor, m, n), {0, 0, NULL, NULL, NULL}};
+    lanczos_op(a, iters, v0, truth, record_timing, res);
+    LEAVE();
+}
+
+/* CsrOperator (operator.hpp:58-74): validated at construction (csr.cpp:9-31) */
+static op csr_op(int64_t m, int64_t n, const int64_t *rp, const int64_t *ci, const double *v, int64_t nnz) {
+    op a = {1, {0, 0, NULL}, {m, n, rp, ci, v}};
+    csr_validate(a.s, nnz);
+    return a;
+}
+
+int orc_lanczos_gk_csr(int64_t m, int64_t n, const int64_t *rp, const int64_t *ci, const double *v, int64_t nnz,
+                       int iters, const double *v0, const msvd_truth *truth, int record_timing,
+                       msvd_lanczos_result *res) {
+    ENTER();
+    lanczos_op(csr_op(m, n, rp, ci, v, nnz), iters, v0, truth, record_timing, res);
+    LEAVE();
+}
+
+int orc_lobpcg_solve_csr(int64_t m, int64_t n, const int64_t *rp, const int64_t *ci, const double *v, int64_t nnz,
+                         const msvd_options *o, const msvd_truth *truth, msvd_result *res) {
+    ENTER();
+    solve_op(csr_op(m, n, rp, ci, v, nnz), o, truth, res);
+    LEAVE();
+}
+
+/* sketch_apply(S, CsrMatrix) of rows [row0, row0 + m) keyed by global row */
+int orc_sketch_csr(int64_t d, int zeta, uint64_t seed, int64_t m, int64_t n, const int64_t *rp, const int64_t *ci,
+                   const double *v, int64_t nnz, int64_t row0, double *sa) {
+    ENTER();
+    op a = csr_op(m, n, rp, ci, v, nnz);
+    sstack full = sstack_build(d, row0 + m, zeta, seed);
+    sstack s = {d, m, zeta, full.pos + row0 * zeta, full.sgn + row0 * zeta};
+    mat out = sstack_apply_csr(s, a.s);
+    memcpy(sa, out.p, sizeof(double) * (size_t)(d * n));
+    LEAVE();
+}
+
+/* y = A x, x = A^T y, column norms of a CSR operator (checker primitives) */
+int orc_csr_products(int64_t m, int64_t n, const int64_t *rp, const int64_t *ci, const double *v, int64_t nnz,
+                     const double *x, double *y, const double *yin, double *xout, double *norms) {
+    ENTER();
+    op a = csr_op(m, n, rp, ci, v, nnz);
+    if (x && y) csr_matvec(a.s, x, y);
+    if (yin && xout) csr_matvec_t(a.s, yin, xout);
+    if (norms) op_colnorms(a, norms);
     LEAVE();
 }
 
@@ -1040,6 +1179,9 @@ int orc_assemble_svd(const double *sigma, int64_t n, int64_t m, uint64_t seed, d
 int orc_lobpcg_solve(const double *a, int64_t m, int64_t n, const msvd_options *o, const msvd_truth *truth,
                      msvd_result *res) {
     ENTER();
-    solve_dense(mview((double *)a, m, n), o, truth, res);
+    mat d = mview((double *)a, m, n);
+    if (!finite_all(d.p, m * n)) raise_err(MSVD_ERR_NUMERICAL, "DenseOperator: non-finite entry");
+    op A = {0, d, {0, 0, NULL, NULL, NULL}};
+    solve_op(A, o, truth, res);
     LEAVE();
 }

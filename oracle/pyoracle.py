@@ -135,6 +135,20 @@ class Oracle:
         self._lz = g("lanczos_gk")
         self._lz.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_int64, C.c_int, C.POINTER(C.c_double),
                              C.POINTER(abi.Truth), C.c_int, C.POINTER(abi.LanczosResult)]
+        I64 = C.POINTER(C.c_int64)
+        csr_args = [C.c_int64, C.c_int64, I64, I64, C.POINTER(C.c_double), C.c_int64]
+        self._solve_csr = g("lobpcg_solve_csr")
+        self._solve_csr.argtypes = csr_args + [C.POINTER(abi.Options), C.POINTER(abi.Truth), C.POINTER(abi.Result)]
+        self._lz_csr = g("lanczos_gk_csr")
+        self._lz_csr.argtypes = csr_args + [C.c_int, C.POINTER(C.c_double), C.POINTER(abi.Truth), C.c_int,
+                                            C.POINTER(abi.LanczosResult)]
+        self._csr_prod = g("csr_products")
+        self._csr_prod.argtypes = csr_args + [C.POINTER(C.c_double)] * 5
+        self._sk_csr = g("sketch_csr")
+        if kind == "port":
+            self._sk_csr.argtypes = [C.c_int64, C.c_int, C.c_uint64] + csr_args + [C.c_int64, C.POINTER(C.c_double)]
+        else:
+            self._sk_csr.argtypes = [C.c_int64, C.c_int, C.c_uint64] + csr_args + [C.POINTER(C.c_double)]
         self._cgs2 = g("cgs2")
         self._cgs2.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_int64, C.POINTER(C.c_double),
                                C.c_int64, C.c_uint64, C.POINTER(C.c_int64)]
@@ -286,6 +300,90 @@ class Oracle:
             tr = abi.Truth(float(truth[0]), _p(vmin))
         self._check(self._solve(_p(a), m, n, C.byref(o), C.byref(tr) if tr else None, C.byref(res)))
         return _result_dict(res, rows, sigma, v, vt, sig, trail, has_truth=truth is not None)
+
+    # -- CSR operator (csr.cpp, operator.hpp:58-74) ---------------------------
+    def _csr(self, a):
+        """a = (row_offsets, col_indices, values, m, n) -> ctypes argument list."""
+        rp, ci, v, m, n = a
+        rp = np.ascontiguousarray(rp, dtype=np.int64)
+        ci = np.ascontiguousarray(ci, dtype=np.int64)
+        v = _f64(v)
+        keep = (rp, ci, v)
+        return keep, [int(m), int(n), _p(rp, C.c_int64), _p(ci, C.c_int64), _p(v), int(v.size)]
+
+    def csr_products(self, a, x=None, y=None, norms=False):
+        keep, args = self._csr(a)
+        m, n = a[3], a[4]
+        yo = np.zeros(m) if x is not None else None
+        xo = np.zeros(n) if y is not None else None
+        no = np.zeros(n) if norms else None
+        xi = _f64(x) if x is not None else None
+        yi = _f64(y) if y is not None else None
+        nul = C.POINTER(C.c_double)()
+        self._check(self._csr_prod(*args, _p(xi) if xi is not None else nul, _p(yo) if yo is not None else nul,
+                                   _p(yi) if yi is not None else nul, _p(xo) if xo is not None else nul,
+                                   _p(no) if no is not None else nul))
+        del keep
+        return yo, xo, no
+
+    def sketch_csr(self, a, d, zeta, seed, row0=0):
+        keep, args = self._csr(a)
+        sa = np.empty((d, a[4]), order="F")
+        if self.kind == "port":
+            self._check(self._sk_csr(d, zeta, seed, *args, row0, _p(sa)))
+        else:
+            if row0:
+                raise ValueError("row-sharded sketch is a port-only helper")
+            self._check(self._sk_csr(d, zeta, seed, *args, _p(sa)))
+        del keep
+        return sa
+
+    def lobpcg_solve_csr(self, a, opts=None, truth=None, want_precond=False, **kw):
+        """solver.cpp:301-477 on a CsrOperator."""
+        keep, args = self._csr(a)
+        n = a[4]
+        o = opts if opts is not None else abi.default_options()
+        for k, v in kw.items():
+            setattr(o, k, int(v) if isinstance(v, bool) else v)
+        b = int(o.block_size)
+        max_iter = o.max_iter if o.max_iter >= 0 else (200 if b == 1 else 100)
+        cap = max_iter + 2
+        sigma = np.zeros(max(b, 1))
+        v = np.zeros((n, max(b, 1)), order="F")
+        rows = (abi.RecordRow * cap)()
+        res = abi.Result()
+        res.sigma = _p(sigma)
+        res.v = _p(v)
+        res.rows = rows
+        res.rows_capacity = cap
+        vt = sig = None
+        if want_precond:
+            vt = np.zeros((n, n), order="F")
+            sig = np.zeros(n)
+            res.vtilde = _p(vt)
+            res.sigma_tilde = _p(sig)
+        res.iterate_cb = abi.ITERATE_FN()
+        tr = None
+        if truth is not None:
+            vmin = _f64(truth[1])
+            tr = abi.Truth(float(truth[0]), _p(vmin))
+        self._check(self._solve_csr(*args, C.byref(o), C.byref(tr) if tr else None, C.byref(res)))
+        del keep
+        return _result_dict(res, rows, sigma, v, vt, sig, {"t": [], "v": []}, has_truth=truth is not None)
+
+    def lanczos_gk_csr(self, a, iters, v0, truth=None, record_timing=False, want_bases=False):
+        keep, args = self._csr(a)
+        m, n = a[3], a[4]
+        v0 = _f64(v0)
+        res, rows, v, vb, ub = _lanczos_buffers(m, n, iters, want_bases)
+        tr = None
+        if truth is not None:
+            vmin = _f64(truth[1])
+            tr = abi.Truth(float(truth[0]), _p(vmin))
+        self._check(self._lz_csr(*args, int(iters), _p(v0), C.byref(tr) if tr else None, int(record_timing),
+                                 C.byref(res)))
+        del keep
+        return lanczos_dict(res, rows, v, vb, ub)
 
     # -- Krylov baseline ----------------------------------------------------
     def lanczos_gk(self, a, iters, v0, truth=None, record_timing=False, want_bases=False):

@@ -221,11 +221,97 @@ int ref_cgs2(double* w, int64_t n, int64_t c, const double* basis, int64_t nb,
     }
 }
 
+namespace {
+CsrMatrix wrap_csr(int64_t m, int64_t n, const int64_t* rp, const int64_t* ci, const double* v, int64_t nnz) {
+    CsrMatrix c;
+    c.rows = m;
+    c.cols = n;
+    c.row_offsets.assign(rp, rp + m + 1);
+    c.col_indices.assign(ci, ci + nnz);
+    c.values.assign(v, v + nnz);
+    return c;
+}
+int solve_on(const LinearOperator& op, int64_t n, const msvd_options* o, const msvd_truth* truth,
+             msvd_result* res);
+int lanczos_on(const LinearOperator& op, int64_t n, int iters, const double* v0, const msvd_truth* truth,
+               int record_timing, msvd_lanczos_result* res);
+}  // namespace
+
 // solver.cpp:301-477 lobpcg_solve on a DenseOperator (A column-major m x n).
 int ref_lobpcg_solve(const double* a, int64_t m, int64_t n, const msvd_options* o,
                      const msvd_truth* truth, msvd_result* res) {
     try {
         DenseOperator op(wrap(a, m, n));
+        return solve_on(op, n, o, truth, res);
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// the same on a CsrOperator (operator.hpp:58-74; validated at construction)
+int ref_lobpcg_solve_csr(int64_t m, int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                         int64_t nnz, const msvd_options* o, const msvd_truth* truth, msvd_result* res) {
+    try {
+        CsrOperator op(wrap_csr(m, n, rp, ci, v, nnz));
+        return solve_on(op, n, o, truth, res);
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// sketch.cpp:97-118 sketch_apply(S, CsrMatrix)
+int ref_sketch_csr(int64_t d, int zeta, uint64_t seed, int64_t m, int64_t n, const int64_t* rp,
+                   const int64_t* ci, const double* v, int64_t nnz, double* sa) {
+    try {
+        SparseStackEmbedding s = build_sparsestack(d, m, zeta, seed);
+        unwrap(sketch_apply(s, wrap_csr(m, n, rp, ci, v, nnz)), sa);
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// csr.cpp:33-57 matvec / matvec_adjoint, operator.cpp:98-104 column_norms
+int ref_csr_products(int64_t m, int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                     int64_t nnz, const double* x, double* y, const double* yin, double* xout,
+                     double* norms) {
+    try {
+        CsrOperator op(wrap_csr(m, n, rp, ci, v, nnz));
+        if (x && y) {
+            Vector r = op.apply(Vector(x, x + n));
+            std::memcpy(y, r.data(), sizeof(double) * r.size());
+        }
+        if (yin && xout) {
+            Vector r = op.apply_adjoint(Vector(yin, yin + m));
+            std::memcpy(xout, r.data(), sizeof(double) * r.size());
+        }
+        if (norms) {
+            Vector r = op.column_norms();
+            std::memcpy(norms, r.data(), sizeof(double) * r.size());
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+int ref_lanczos_gk_csr(int64_t m, int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                       int64_t nnz, int iters, const double* v0, const msvd_truth* truth,
+                       int record_timing, msvd_lanczos_result* res) {
+    try {
+        CsrOperator op(wrap_csr(m, n, rp, ci, v, nnz));
+        return lanczos_on(op, n, iters, v0, truth, record_timing, res);
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+}  // extern "C"
+
+namespace {
+int solve_on(const LinearOperator& op, int64_t n, const msvd_options* o, const msvd_truth* truth,
+             msvd_result* res) {
+    try {
         SolverOptions opts = to_opts(o);
         GroundTruth gt;
         const GroundTruth* gtp = nullptr;
@@ -285,10 +371,9 @@ int ref_lobpcg_solve(const double* a, int64_t m, int64_t n, const msvd_options* 
 }
 
 // baselines.cpp:51-166 lanczos_gk on a DenseOperator (A column-major m x n).
-int ref_lanczos_gk(const double* a, int64_t m, int64_t n, int iters, const double* v0,
-                   const msvd_truth* truth, int record_timing, msvd_lanczos_result* res) {
+int lanczos_on(const LinearOperator& op, int64_t n, int iters, const double* v0, const msvd_truth* truth,
+               int record_timing, msvd_lanczos_result* res) {
     try {
-        DenseOperator op(wrap(a, m, n));
         GroundTruth gt;
         const GroundTruth* gtp = nullptr;
         if (truth) {
@@ -325,4 +410,16 @@ int ref_lanczos_gk(const double* a, int64_t m, int64_t n, int iters, const doubl
     }
 }
 
+}  // namespace
+
+extern "C" {
+int ref_lanczos_gk(const double* a, int64_t m, int64_t n, int iters, const double* v0,
+                   const msvd_truth* truth, int record_timing, msvd_lanczos_result* res) {
+    try {
+        DenseOperator op(wrap(a, m, n));
+        return lanczos_on(op, n, iters, v0, truth, record_timing, res);
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
 }  // extern "C"

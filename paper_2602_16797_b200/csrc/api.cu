@@ -201,6 +201,51 @@ DevState read_state(Ctx& c, const DevState* st) {
 
 void set_device(const Ctx& c) { MSVD_CUDA(cudaSetDevice(c.device)); }
 
+StreamGeom geom_of(const Ctx& c, const msvd_matrix& M) {
+    return make_geom(c, M.kind == kMatCsr ? nullptr : M.A, M.m_local, static_cast<int32_t>(M.n),
+                     M.kind == kMatCsr ? M.n : M.ld);
+}
+
+}  // namespace
+
+// ---- operator-generic passes (declared in msvd_internal.h) ----------------
+void op_apply(Ctx& c, const msvd_matrix& M, const double* W, int b, OutCols out) {
+    if (M.kind == kMatCsr) {
+        csr_apply(c, M, W, b, out);
+        return;
+    }
+    launch_apply(c, geom_of(c, M), W, b, out);
+}
+
+int op_parts(const Ctx& c, const msvd_matrix& M) {
+    return M.kind == kMatCsr ? csr_parts(c, M) : geom_of(c, M).grid;
+}
+
+int op_adjoint(Ctx& c, const msvd_matrix& M, Cols Y, int b, double* Gpart) {
+    if (M.kind == kMatCsr) return csr_adjoint_parts(c, M, Y, b, Gpart);
+    const StreamGeom g = geom_of(c, M);
+    launch_gram(c, g, Y, b, nullptr, b, b, OutCols{}, true, Gpart);
+    return g.grid;
+}
+
+// Y = T C into `out` (q columns), then the partials of A^T Y[:, :b]
+int op_gram(Ctx& c, const msvd_matrix& M, const StreamGeom& g, Cols T, int k, const double* Cm, int q, int b,
+            OutCols out, double* Gpart) {
+    if (M.kind == kMatCsr) {
+        {
+            ProfScope prof(c, kProfReduce);
+            launch_tcombine(c, T, k, Cm, q, out, M.m_local);
+        }
+        Cols Y{};
+        for (int j = 0; j < b; ++j) Y.p[j] = out.p[j];
+        return csr_adjoint_parts(c, M, Y, b, Gpart);
+    }
+    launch_gram(c, g, T, k, Cm, q, b, out, false, Gpart);
+    return g.grid;
+}
+
+namespace {
+
 float ev_ms(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
@@ -229,7 +274,9 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     const int kind = o.precond_kind;
     if (!res || !res->sigma || !res->v) fail(MSVD_ERR_INVALID, "msvd: result buffers missing");
     if (truth && !truth->v_min) fail(MSVD_ERR_DIMENSION, "solver: ground-truth vector length mismatch");
-    const StreamGeom geom = make_geom(c, M->A, ml, static_cast<int32_t>(n), M->ld);
+    const StreamGeom geom = geom_of(c, *M);
+    const bool csr = M->kind == kMatCsr;
+    const int gparts = op_parts(c, *M);  // partials of one A^T pass
     const int nparts = tsqr_parts(c);
     const int ranks = comm.nranks();
     const int kmax = 3 * b;
@@ -265,7 +312,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     ar.add(&Rres, n * b);
     ar.add(&tmp, n * b);
     ar.add(&Cm, kMaxK * 2 * kMaxB);
-    ar.add(&Gpart, static_cast<size_t>(geom.grid) * b * n);
+    ar.add(&Gpart, static_cast<size_t>(std::max(geom.grid, gparts)) * b * n);
     ar.add(&Gout, n * b);
     ar.add(&nrm, static_cast<size_t>(b) * nblk);
     const int nparts_max = std::max(nparts, geom.grid);
@@ -299,7 +346,8 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
             MSVD_CUDA(cudaMalloc(&Arm, sizeof(double) * m * n));
             MSVD_CUDA(cudaMalloc(&SA, sizeof(double) * m * n));
             MSVD_CUDA(cudaMemsetAsync(Arm, 0, sizeof(double) * m * n, c.stream));
-            if (ml > 0)
+            if (ml > 0 && csr) csr_scatter_dense(c, *M, Arm + M->row0 * n);
+            if (ml > 0 && !csr)
                 MSVD_CUDA(cudaMemcpy2DAsync(Arm + M->row0 * n, sizeof(double) * n, M->A, sizeof(double) * M->ld,
                                             sizeof(double) * n, ml, cudaMemcpyDeviceToDevice, c.stream));
             comm.allreduce_sum(Arm, static_cast<size_t>(m * n), c.stream);
@@ -307,11 +355,14 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
             MSVD_CUDA(cudaStreamSynchronize(c.stream));
             MSVD_CUDA(cudaFree(Arm));
             sa_rows = m;
-            // DenseOperator construction rejects non-finite data (operator.cpp:35-37)
-            launch_colnorms(c, make_geom(c, M->A, ml, static_cast<int32_t>(n), M->ld), cpart, tmp);
+            // DenseOperator construction rejects non-finite data (operator.cpp:35-37);
+            // a CSR operator was validated at attach (csr.cpp:29-30)
+            if (!csr) launch_colnorms(c, geom, cpart, tmp);
         } else {
             SA = static_cast<double*>(c.ensure_sa(sizeof(double) * plan.d * n));
-            if (!hs) {
+            if (csr) {
+                csr_sketch(c, *M, plan.d, o.zeta, o.seed, SA);
+            } else if (!hs) {
                 sketch_dev(c, geom, M->row0, plan.d, o.zeta, o.seed, SA, st);
             } else {
                 // overlap: chunk i is copied on the side stream while chunk i-1 is sketched
@@ -340,7 +391,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         MSVD_CUDA(cudaEventRecord(c.ev[1], c.stream));
         try {
             read_state(c, st);  // non-finite A surfaces here, like the DenseOperator ctor
-            if (plan.skip) {
+            if (plan.skip && !csr) {
                 // finite check of A for the skip path: column sums of squares
                 std::vector<double> h(n);
                 MSVD_CUDA(cudaMemcpy(h.data(), tmp, sizeof(double) * n, cudaMemcpyDeviceToHost));
@@ -368,7 +419,8 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     }
     MSVD_CUDA(cudaEventRecord(c.ev[2], c.stream));
     if (kind == MSVD_PRECOND_DIAGONAL) {  // solver.cpp:336-340
-        launch_colnorms(c, geom, cpart, dinv);
+        if (csr) csr_colsq(c, *M, dinv);
+        else launch_colnorms(c, geom, cpart, dinv);
         comm.allreduce_sum(dinv, static_cast<size_t>(n), c.stream);
         std::vector<double> h(n);
         MSVD_CUDA(cudaMemcpyAsync(h.data(), dinv, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
@@ -399,7 +451,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     // are then gathered in rank order.
     // fused TSQR only for b = 1 (k <= 3): measured, the fold's registers slow
     // the wider A*W kernels more than a separate TSQR pass costs
-    const bool fuse = b == 1 && !std::getenv("MSVD_NO_FUSED_TSQR");
+    const bool fuse = !csr && b == 1 && !std::getenv("MSVD_NO_FUSED_TSQR");
     // One-pass mode: the A*W pass also forms A^T A W, and the n-side images
     // Z = A^T A [V X W] are carried through the Rayleigh-Ritz recurrences next
     // to V and X, so between checks the residual A^T A V' = Z C needs no
@@ -418,7 +470,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         // the stagnation test also reads the residual 5 rows back
         // (solver.cpp:190-200): that row must be a check row too
         const bool rows_exact = !o.use_stagnation || 5 % o.check_every == 0;
-        one_pass = !(e && std::atoi(e) == 0) && o.check_every > 1 && rows_exact &&
+        one_pass = !csr && !(e && std::atoi(e) == 0) && o.check_every > 1 && rows_exact &&
                    apply_gram_supported(c, geom, b, fuse ? &probe : nullptr);
     }
     auto apply_tsqr = [&](Cols Tlead, int nlead, OutCols aw, Cols Tall, int k, int iter) -> std::pair<const double*, int> {
@@ -430,7 +482,10 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         fz.iter = iter;
         (void)nlead;
         int np = nparts;
-        if (launch_apply(c, geom, W, b, aw, fuse ? &fz : nullptr, one_pass ? Gpart : nullptr)) {
+        bool fused = false;
+        if (csr) csr_apply(c, *M, W, b, aw);
+        else fused = launch_apply(c, geom, W, b, aw, fuse ? &fz : nullptr, one_pass ? Gpart : nullptr);
+        if (fused) {
             np = geom.grid;
         } else {
             launch_tsqr(c, Tall, ml, k, Rparts, st, iter);
@@ -445,9 +500,9 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     };
     auto residual = [&](const double* V) {  // G = A^T Y summed over ranks; R = G - theta^2 V
         if (ranks == 1) {
-            launch_reduce_g(c, Gpart, geom.grid, n, b, V, st, 1, Rres, nrm, nblk);
+            launch_reduce_g(c, Gpart, gparts, n, b, V, st, 1, Rres, nrm, nblk);
         } else {
-            launch_reduce_g(c, Gpart, geom.grid, n, b, V, st, 0, Gout, nrm, nblk);
+            launch_reduce_g(c, Gpart, gparts, n, b, V, st, 0, Gout, nrm, nblk);
             comm.allreduce_sum(Gout, static_cast<size_t>(n * b), c.stream);
             launch_reduce_g(c, Gout, 1, n, b, V, st, 1, Rres, nrm, nblk);
         }
@@ -455,7 +510,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     // one-pass check iterations: G = A^T (AT C) from the gram pass, summed over
     // CTAs and ranks, becomes the image A^T A V' carried forward
     auto exact_images = [&](double* ZV) {
-        launch_reduce_g(c, Gpart, geom.grid, n, b, nullptr, st, 0, ZV, nrm, nblk);
+        launch_reduce_g(c, Gpart, gparts, n, b, nullptr, st, 0, ZV, nrm, nblk);
         if (ranks > 1) comm.allreduce_sum(ZV, static_cast<size_t>(n * b), c.stream);
     };
     // gated checks (opt-in, MSVD_CHECK_GATE = 1; tolerance-only stop, one rank).
@@ -537,7 +592,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
             }
             launch_reduce_g(c, ZVb[0], 1, n, b, Vb[0], st, 1, Rres, nrm, nblk);
         } else {
-            launch_gram(c, geom, cols_m({{AW, b}}), b, Cm, b, b, yo, false, Gpart);
+            op_gram(c, *M, geom, cols_m({{AW, b}}), b, Cm, b, b, yo, Gpart);
             if (one_pass) {
                 exact_images(ZVb[0]);
                 launch_reduce_g(c, ZVb[0], 1, n, b, Vb[0], st, 1, Rres, nrm, nblk);
@@ -615,7 +670,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
             launch_reduce_g(c, Gpart, geom.grid, n, b, nullptr, st, 0, ZVb[nxt], nrm, nblk, skip_flag);
             launch_reduce_g(c, ZVb[nxt], 1, n, b, Vb[nxt], st, 1, Rres, nrm, nblk, skip_flag);
         } else {
-            launch_gram(c, geom, Tm, k, Cm, 2 * b, b, yo, false, Gpart);
+            op_gram(c, *M, geom, Tm, k, Cm, 2 * b, b, yo, Gpart);
             if (one_pass) {  // check iteration: the reference's residual, and a fresh A^T A V'
                 exact_images(ZVb[nxt]);
                 launch_reduce_g(c, ZVb[nxt], 1, n, b, Vb[nxt], st, 1, Rres, nrm, nblk);
@@ -635,7 +690,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         if (o.verify_cached_products && (i + 1) % 25 == 0) {  // solver.cpp:430-436
             OutCols fo{};
             for (int j = 0; j < b; ++j) fo.p[j] = fresh + static_cast<int64_t>(j) * ml;
-            launch_apply(c, geom, Vb[nxt], b, fo);
+            op_apply(c, *M, Vb[nxt], b, fo);
             launch_drift(c, fresh, AVb[nxt], ml * b, st, 1e-10 * sigma1, i);
             if (ranks > 1) {
                 double* dm = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(st) +
@@ -900,7 +955,48 @@ int32_t msvd_matrix_attach(msvd_ctx* ctx, const double* dA, int64_t m_local, int
 }
 
 int32_t msvd_matrix_detach(msvd_matrix* mat) {
-    return guard([&] { delete mat; });
+    return guard([&] {
+        if (mat) {
+            set_device(mat->ctx->c);
+            csr_release(*mat);
+        }
+        delete mat;
+    });
+}
+
+int32_t msvd_csr_attach(msvd_ctx* ctx, const int64_t* dRowOffsets, const void* dColIndices, int32_t index_bytes,
+                        const double* dValues, int64_t m_local, int64_t n, int64_t nnz, int64_t row0, int64_t m_global,
+                        msvd_matrix** out) {
+    return guard([&] {
+        need(ctx, "context");
+        need(out, "output handle");
+        need(dRowOffsets, "row offsets");
+        if (nnz > 0) {
+            need(dColIndices, "column indices");
+            need(dValues, "values");
+        }
+        if (index_bytes != 4 && index_bytes != 8) fail(MSVD_ERR_INVALID, "msvd: CSR column indices must be 4 or 8 bytes");
+        if (m_local < 0 || n < 0) fail(MSVD_ERR_DIMENSION, "CsrMatrix: negative dimension");
+        if (row0 < 0 || row0 + m_local > m_global) fail(MSVD_ERR_DIMENSION, "msvd: local rows outside the global range");
+        if (n < 1 || n > kMaxN) fail(MSVD_ERR_DIMENSION, "msvd: column count outside the supported range [1, 2048]");
+        Ctx& c = ctx->c;
+        set_device(c);
+        auto* M = new msvd_matrix{ctx, nullptr, m_local, n, n, row0, m_global};
+        M->kind = kMatCsr;
+        M->csr_rp = dRowOffsets;
+        M->csr_ci = dColIndices;
+        M->csr_idx64 = index_bytes == 8;
+        M->csr_v = dValues;
+        M->csr_nnz = nnz;
+        try {
+            csr_prepare(c, *M);
+        } catch (...) {
+            csr_release(*M);
+            delete M;
+            throw;
+        }
+        *out = M;
+    });
 }
 
 int32_t msvd_apply(msvd_matrix* M, const double* dX, int64_t b, double* dY) {
@@ -909,10 +1005,9 @@ int32_t msvd_apply(msvd_matrix* M, const double* dX, int64_t b, double* dY) {
         Ctx& c = M->ctx->c;
         set_device(c);
         if (b < 1 || b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size must lie in [1, 8]");
-        const StreamGeom g = make_geom(c, M->A, M->m_local, static_cast<int32_t>(M->n), M->ld);
         OutCols out{};
         for (int j = 0; j < b; ++j) out.p[j] = dY + j * M->m_local;
-        launch_apply(c, g, dX, static_cast<int>(b), out);
+        op_apply(c, *M, dX, static_cast<int>(b), out);
         MSVD_CUDA(cudaStreamSynchronize(c.stream));
     });
 }
@@ -924,15 +1019,13 @@ int32_t msvd_apply_adjoint(msvd_matrix* M, const double* dY, int64_t b, double* 
         set_device(c);
         if (b < 1 || b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size must lie in [1, 8]");
         const int64_t n = M->n;
-        const StreamGeom g = make_geom(c, M->A, M->m_local, static_cast<int32_t>(n), M->ld);
         const int nblk = static_cast<int>(ceil_div(n, 256));
-        const size_t gp = static_cast<size_t>(g.grid) * b * n;
+        const size_t gp = static_cast<size_t>(op_parts(c, *M)) * b * n;
         double* s = static_cast<double*>(c.ensure_scratch(sizeof(double) * (gp + static_cast<size_t>(b) * nblk)));
         Cols T{};
         for (int j = 0; j < b; ++j) T.p[j] = dY + j * M->m_local;
-        launch_gram(c, g, T, static_cast<int>(b), nullptr, static_cast<int>(b), static_cast<int>(b), OutCols{},
-                    true, s);
-        launch_reduce_g(c, s, g.grid, n, static_cast<int>(b), nullptr, nullptr, 0, dX, s + gp, nblk);
+        const int np = op_adjoint(c, *M, T, static_cast<int>(b), s);
+        launch_reduce_g(c, s, np, n, static_cast<int>(b), nullptr, nullptr, 0, dX, s + gp, nblk);
         c.comm->allreduce_sum(dX, static_cast<size_t>(n * b), c.stream);
         MSVD_CUDA(cudaStreamSynchronize(c.stream));
     });
@@ -943,9 +1036,13 @@ int32_t msvd_column_norms(msvd_matrix* M, double* dNorms) {
         need(M, "matrix");
         Ctx& c = M->ctx->c;
         set_device(c);
-        const StreamGeom g = make_geom(c, M->A, M->m_local, static_cast<int32_t>(M->n), M->ld);
-        double* part = static_cast<double*>(c.ensure_scratch(sizeof(double) * c.num_sms * M->n));
-        launch_colnorms(c, g, part, dNorms);
+        if (M->kind == kMatCsr) {
+            csr_colsq(c, *M, dNorms);
+        } else {
+            const StreamGeom g = geom_of(c, *M);
+            double* part = static_cast<double*>(c.ensure_scratch(sizeof(double) * c.num_sms * M->n));
+            launch_colnorms(c, g, part, dNorms);
+        }
         c.comm->allreduce_sum(dNorms, static_cast<size_t>(M->n), c.stream);
         std::vector<double> h(M->n);
         MSVD_CUDA(cudaMemcpyAsync(h.data(), dNorms, sizeof(double) * M->n, cudaMemcpyDeviceToHost, c.stream));
@@ -984,7 +1081,8 @@ int32_t msvd_sketch(msvd_matrix* M, int64_t d, int32_t zeta, uint64_t seed, doub
         const StreamGeom g = make_geom(c, M->A, M->m_local, static_cast<int32_t>(M->n), M->ld);
         DevState* st = prim_state(c);
         MSVD_CUDA(cudaMemsetAsync(st, 0, sizeof(DevState), c.stream));
-        sketch_dev(c, g, M->row0, d, zeta, seed, dSA, st);
+        if (M->kind == kMatCsr) csr_sketch(c, *M, d, zeta, seed, dSA);
+        else sketch_dev(c, g, M->row0, d, zeta, seed, dSA, st);
         c.comm->allreduce_sum(dSA, static_cast<size_t>(d * M->n), c.stream);
         read_state(c, st);
     });
@@ -1069,9 +1167,9 @@ int32_t msvd_gram_apply(msvd_matrix* M, const double* dT, int64_t k, const doubl
         if (!direct && (q < b || q > 2 * b)) fail(MSVD_ERR_DIMENSION, "msvd_gram_apply: q must lie in [b, 2b]");
         if (!direct && !dY) fail(MSVD_ERR_INVALID, "msvd_gram_apply: dY missing");
         const int64_t n = M->n, ml = M->m_local;
-        const StreamGeom g = make_geom(c, M->A, ml, static_cast<int32_t>(n), M->ld);
+        const StreamGeom g = geom_of(c, *M);
         const int nblk = static_cast<int>(ceil_div(n, 256));
-        const size_t gp = static_cast<size_t>(g.grid) * b * n;
+        const size_t gp = static_cast<size_t>(std::max(g.grid, op_parts(c, *M))) * b * n;
         double* s = static_cast<double*>(c.ensure_scratch(sizeof(double) * (gp + static_cast<size_t>(b) * nblk +
                                                                             kMaxK * 2 * kMaxB)));
         double* Cs = s + gp + static_cast<size_t>(b) * nblk;
@@ -1082,9 +1180,10 @@ int32_t msvd_gram_apply(msvd_matrix* M, const double* dT, int64_t k, const doubl
             for (int j = 0; j < q; ++j) out.p[j] = dY + j * ml;
             MSVD_CUDA(cudaMemcpyAsync(Cs, dC, sizeof(double) * k * q, cudaMemcpyDeviceToDevice, c.stream));
         }
-        launch_gram(c, g, T, static_cast<int>(k), direct ? nullptr : Cs, static_cast<int>(q), static_cast<int>(b), out,
-                    direct, s);
-        launch_reduce_g(c, s, g.grid, n, static_cast<int>(b), nullptr, nullptr, 0, dG, s + gp, nblk);
+        int np = g.grid;
+        if (direct) np = op_adjoint(c, *M, T, static_cast<int>(b), s);
+        else np = op_gram(c, *M, g, T, static_cast<int>(k), Cs, static_cast<int>(q), static_cast<int>(b), out, s);
+        launch_reduce_g(c, s, np, n, static_cast<int>(b), nullptr, nullptr, 0, dG, s + gp, nblk);
         c.comm->allreduce_sum(dG, static_cast<size_t>(n * b), c.stream);
         MSVD_CUDA(cudaStreamSynchronize(c.stream));
     });
@@ -1100,7 +1199,7 @@ int32_t msvd_aw_tsqr(msvd_matrix* M, const double* dW, int64_t b, const double* 
         const int64_t k = kl + b, ml = M->m_local, n = M->n;
         if (kl < 0 || k > kMaxK) fail(MSVD_ERR_DIMENSION, "msvd: trial width must lie in [1, 24]");
         if (M->m_global < k) fail(MSVD_ERR_DIMENSION, "householder_qr: requires rows >= cols");
-        const StreamGeom g = make_geom(c, M->A, ml, static_cast<int32_t>(n), M->ld);
+        const StreamGeom g = geom_of(c, *M);
         const int np_max = std::max(tsqr_parts(c), g.grid);
         const int ranks = c.comm->nranks();
         const size_t pk = static_cast<size_t>(np_max) * k * k;
@@ -1116,7 +1215,10 @@ int32_t msvd_aw_tsqr(msvd_matrix* M, const double* dW, int64_t b, const double* 
         fz.Rparts = parts;
         fz.st = st;
         int np = tsqr_parts(c);
-        if (launch_apply(c, g, dW, static_cast<int>(b), out, &fz)) {
+        bool fused = false;
+        if (M->kind == kMatCsr) csr_apply(c, *M, dW, static_cast<int>(b), out);
+        else fused = launch_apply(c, g, dW, static_cast<int>(b), out, &fz);
+        if (fused) {
             np = g.grid;
         } else {
             Cols T{};
@@ -1149,22 +1251,22 @@ int32_t msvd_aw_gram(msvd_matrix* M, const double* dW, int64_t b, double* dAW, d
         set_device(c);
         if (b < 1 || b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size must lie in [1, 8]");
         const int64_t n = M->n, ml = M->m_local;
-        const StreamGeom g = make_geom(c, M->A, ml, static_cast<int32_t>(n), M->ld);
+        const StreamGeom g = geom_of(c, *M);
         const int nblk = static_cast<int>(ceil_div(n, 256));
-        const size_t gp = static_cast<size_t>(g.grid) * b * n;
+        const size_t gp = static_cast<size_t>(std::max(g.grid, op_parts(c, *M))) * b * n;
         double* s = static_cast<double*>(c.ensure_scratch(sizeof(double) * (gp + static_cast<size_t>(b) * nblk)));
         OutCols out{};
         for (int j = 0; j < b; ++j) out.p[j] = dAW + j * ml;
-        if (apply_gram_supported(c, g, static_cast<int>(b), nullptr)) {
+        int np = g.grid;
+        if (M->kind == kMatDense && apply_gram_supported(c, g, static_cast<int>(b), nullptr)) {
             launch_apply(c, g, dW, static_cast<int>(b), out, nullptr, s);
         } else {  // two passes
-            launch_apply(c, g, dW, static_cast<int>(b), out);
+            op_apply(c, *M, dW, static_cast<int>(b), out);
             Cols T{};
             for (int j = 0; j < b; ++j) T.p[j] = dAW + j * ml;
-            launch_gram(c, g, T, static_cast<int>(b), nullptr, static_cast<int>(b), static_cast<int>(b), OutCols{},
-                        true, s);
+            np = op_adjoint(c, *M, T, static_cast<int>(b), s);
         }
-        launch_reduce_g(c, s, g.grid, n, static_cast<int>(b), nullptr, nullptr, 0, dZ, s + gp, nblk);
+        launch_reduce_g(c, s, np, n, static_cast<int>(b), nullptr, nullptr, 0, dZ, s + gp, nblk);
         c.comm->allreduce_sum(dZ, static_cast<size_t>(n * b), c.stream);
         MSVD_CUDA(cudaStreamSynchronize(c.stream));
     });

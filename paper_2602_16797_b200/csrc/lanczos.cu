@@ -323,14 +323,14 @@ void lanczos_run(Ctx& c, const msvd_matrix& M, int iters, const double* v0h, con
                       : 0.0;
     };
 
-    const StreamGeom g = make_geom(c, M.A, ml, static_cast<int32_t>(n), M.ld);
+    const int gparts = op_parts(c, M);
     const int nblk = static_cast<int>(ceil_div(n, 256));
     const int pm = static_cast<int>(ceil_div(ml > 0 ? ml : 1, kRowsPerCta));  // m-side row blocks
     const int pn = static_cast<int>(ceil_div(n, kRowsPerCta));
     const int N2 = 2 * iters;
     // device layout (doubles)
     const size_t szV = static_cast<size_t>(n) * (iters + 1), szU = static_cast<size_t>(ml) * iters;
-    const size_t szG = static_cast<size_t>(g.grid) * n + nblk;
+    const size_t szG = static_cast<size_t>(gparts) * n + nblk;
     const size_t szPart = static_cast<size_t>(pm > pn ? pm : pn) * iters + pm;
     const size_t total = szV + szU + 2 * static_cast<size_t>(ml) + 4 * static_cast<size_t>(n) + szG + szPart +
                          3 * static_cast<size_t>(iters) + 6 * static_cast<size_t>(N2) + 16 + iters;
@@ -345,7 +345,7 @@ void lanczos_run(Ctx& c, const msvd_matrix& M, int iters, const double* v0h, con
     double* tv = vest + n;
     double* cvec = tv + n;         // n >= iters: projection coefficients
     double* gpart = cvec + n;
-    double* nrm = gpart + static_cast<size_t>(g.grid) * n;
+    double* nrm = gpart + static_cast<size_t>(gparts) * n;
     double* part = gpart + szG;
     double* alpha = part + szPart;
     double* beta = alpha + iters;
@@ -403,7 +403,7 @@ void lanczos_run(Ctx& c, const msvd_matrix& M, int iters, const double* v0h, con
 
     OutCols out{};
     out.p[0] = u;
-    launch_apply(c, g, Vb, 1, out);  // u = A v
+    op_apply(c, M, Vb, 1, out);  // u = A v
     long mva = 1, mvat = 0;
     sumsq(u, ml, sharded);
     double h[8];
@@ -438,8 +438,8 @@ void lanczos_run(Ctx& c, const msvd_matrix& M, int iters, const double* v0h, con
         // w = A^T u_{j-1} - alpha_{j-1} v_{j-1}, reorthogonalized against V
         Cols T{};
         T.p[0] = Ub + static_cast<int64_t>(j - 1) * ml;
-        launch_gram(c, g, T, 1, nullptr, 1, 1, OutCols{}, true, gpart);
-        launch_reduce_g(c, gpart, g.grid, n, 1, nullptr, nullptr, 0, w, nrm, nblk);
+        const int np = op_adjoint(c, M, T, 1, gpart);
+        launch_reduce_g(c, gpart, np, n, 1, nullptr, nullptr, 0, w, nrm, nblk);
         if (sharded) comm.allreduce_sum(w, static_cast<size_t>(n), s);
         ++mvat;
         axpy_neg_kernel<<<static_cast<unsigned>(ceil_div(n, 256)), 256, 0, s>>>(Vb + (j - 1) * n, n, alpha + (j - 1), w);
@@ -488,7 +488,7 @@ void lanczos_run(Ctx& c, const msvd_matrix& M, int iters, const double* v0h, con
 
         // v_j = w / beta; u = A v_j - beta u_{j-1}, reorthogonalized against U
         scale_norm(w, n, nullptr, Vb + static_cast<int64_t>(j) * n);  // sc[0] still holds ||w||^2
-        launch_apply(c, g, Vb + static_cast<int64_t>(j) * n, 1, out);
+        op_apply(c, M, Vb + static_cast<int64_t>(j) * n, 1, out);
         ++mva;
         if (ml > 0) {
             axpy_neg_kernel<<<static_cast<unsigned>(ceil_div(ml, 256)), 256, 0, s>>>(Ub + (j - 1) * ml, ml,

@@ -203,6 +203,24 @@ void sketch_finish(Ctx& c, const double* SAr, int64_t d, int64_t n, double* SA);
 void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double* Vcol,
                        double* Vrow, double* sig, double* sigma_max, int64_t* nfloor, int tail_hint = 8);
 
+// ---- operator kinds --------------------------------------------------------
+enum MatKind { kMatDense = 0, kMatCsr = 1 };
+// CSR operator (csr.cu): validate + build the transpose at attach
+void csr_prepare(Ctx& c, msvd_matrix& M);
+void csr_release(msvd_matrix& M);
+void csr_apply(Ctx& c, const msvd_matrix& M, const double* W, int b, OutCols out);
+int csr_parts(const Ctx& c, const msvd_matrix& M);
+int csr_adjoint_parts(Ctx& c, const msvd_matrix& M, Cols Y, int b, double* Gpart);
+void csr_colsq(Ctx& c, const msvd_matrix& M, double* out);
+void csr_sketch(Ctx& c, const msvd_matrix& M, int64_t d, int zeta, uint64_t seed, double* SA);
+void csr_scatter_dense(Ctx& c, const msvd_matrix& M, double* out_rows);
+// operator-generic passes (api.cu): dense -> the streaming kernels, CSR -> csr.cu
+void op_apply(Ctx& c, const msvd_matrix& M, const double* W, int b, OutCols out);
+int op_parts(const Ctx& c, const msvd_matrix& M);
+int op_adjoint(Ctx& c, const msvd_matrix& M, Cols Y, int b, double* Gpart);  // returns the partial count
+int op_gram(Ctx& c, const msvd_matrix& M, const StreamGeom& g, Cols T, int k, const double* Cm, int q, int b,
+            OutCols out, double* Gpart);
+
 // ---- Golub-Kahan-Lanczos baseline (lanczos.cu) ---------------------------
 void lanczos_run(Ctx& c, const msvd_matrix& M, int iters, const double* v0h, const msvd_truth* truth, bool timing,
                  msvd_lanczos_result* res);
@@ -284,6 +302,18 @@ struct msvd_ctx {
 };
 struct msvd_matrix {
     msvd_ctx* ctx;
-    const double* A;
+    const double* A;  // dense: row-major rows (kind 0)
     int64_t m_local, n, ld, row0, m_global;
+    int kind = msvd::kMatDense;
+    // CSR (kind 1): borrowed arrays, local rows; owned transpose (CSC)
+    const int64_t* csr_rp = nullptr;
+    const void* csr_ci = nullptr;
+    int csr_idx64 = 1;
+    const double* csr_v = nullptr;
+    int64_t csr_nnz = 0;
+    int csr_lanes = 1;
+    void* csr_owned = nullptr;
+    int64_t* csc_cp = nullptr;
+    uint32_t* csc_ri = nullptr;
+    double* csc_cv = nullptr;
 };

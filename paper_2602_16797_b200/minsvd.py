@@ -95,6 +95,7 @@ def _declare(lib):
         "msvd_ctx_synchronize": (i32, [vp]),
         "msvd_matrix_attach": (i32, [vp, vp, i64, i64, i64, i64, i64, P(vp)]),
         "msvd_matrix_detach": (i32, [vp]),
+        "msvd_csr_attach": (i32, [vp, vp, vp, i32, vp, i64, i64, i64, i64, i64, P(vp)]),
         "msvd_apply": (i32, [vp, vp, i64, vp]),
         "msvd_apply_adjoint": (i32, [vp, vp, i64, vp]),
         "msvd_column_norms": (i32, [vp, vp]),
@@ -129,7 +130,7 @@ EXPORTED = (
     "msvd_abi_version msvd_last_error msvd_status_name msvd_options_default msvd_default_tolerance "
     "msvd_validate_options msvd_shard_rows msvd_get_nccl_unique_id msvd_fake_group_create "
     "msvd_fake_group_destroy msvd_ctx_create msvd_ctx_destroy msvd_ctx_synchronize msvd_matrix_attach "
-    "msvd_matrix_detach msvd_apply msvd_apply_adjoint msvd_column_norms msvd_build_sparsestack msvd_sketch "
+    "msvd_matrix_detach msvd_csr_attach msvd_apply msvd_apply_adjoint msvd_column_norms msvd_build_sparsestack msvd_sketch "
     "msvd_precond_build msvd_precond_apply msvd_tsqr_r msvd_gram_apply msvd_aw_tsqr msvd_aw_gram msvd_small_svd "
     "msvd_lanczos_gk msvd_lobpcg_solve msvd_rlobpcg_single "
     "msvd_rlobpcg_block msvd_solve_host msvd_launch_count msvd_abi_sizes msvd_ctx_profile msvd_ctx_profile_read"
@@ -394,6 +395,7 @@ class DeviceDenseOperator:
         if a.stride(1) != 1:
             raise DimensionError("DeviceDenseOperator needs row-major storage (unit column stride)")
         self.a = a
+        self.device = a.device
         self.ctx = ctx or default_context(a.device.index or 0)
         self.m_local, self.n = a.shape
         self.ld = a.stride(0) if self.m_local > 1 else self.n
@@ -416,7 +418,7 @@ class DeviceDenseOperator:
     def _cm(self, x, rows):
         """column-major (rows x b) device copy of x"""
         torch = _torch()
-        x = torch.as_tensor(x, dtype=torch.float64, device=self.a.device)
+        x = torch.as_tensor(x, dtype=torch.float64, device=self.device)
         if x.dim() == 1:
             x = x.reshape(-1, 1)
         if x.shape[0] != rows:
@@ -427,7 +429,7 @@ class DeviceDenseOperator:
         """operator.cpp:7-12: Y = A X (local rows)."""
         torch = _torch()
         xt, b = self._cm(x, self.n)
-        y = torch.empty((b, self.m_local), dtype=torch.float64, device=self.a.device)
+        y = torch.empty((b, self.m_local), dtype=torch.float64, device=self.device)
         check(lib().msvd_apply(self.handle, C.c_void_p(xt.data_ptr()), b, C.c_void_p(y.data_ptr())))
         return y.t()
 
@@ -435,7 +437,7 @@ class DeviceDenseOperator:
         """operator.cpp:14-19: X = A^T Y (summed over ranks)."""
         torch = _torch()
         yt, b = self._cm(y, self.m_local)
-        x = torch.empty((b, self.n), dtype=torch.float64, device=self.a.device)
+        x = torch.empty((b, self.n), dtype=torch.float64, device=self.device)
         check(lib().msvd_apply_adjoint(self.handle, C.c_void_p(yt.data_ptr()), b, C.c_void_p(x.data_ptr())))
         return x.t()
 
@@ -448,12 +450,12 @@ class DeviceDenseOperator:
             q = k
             ct = None
         else:
-            c = torch.as_tensor(c, dtype=torch.float64, device=self.a.device)
+            c = torch.as_tensor(c, dtype=torch.float64, device=self.device)
             q = c.shape[1]
             b = q if b is None else b
             ct = c.t().contiguous()  # column-major k x q
-        g = torch.empty((b, self.n), dtype=torch.float64, device=self.a.device)
-        y = torch.empty((q, self.m_local), dtype=torch.float64, device=self.a.device) if ct is not None else None
+        g = torch.empty((b, self.n), dtype=torch.float64, device=self.device)
+        y = torch.empty((q, self.m_local), dtype=torch.float64, device=self.device) if ct is not None else None
         check(lib().msvd_gram_apply(self.handle, C.c_void_p(tt.data_ptr()), k,
                                     C.c_void_p(ct.data_ptr()) if ct is not None else None, q, b,
                                     C.c_void_p(g.data_ptr()), C.c_void_p(y.data_ptr()) if y is not None else None))
@@ -468,8 +470,8 @@ class DeviceDenseOperator:
         else:
             lt, kl = None, 0
         k = kl + b
-        aw = torch.empty((b, self.m_local), dtype=torch.float64, device=self.a.device)
-        r = torch.empty((k, k), dtype=torch.float64, device=self.a.device)
+        aw = torch.empty((b, self.m_local), dtype=torch.float64, device=self.device)
+        r = torch.empty((k, k), dtype=torch.float64, device=self.device)
         check(lib().msvd_aw_tsqr(self.handle, C.c_void_p(wt.data_ptr()), b,
                                  C.c_void_p(lt.data_ptr()) if lt is not None else None, kl,
                                  C.c_void_p(aw.data_ptr()), C.c_void_p(r.data_ptr())))
@@ -479,8 +481,8 @@ class DeviceDenseOperator:
         """One pass: AW = A W and Z = A^T A W."""
         torch = _torch()
         wt, b = self._cm(w, self.n)
-        aw = torch.empty((b, self.m_local), dtype=torch.float64, device=self.a.device)
-        z = torch.empty((b, self.n), dtype=torch.float64, device=self.a.device)
+        aw = torch.empty((b, self.m_local), dtype=torch.float64, device=self.device)
+        z = torch.empty((b, self.n), dtype=torch.float64, device=self.device)
         check(lib().msvd_aw_gram(self.handle, C.c_void_p(wt.data_ptr()), b, C.c_void_p(aw.data_ptr()),
                                  C.c_void_p(z.data_ptr())))
         return aw.t(), z.t()
@@ -493,7 +495,7 @@ class DeviceDenseOperator:
 
     def column_norms(self):
         torch = _torch()
-        out = torch.empty(self.n, dtype=torch.float64, device=self.a.device)
+        out = torch.empty(self.n, dtype=torch.float64, device=self.device)
         check(lib().msvd_column_norms(self.handle, C.c_void_p(out.data_ptr())))
         return out
 
@@ -510,6 +512,65 @@ class DeviceDenseOperator:
             self.close()
         except Exception:
             pass
+
+
+class DeviceCsrOperator(DeviceDenseOperator):
+    """operator.hpp:58-74 CsrOperator over device memory (csr.hpp:10-25).
+
+    `row_offsets` (int64, m_local + 1), `col_indices` (int32 or int64, sorted
+    and unique within each row) and `values` (float64) are CUDA tensors holding
+    this rank's rows; row0/m_global place them in the global matrix.  The
+    structure is validated like CsrMatrix::validate (csr.cpp:9-31) when the
+    operator is built, and its transpose is formed once on the device.
+    """
+
+    def __init__(self, row_offsets, col_indices, values, n, ctx: Optional[Context] = None, row0=0, m_global=None):
+        torch = _torch()
+        for t, name in ((row_offsets, "row_offsets"), (col_indices, "col_indices"), (values, "values")):
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dim() == 1 and t.is_contiguous()):
+                raise DimensionError(f"DeviceCsrOperator: {name} must be a contiguous 1-D CUDA tensor")
+        if row_offsets.dtype != torch.int64 or values.dtype != torch.float64:
+            raise DimensionError("DeviceCsrOperator: row_offsets int64 and values float64 required")
+        if col_indices.dtype not in (torch.int32, torch.int64):
+            raise DimensionError("DeviceCsrOperator: col_indices must be int32 or int64")
+        if col_indices.numel() != values.numel():
+            raise DimensionError("CsrMatrix: col_indices and values length mismatch")
+        self.rp, self.ci, self.vals = row_offsets, col_indices, values
+        self.device = values.device
+        self.ctx = ctx or default_context(self.device.index or 0)
+        self.m_local = row_offsets.numel() - 1
+        self.n = int(n)
+        self.row0 = row0
+        self.m_global = self.m_local if m_global is None else m_global
+        self.nnz_local = values.numel()
+        h = C.c_void_p()
+        check(lib().msvd_csr_attach(self.ctx.handle, C.c_void_p(row_offsets.data_ptr()),
+                                    C.c_void_p(col_indices.data_ptr()), col_indices.element_size(),
+                                    C.c_void_p(values.data_ptr()), self.m_local, self.n, self.nnz_local, row0,
+                                    self.m_global, C.byref(h)))
+        self.handle = h
+
+    @classmethod
+    def from_scipy(cls, a, device="cuda:0", index_dtype=None, **kw):
+        """Upload a scipy.sparse CSR matrix (indices sorted) to the device."""
+        torch = _torch()
+        a = a.tocsr()
+        a.sort_indices()
+        idx = index_dtype or torch.int64
+        rp = torch.as_tensor(np.asarray(a.indptr, dtype=np.int64), device=device)
+        ci = torch.as_tensor(np.asarray(a.indices), device=device).to(idx)
+        v = torch.as_tensor(np.asarray(a.data, dtype=np.float64), device=device)
+        return cls(rp, ci, v, a.shape[1], **kw)
+
+    def nnz(self):
+        return self.nnz_local
+
+    def to_dense(self):
+        torch = _torch()
+        out = torch.zeros((self.m_local, self.n), dtype=torch.float64, device=self.device)
+        rows = torch.repeat_interleave(torch.arange(self.m_local, device=self.device), self.rp[1:] - self.rp[:-1])
+        out[rows, self.ci.long()] = self.vals
+        return out
 
 
 # ------------------------------------------------------------------ solve
@@ -569,7 +630,8 @@ def _truth(truth, n):
 
 def _run(fn, a, kind, opts, truth, want_precond):
     if not isinstance(a, DeviceDenseOperator):
-        raise DimensionError("msvd: the GPU solver accepts a DeviceDenseOperator only (no CPU fallback)")
+        raise DimensionError("msvd: the GPU solver accepts a DeviceDenseOperator or DeviceCsrOperator only "
+                             "(no CPU fallback)")
     opts = opts or SolverOptions()
     o = opts.to_abi(kind)
     if fn == "msvd_rlobpcg_single":

@@ -133,3 +133,32 @@ def make_problem_gpu(m, n, sigma, seed=DATA_SEED, device="cuda:0", block_rows=2_
         out = u
     vmin = v[:, n - 1].cpu().numpy().copy()
     return out, vmin
+
+
+def random_csr(m, n, density, seed, decay=1e-4):
+    """A seeded sparse test operator for the CSR path (no BASELINE config is
+    sparse): each row holds ~density*n distinct columns drawn uniformly,
+    N(0,1) values, column j scaled by decay**(j/(n-1)) so the spectrum spans
+    several decades.  Returns (row_offsets int64, col_indices int64, values
+    float64) with sorted, unique columns per row (csr.hpp:10-25).
+    numpy's PCG64 stream is stable across versions, so the bytes are
+    reproducible from (m, n, density, seed)."""
+    rng = np.random.default_rng(seed)
+    k = max(1, int(round(density * n)))
+    scale = decay ** (np.arange(n) / max(n - 1, 1))
+    cols = np.argsort(rng.random((m, n)), axis=1)[:, :k] if n <= 256 else None
+    if cols is None:  # large n: sample with replacement, then dedupe per row
+        raw = rng.integers(0, n, size=(m, k))
+        raw.sort(axis=1)
+        keep = np.ones_like(raw, dtype=bool)
+        keep[:, 1:] = raw[:, 1:] != raw[:, :-1]
+        counts = keep.sum(axis=1)
+        ci = raw[keep]
+    else:
+        cols.sort(axis=1)
+        counts = np.full(m, k)
+        ci = cols.ravel()
+    rp = np.zeros(m + 1, dtype=np.int64)
+    np.cumsum(counts, out=rp[1:])
+    v = rng.standard_normal(ci.size) * scale[ci]
+    return rp, ci.astype(np.int64), v

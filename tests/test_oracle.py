@@ -290,3 +290,78 @@ def test_lanczos_validation_errors(port, ref):
             with pytest.raises(OracleError) as e:
                 o.lanczos_gk(mat, iters, v0)
             assert e.value.code == code, (iters, e.value)
+
+
+# ------------------------------------------- CSR operator (csr.cpp, sketch.cpp:97-118)
+def csr_case(case):
+    rp, ci, v = problems.random_csr(case["m"], case["n"], case["density"], case["seed"])
+    assert hashlib.sha256(rp.tobytes() + ci.tobytes() + v.tobytes()).hexdigest() == case["csr_sha256"]
+    return (rp, ci, v, case["m"], case["n"])
+
+
+@pytest.mark.parametrize("name", sorted(GOLDEN["csr"]))
+def test_port_reproduces_csr_golden(port, name):
+    case = GOLDEN["csr"][name]
+    a = csr_case(case)
+    opts = abi.default_options(seed=GOLDEN["solver_seed"], sketch_dim=case["d"], tol=case["tol"],
+                               block_size=case["b"], use_stagnation=0, record_timing=0)
+    r = port.lobpcg_solve_csr(a, opts)
+    assert r["iterations"] == case["iterations"] and r["status"] == case["status"]
+    assert np.array_equal(r["sigma"], unhex(case["sigma"]))
+    assert np.array_equal(r["v"].ravel(order="F"), unhex(case["v"]))
+    assert [[x["iter"], x["matvecs_a"], x["matvecs_at"], float(x["theta"]).hex(), float(x["resid"]).hex()]
+            for x in r["record"]] == case["record"]
+    _, _, norms = port.csr_products(a, norms=True)
+    assert np.array_equal(norms, unhex(case["column_norms"]))
+    sa = port.sketch_csr(a, case["d"], 4, GOLDEN["solver_seed"])
+    assert sha(sa) == case["sketch_sha256"]
+    lz = port.lanczos_gk_csr(a, case["lanczos"]["iters"], np.ones(case["n"]))
+    assert float(lz["sigma_min"]).hex() == case["lanczos"]["sigma_min"]
+    assert [float(x["theta"]).hex() for x in lz["record"]] == case["lanczos"]["theta"]
+
+
+def test_csr_port_equals_reference(port, ref):
+    """Products, sketch (sketch.cpp:97-118), every preconditioner kind, the
+    sketch-skip path (m <= 4n densifies, solver.cpp:132-134)."""
+    rp, ci, v = problems.random_csr(900, 40, 0.15, 5)
+    a = (rp, ci, v, 900, 40)
+    rng = np.random.default_rng(8)
+    x, y = rng.standard_normal(40), rng.standard_normal(900)
+    y[::7] = 0.0  # the adjoint skips zero y_i (csr.cpp:51)
+    for u, w in zip(port.csr_products(a, x, y, True), ref.csr_products(a, x, y, True)):
+        assert np.array_equal(u, w)
+    assert np.array_equal(port.sketch_csr(a, 160, 4, 3), ref.sketch_csr(a, 160, 4, 3))
+    assert np.array_equal(port.sketch_csr(a, 120, 2, 3), ref.sketch_csr(a, 120, 2, 3))
+    for kw in (dict(seed=4, max_iter=30, record_timing=0), dict(seed=4, block_size=2, max_iter=25, record_timing=0),
+               dict(seed=4, precond_kind=abi.PRECOND_NONE, max_iter=20, record_timing=0),
+               dict(seed=4, precond_kind=abi.PRECOND_DIAGONAL, max_iter=20, record_timing=0)):
+        r1 = port.lobpcg_solve_csr(a, abi.default_options(**kw), want_precond=True)
+        r2 = ref.lobpcg_solve_csr(a, abi.default_options(**kw), want_precond=True)
+        for key in ("sigma", "v", "vtilde", "sigma_tilde"):
+            assert np.array_equal(r1[key], r2[key]), (kw, key)
+        assert r1["record"] == r2["record"] and r1["iterations"] == r2["iterations"]
+    sq = (rp[:151], ci[:rp[150]], v[:rp[150]], 150, 40)  # m = 150 <= 4n: sketch skipped
+    r1 = port.lobpcg_solve_csr(sq, abi.default_options(seed=1, max_iter=15, record_timing=0))
+    r2 = ref.lobpcg_solve_csr(sq, abi.default_options(seed=1, max_iter=15, record_timing=0))
+    assert r1["sketch_skipped"] and r1["record"] == r2["record"] and np.array_equal(r1["v"], r2["v"])
+
+
+def test_csr_validation_errors(port, ref):
+    """csr.cpp:9-31: the same exception class and message, in the same order."""
+    from oracle.pyoracle import OracleError
+
+    rp = np.array([0, 2, 3, 5], dtype=np.int64)
+    ci = np.array([0, 2, 1, 0, 3], dtype=np.int64)
+    v = np.array([1.0, 2.0, 3.0, 4.0, 5.0])
+    cases = [
+        ((np.array([1, 2, 3, 5]), ci, v), abi.MSVD_ERR_DIMENSION, "endpoints"),
+        ((np.array([0, 2, 1, 5]), ci, v), abi.MSVD_ERR_DIMENSION, "nondecreasing at row 1"),
+        ((rp, np.array([0, 2, 1, 0, 4]), v), abi.MSVD_ERR_DIMENSION, "out of range in row 2"),
+        ((rp, np.array([2, 0, 1, 0, 3]), v), abi.MSVD_ERR_DIMENSION, "strictly increasing in row 0"),
+        ((rp, ci, np.array([1.0, np.inf, 3.0, 4.0, 5.0])), abi.MSVD_ERR_NUMERICAL, "non-finite"),
+    ]
+    for o in (port, ref):
+        for (r, c, vv), code, msg in cases:
+            with pytest.raises(OracleError) as e:
+                o.csr_products((r, c, vv, 3, 4), x=np.ones(4))
+            assert e.value.code == code and msg in str(e.value), (o.kind, msg, e.value)
