@@ -280,7 +280,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     const int nparts = tsqr_parts(c);
     const int ranks = comm.nranks();
     const int kmax = 3 * b;
-    const int nblk = static_cast<int>(ceil_div(n, 256));
+    const int nblk = static_cast<int>(ceil_div(n, 64));  // reduce_g column blocks
 
     for (int i = 0; i < 6; ++i)
         if (!c.ev[i]) MSVD_CUDA(cudaEventCreate(&c.ev[i]));
@@ -1019,7 +1019,7 @@ int32_t msvd_apply_adjoint(msvd_matrix* M, const double* dY, int64_t b, double* 
         set_device(c);
         if (b < 1 || b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size must lie in [1, 8]");
         const int64_t n = M->n;
-        const int nblk = static_cast<int>(ceil_div(n, 256));
+        const int nblk = static_cast<int>(ceil_div(n, 64));  // reduce_g column blocks
         const size_t gp = static_cast<size_t>(op_parts(c, *M)) * b * n;
         double* s = static_cast<double*>(c.ensure_scratch(sizeof(double) * (gp + static_cast<size_t>(b) * nblk)));
         Cols T{};
@@ -1168,7 +1168,7 @@ int32_t msvd_gram_apply(msvd_matrix* M, const double* dT, int64_t k, const doubl
         if (!direct && !dY) fail(MSVD_ERR_INVALID, "msvd_gram_apply: dY missing");
         const int64_t n = M->n, ml = M->m_local;
         const StreamGeom g = geom_of(c, *M);
-        const int nblk = static_cast<int>(ceil_div(n, 256));
+        const int nblk = static_cast<int>(ceil_div(n, 64));  // reduce_g column blocks
         const size_t gp = static_cast<size_t>(std::max(g.grid, op_parts(c, *M))) * b * n;
         double* s = static_cast<double*>(c.ensure_scratch(sizeof(double) * (gp + static_cast<size_t>(b) * nblk +
                                                                             kMaxK * 2 * kMaxB)));
@@ -1252,7 +1252,7 @@ int32_t msvd_aw_gram(msvd_matrix* M, const double* dW, int64_t b, double* dAW, d
         if (b < 1 || b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size must lie in [1, 8]");
         const int64_t n = M->n, ml = M->m_local;
         const StreamGeom g = geom_of(c, *M);
-        const int nblk = static_cast<int>(ceil_div(n, 256));
+        const int nblk = static_cast<int>(ceil_div(n, 64));  // reduce_g column blocks
         const size_t gp = static_cast<size_t>(std::max(g.grid, op_parts(c, *M))) * b * n;
         double* s = static_cast<double*>(c.ensure_scratch(sizeof(double) * (gp + static_cast<size_t>(b) * nblk)));
         OutCols out{};

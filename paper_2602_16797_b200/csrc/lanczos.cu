@@ -324,7 +324,7 @@ void lanczos_run(Ctx& c, const msvd_matrix& M, int iters, const double* v0h, con
     };
 
     const int gparts = op_parts(c, M);
-    const int nblk = static_cast<int>(ceil_div(n, 256));
+    const int nblk = static_cast<int>(ceil_div(n, 64));  // reduce_g column blocks
     const int pm = static_cast<int>(ceil_div(ml > 0 ? ml : 1, kRowsPerCta));  // m-side row blocks
     const int pn = static_cast<int>(ceil_div(n, kRowsPerCta));
     const int N2 = 2 * iters;

@@ -218,12 +218,107 @@ __device__ bool jacobi_svd(double* Bm, double* V, int k, double* sig, double* Vs
 // ---------------------------------------------------------------------------
 // Rayleigh-Ritz (solver.cpp:352-355 init, :417-421 and :453-462 iteration)
 // ---------------------------------------------------------------------------
+// Merge of the per-CTA R factors as ONE Householder QR of the stacked
+// (nparts k) x k matrix with the whole CTA (small k): each reflector is two
+// fixed-order block reductions instead of a chain of per-part warp folds.
+// Same reflector arithmetic as fold_rows (svd.cpp:37 sign convention), so the
+// merged R is the TSQR's up to roundoff.  Ms: rows x (KM + 1) scratch;
+// red: 2 x 16 x (KM + 1) scratch.  Called by all threads; R -> Rout (ld KM).
+template <int KM>
+__device__ void stacked_qr(const double* Rparts, int nparts, int k, double* Ms, double* red, double* Rout) {
+    constexpr int LD = KM + 1;
+    const int rows = nparts * k;
+    const int nthr = blockDim.x, nw = nthr >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int idx = threadIdx.x; idx < rows * k; idx += nthr) {
+        const int r = idx / k, l = idx - r * k;
+        const int p = r / k, i = r - p * k;
+        Ms[r * LD + l] = l >= i ? Rparts[static_cast<size_t>(p) * k * k + i + l * k] : 0.0;
+    }
+    __syncthreads();
+    int buf = 0;
+    // sum over warps in fixed order of per-thread values v[0..cnt)
+    auto block_sums = [&](double (&v)[KM], int cnt, double (&out)[KM]) {
+        double* rb = red + buf * 16 * LD;
+        buf ^= 1;
+#pragma unroll
+        for (int l = 0; l < KM; ++l)
+            if (l < cnt) {
+                const double t = warp_sum(v[l]);
+                if (lane == 0) rb[warp * LD + l] = t;
+            }
+        __syncthreads();
+#pragma unroll
+        for (int l = 0; l < KM; ++l) {
+            double t = 0.0;
+            if (l < cnt)
+                for (int w = 0; w < nw; ++w) t += rb[w * LD + l];
+            out[l] = t;
+        }
+    };
+    for (int j = 0; j < k; ++j) {
+        double v[KM], o[KM];
+#pragma unroll
+        for (int l = 0; l < KM; ++l) v[l] = 0.0;
+        for (int r = j + 1 + threadIdx.x; r < rows; r += nthr) v[0] += Ms[r * LD + j] * Ms[r * LD + j];
+        block_sums(v, 1, o);
+        const double rjj = Ms[j * LD + j];
+        const double nrm2 = rjj * rjj + o[0];
+        if (nrm2 == 0.0) continue;  // svd.cpp:33-36
+        const double xnorm = sqrt(nrm2);
+        const double alpha = rjj >= 0.0 ? -xnorm : xnorm;
+        const double v0 = rjj - alpha;
+        const double beta = -v0 / alpha;
+#pragma unroll
+        for (int l = 0; l < KM; ++l) v[l] = 0.0;
+        for (int r = j + 1 + threadIdx.x; r < rows; r += nthr) {
+            const double vr = Ms[r * LD + j] / v0;
+#pragma unroll
+            for (int l = 0; l < KM; ++l)
+                if (l > j && l < k) v[l] += vr * Ms[r * LD + l];
+        }
+        block_sums(v, k, o);
+        __syncthreads();  // every thread has read row j and column j before they change
+        for (int r = j + 1 + threadIdx.x; r < rows; r += nthr) {
+            const double vr = Ms[r * LD + j] / v0;
+#pragma unroll
+            for (int l = 0; l < KM; ++l)
+                if (l > j && l < k) {
+                    const double sl = (Ms[j * LD + l] + o[l]) * beta;
+                    Ms[r * LD + l] -= sl * vr;
+                }
+            Ms[r * LD + j] = 0.0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+#pragma unroll
+            for (int l = 0; l < KM; ++l)
+                if (l > j && l < k) {
+                    const double rjl = Ms[j * LD + l];
+                    Ms[j * LD + l] = rjl - (rjl + o[l]) * beta;
+                }
+            Ms[j * LD + j] = alpha;
+        }
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < KM * KM; i += nthr) {
+        const int r = i % KM, c = i / KM;
+        Rout[i] = (r < k && c < k && r <= c) ? Ms[r * LD + c] : 0.0;
+    }
+    __syncthreads();
+}
+
 // the rr kernel's fold scratch lives after its other shared arrays
 template <int KM>
 __device__ __forceinline__ double* rr_scratch(double* sh) {
     return sh + (16 * KM * KM + 3 * KM * KM + KM + 2 * KM * kMaxB + 2) + (KM + 1) / 2 + 2;
 }
 #define ord_end_scratch(sh, KM) rr_scratch<KM>(sh)
+// doubles of the rr kernel's fixed shared layout (arrays + per-warp fold scratch)
+template <int KM>
+__host__ __device__ constexpr size_t rr_base_words() {
+    return (16 * KM * KM + 3 * KM * KM + KM + 2 * KM * kMaxB + 2) + (KM + 1) / 2 + 2 + 16 * 32 * (KM + 1) + 8;
+}
 
 template <int KM>
 __global__ void __launch_bounds__(512) rr_kernel(RRArgs a) {
@@ -240,11 +335,27 @@ __global__ void __launch_bounds__(512) rr_kernel(RRArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int k = a.k, b = a.b;
 
-    // 1. merge the partial R factors: warp w folds parts w, w+16, ...; then a tree
+    // 1. merge the partial R factors.  Small k with room in shared memory:
+    // one stacked Householder QR with the whole CTA; otherwise warp w folds
+    // parts w, w+16, ... and a tree merges the warps.
+    unsigned dyn_smem;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn_smem));
+    const size_t stacked_words = static_cast<size_t>(a.nparts) * k * (KM + 1) + 2 * 16 * (KM + 1);
+    const size_t base_words = rr_base_words<KM>();
+    if (KM <= 8 && (base_words + stacked_words) * sizeof(double) <= dyn_smem) {
+        double* Ms = sh + base_words;
+        stacked_qr<KM>(a.Rparts, a.nparts, k, Ms + 2 * 16 * (KM + 1), Ms, Bm);
+    } else {
     for (int i = lane; i < KM * KM; i += 32) Rw[warp * KM * KM + i] = 0.0;
     __syncwarp();
     const int nw = blockDim.x >> 5;
     double* Xs = ord_end_scratch(sh, KM) + warp * 32 * (KM + 1);
+    double xn[KM];
+    if (warp < a.nparts) {
+        const double* R0 = a.Rparts + static_cast<size_t>(warp) * k * k;
+#pragma unroll
+        for (int l = 0; l < KM; ++l) xn[l] = (lane < k && l >= lane && l < k) ? R0[lane + l * k] : 0.0;
+    }
     for (int pi = warp; pi < a.nparts; pi += nw) {
         const double* R2 = a.Rparts + static_cast<size_t>(pi) * k * k;
         if constexpr (KM >= 8) {
@@ -258,7 +369,12 @@ __global__ void __launch_bounds__(512) rr_kernel(RRArgs a) {
         } else {
             double x[KM];
 #pragma unroll
-            for (int l = 0; l < KM; ++l) x[l] = (lane < k && l >= lane && l < k) ? R2[lane + l * k] : 0.0;
+            for (int l = 0; l < KM; ++l) x[l] = xn[l];
+            if (pi + nw < a.nparts) {  // prefetch the next part while this one folds
+                const double* Rn = a.Rparts + static_cast<size_t>(pi + nw) * k * k;
+#pragma unroll
+                for (int l = 0; l < KM; ++l) xn[l] = (lane < k && l >= lane && l < k) ? Rn[lane + l * k] : 0.0;
+            }
             fold_rows<KM>(Rw + warp * KM * KM, x, k);
         }
     }
@@ -279,6 +395,7 @@ __global__ void __launch_bounds__(512) rr_kernel(RRArgs a) {
     for (int i = threadIdx.x; i < KM * KM; i += blockDim.x) {
         const int r = i % KM, c = i / KM;
         Bm[i] = (r < k && c < k && r <= c) ? Rw[i] : 0.0;
+    }
     }
     __syncthreads();
     if (a.R_out)
@@ -386,42 +503,61 @@ __global__ void __launch_bounds__(512) rr_kernel(RRArgs a) {
 }
 
 // m-side recurrence products without A: out[j][i] = sum_l T[l][i] Cm[l + j k]
-// (solver.cpp:421, :462 -- AV' = AT C, AX' = AT mix), one thread per row
-__global__ void tcombine_kernel(Cols T, int k, const double* Cm, int q, OutCols out, int64_t m) {
-    __shared__ double Cs[kMaxK * 2 * kMaxB];
-    for (int i = threadIdx.x; i < k * q; i += blockDim.x) Cs[i] = Cm[i];
+// (solver.cpp:421, :462 -- AV' = AT C, AX' = AT mix).  K, Q are compile-time
+// so the column pointers stay in registers; each thread handles kTcRows rows
+// (stride blockDim) with all of their loads issued before the FMAs.
+constexpr int kTcRows = 4;
+template <int K, int Q>
+__global__ void __launch_bounds__(256) tcombine_kernel(Cols T, const double* Cm, OutCols out, int64_t m) {
+    __shared__ double Cs[K * Q];
+    for (int i = threadIdx.x; i < K * Q; i += blockDim.x) Cs[i] = Cm[i];
     __syncthreads();
-    for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < m;
-         r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        double t[kMaxK];
+    const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x * kTcRows;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x * kTcRows + threadIdx.x; base < m;
+         base += step) {
+        double t[kTcRows][K];
 #pragma unroll
-        for (int l = 0; l < kMaxK; ++l) t[l] = l < k ? T.p[l][r] : 0.0;
-        for (int j = 0; j < q; ++j) {
-            double y = 0.0;
+        for (int u = 0; u < kTcRows; ++u) {
+            const int64_t r = base + static_cast<int64_t>(u) * blockDim.x;
 #pragma unroll
-            for (int l = 0; l < kMaxK; ++l)
-                if (l < k) y = fma(Cs[l + j * k], t[l], y);
-            out.p[j][r] = y;
+            for (int l = 0; l < K; ++l) t[u][l] = r < m ? __ldcs(T.p[l] + r) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kTcRows; ++u) {
+            const int64_t r = base + static_cast<int64_t>(u) * blockDim.x;
+            if (r < m) {
+#pragma unroll
+                for (int j = 0; j < Q; ++j) {
+                    double y = 0.0;
+#pragma unroll
+                    for (int l = 0; l < K; ++l) y = fma(Cs[l + j * K], t[u][l], y);
+                    out.p[j][r] = y;
+                }
+            }
         }
     }
 }
 
 // G = sum of per-CTA partials (fixed order); R = G - theta^2 V; partial norms.
-// A block covers 256 columns with 4 thread groups; group g sums partials
-// g, g+4, ... in order, and the 4 group sums are added in fixed order.
-constexpr int kRedGroups = 4;
-__global__ void __launch_bounds__(256 * kRedGroups) reduce_g_kernel(const double* Gpart, int nparts, int64_t n, int b,
-                                                                    const double* V, const DevState* st, int residual,
-                                                                    double* Gout, double* nrm_part, const int* skip) {
+// A block covers kRedCols columns with kRedGroups thread groups; group g sums
+// partials g, g + kRedGroups, ... in order (all loads in flight together),
+// and the group sums are added in fixed order.  Many small blocks, so the
+// partials stream from L2 through many SMs at once.
+constexpr int kRedCols = 64;
+constexpr int kRedGroups = 16;
+__global__ void __launch_bounds__(kRedCols * kRedGroups) reduce_g_kernel(const double* Gpart, int nparts, int64_t n,
+                                                                         int b, const double* V, const DevState* st,
+                                                                         int residual, double* Gout, double* nrm_part,
+                                                                         const int* skip) {
     if (skip && *skip) return;
-    __shared__ double part[kRedGroups][256];
-    __shared__ double red[8];
+    __shared__ double part[kRedGroups][kRedCols];
+    __shared__ double red[kRedCols / 32];
     const int j = blockIdx.y;
-    const int t = threadIdx.x & 255, grp = threadIdx.x >> 8;
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * 256 + t;
+    const int t = threadIdx.x % kRedCols, grp = threadIdx.x / kRedCols;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * kRedCols + t;
     double s = 0.0;
     if (i < n) {
-#pragma unroll 8
+#pragma unroll 16
         for (int p = grp; p < nparts; p += kRedGroups) s += Gpart[(static_cast<size_t>(p) * b + j) * n + i];
     }
     part[grp][t] = s;
@@ -441,10 +577,10 @@ __global__ void __launch_bounds__(256 * kRedGroups) reduce_g_kernel(const double
     }
     v = warp_sum(v);
     if ((t & 31) == 0) red[t >> 5] = v;
-    named_sync(1, 256);
+    named_sync(1, kRedCols);
     if (t == 0) {
         double tt = 0.0;
-        for (int w = 0; w < 8; ++w) tt += red[w];
+        for (int w = 0; w < kRedCols / 32; ++w) tt += red[w];
         nrm_part[j * gridDim.x + blockIdx.x] = tt;
     }
 }
@@ -537,22 +673,32 @@ __global__ void __launch_bounds__(256) control_kernel(ControlArgs a) {
 // warp-per-vector coalesced dot products over an L2-resident n x n matrix.
 // ---------------------------------------------------------------------------
 template <int B>
-__global__ void __launch_bounds__(256) dots_kernel(const double* __restrict__ M, int64_t n,
+__global__ void __launch_bounds__(128) dots_kernel(const double* __restrict__ M, int64_t n,
                                                    const double* __restrict__ X, const double* __restrict__ sig,
                                                    double* __restrict__ out, DevState* st, int iter,
                                                    int check_finite) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t c = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * 4 + warp;
     if (c >= n) return;
     const double* mc = M + c * n;
     double acc[B];
 #pragma unroll
     for (int j = 0; j < B; ++j) acc[j] = 0.0;
-#pragma unroll 8
-    for (int64_t i = lane; i < n; i += 32) {  // unrolled: the L2 loads of 8 steps in flight together
-        const double mv = mc[i];
+    constexpr int U = 16;  // the L2 loads of 16 steps in flight together
+    for (int64_t base = 0; base < n; base += 32 * U) {
+        double mv[U];
 #pragma unroll
-        for (int j = 0; j < B; ++j) acc[j] = fma(mv, X[i + j * n], acc[j]);
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + u * 32 + lane;
+            mv[u] = i < n ? mc[i] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + u * 32 + lane;
+            if (i < n)
+#pragma unroll
+                for (int j = 0; j < B; ++j) acc[j] = fma(mv[u], X[i + j * n], acc[j]);
+        }
     }
 #pragma unroll
     for (int j = 0; j < B; ++j) acc[j] = warp_sum(acc[j]);
@@ -809,8 +955,7 @@ __global__ void __launch_bounds__(512) small_svd_kernel(const double* B, int k, 
 
 template <int KM>
 size_t rr_smem() {
-    return sizeof(double) * ((16 * KM * KM + 3 * KM * KM + KM + 2 * KM * kMaxB + 2) + (KM + 1) / 2 + 2 +
-                             16 * 32 * (KM + 1)) + 64;
+    return sizeof(double) * rr_base_words<KM>() + 64;
 }
 
 int km_for(int k) {
@@ -823,7 +968,9 @@ int km_for(int k) {
 
 template <int KM>
 void rr_launch(Ctx& c, const RRArgs& a) {
-    const size_t sm = rr_smem<KM>();
+    size_t sm = rr_smem<KM>();
+    const size_t stacked = sizeof(double) * (static_cast<size_t>(a.nparts) * a.k * (KM + 1) + 2 * 16 * (KM + 1));
+    if (KM <= 8 && sm + stacked <= c.smem_optin) sm += stacked;  // room for the stacked-QR merge
     MSVD_CUDA(cudaFuncSetAttribute(rr_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
     rr_kernel<KM><<<1, 512, sm, c.stream>>>(a);
     MSVD_CUDA(cudaGetLastError());
@@ -853,10 +1000,29 @@ void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st,
     ++c.launches;
 }
 
+template <int B>
+static void tcombine_b(Ctx& c, Cols T, int k, const double* Cm, int q, OutCols out, int64_t m, unsigned grid) {
+    if (k == 2 * B && q == 2 * B) tcombine_kernel<2 * B, 2 * B><<<grid, 256, 0, c.stream>>>(T, Cm, out, m);
+    else if (k == 3 * B && q == 2 * B) tcombine_kernel<3 * B, 2 * B><<<grid, 256, 0, c.stream>>>(T, Cm, out, m);
+    else if (k == B && q == B) tcombine_kernel<B, B><<<grid, 256, 0, c.stream>>>(T, Cm, out, m);
+    else fail(MSVD_ERR_INVALID, "msvd: unsupported recurrence-product shape");
+}
+
 void launch_tcombine(Ctx& c, Cols T, int k, const double* Cm, int q, OutCols out, int64_t m) {
     if (m == 0) return;
-    const int grid = static_cast<int>(std::min<int64_t>(ceil_div(m, 256), 64 * c.num_sms));
-    tcombine_kernel<<<grid, 256, 0, c.stream>>>(T, k, Cm, q, out, m);
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ceil_div(m, 256 * kTcRows), 16 * c.num_sms));
+    const int b = q == k ? q : q / 2;  // (k, q) = (b, b), (2b, 2b) or (3b, 2b)
+    switch (b) {
+        case 1: tcombine_b<1>(c, T, k, Cm, q, out, m, grid); break;
+        case 2: tcombine_b<2>(c, T, k, Cm, q, out, m, grid); break;
+        case 3: tcombine_b<3>(c, T, k, Cm, q, out, m, grid); break;
+        case 4: tcombine_b<4>(c, T, k, Cm, q, out, m, grid); break;
+        case 5: tcombine_b<5>(c, T, k, Cm, q, out, m, grid); break;
+        case 6: tcombine_b<6>(c, T, k, Cm, q, out, m, grid); break;
+        case 7: tcombine_b<7>(c, T, k, Cm, q, out, m, grid); break;
+        case 8: tcombine_b<8>(c, T, k, Cm, q, out, m, grid); break;
+        default: fail(MSVD_ERR_INVALID, "msvd: unsupported recurrence-product shape");
+    }
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
 }
@@ -887,8 +1053,8 @@ void launch_reduce_g(Ctx& c, const double* Gpart, int nparts, int64_t n, int b, 
                      const int* skip) {
     ProfScope prof(c, kProfReduce);
     dim3 grid(static_cast<unsigned>(nblk), static_cast<unsigned>(b));
-    reduce_g_kernel<<<grid, 256 * kRedGroups, 0, c.stream>>>(Gpart, nparts, n, b, V, st, residual, Gout, nrm_part,
-                                                             skip);
+    reduce_g_kernel<<<grid, kRedCols * kRedGroups, 0, c.stream>>>(Gpart, nparts, n, b, V, st, residual, Gout,
+                                                                   nrm_part, skip);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
 }
@@ -910,9 +1076,9 @@ void launch_control(Ctx& c, const ControlArgs& a) {
 template <int B>
 static void precond_b(Ctx& c, const double* Vcol, const double* Vrow, const double* sig, int64_t n,
                       const double* R, double* tmp, double* W, DevState* st, int iter) {
-    const unsigned grid = static_cast<unsigned>(ceil_div(n, 8));
-    dots_kernel<B><<<grid, 256, 0, c.stream>>>(Vcol, n, R, sig, tmp, st, iter, 0);
-    dots_kernel<B><<<grid, 256, 0, c.stream>>>(Vrow, n, tmp, nullptr, W, st, iter, 1);
+    const unsigned grid = static_cast<unsigned>(ceil_div(n, 4));
+    dots_kernel<B><<<grid, 128, 0, c.stream>>>(Vcol, n, R, sig, tmp, st, iter, 0);
+    dots_kernel<B><<<grid, 128, 0, c.stream>>>(Vrow, n, tmp, nullptr, W, st, iter, 1);
     MSVD_CUDA(cudaGetLastError());
     c.launches += 2;
 }
