@@ -669,18 +669,29 @@ static void eig_jacobi(Ctx& c, const double* SA, int64_t rows, int64_t n, double
                 if (hflag[j]) hcols.push_back(static_cast<int>(j));
         }
         if (fro > 4.0 || static_cast<int>(hcols.size()) > kMaxCluster) break;  // -> exact sweeps
+        // the rotation that reaches the GEMM-cosine floor is the last one
+        const bool last = mrel <= 1e-13 && hcols.empty();
         if (st > 0.0) {
-            // exp(K) = exp(K / 2^sq)^(2^sq), with ||K / 2^sq||_F <= 1e-3
+            // exp(K) = exp(K / 2^sq)^(2^sq), with ||K / 2^sq||_F <= 1e-3, and a
+            // Taylor degree just high enough that the first dropped term
+            // x^(d+1) / (d+1)! is below 1e-17 (x = ||K / 2^sq||_F): near
+            // convergence Q = I + K needs no GEMM at all
             int sq = 0;
             while (fro / std::ldexp(1.0, sq) > 1e-3) ++sq;
             const double sc = std::ldexp(1.0, -sq);
-            ident_axpy_kernel<<<pgrid, 256, 0, c.stream>>>(K, 0.2 * sc, n, T2);
+            const double x = fro * sc;
+            int deg = 1;
+            double term = x * x / 2.0;
+            while (deg < 5 && term > 1e-17) {
+                ++deg;
+                term *= x / (deg + 1);
+            }
+            ident_axpy_kernel<<<pgrid, 256, 0, c.stream>>>(K, sc / deg, n, T2);
             double* Ta = T1;
             double* Tb = T2;
-            const double coef[4] = {0.25, 1.0 / 3.0, 0.5, 1.0};
-            for (double a : coef) {
+            for (int dd = deg - 1; dd >= 1; --dd) {  // Horner: I + K/dd (...)
                 ident_axpy_kernel<<<pgrid, 256, 0, c.stream>>>(nullptr, 0.0, n, Ta);
-                gemm(CUBLAS_OP_N, in, in, in, K, in, Tb, in, a * sc, 1.0, Ta, in, "Taylor");
+                gemm(CUBLAS_OP_N, in, in, in, K, in, Tb, in, sc / dd, 1.0, Ta, in, "Taylor");
                 std::swap(Ta, Tb);
             }
             for (int k = 0; k < sq; ++k) {
@@ -692,12 +703,16 @@ static void eig_jacobi(Ctx& c, const double* SA, int64_t rows, int64_t n, double
                 Tb = T2;
             }
             c.launches += sq;
-            // Q = exp(K) in Tb == T2
-            gemm(CUBLAS_OP_N, ir, in, in, B, ir, Tb, in, 1.0, 0.0, T1, ir, "B Q");
-            std::swap(B, T1);
+            // Q = exp(K) in Tb == T2.  After the last rotation only V is
+            // needed: sigma = column norms of B Q = those of B to O(||K||^2)
+            // relative (below 1e-26 here), so B is not rotated again
+            if (!last) {
+                gemm(CUBLAS_OP_N, ir, in, in, B, ir, Tb, in, 1.0, 0.0, T1, ir, "B Q");
+                std::swap(B, T1);
+            }
             gemm(CUBLAS_OP_N, in, in, in, Vp, in, Tb, in, 1.0, 0.0, K, in, "V Q");
             std::swap(Vp, K);
-            c.launches += 11;
+            c.launches += 2 * deg + 1;
         }
         if (!hcols.empty()) {
             MSVD_CUDA(cudaMemcpyAsync(clist, hcols.data(), sizeof(int) * hcols.size(), cudaMemcpyHostToDevice,
