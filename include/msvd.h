@@ -233,6 +233,23 @@ int32_t msvd_aw_gram(msvd_matrix* mat, const double* dW, int64_t b, double* dAW,
 int32_t msvd_small_svd(msvd_ctx* ctx, const double* dB, int64_t k,
                        double* dSigma, double* dV);
 
+/* ---- raw binary A interchange -----------------------
+ * The dense-matrix counterpart of write_matrix_market_array / read (io.cpp:
+ * 174-184, :96-172) without the text: a 32-byte header ("MSVDRAW1", int64 m,
+ * int64 n, int32 layout = 0 row-major, int32 0) then m*n little-endian fp64,
+ * row-major.  Exact round trip; a row range is one contiguous byte range.
+ * Errors: MSVD_ERR_IO (IoError) for open / read / write / format failures.  */
+int32_t msvd_raw_write(const char* path, const double* hA, int64_t m, int64_t n,
+                       int64_t ld);
+int32_t msvd_raw_info(const char* path, int64_t* m, int64_t* n);
+/* rows [row0, row0 + rows) into host memory (leading dimension ld)          */
+int32_t msvd_raw_read_rows(const char* path, int64_t row0, int64_t rows,
+                           double* hA, int64_t ld);
+/* the same rows straight into device memory (row-major, leading dimension
+ * ld), through pinned staging buffers: a rank's shard of a row-sharded run */
+int32_t msvd_raw_load_device(msvd_ctx* ctx, const char* path, int64_t row0,
+                             int64_t rows, double* dA, int64_t ld);
+
 /* ---- Krylov baseline (baselines.cpp:51-166 lanczos_gk) ----------------- */
 /* baselines.hpp:20-23 LanczosStatus */
 typedef enum msvd_lanczos_status {

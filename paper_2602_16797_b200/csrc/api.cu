@@ -20,6 +20,14 @@
 #include "msvd_internal.h"
 
 namespace msvd {
+// rawio.cu: raw binary interchange of A
+void raw_write(const char* path, const double* hA, int64_t m, int64_t n, int64_t ld);
+void raw_info(const char* path, int64_t* m, int64_t* n);
+void raw_read_rows(const char* path, int64_t row0, int64_t rows, double* hA, int64_t ld);
+void raw_load_device(Ctx& c, const char* path, int64_t row0, int64_t rows, double* dA, int64_t ld);
+}  // namespace msvd
+
+namespace msvd {
 
 thread_local std::string g_last_error;
 
@@ -1284,6 +1292,41 @@ int32_t msvd_small_svd(msvd_ctx* ctx, const double* dB, int64_t k, double* dSigm
         const DevState h = read_state(c, st);
         if (std::getenv("MSVD_DEBUG_JACOBI")) std::fprintf(stderr, "msvd_small_svd: k=%lld sweeps=%g\n",
                                                          static_cast<long long>(k), h.worst_jacobi);
+    });
+}
+
+int32_t msvd_raw_write(const char* path, const double* hA, int64_t m, int64_t n, int64_t ld) {
+    return guard([&] {
+        need(path, "path");
+        if (m * n > 0) need(hA, "matrix");
+        raw_write(path, hA, m, n, ld);
+    });
+}
+
+int32_t msvd_raw_info(const char* path, int64_t* m, int64_t* n) {
+    return guard([&] {
+        need(path, "path");
+        need(m, "rows");
+        need(n, "cols");
+        raw_info(path, m, n);
+    });
+}
+
+int32_t msvd_raw_read_rows(const char* path, int64_t row0, int64_t rows, double* hA, int64_t ld) {
+    return guard([&] {
+        need(path, "path");
+        if (rows > 0) need(hA, "matrix");
+        raw_read_rows(path, row0, rows, hA, ld);
+    });
+}
+
+int32_t msvd_raw_load_device(msvd_ctx* ctx, const char* path, int64_t row0, int64_t rows, double* dA, int64_t ld) {
+    return guard([&] {
+        need(ctx, "context");
+        need(path, "path");
+        if (rows > 0) need(dA, "matrix");
+        set_device(ctx->c);
+        raw_load_device(ctx->c, path, row0, rows, dA, ld);
     });
 }
 

@@ -108,6 +108,10 @@ def _declare(lib):
         "msvd_aw_tsqr": (i32, [vp, vp, i64, vp, i64, vp, vp]),
         "msvd_aw_gram": (i32, [vp, vp, i64, vp, vp]),
         "msvd_small_svd": (i32, [vp, vp, i64, vp, vp]),
+        "msvd_raw_write": (i32, [C.c_char_p, vp, i64, i64, i64]),
+        "msvd_raw_info": (i32, [C.c_char_p, P(i64), P(i64)]),
+        "msvd_raw_read_rows": (i32, [C.c_char_p, i64, i64, vp, i64]),
+        "msvd_raw_load_device": (i32, [vp, C.c_char_p, i64, i64, vp, i64]),
         "msvd_lanczos_gk": (i32, [vp, i32, vp, P(abi.Truth), i32, P(abi.LanczosResult)]),
         "msvd_lobpcg_solve": (i32, [vp, P(abi.Options), P(abi.Truth), P(abi.Result)]),
         "msvd_rlobpcg_single": (i32, [vp, P(abi.Options), P(abi.Truth), P(abi.Result)]),
@@ -132,7 +136,7 @@ EXPORTED = (
     "msvd_fake_group_destroy msvd_ctx_create msvd_ctx_destroy msvd_ctx_synchronize msvd_matrix_attach "
     "msvd_matrix_detach msvd_csr_attach msvd_apply msvd_apply_adjoint msvd_column_norms msvd_build_sparsestack msvd_sketch "
     "msvd_precond_build msvd_precond_apply msvd_tsqr_r msvd_gram_apply msvd_aw_tsqr msvd_aw_gram msvd_small_svd "
-    "msvd_lanczos_gk msvd_lobpcg_solve msvd_rlobpcg_single "
+    "msvd_raw_write msvd_raw_info msvd_raw_read_rows msvd_raw_load_device msvd_lanczos_gk msvd_lobpcg_solve msvd_rlobpcg_single "
     "msvd_rlobpcg_block msvd_solve_host msvd_launch_count msvd_abi_sizes msvd_ctx_profile msvd_ctx_profile_read"
 ).split()
 
@@ -658,6 +662,44 @@ def rlobpcg_single(a, opts=None, truth=None, want_precond=False):
 def rlobpcg_block(a, opts=None, truth=None, want_precond=False):
     """solver.hpp:180-181"""
     return _run("msvd_rlobpcg_block", a, abi.PRECOND_RANDOMIZED, opts, truth, want_precond)
+
+
+# ------------------------------------------- raw binary A interchange
+def raw_write(path, a):
+    """Write a 2-D float64 array (row-major rows) as an MSVDRAW1 file."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.ndim != 2:
+        raise DimensionError("raw_write: need a 2-D array")
+    check(lib().msvd_raw_write(os.fsencode(path), a.ctypes.data_as(C.c_void_p), a.shape[0], a.shape[1],
+                               a.shape[1]))
+
+
+def raw_info(path):
+    """(m, n) of an MSVDRAW1 file."""
+    m, n = C.c_int64(), C.c_int64()
+    check(lib().msvd_raw_info(os.fsencode(path), C.byref(m), C.byref(n)))
+    return m.value, n.value
+
+
+def raw_read(path, row0=0, rows=None):
+    """Rows [row0, row0 + rows) as a host float64 array."""
+    m, n = raw_info(path)
+    rows = m - row0 if rows is None else rows
+    out = np.empty((max(rows, 0), n), dtype=np.float64)
+    check(lib().msvd_raw_read_rows(os.fsencode(path), row0, rows, out.ctypes.data_as(C.c_void_p), n))
+    return out
+
+
+def raw_load_device(path, row0=0, rows=None, ctx: Optional["Context"] = None, device=0):
+    """Rows [row0, row0 + rows) straight into a row-major CUDA float64 tensor
+    (a rank's shard of a row-sharded run)."""
+    torch = _torch()
+    m, n = raw_info(path)
+    rows = m - row0 if rows is None else rows
+    ctx = ctx or default_context(device)
+    out = torch.empty((max(rows, 0), n), dtype=torch.float64, device=f"cuda:{ctx.device}")
+    check(lib().msvd_raw_load_device(ctx.handle, os.fsencode(path), row0, rows, C.c_void_p(out.data_ptr()), n))
+    return out
 
 
 # ------------------------------------------------ baselines.hpp:12-42
