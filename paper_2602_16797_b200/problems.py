@@ -105,10 +105,11 @@ def _haar_gpu(torch, rows, cols, gen, device, block_rows=None):
     return q
 
 
-def make_problem_gpu(m, n, sigma, seed=DATA_SEED, device="cuda:0", block_rows=2_000_000, ld=None):
+def make_problem_gpu(m, n, sigma, seed=DATA_SEED, device="cuda:0", block_rows=2_000_000, ld=None, tail=None):
     """Row-major A (m x n, leading dimension ld >= n) on the device plus the
-    true v_min (numpy).  A = U diag(sigma) V^T is formed block by block in
-    U's own storage."""
+    true v_min (numpy) -- or, with `tail`, the last `tail` columns of V (the
+    right singular vectors of the smallest sigma).  A = U diag(sigma) V^T is
+    formed block by block in U's own storage."""
     import torch
 
     gen = torch.Generator(device=device)
@@ -131,6 +132,8 @@ def make_problem_gpu(m, n, sigma, seed=DATA_SEED, device="cuda:0", block_rows=2_
             r1 = min(m, r0 + step)
             u[r0:r1] = u[r0:r1] @ vt_scaled
         out = u
+    if tail:
+        return out, v[:, n - tail:].cpu().numpy().copy()
     vmin = v[:, n - 1].cpu().numpy().copy()
     return out, vmin
 
