@@ -704,6 +704,160 @@ __global__ void __launch_bounds__(256, 1) apply_self_kernel(ApplyArgs a) {
     }
 }
 
+// One-pass form for wider blocks: a row is split across a warp PAIR (warp
+// 2q + h takes the column pairs [h * half, (h + 1) * half)), so W, the
+// A^T (A W) accumulators and the row values of half a row fit in registers
+// where a whole row does not (b = 2 up to n = 1024, b = 3, 4 up to n = 512,
+// b = 1 up to n = 2048).  Chunk c belongs to pair c % 4 and stage c % stages
+// (stages a multiple of 4), both warps wait on the stage's mbarrier, and
+// the half-row dot products meet through shared memory behind a per-pair
+// named barrier (the sum is formed in fixed order, the same bits in both
+// warps).  No fused TSQR: the caller runs the separate TSQR pass.
+template <int B, int PL>
+__global__ void __launch_bounds__(256, 1) apply_pair_kernel(ApplyArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const StreamGeom& g = a.g;
+    unsigned char* extra;
+    constexpr size_t kXBytes = sizeof(double) * 4 * 2 * 2 * B;  // [pair][buffer][half][B]
+    Pipe p = carve(smem, g, kXBytes, &extra);
+    double* xbuf = reinterpret_cast<double*>(extra);
+    int64_t r_begin, r_end;
+    cta_rows(g.m, r_begin, r_end);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < g.stages; ++s) mbar_init(&p.full[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int cw = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pr = cw >> 1, h = cw & 1;
+    const int bar = 1 + pr;  // named barrier of this pair (ids 1..4)
+    const int per_pair = g.stages / 4;
+    const int64_t nchunks = ceil_div(r_end - r_begin, g.rc);
+    const uint64_t pol = l2_evict_first_policy();
+    auto issue = [&](int64_t c, int s) {
+        const int64_t r0 = r_begin + c * g.rc;
+        const int64_t rc = min(static_cast<int64_t>(g.rc), r_end - r0);
+        const uint32_t bytes = static_cast<uint32_t>(rc * g.ld * 8);
+        mbar_arrive_expect_tx(&p.full[s], bytes);
+        bulk_g2s(p.stage0 + s * p.stage_bytes, g.A + r0 * g.ld, bytes, &p.full[s], pol);
+    };
+    if (h == 0 && lane == 0)
+        for (int j = 0; j < per_pair; ++j) {
+            const int64_t c = pr + 4 * static_cast<int64_t>(j);
+            if (c < nchunks) issue(c, pr + 4 * j);
+        }
+    const int n = g.n;
+    const int npairs = (n + 1) >> 1;
+    const int half = (npairs + 1) >> 1;
+    const int p0 = h * half;
+    const int pend = min(npairs, p0 + half);
+    double w[PL][2][B], ga[PL][2][B];
+    int off[PL];
+    bool keepy[PL], mine[PL];
+#pragma unroll
+    for (int i = 0; i < PL; ++i) {
+        const int pi = p0 + lane + 32 * i;
+        mine[i] = pi < pend;
+        const int pc = mine[i] ? pi : max(0, min(npairs - 1, pend - 1));
+        off[i] = 2 * pc;
+        keepy[i] = 2 * pc + 1 < n;
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            w[i][0][j] = mine[i] ? a.W[2 * pc + static_cast<int64_t>(j) * n] : 0.0;
+            w[i][1][j] = mine[i] && keepy[i] ? a.W[2 * pc + 1 + static_cast<int64_t>(j) * n] : 0.0;
+            ga[i][0][j] = ga[i][1][j] = 0.0;
+        }
+    }
+    int s = pr, xb = 0;
+    uint32_t ph = 0;
+    for (int64_t c = pr; c < nchunks; c += 4) {
+        mbar_wait(&p.full[s], ph);
+        const double* As = reinterpret_cast<const double*>(p.stage0 + s * p.stage_bytes);
+        const int64_t r0 = r_begin + c * g.rc;
+        const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
+        for (int r = 0; r < rc; ++r) {
+            const double* row = As + static_cast<int64_t>(r) * g.ld_s;
+            constexpr int NA = PL >= 8 ? 4 : (PL >= 4 ? 2 : 1);
+            double part[NA][B];
+#pragma unroll
+            for (int q = 0; q < NA; ++q)
+#pragma unroll
+                for (int j = 0; j < B; ++j) part[q][j] = 0.0;
+            double2 xr[PL];
+#pragma unroll
+            for (int i = 0; i < PL; ++i) {
+                double2 x = *reinterpret_cast<const double2*>(row + off[i]);
+                x.y = keepy[i] ? x.y : 0.0;  // odd n: the pad column is not A
+                xr[i] = x;
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                    part[i % NA][j] = fma(x.x, w[i][0][j], part[i % NA][j]);
+                    part[i % NA][j] = fma(x.y, w[i][1][j], part[i % NA][j]);
+                }
+            }
+            double acc[B];
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                acc[j] = part[0][j];
+#pragma unroll
+                for (int q = 1; q < NA; ++q) acc[j] += part[q][j];
+                acc[j] = warp_sum(acc[j]);
+            }
+            double* xs = xbuf + (pr * 2 + xb) * 2 * B;
+            if (lane == 0)
+#pragma unroll
+                for (int j = 0; j < B; ++j) xs[h * B + j] = acc[j];
+            named_sync(bar, 64);
+            double y[B];
+#pragma unroll
+            for (int j = 0; j < B; ++j) y[j] = xs[j] + xs[B + j];  // half 0 + half 1, both warps alike
+            xb ^= 1;
+#pragma unroll
+            for (int i = 0; i < PL; ++i)
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                    ga[i][0][j] = fma(xr[i].x, y[j], ga[i][0][j]);
+                    ga[i][1][j] = fma(xr[i].y, y[j], ga[i][1][j]);
+                }
+            if (h == 0 && lane < B) {
+                double v = y[0];
+#pragma unroll
+                for (int j = 1; j < B; ++j)
+                    if (lane == j) v = y[j];
+                a.out.p[lane][r0 + r] = v;
+            }
+        }
+        // both halves of every row of the stage are read: refill it
+        named_sync(bar, 64);
+        if (h == 0 && lane == 0 && c + g.stages < nchunks) issue(c + g.stages, s);
+        s += 4;
+        if (s >= g.stages) {
+            s -= g.stages;
+            ph ^= 1;
+        }
+    }
+    __syncthreads();  // every chunk consumed: the stage ring is free
+    double* red = reinterpret_cast<double*>(p.stage0);  // [4 pairs][B][n]
+#pragma unroll
+    for (int i = 0; i < PL; ++i) {
+        if (!mine[i]) continue;
+        const int c0 = off[i];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            red[(static_cast<size_t>(pr) * B + j) * n + c0] = ga[i][0][j];
+            if (keepy[i]) red[(static_cast<size_t>(pr) * B + j) * n + c0 + 1] = ga[i][1][j];
+        }
+    }
+    __syncthreads();
+    double* gp = a.gpart + static_cast<size_t>(blockIdx.x) * B * n;
+    for (int i = threadIdx.x; i < B * n; i += blockDim.x) {
+        double sum = red[i];
+#pragma unroll
+        for (int q = 1; q < 4; ++q) sum += red[static_cast<size_t>(q) * B * n + i];
+        gp[i] = sum;
+    }
+}
+
 struct GramArgs {
     StreamGeom g;
     Cols T;            // k columns of length m
@@ -989,6 +1143,8 @@ bool rows_ok(const Ctx& c, const StreamGeom& g0, int b, const TsqrFuse* ts, bool
     const int pl = (npairs + 31) / 32;
     const bool pl_ok = (b == 1 && pl <= 32) || (b == 2 && pl <= 16) || ((b == 3 || b == 4) && pl <= 8);
     if (!pl_ok) return false;
+    const int plt = pl <= 4 ? 4 : (pl <= 8 ? 8 : (pl <= 16 ? 16 : 32));
+    if (gram && b * plt > 16) return false;  // one-pass registers: the pair kernel takes it
     if (ts && ts->Rparts && (ts->k > (gram ? 4 : 16) || ts->k < b)) return false;
     const size_t extra = rows_extra_bytes(g0, b, ts, gram);
     const StreamGeom g = rows_geom(c, g0, extra);
@@ -996,6 +1152,66 @@ bool rows_ok(const Ctx& c, const StreamGeom& g0, int b, const TsqrFuse* ts, bool
     if (g.stages * g.stage_bytes + bar_bytes(g.stages) + extra > c.smem_optin) return false;
     if (gram && sizeof(double) * 8 * b * g0.n > static_cast<size_t>(g.stages) * g.stage_bytes) return false;
     return true;
+}
+
+// ---- warp-pair one-pass kernel -------------------------------------------
+int pair_pl(int n) {
+    const int half = ((n + 1) / 2 + 1) / 2;
+    const int pl = (half + 31) / 32;
+    return pl <= 4 ? 4 : (pl <= 8 ? 8 : (pl <= 16 ? 16 : 32));
+}
+
+StreamGeom pair_geom(const Ctx& c, StreamGeom g) {
+    const int64_t row_bytes = static_cast<int64_t>(g.ld_s) * 8;
+    const int64_t target = env_int("MSVD_PAIR_STAGE_KB", 8) * 1024;
+    g.rc = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(target / row_bytes, 64)));
+    g.stage_bytes = ((static_cast<size_t>(g.rc) * row_bytes + 127) / 128) * 128;
+    const int64_t avail = static_cast<int64_t>(c.smem_optin) - 2048;
+    const int64_t budget = std::min<int64_t>(env_int("MSVD_PAIR_BUDGET_KB", 168) * 1024, avail);
+    // stages a multiple of 4: a stage is only ever consumed by one pair, in order
+    const int64_t per_pair = std::max<int64_t>(2, std::min<int64_t>(8, budget / (4 * static_cast<int64_t>(g.stage_bytes))));
+    g.stages = static_cast<int32_t>(4 * per_pair);
+    return g;
+}
+
+// b * (register pairs per lane) <= 16 keeps W, the accumulators and the
+// half-row values in registers
+bool pair_ok(const Ctx& c, const StreamGeom& g0, int b) {
+    if (!g0.tma || b < 1 || b > 4 || std::getenv("MSVD_NO_PAIR")) return false;
+    if (b * pair_pl(g0.n) > 16) return false;
+    const StreamGeom g = pair_geom(c, g0);
+    if (g.stages * g.stage_bytes + bar_bytes(g.stages) + 1024 > c.smem_optin) return false;
+    return sizeof(double) * 4 * b * g0.n <= static_cast<size_t>(g.stages) * g.stage_bytes;
+}
+
+template <int B, int PL>
+void apply_pair_b(Ctx& c, const ApplyArgs& a) {
+    static bool attr = false;
+    if (!attr) {
+        MSVD_CUDA(cudaFuncSetAttribute(apply_pair_kernel<B, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(c.smem_optin)));
+        attr = true;
+    }
+    const size_t sm = bar_bytes(a.g.stages) + 128 * ((sizeof(double) * 16 * B + 127) / 128) + a.g.stages * a.g.stage_bytes;
+    apply_pair_kernel<B, PL><<<a.g.grid, 256, sm, c.stream>>>(a);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void launch_pair(Ctx& c, const ApplyArgs& a0, int b) {
+    ApplyArgs a = a0;
+    a.g = pair_geom(c, a0.g);
+    const int pl = pair_pl(a0.g.n);
+    switch (b * 100 + pl) {
+        case 104: apply_pair_b<1, 4>(c, a); break;
+        case 108: apply_pair_b<1, 8>(c, a); break;
+        case 116: apply_pair_b<1, 16>(c, a); break;
+        case 204: apply_pair_b<2, 4>(c, a); break;
+        case 208: apply_pair_b<2, 8>(c, a); break;
+        case 304: apply_pair_b<3, 4>(c, a); break;
+        case 404: apply_pair_b<4, 4>(c, a); break;
+        default: fail(MSVD_ERR_INVALID, "msvd: one-pass pair kernel on an unsupported shape");
+    }
 }
 
 // true if launched (the fused TSQR, when requested, was then done too)
@@ -1077,7 +1293,8 @@ StreamGeom make_geom(const Ctx& c, const double* A, int64_t m, int32_t n, int64_
 bool apply_gram_supported(const Ctx& c, const StreamGeom& g, int b, const TsqrFuse* fuse) {
     const int pl = ((g.n + 1) / 2 + 31) / 32;
     const int plt = pl <= 4 ? 4 : (pl <= 8 ? 8 : (pl <= 16 ? 16 : 32));  // the PL template the launch picks
-    return b * plt <= 16 && rows_ok(c, g, b, fuse, true);
+    if (b * plt <= 16 && rows_ok(c, g, b, fuse, true)) return true;
+    return !fuse && pair_ok(c, g, b);  // the pair kernel has no fused TSQR
 }
 
 bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out, const TsqrFuse* fuse,
@@ -1089,6 +1306,10 @@ bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
     ProfScope prof(c, kProfApply);
     TsqrFuse none{};
     if (try_apply_rows(c, ApplyArgs{g, W, out, fuse ? *fuse : none, gpart}, b)) return fuse != nullptr;
+    if (gpart && pair_ok(c, g, b)) {  // one-pass, rows split over warp pairs (no fused TSQR)
+        launch_pair(c, ApplyArgs{g, W, out, none, gpart}, b);
+        return false;
+    }
     if (gpart) fail(MSVD_ERR_INVALID, "msvd: one-pass A*W / A^T A W launch on an unsupported shape");
     // ticket variant: large stages amortize the per-chunk cross-warp finish
     // (measured: 48 KB x 3 stages best at n = 2000, b = 5)
