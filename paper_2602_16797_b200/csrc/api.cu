@@ -320,9 +320,9 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     ar.add(&Rres, n * b);
     ar.add(&tmp, n * b);
     ar.add(&Cm, kMaxK * 2 * kMaxB);
-    ar.add(&Gpart, static_cast<size_t>(std::max(geom.grid, gparts)) * b * n);
-    ar.add(&Gout, n * b);
-    ar.add(&nrm, static_cast<size_t>(b) * nblk);
+    ar.add(&Gpart, static_cast<size_t>(std::max(geom.grid, gparts)) * (b + 1) * n);
+    ar.add(&Gout, n * (b + 1));
+    ar.add(&nrm, static_cast<size_t>(b + 1) * nblk);
     const int nparts_max = std::max(nparts, geom.grid);
     ar.add(&Rparts, static_cast<size_t>(nparts_max) * kmax * kmax);
     ar.add(&Rall, static_cast<size_t>(ranks) * nparts_max * kmax * kmax);
@@ -481,7 +481,10 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         one_pass = !csr && !(e && std::atoi(e) == 0) && o.check_every > 1 && rows_exact &&
                    apply_gram_supported(c, geom, b, fuse ? &probe : nullptr);
     }
-    auto apply_tsqr = [&](Cols Tlead, int nlead, OutCols aw, Cols Tall, int k, int iter) -> std::pair<const double*, int> {
+    // ex != nullptr (one-pass check refresh): the pass also forms A^T ex into
+    // Gout[n : 2n] (b = 1), next to A^T A W
+    auto apply_tsqr = [&](Cols Tlead, int nlead, OutCols aw, Cols Tall, int k, int iter,
+                          const double* ex = nullptr) -> std::pair<const double*, int> {
         TsqrFuse fz{};
         fz.T = Tlead;
         fz.k = k;
@@ -491,6 +494,16 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         (void)nlead;
         int np = nparts;
         bool fused = false;
+        if (ex) {
+            launch_apply_ex(c, geom, W, aw, ex, Gpart);
+            launch_tsqr(c, Tall, ml, k, Rparts, st, iter);
+            launch_reduce_g(c, Gpart, geom.grid, n, 2, nullptr, st, 0, Gout, nrm, nblk);
+            if (ranks > 1) comm.allreduce_sum(Gout, static_cast<size_t>(2 * n), c.stream);
+            MSVD_CUDA(cudaMemcpyAsync(ZW, Gout, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+            if (ranks == 1) return {Rparts, np};
+            comm.allgather(Rparts, Rall, static_cast<size_t>(np) * k * k, c.stream);
+            return {Rall, np * ranks};
+        }
         if (csr) csr_apply(c, *M, W, b, aw);
         else fused = launch_apply(c, geom, W, b, aw, fuse ? &fz : nullptr, one_pass ? Gpart : nullptr);
         if (fused) {
@@ -527,6 +540,15 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     // tol (C5 shape: 91 iterations instead of the reference's 100).
     const bool gate_checks = one_pass && !o.use_stagnation && ranks == 1 && std::getenv("MSVD_CHECK_GATE") &&
                              std::atoi(std::getenv("MSVD_CHECK_GATE")) != 0;
+    // one-pass check refresh (b = 1): a check iteration forms its residual
+    // from the images like the others; the NEXT A*W pass also forms the exact
+    // A^T (A V') of that iterate (one sweep of A instead of a separate Gram
+    // pass), the check row is rewritten with the exact residual and the stop
+    // rule runs on it (solver.cpp:439).  A stop returns that iterate; the
+    // refreshed image A^T A V' feeds the Rayleigh-Ritz step otherwise.
+    const bool fused_check = one_pass && b == 1 && !gate_checks && apply_ex_supported(c, geom) &&
+                             !(std::getenv("MSVD_FUSED_CHECK") && std::atoi(std::getenv("MSVD_FUSED_CHECK")) == 0);
+    bool pending = false;  // a check row waits for the next pass
     const int* skip_flag = reinterpret_cast<const int*>(reinterpret_cast<unsigned char*>(st) +
                                                          offsetof(DevState, skip_exact));
     ControlArgs ca{};
@@ -629,7 +651,24 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         launch_cgs2(c, W, n, b, cols_n({{Vb[cur], b}, {Xb[cur], nx}}), b + nx, st, i);
         for (int j = 0; j < b; ++j) out.p[j] = AW + static_cast<int64_t>(j) * ml;
         const Cols Tm = cols_m({{AVb[cur], b}, {AXb[cur], nx}, {AW, b}});
-        auto parts = apply_tsqr(cols_m({{AVb[cur], b}, {AXb[cur], nx}}), b + nx, out, Tm, k, i);
+        auto parts = apply_tsqr(cols_m({{AVb[cur], b}, {AXb[cur], nx}}), b + nx, out, Tm, k, i,
+                                pending ? AVb[cur] : nullptr);
+        if (pending) {
+            // the deferred check row i: R = A^T (A V') - theta^2 V' exactly,
+            // the image refreshed, then the stop rule (row i, loop counter i-1)
+            launch_reduce_g(c, Gout + n, 1, n, b, Vb[cur], st, 1, Rres, nrm, nblk);
+            MSVD_CUDA(cudaMemcpyAsync(ZVb[cur], Gout + n, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+            ca.V = Vb[cur];
+            ca.row = i;
+            ca.check = 1;
+            launch_control(c, ca);
+            pending = false;
+            const DevState h = read_state(c, st);
+            if (h.stop) {
+                status = 0;
+                break;
+            }
+        }
         RRArgs ra{};
         ra.Rparts = parts.first;
         ra.nparts = parts.second;
@@ -656,7 +695,8 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
             yo.p[b + j] = AXb[nxt] + static_cast<int64_t>(j) * ml;
         }
         const bool check_it = (i % o.check_every) == 0;
-        if (one_pass && !check_it) {
+        const bool defer = fused_check && check_it && i + 1 < max_iter;
+        if (one_pass && (!check_it || defer)) {
             {
                 ProfScope prof(c, kProfReduce);  // m x k recurrence products: no pass over A
                 launch_tcombine(c, Tm, k, Cm, 2 * b, yo, ml);
@@ -688,9 +728,10 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         }
         ca.V = Vb[nxt];
         ca.row = i + 1;
-        ca.check = check_it;
+        ca.check = check_it && !defer;
         launch_control(c, ca);
         last_row = i + 1;
+        pending = defer;
         if (o.store_iterates) {
             emit(0, i, {{Vb[cur], b}, {Xb[cur], nx}, {W, b}});
             emit(1, i + 1, {{Vb[nxt], b}});

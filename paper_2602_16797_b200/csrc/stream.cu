@@ -108,6 +108,7 @@ struct ApplyArgs {
     OutCols out;      // b columns of length m
     TsqrFuse ts;      // ts.Rparts == nullptr: no fused TSQR
     double* gpart;    // [grid][b][n] A_cta^T (A_cta W) partials (one-pass mode), or nullptr
+    const double* ex; // pair kernel, EX: an m-vector e whose A_cta^T e fills column b of gpart
 };
 
 // K3: Y = A W.  Warps 1..8 consume.  Each warp reduces its threads'
@@ -713,7 +714,7 @@ __global__ void __launch_bounds__(256, 1) apply_self_kernel(ApplyArgs a) {
 // the half-row dot products meet through shared memory behind a per-pair
 // named barrier (the sum is formed in fixed order, the same bits in both
 // warps).  No fused TSQR: the caller runs the separate TSQR pass.
-template <int B, int PL>
+template <int B, int PL, bool EX>
 __global__ void __launch_bounds__(256, 1) apply_pair_kernel(ApplyArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const StreamGeom& g = a.g;
@@ -751,7 +752,8 @@ __global__ void __launch_bounds__(256, 1) apply_pair_kernel(ApplyArgs a) {
     const int half = (npairs + 1) >> 1;
     const int p0 = h * half;
     const int pend = min(npairs, p0 + half);
-    double w[PL][2][B], ga[PL][2][B];
+    constexpr int BG = B + (EX ? 1 : 0);  // accumulated columns: A^T (A W) and, with EX, A^T e
+    double w[PL][2][B], ga[PL][2][BG];
     int off[PL];
     bool keepy[PL], mine[PL];
 #pragma unroll
@@ -765,12 +767,29 @@ __global__ void __launch_bounds__(256, 1) apply_pair_kernel(ApplyArgs a) {
         for (int j = 0; j < B; ++j) {
             w[i][0][j] = mine[i] ? a.W[2 * pc + static_cast<int64_t>(j) * n] : 0.0;
             w[i][1][j] = mine[i] && keepy[i] ? a.W[2 * pc + 1 + static_cast<int64_t>(j) * n] : 0.0;
-            ga[i][0][j] = ga[i][1][j] = 0.0;
         }
+#pragma unroll
+        for (int j = 0; j < BG; ++j) ga[i][0][j] = ga[i][1][j] = 0.0;
     }
+    // EX: the chunk's e values, lane l holding rows l and 32 + l, loaded one
+    // chunk ahead so the row loop never waits on them
+    double exc[2] = {0.0, 0.0}, exn[2] = {0.0, 0.0};
+    auto ex_load = [&](int64_t cc, double (&dst)[2]) {
+        if (!EX || cc >= nchunks) return;
+        const int64_t rr0 = r_begin + cc * g.rc;
+        const int rcc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - rr0));
+        dst[0] = lane < rcc ? a.ex[rr0 + lane] : 0.0;
+        dst[1] = 32 + lane < rcc ? a.ex[rr0 + 32 + lane] : 0.0;
+    };
+    ex_load(pr, exn);
     int s = pr, xb = 0;
     uint32_t ph = 0;
     for (int64_t c = pr; c < nchunks; c += 4) {
+        if (EX) {
+            exc[0] = exn[0];
+            exc[1] = exn[1];
+            ex_load(c + 4, exn);
+        }
         mbar_wait(&p.full[s], ph);
         const double* As = reinterpret_cast<const double*>(p.stage0 + s * p.stage_bytes);
         const int64_t r0 = r_begin + c * g.rc;
@@ -812,13 +831,20 @@ __global__ void __launch_bounds__(256, 1) apply_pair_kernel(ApplyArgs a) {
 #pragma unroll
             for (int j = 0; j < B; ++j) y[j] = xs[j] + xs[B + j];  // half 0 + half 1, both warps alike
             xb ^= 1;
+            double e = 0.0;
+            if (EX) e = __shfl_sync(kFull, r < 32 ? exc[0] : exc[1], r & 31);
 #pragma unroll
-            for (int i = 0; i < PL; ++i)
+            for (int i = 0; i < PL; ++i) {
 #pragma unroll
                 for (int j = 0; j < B; ++j) {
                     ga[i][0][j] = fma(xr[i].x, y[j], ga[i][0][j]);
                     ga[i][1][j] = fma(xr[i].y, y[j], ga[i][1][j]);
                 }
+                if (EX) {
+                    ga[i][0][BG - 1] = fma(xr[i].x, e, ga[i][0][BG - 1]);
+                    ga[i][1][BG - 1] = fma(xr[i].y, e, ga[i][1][BG - 1]);
+                }
+            }
             if (h == 0 && lane < B) {
                 double v = y[0];
 #pragma unroll
@@ -837,23 +863,23 @@ __global__ void __launch_bounds__(256, 1) apply_pair_kernel(ApplyArgs a) {
         }
     }
     __syncthreads();  // every chunk consumed: the stage ring is free
-    double* red = reinterpret_cast<double*>(p.stage0);  // [4 pairs][B][n]
+    double* red = reinterpret_cast<double*>(p.stage0);  // [4 pairs][BG][n]
 #pragma unroll
     for (int i = 0; i < PL; ++i) {
         if (!mine[i]) continue;
         const int c0 = off[i];
 #pragma unroll
-        for (int j = 0; j < B; ++j) {
-            red[(static_cast<size_t>(pr) * B + j) * n + c0] = ga[i][0][j];
-            if (keepy[i]) red[(static_cast<size_t>(pr) * B + j) * n + c0 + 1] = ga[i][1][j];
+        for (int j = 0; j < BG; ++j) {
+            red[(static_cast<size_t>(pr) * BG + j) * n + c0] = ga[i][0][j];
+            if (keepy[i]) red[(static_cast<size_t>(pr) * BG + j) * n + c0 + 1] = ga[i][1][j];
         }
     }
     __syncthreads();
-    double* gp = a.gpart + static_cast<size_t>(blockIdx.x) * B * n;
-    for (int i = threadIdx.x; i < B * n; i += blockDim.x) {
+    double* gp = a.gpart + static_cast<size_t>(blockIdx.x) * BG * n;
+    for (int i = threadIdx.x; i < BG * n; i += blockDim.x) {
         double sum = red[i];
 #pragma unroll
-        for (int q = 1; q < 4; ++q) sum += red[static_cast<size_t>(q) * B * n + i];
+        for (int q = 1; q < 4; ++q) sum += red[static_cast<size_t>(q) * BG * n + i];
         gp[i] = sum;
     }
 }
@@ -1176,24 +1202,25 @@ StreamGeom pair_geom(const Ctx& c, StreamGeom g) {
 
 // b * (register pairs per lane) <= 16 keeps W, the accumulators and the
 // half-row values in registers
-bool pair_ok(const Ctx& c, const StreamGeom& g0, int b) {
+bool pair_ok(const Ctx& c, const StreamGeom& g0, int b, bool ex) {
     if (!g0.tma || b < 1 || b > 4 || std::getenv("MSVD_NO_PAIR")) return false;
-    if (b * pair_pl(g0.n) > 16) return false;
+    const int bg = b + (ex ? 1 : 0);
+    if (bg * pair_pl(g0.n) > 16) return false;
     const StreamGeom g = pair_geom(c, g0);
     if (g.stages * g.stage_bytes + bar_bytes(g.stages) + 1024 > c.smem_optin) return false;
-    return sizeof(double) * 4 * b * g0.n <= static_cast<size_t>(g.stages) * g.stage_bytes;
+    return sizeof(double) * 4 * bg * g0.n <= static_cast<size_t>(g.stages) * g.stage_bytes;
 }
 
-template <int B, int PL>
+template <int B, int PL, bool EX = false>
 void apply_pair_b(Ctx& c, const ApplyArgs& a) {
     static bool attr = false;
     if (!attr) {
-        MSVD_CUDA(cudaFuncSetAttribute(apply_pair_kernel<B, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MSVD_CUDA(cudaFuncSetAttribute(apply_pair_kernel<B, PL, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(c.smem_optin)));
         attr = true;
     }
     const size_t sm = bar_bytes(a.g.stages) + 128 * ((sizeof(double) * 16 * B + 127) / 128) + a.g.stages * a.g.stage_bytes;
-    apply_pair_kernel<B, PL><<<a.g.grid, 256, sm, c.stream>>>(a);
+    apply_pair_kernel<B, PL, EX><<<a.g.grid, 256, sm, c.stream>>>(a);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
 }
@@ -1294,7 +1321,26 @@ bool apply_gram_supported(const Ctx& c, const StreamGeom& g, int b, const TsqrFu
     const int pl = ((g.n + 1) / 2 + 31) / 32;
     const int plt = pl <= 4 ? 4 : (pl <= 8 ? 8 : (pl <= 16 ? 16 : 32));  // the PL template the launch picks
     if (b * plt <= 16 && rows_ok(c, g, b, fuse, true)) return true;
-    return !fuse && pair_ok(c, g, b);  // the pair kernel has no fused TSQR
+    return !fuse && pair_ok(c, g, b, false);  // the pair kernel has no fused TSQR
+}
+
+// b = 1 pass that also accumulates A^T e for an m-vector e: gpart[grid][2][n]
+// = [A_cta^T (A_cta w), A_cta^T e_cta] (the one-pass check refresh)
+bool apply_ex_supported(const Ctx& c, const StreamGeom& g) { return pair_ok(c, g, 1, true); }
+
+void launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, OutCols out, const double* ex, double* gpart) {
+    if (!pair_ok(c, g, 1, true)) fail(MSVD_ERR_INVALID, "msvd: A*W + A^T e pass on an unsupported shape");
+    if (g.m == 0) {
+        MSVD_CUDA(cudaMemsetAsync(gpart, 0, sizeof(double) * g.grid * 2 * g.n, c.stream));
+        return;
+    }
+    ProfScope prof(c, kProfApply);
+    ApplyArgs a{pair_geom(c, g), W, out, TsqrFuse{}, gpart, ex};
+    switch (pair_pl(g.n)) {
+        case 4: apply_pair_b<1, 4, true>(c, a); break;
+        case 8: apply_pair_b<1, 8, true>(c, a); break;
+        default: fail(MSVD_ERR_INVALID, "msvd: A*W + A^T e pass on an unsupported shape");
+    }
 }
 
 bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out, const TsqrFuse* fuse,
@@ -1305,9 +1351,9 @@ bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
     }
     ProfScope prof(c, kProfApply);
     TsqrFuse none{};
-    if (try_apply_rows(c, ApplyArgs{g, W, out, fuse ? *fuse : none, gpart}, b)) return fuse != nullptr;
-    if (gpart && pair_ok(c, g, b)) {  // one-pass, rows split over warp pairs (no fused TSQR)
-        launch_pair(c, ApplyArgs{g, W, out, none, gpart}, b);
+    if (try_apply_rows(c, ApplyArgs{g, W, out, fuse ? *fuse : none, gpart, nullptr}, b)) return fuse != nullptr;
+    if (gpart && pair_ok(c, g, b, false)) {  // one-pass, rows split over warp pairs (no fused TSQR)
+        launch_pair(c, ApplyArgs{g, W, out, none, gpart, nullptr}, b);
         return false;
     }
     if (gpart) fail(MSVD_ERR_INVALID, "msvd: one-pass A*W / A^T A W launch on an unsupported shape");
