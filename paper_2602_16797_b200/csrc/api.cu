@@ -495,8 +495,8 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         int np = nparts;
         bool fused = false;
         if (ex) {
-            launch_apply_ex(c, geom, W, aw, ex, Gpart);
-            launch_tsqr(c, Tall, ml, k, Rparts, st, iter);
+            if (launch_apply_ex(c, geom, W, aw, ex, Gpart, fuse ? &fz : nullptr)) np = geom.grid;
+            else launch_tsqr(c, Tall, ml, k, Rparts, st, iter);
             launch_reduce_g(c, Gpart, geom.grid, n, 2, nullptr, st, 0, Gout, nrm, nblk);
             if (ranks > 1) comm.allreduce_sum(Gout, static_cast<size_t>(2 * n), c.stream);
             MSVD_CUDA(cudaMemcpyAsync(ZW, Gout, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));

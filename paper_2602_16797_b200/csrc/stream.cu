@@ -483,7 +483,12 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_rows_kernel(ApplyArg
 // refills it with its own chunk c + stages.  Eight warps per CTA instead of
 // nine lifts the register cap from 168 to 255 -- room for W and, in one-pass
 // mode (GR), the A^T (A W) accumulators and the row values in registers.
-template <int B, int PL, int KM, bool GR>
+// EX (b = 1, one-pass, fused TSQR): the pass also accumulates A^T e for e =
+// the first trial column (A V' of the previous check iterate), whose rows the
+// TSQR prefetch already brings in; gpart then holds [grid][2][n].  The row
+// values are re-read from shared memory for the two accumulations instead of
+// being held in registers.
+template <int B, int PL, int KM, bool GR, bool EX = false>
 __global__ void __launch_bounds__(256, 1) apply_self_kernel(ApplyArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const StreamGeom& g = a.g;
@@ -526,8 +531,10 @@ __global__ void __launch_bounds__(256, 1) apply_self_kernel(ApplyArgs a) {
     bool finite = true;
     const int n = g.n;
     const int npairs = (n + 1) >> 1;
+    static_assert(!EX || (GR && KM > 0 && B == 1), "EX: one-pass b = 1 with the fused TSQR");
     double w[PL][2][B];
     double ga[GR ? PL : 1][2][B];
+    double ge[EX ? PL : 1][2];
 #pragma unroll
     for (int i = 0; i < PL; ++i) {
         const int c0 = 2 * (lane + 32 * i);
@@ -537,6 +544,7 @@ __global__ void __launch_bounds__(256, 1) apply_self_kernel(ApplyArgs a) {
             w[i][1][j] = c0 + 1 < n ? a.W[c0 + 1 + static_cast<int64_t>(j) * n] : 0.0;
             if (GR) ga[GR ? i : 0][0][j] = ga[GR ? i : 0][1][j] = 0.0;
         }
+        if (EX) ge[EX ? i : 0][0] = ge[EX ? i : 0][1] = 0.0;
     }
     auto prefetch = [&](int64_t cc, int buf) {
         if (KM > 0 && cc < nchunks && lane < kt) {
@@ -584,12 +592,12 @@ __global__ void __launch_bounds__(256, 1) apply_self_kernel(ApplyArgs a) {
             for (int q = 0; q < NA; ++q)
 #pragma unroll
                 for (int j = 0; j < B; ++j) part[q][j] = 0.0;
-            double2 xr[GR ? PL : 1];
+            double2 xr[GR && !EX ? PL : 1];
 #pragma unroll
             for (int i = 0; i < PL; ++i) {
                 double2 x = *reinterpret_cast<const double2*>(row + off[i]);
                 x.y = keepy[i] ? x.y : 0.0;  // odd n: the pad column is not A
-                if (GR) xr[GR ? i : 0] = x;
+                if (GR && !EX) xr[GR && !EX ? i : 0] = x;
 #pragma unroll
                 for (int j = 0; j < B; ++j) {
                     part[i % NA][j] = fma(x.x, w[i][0][j], part[i % NA][j]);
@@ -605,7 +613,7 @@ __global__ void __launch_bounds__(256, 1) apply_self_kernel(ApplyArgs a) {
             }
 #pragma unroll
             for (int j = 0; j < B; ++j) acc[j] = warp_sum(acc[j]);
-            if constexpr (GR) {
+            if constexpr (GR && !EX) {
 #pragma unroll
                 for (int i = 0; i < PL; ++i)
 #pragma unroll
@@ -613,6 +621,18 @@ __global__ void __launch_bounds__(256, 1) apply_self_kernel(ApplyArgs a) {
                         ga[i][0][j] = fma(xr[i].x, acc[j], ga[i][0][j]);
                         ga[i][1][j] = fma(xr[i].y, acc[j], ga[i][1][j]);
                     }
+            }
+            if constexpr (EX) {
+                const double e = __shfl_sync(kFull, tv, 0);  // row r of the first trial column
+#pragma unroll
+                for (int i = 0; i < PL; ++i) {
+                    double2 x = *reinterpret_cast<const double2*>(row + off[i]);
+                    x.y = keepy[i] ? x.y : 0.0;
+                    ga[i][0][0] = fma(x.x, acc[0], ga[i][0][0]);
+                    ga[i][1][0] = fma(x.y, acc[0], ga[i][1][0]);
+                    ge[i][0] = fma(x.x, e, ge[i][0]);
+                    ge[i][1] = fma(x.y, e, ge[i][1]);
+                }
             }
             if (lane < B) {
                 double v = acc[0];
@@ -683,23 +703,26 @@ __global__ void __launch_bounds__(256, 1) apply_self_kernel(ApplyArgs a) {
         }
     }
     if constexpr (GR) {
+        constexpr int BG = B + (EX ? 1 : 0);
         __syncthreads();  // every chunk consumed: the stage ring is free
-        double* red = reinterpret_cast<double*>(p.stage0);  // [8][B][n]
+        double* red = reinterpret_cast<double*>(p.stage0);  // [8][BG][n]
 #pragma unroll
         for (int i = 0; i < PL; ++i) {
             const int c0 = 2 * (lane + 32 * i);
 #pragma unroll
-            for (int j = 0; j < B; ++j) {
-                if (c0 < n) red[(static_cast<size_t>(cw) * B + j) * n + c0] = ga[i][0][j];
-                if (c0 + 1 < n) red[(static_cast<size_t>(cw) * B + j) * n + c0 + 1] = ga[i][1][j];
+            for (int j = 0; j < BG; ++j) {
+                const double v0 = j < B ? ga[i][0][j < B ? j : 0] : ge[EX ? i : 0][0];
+                const double v1 = j < B ? ga[i][1][j < B ? j : 0] : ge[EX ? i : 0][1];
+                if (c0 < n) red[(static_cast<size_t>(cw) * BG + j) * n + c0] = v0;
+                if (c0 + 1 < n) red[(static_cast<size_t>(cw) * BG + j) * n + c0 + 1] = v1;
             }
         }
         __syncthreads();
-        double* gp = a.gpart + static_cast<size_t>(blockIdx.x) * B * n;
-        for (int i = threadIdx.x; i < B * n; i += blockDim.x) {
+        double* gp = a.gpart + static_cast<size_t>(blockIdx.x) * BG * n;
+        for (int i = threadIdx.x; i < BG * n; i += blockDim.x) {
             double sum = red[i];
 #pragma unroll
-            for (int q = 1; q < 8; ++q) sum += red[static_cast<size_t>(q) * B * n + i];
+            for (int q = 1; q < 8; ++q) sum += red[static_cast<size_t>(q) * BG * n + i];
             gp[i] = sum;
         }
     }
@@ -1085,7 +1108,7 @@ size_t gram_smem(const StreamGeom& g, int B) {
     return bar_bytes(g.stages) + ((extra + 127) / 128) * 128 + g.stages * g.stage_bytes;
 }
 
-template <int B, int PL, int KM, bool GR>
+template <int B, int PL, int KM, bool GR, bool EX = false>
 void apply_rows_b(Ctx& c, const ApplyArgs& a) {
     static bool attr = false;
     if (!attr) {
@@ -1099,14 +1122,14 @@ void apply_rows_b(Ctx& c, const ApplyArgs& a) {
     if (self) {
         static bool attr2 = false;
         if (!attr2) {
-            MSVD_CUDA(cudaFuncSetAttribute(apply_self_kernel<B, PL, KM, GR>,
+            MSVD_CUDA(cudaFuncSetAttribute(apply_self_kernel<B, PL, KM, GR, EX>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(c.smem_optin)));
             attr2 = true;
         }
         const size_t tsqr = KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM + 2 * kRowsFused * KM) : 0;
         const size_t sm = bar_bytes(a.g.stages) + ((tsqr + 127) / 128) * 128 + a.g.stages * a.g.stage_bytes;
-        apply_self_kernel<B, PL, KM, GR><<<a.g.grid, 256, sm, c.stream>>>(a);
+        apply_self_kernel<B, PL, KM, GR, EX><<<a.g.grid, 256, sm, c.stream>>>(a);
         MSVD_CUDA(cudaGetLastError());
         ++c.launches;
         return;
@@ -1328,19 +1351,35 @@ bool apply_gram_supported(const Ctx& c, const StreamGeom& g, int b, const TsqrFu
 // = [A_cta^T (A_cta w), A_cta^T e_cta] (the one-pass check refresh)
 bool apply_ex_supported(const Ctx& c, const StreamGeom& g) { return pair_ok(c, g, 1, true); }
 
-void launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, OutCols out, const double* ex, double* gpart) {
+bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, OutCols out, const double* ex, double* gpart,
+                     const TsqrFuse* fuse) {
     if (!pair_ok(c, g, 1, true)) fail(MSVD_ERR_INVALID, "msvd: A*W + A^T e pass on an unsupported shape");
     if (g.m == 0) {
         MSVD_CUDA(cudaMemsetAsync(gpart, 0, sizeof(double) * g.grid * 2 * g.n, c.stream));
-        return;
+        return false;
     }
     ProfScope prof(c, kProfApply);
+    // single-warp form with the fused TSQR when e is its first trial column
+    // (the TSQR prefetch brings e's rows) and [8][2][n] fits the stage ring
+    if (std::getenv("MSVD_EX_SINGLE") && fuse && fuse->Rparts && fuse->k <= 4 && fuse->k > 1 && fuse->T.p[0] == ex &&
+        g.tma && !std::getenv("MSVD_APPLY_PRODUCER") && rows_ok(c, g, 1, fuse, true)) {
+        const int npairs = (g.n + 1) / 2;
+        const int pl = (npairs + 31) / 32;
+        ApplyArgs a1{g, W, out, *fuse, gpart, nullptr};
+        a1.g = rows_geom(c, g, rows_extra_bytes(g, 1, fuse, true));
+        if (sizeof(double) * 8 * 2 * g.n <= static_cast<size_t>(a1.g.stages) * a1.g.stage_bytes) {
+            if (pl <= 4) return apply_rows_b<1, 4, 4, true, true>(c, a1), true;
+            if (pl <= 8) return apply_rows_b<1, 8, 4, true, true>(c, a1), true;
+            if (pl <= 16) return apply_rows_b<1, 16, 4, true, true>(c, a1), true;
+        }
+    }
     ApplyArgs a{pair_geom(c, g), W, out, TsqrFuse{}, gpart, ex};
     switch (pair_pl(g.n)) {
         case 4: apply_pair_b<1, 4, true>(c, a); break;
         case 8: apply_pair_b<1, 8, true>(c, a); break;
         default: fail(MSVD_ERR_INVALID, "msvd: A*W + A^T e pass on an unsupported shape");
     }
+    return false;
 }
 
 bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out, const TsqrFuse* fuse,
