@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Summarise ncu captures of bench.py into committed text files.
 
-    python profiles/summarize.py <tag> <launches.csv> <full.ncu-rep>
+    python profiles/summarize.py <tag> <launches.csv> <full.ncu-rep>[,<more captures>]
 
 Writes profiles/<tag>_launches.txt (per-kernel device time of one bench
 process, from `ncu --metrics gpu__time_duration.sum`), profiles/<tag>_full.txt
@@ -70,7 +70,8 @@ def to_bytes(val_unit):
 def to_ms(val_unit):
     v, u = val_unit
     v = float(v.replace(",", ""))
-    return v * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}.get(u, 1)
+    return v * {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
+                "second": 1e3, "s": 1e3}.get(u, 1)
 
 
 def main():
@@ -92,7 +93,7 @@ def main():
     open(os.path.join(HERE, f"{tag}_launches.txt"), "w").write("\n".join(lines) + "\n")
 
     res, seen = [], set()
-    for d in full(fpath):  # first launch of each kernel
+    for d in [x for fp in fpath.split(",") for x in full(fp)]:  # first launch of each kernel
         if d["kernel"] not in seen:
             seen.add(d["kernel"])
             res.append(d)
