@@ -114,6 +114,54 @@ int main() {
         cudaFree(d);
         cudaFree(dw);
     }
+    {   // CsrOperator (operator.hpp:58-74): the same diagonal instance as CSR,
+        // a solve, the column norms, and the reference's validation errors
+        const int m = 60, n = 6;
+        std::vector<int64_t> rp(m + 1, 0), ci;
+        std::vector<double> v;
+        for (int i = 0; i < m; ++i) {
+            if (i < n) {
+                ci.push_back(i);
+                v.push_back(6.0 - i);
+            }
+            rp[i + 1] = static_cast<int64_t>(ci.size());
+        }
+        int64_t *drp = nullptr, *dci = nullptr;
+        cudaMalloc(&drp, rp.size() * sizeof(int64_t));
+        cudaMalloc(&dci, ci.size() * sizeof(int64_t));
+        cudaMemcpy(drp, rp.data(), rp.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+        cudaMemcpy(dci, ci.data(), ci.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+        double* dv = upload(v);
+        DeviceCsrOperator op(ctx, drp, dci, 8, dv, m, n, static_cast<index_t>(v.size()));
+        CHECK(op.nnz() == n && op.rows() == m && op.cols() == n);
+        SolverOptions o;
+        o.seed = 3;
+        GroundTruth t{1.0, {0, 0, 0, 0, 0, 1.0}};
+        SolveResult r = rlobpcg_single(op, o, &t);
+        CHECK(r.status == SolveStatus::converged);
+        CHECK(std::fabs(r.sigma[0] - 1.0) <= 1e-12);
+        double* dn = nullptr;
+        cudaMalloc(&dn, n * sizeof(double));
+        op.column_norms(dn);
+        std::vector<double> hn(n);
+        cudaMemcpy(hn.data(), dn, n * sizeof(double), cudaMemcpyDeviceToHost);
+        for (int j = 0; j < n; ++j) CHECK(hn[j] == 6.0 - j);  // operator.cpp:98-104
+        // lanczos_gk over the CSR operator (baselines.cpp:51-166): n steps end
+        // in an invariant subspace with the exact smallest sigma
+        LanczosResult lz = lanczos_gk(op, n, Vector(n, 1.0), &t, false, m);
+        CHECK(std::fabs(lz.sigma_min - 1.0) <= 1e-12);
+        CHECK(lz.steps >= 1 && lz.steps <= n);
+        CHECK(lz.v_basis.size() == static_cast<size_t>(n) * lz.steps);
+        // csr.cpp:9-31 errors: a column index out of range
+        std::vector<int64_t> bad = ci;
+        bad[2] = n + 1;
+        cudaMemcpy(dci, bad.data(), bad.size() * sizeof(int64_t), cudaMemcpyHostToDevice);
+        CHECK(throws<DimensionError>([&] { DeviceCsrOperator b(ctx, drp, dci, 8, dv, m, n, 6); }));
+        cudaFree(drp);
+        cudaFree(dci);
+        cudaFree(dv);
+        cudaFree(dn);
+    }
     std::printf("cpp api: %s (%d failures)\n", failures ? "FAIL" : "OK", failures);
     return failures ? 1 : 0;
 }
