@@ -98,7 +98,9 @@ def test_apply_and_adjoint(msvd, cuda, m, n, b):
 
 
 @pytest.mark.parametrize("m,n,b,kl", [(5000, 100, 1, 2), (20_000, 1000, 1, 2), (20_000, 1000, 2, 4), (9_999, 500, 4, 8),
-                                      (4096, 2000, 5, 10), (3000, 64, 1, 0), (100, 7, 2, 0)])
+                                      (4096, 2000, 5, 10), (3000, 64, 1, 0), (100, 7, 2, 0),
+                                      # warp-pair one-pass kernel shapes (b * pairs per lane > 16)
+                                      (8192, 2000, 1, 2), (10_001, 511, 3, 6), (7777, 999, 2, 0)])
 def test_pass_primitives(msvd, cuda, m, n, b, kl):
     """msvd_gram_apply (K2), msvd_aw_tsqr (K3 + TSQR) and msvd_aw_gram (one pass)
     against torch fp64: solver.cpp:357-369/:421 and :412-416."""
