@@ -435,6 +435,51 @@ def test_fake_group_two_ranks(msvd, cuda, port):
         grp.close()
 
 
+def test_fake_group_one_pass_check_refresh(msvd, cuda, port):
+    """Row-sharded one-pass solve (b = 1, n = 500: the deferred check refresh
+    with its 2n allreduce; b = 2: the warp-pair kernel) over 2 ranks on one
+    GPU: the same answer as one rank and as the oracle, to the parity gates."""
+    import threading
+
+    import torch
+
+    for name, shape in (("c2", dict(m=30_000, n=500)), ("c5", dict(m=30_000, n=600))):
+        cfg = problems.CONFIGS[name].scaled(**shape)
+        sig = cfg.spectrum()
+        a_dev, vmin = problems.make_problem_gpu(cfg.m, cfg.n, sig, device=cuda)
+        opts = msvd.SolverOptions(seed=problems.SOLVER_SEED, sketch_dim=cfg.d, tol=cfg.tol, block_size=cfg.b,
+                                  use_stagnation=False, record_timing=False, max_iter=60)
+        one = msvd.rlobpcg_block(msvd.DeviceDenseOperator(a_dev), opts)
+        ref = port.lobpcg_solve(a_dev.cpu().numpy(), opts.to_abi())
+        nr = 2
+        grp = msvd.FakeGroup(nr)
+        out = [None] * nr
+        errs = []
+
+        def run(r):
+            try:
+                torch.cuda.set_device(0)
+                ctx = grp.context(r)
+                r0, rows = msvd.shard_rows(cfg.m, nr, r)
+                op = msvd.DeviceDenseOperator(a_dev[r0:r0 + rows], ctx=ctx, row0=r0, m_global=cfg.m)
+                out[r] = msvd.rlobpcg_block(op, opts)
+            except Exception as e:  # pragma: no cover - reported below
+                errs.append(e)
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(nr)]
+        [t.start() for t in th]
+        [t.join() for t in th]
+        assert not errs, errs
+        smax = ref["sigma_max_estimate"]
+        for r in range(nr):
+            assert out[r].record.to_csv() == out[0].record.to_csv()
+            assert abs(out[r].iterations() - one.iterations()) <= 1
+            assert abs(out[r].iterations() - ref["iterations"]) <= 1
+            assert np.all(np.abs(out[r].sigma - ref["sigma"]) <= SIGMA_TOL * smax)
+            assert subspace_sin(ref["v"][:, 0], out[r].v[:, 0]) <= ANGLE_TOL
+        grp.close()
+
+
 @pytest.mark.slow
 def test_c2_full_size(msvd, cuda):
     """Headline config at full size (8 GB): converges in the oracle's 21
