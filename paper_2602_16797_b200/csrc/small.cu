@@ -223,37 +223,62 @@ __device__ bool jacobi_svd(double* Bm, double* V, int k, double* sig, double* Vs
 // fixed-order block reductions instead of a chain of per-part warp folds.
 // Same reflector arithmetic as fold_rows (svd.cpp:37 sign convention), so the
 // merged R is the TSQR's up to roundoff.  Ms: rows x (KM + 1) scratch;
-// red: 2 x 16 x (KM + 1) scratch.  Called by all threads; R -> Rout (ld KM).
-template <int KM>
-__device__ void stacked_qr(const double* Rparts, int nparts, int k, double* Ms, double* red, double* Rout) {
+// red: 2 x 17 x (KM + 1) scratch.  Called by all threads; R -> Rout (ld KM).
+// TOP: Rprev (shared memory, ld KM), an R already merged, is stacked on top,
+// so parts that do not all fit in shared memory are merged group by group.
+template <int KM, bool TOP = false>
+__device__ void stacked_qr(const double* Rparts, int nparts, int k, double* Ms, double* red, double* Rout,
+                           const double* Rprev = nullptr) {
     constexpr int LD = KM + 1;
-    const int rows = nparts * k;
+    const int top = TOP ? k : 0;
+    const int rows = top + nparts * k;
     const int nthr = blockDim.x, nw = nthr >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int idx = threadIdx.x; idx < rows * k; idx += nthr) {
         const int r = idx / k, l = idx - r * k;
-        const int p = r / k, i = r - p * k;
-        Ms[r * LD + l] = l >= i ? Rparts[static_cast<size_t>(p) * k * k + i + l * k] : 0.0;
+        if (TOP && r < top) {
+            Ms[r * LD + l] = l >= r ? Rprev[r + l * KM] : 0.0;
+        } else {
+            const int p = (r - top) / k, i = (r - top) - p * k;
+            Ms[r * LD + l] = l >= i ? Rparts[static_cast<size_t>(p) * k * k + i + l * k] : 0.0;
+        }
     }
     __syncthreads();
     int buf = 0;
     // sum over warps in fixed order of per-thread values v[0..cnt)
     auto block_sums = [&](double (&v)[KM], int cnt, double (&out)[KM]) {
-        double* rb = red + buf * 16 * LD;
+        double* rb = red + buf * 17 * LD;
         buf ^= 1;
+        if constexpr (KM <= 8) {  // few values: per-value butterflies, every thread adds the warps
 #pragma unroll
-        for (int l = 0; l < KM; ++l)
-            if (l < cnt) {
-                const double t = warp_sum(v[l]);
-                if (lane == 0) rb[warp * LD + l] = t;
+            for (int l = 0; l < KM; ++l)
+                if (l < cnt) {
+                    const double t = warp_sum(v[l]);
+                    if (lane == 0) rb[warp * LD + l] = t;
+                }
+            __syncthreads();
+#pragma unroll
+            for (int l = 0; l < KM; ++l) {
+                double t = 0.0;
+                if (l < cnt)
+                    for (int w = 0; w < nw; ++w) t += rb[w * LD + l];
+                out[l] = t;
             }
-        __syncthreads();
+        } else {  // many: one transpose-reduce per warp, threads l < cnt add the warps
+            double t16[16];
 #pragma unroll
-        for (int l = 0; l < KM; ++l) {
-            double t = 0.0;
-            if (l < cnt)
-                for (int w = 0; w < nw; ++w) t += rb[w * LD + l];
-            out[l] = t;
+            for (int l = 0; l < 16; ++l) t16[l] = l < KM && l < cnt ? v[l < KM ? l : 0] : 0.0;
+            const double t = warp_transpose_reduce<16>(t16);
+            if (lane < cnt) rb[warp * LD + lane] = t;
+            __syncthreads();
+            if (threadIdx.x < cnt) {
+                double sum = 0.0;
+                for (int w = 0; w < nw; ++w) sum += rb[w * LD + threadIdx.x];
+                rb[16 * LD + threadIdx.x] = sum;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int l = 0; l < KM; ++l) out[l] = l < cnt ? rb[16 * LD + l] : 0.0;
         }
     };
     for (int j = 0; j < k; ++j) {
@@ -340,11 +365,21 @@ __global__ void __launch_bounds__(512) rr_kernel(RRArgs a) {
     // parts w, w+16, ... and a tree merges the warps.
     unsigned dyn_smem;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn_smem));
-    const size_t stacked_words = static_cast<size_t>(a.nparts) * k * (KM + 1) + 2 * 16 * (KM + 1);
+    const size_t stacked_words = static_cast<size_t>(a.nparts) * k * (KM + 1) + 2 * 17 * (KM + 1);
     const size_t base_words = rr_base_words<KM>();
+    // KM = 16: the parts in groups that fit, each group stacked under the R so far
+    const int64_t room = static_cast<int64_t>(dyn_smem / sizeof(double)) -
+                         static_cast<int64_t>(base_words + 2 * 17 * (KM + 1));
+    const int group = KM == 16 && room > 0 ? static_cast<int>(room / (k * (KM + 1))) - 1 : 0;
     if (KM <= 8 && (base_words + stacked_words) * sizeof(double) <= dyn_smem) {
         double* Ms = sh + base_words;
-        stacked_qr<KM>(a.Rparts, a.nparts, k, Ms + 2 * 16 * (KM + 1), Ms, Bm);
+        stacked_qr<KM>(a.Rparts, a.nparts, k, Ms + 2 * 17 * (KM + 1), Ms, Bm);
+    } else if (KM == 16 && group >= 8) {
+        double* Ms = sh + base_words;
+        stacked_qr<KM>(a.Rparts, min(group, a.nparts), k, Ms + 2 * 17 * (KM + 1), Ms, Bm);
+        for (int p0 = group; p0 < a.nparts; p0 += group)
+            stacked_qr<KM, true>(a.Rparts + static_cast<size_t>(p0) * k * k, min(group, a.nparts - p0), k,
+                                 Ms + 2 * 17 * (KM + 1), Ms, Bm, Bm);
     } else {
     for (int i = lane; i < KM * KM; i += 32) Rw[warp * KM * KM + i] = 0.0;
     __syncwarp();
@@ -969,8 +1004,9 @@ int km_for(int k) {
 template <int KM>
 void rr_launch(Ctx& c, const RRArgs& a) {
     size_t sm = rr_smem<KM>();
-    const size_t stacked = sizeof(double) * (static_cast<size_t>(a.nparts) * a.k * (KM + 1) + 2 * 16 * (KM + 1));
+    const size_t stacked = sizeof(double) * (static_cast<size_t>(a.nparts) * a.k * (KM + 1) + 2 * 17 * (KM + 1));
     if (KM <= 8 && sm + stacked <= c.smem_optin) sm += stacked;  // room for the stacked-QR merge
+    if (KM == 16) sm = c.smem_optin;                             // the stacked merge in groups of parts
     MSVD_CUDA(cudaFuncSetAttribute(rr_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
     rr_kernel<KM><<<1, 512, sm, c.stream>>>(a);
     MSVD_CUDA(cudaGetLastError());
