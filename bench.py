@@ -46,6 +46,9 @@ def parse():
     p.add_argument("--m", type=int, default=0, help="override rows (debug only; invalidates the metric)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--workload", default="solve", choices=["solve", "csr", "lanczos"],
+                   help="solve: the BASELINE metric (default); csr / lanczos: the SURVEY 8f rows, "
+                        "measured on their own lines")
     return p.parse_args()
 
 
@@ -364,11 +367,93 @@ def e2e(msvd, ctx, a, res, opts, args, cfg, solve):
             "note": "wall clock around msvd_solve_host (synchronous call), pinned host A"}
 
 
+def extra_workload(args, cfg):
+    """Measurement lines for the SURVEY 8f rows (not the headline metric):
+    csr     -- rlobpcg on a seeded sparse operator (problems.random_csr,
+               m = 2e6, n = 1000, ~10 nonzeros per row, int32 indices) through
+               DeviceCsrOperator; roofline of the CSR apply (SpMM) and adjoint
+               (CSC gather) against their algorithmic bytes (nnz * (8 + 4) +
+               8 m, + the gathered vector traffic not counted).
+    lanczos -- lanczos_gk (baselines.cpp:51-166) on the C2 matrix, 200 steps
+               from the randomized preconditioner's start vector (the compare
+               client's run); two passes over A per step."""
+    import torch
+
+    from paper_2602_16797_b200 import minsvd as msvd
+    from paper_2602_16797_b200 import problems
+
+    dev = torch.device("cuda", 0)
+    ctx = msvd.Context(0, stream=torch.cuda.current_stream(dev).cuda_stream or 1)
+    peak, peak_kind = peaks()
+    line = {"higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "data": "synthetic"}
+    if args.workload == "csr":
+        m, n, dens = args.m or 2_000_000, 1000, 0.01
+        rp, ci, v = problems.random_csr(m, n, dens, 41)
+        op = msvd.DeviceCsrOperator(torch.as_tensor(rp, device=dev), torch.as_tensor(ci, device=dev).to(torch.int32),
+                                    torch.as_tensor(v, device=dev), n, ctx=ctx)
+        opts = msvd.SolverOptions(seed=problems.SOLVER_SEED, sketch_dim=4 * n, tol=1e-10, use_stagnation=False,
+                                  record_timing=False)
+        run = lambda: msvd.rlobpcg_single(op, opts)  # noqa: E731
+        nnz = int(v.size)
+        work = f"csr: m={m} n={n} nnz={nnz} (density {dens:g}, int32 indices) b=1 d={4 * n} tol=1e-10 tol-only"
+        bytes_pass = nnz * (8 + 4) + 8 * (m + 1)
+    else:
+        cfg2 = problems.CONFIGS["c2"]
+        a, vmin = problems.make_problem_gpu(cfg2.m, cfg2.n, cfg2.spectrum(), device=dev)
+        op = msvd.DeviceDenseOperator(a, ctx=ctx)
+        opts = msvd.SolverOptions(seed=problems.SOLVER_SEED, sketch_dim=cfg2.d, tol=cfg2.tol, use_stagnation=False,
+                                  record_timing=False, max_iter=0)
+        pre = msvd.lobpcg_solve(op, msvd.PrecondKind.randomized, opts, want_precond=True)
+        v0 = msvd.sketch_and_solve_init(pre.precond, 1)[:, 0]
+        iters = 200
+        run = lambda: msvd.lanczos_gk(op, iters, v0, record_timing=False)  # noqa: E731
+        m, n = cfg2.m, cfg2.n
+        work = f"lanczos_gk: c2 matrix m={m} n={n}, {iters} steps from the rlobpcg start vector"
+        bytes_pass = 8 * m * n
+    for _ in range(args.warmup):
+        run()
+    torch.cuda.synchronize()
+    ctx.profile(True)
+    l0 = ctx.launch_count()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = run()
+    torch.cuda.synchronize()
+    t = (time.perf_counter() - t0) / args.steps
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    launches = (ctx.launch_count() - l0) // args.steps
+    a_ms, a_cnt = prof["apply"]
+    g_ms, g_cnt = prof["gram"]
+    ach_a = bytes_pass / (a_ms / a_cnt / 1e3) / 1e9 if a_cnt else None
+    ach_g = bytes_pass / (g_ms / g_cnt / 1e3) / 1e9 if g_cnt else None
+    line.update({"metric": f"time-to-solution (s), {args.workload}", "value": t, "unit": "s",
+                 "ms_per_step": t * 1e3, "config": {"workload": work},
+                 "kernel_ms": {k: round(v[0] / max(1, args.steps), 3) for k, v in prof.items()},
+                 "roofline": {"kernel": "apply pass (A W)" if args.workload == "lanczos" else "CSR SpMM (A W)",
+                              "bound": "hbm", "achieved": ach_a, "peak": peak, "peak_kind": peak_kind,
+                              "unit": "GB/s", "frac": ach_a / peak if ach_a else None,
+                              "bytes_per_launch": bytes_pass, "adjoint_achieved": ach_g,
+                              "adjoint_frac": ach_g / peak if ach_g else None},
+                 "gpu_launches": launches})
+    if args.workload == "csr":
+        line["iterations"] = res.iterations()
+        line["sigma_min"] = float(res.sigma[0])
+    else:
+        line["steps_run"] = res.steps
+        line["sigma_min"] = float(res.sigma_min)
+    return line
+
+
 def main():
     args = parse()
     from paper_2602_16797_b200 import problems
 
     cfg = problems.CONFIGS[args.config]
+    if args.workload != "solve":
+        print(json.dumps(extra_workload(args, cfg)), flush=True)
+        return
     if args.impl == "reference":
         line = reference_arm(args, cfg)
         if line is not None:
