@@ -28,8 +28,10 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "msvd_internal.h"
@@ -113,63 +115,74 @@ __global__ void csc_ptr_kernel(const uint32_t* keys, int64_t nnz, int64_t n, int
 }
 
 // ------------------------------------------------------------- Y = A W
-template <int G, typename Idx>
+template <int G, int B, typename Idx>
 __global__ void __launch_bounds__(kT) csr_spmm_kernel(const int64_t* __restrict__ rp, const Idx* __restrict__ ci,
                                                       const double* __restrict__ v, int64_t m,
-                                                      const double* __restrict__ W, int64_t n, int b, OutCols out) {
+                                                      const double* __restrict__ W, int64_t n, OutCols out) {
     const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t row = t / G;
     const int sub = static_cast<int>(t % G);
-    double acc[kMaxB];
+    double acc[B];
 #pragma unroll
-    for (int c = 0; c < kMaxB; ++c) acc[c] = 0.0;
+    for (int c = 0; c < B; ++c) acc[c] = 0.0;
     if (row < m) {
         const int64_t e = rp[row + 1];
         for (int64_t k = rp[row] + sub; k < e; k += G) {
             const double a = __ldg(v + k);
             const int64_t j = ld_idx(ci, k);
 #pragma unroll
-            for (int c = 0; c < kMaxB; ++c)
-                if (c < b) acc[c] += a * __ldg(W + j + c * n);
+            for (int c = 0; c < B; ++c) acc[c] += a * __ldg(W + j + c * n);
         }
     }
 #pragma unroll
-    for (int c = 0; c < kMaxB; ++c) {
-        if (c >= b) break;
+    for (int c = 0; c < B; ++c)
 #pragma unroll
         for (int o = G / 2; o >= 1; o >>= 1) acc[c] += __shfl_xor_sync(kFull, acc[c], o);
-    }
     if (row < m && sub == 0)
 #pragma unroll
-        for (int c = 0; c < kMaxB; ++c)
-            if (c < b) out.p[c][row] = acc[c];
+        for (int c = 0; c < B; ++c) out.p[c][row] = acc[c];
 }
 
 // ------------------------------------------------------------ G = A^T Y
 // Gpart[(s * b + c) * n + j] = sum over segment s of column j of the CSC
+template <int B>
 __global__ void __launch_bounds__(kT) csc_gather_kernel(const int64_t* __restrict__ cp,
                                                         const uint32_t* __restrict__ ri,
-                                                        const double* __restrict__ cv, int64_t n, Cols Y, int b,
+                                                        const double* __restrict__ cv, int64_t n, Cols Y,
                                                         int S, double* Gpart) {
+    constexpr int b = B;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t j = static_cast<int64_t>(blockIdx.x) * (kT / 32) + warp;
     const int s = blockIdx.y;
     if (j >= n) return;
     const int64_t c0 = cp[j], len = cp[j + 1] - c0;
     const int64_t q0 = c0 + (len * s) / S, q1 = c0 + (len * (s + 1)) / S;
-    double acc[kMaxB];
+    double acc[B];
 #pragma unroll
-    for (int c = 0; c < kMaxB; ++c) acc[c] = 0.0;
-    for (int64_t q = q0 + lane; q < q1; q += 32) {
+    for (int c = 0; c < B; ++c) acc[c] = 0.0;
+    constexpr int U = 4;  // four entries per lane in flight: the row-index -> Y loads overlap
+    int64_t q = q0 + lane;
+    for (; q + 32 * (U - 1) < q1; q += 32 * U) {
+        double a[U];
+        uint32_t r[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            a[u] = __ldg(cv + q + 32 * u);
+            r[u] = __ldg(ri + q + 32 * u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int c = 0; c < B; ++c) acc[c] += a[u] * __ldg(Y.p[c] + r[u]);
+    }
+    for (; q < q1; q += 32) {
         const double a = __ldg(cv + q);
         const uint32_t r = __ldg(ri + q);
 #pragma unroll
-        for (int c = 0; c < kMaxB; ++c)
-            if (c < b) acc[c] += a * __ldg(Y.p[c] + r);
+        for (int c = 0; c < B; ++c) acc[c] += a * __ldg(Y.p[c] + r);
     }
 #pragma unroll
-    for (int c = 0; c < kMaxB; ++c) {
-        if (c >= b) break;
+    for (int c = 0; c < B; ++c) {
         const double t = warp_sum(acc[c]);
         if (lane == 0) Gpart[(static_cast<int64_t>(s) * b + c) * n + j] = t;
     }
@@ -309,8 +322,11 @@ void csr_prepare(Ctx& c, msvd_matrix& M) {
     }
     // lanes per row from the mean row length
     const double mean = m > 0 ? static_cast<double>(nnz) / static_cast<double>(m) : 0.0;
+    // ~4 or more nonzeros per lane (measured at 10 per row: 2 lanes 4.6 TB/s,
+    // 4 lanes 3.4, 16 lanes 1.2)
     int g = 1;
-    while (g < 32 && g < mean) g <<= 1;
+    while (g < 32 && 4 * (2 * g) <= mean) g <<= 1;
+    if (const char* e = std::getenv("MSVD_CSR_LANES")) g = std::max(1, std::min(32, std::atoi(e)));
     M.csr_lanes = g;
     MSVD_CUDA(cudaStreamSynchronize(s));
 }
@@ -327,13 +343,27 @@ void csr_apply(Ctx& c, const msvd_matrix& M, const double* W, int b, OutCols out
     const int g = M.csr_lanes;
     const unsigned grid = grid_for(m * g);
     with_idx(M, [&](auto* ci) {
+        using Idx = std::remove_const_t<std::remove_pointer_t<decltype(ci)>>;
+        auto go = [&](auto gtag) {
+            constexpr int G = decltype(gtag)::value;
+            switch (b) {
+                case 1: csr_spmm_kernel<G, 1, Idx><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, out); break;
+                case 2: csr_spmm_kernel<G, 2, Idx><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, out); break;
+                case 3: csr_spmm_kernel<G, 3, Idx><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, out); break;
+                case 4: csr_spmm_kernel<G, 4, Idx><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, out); break;
+                case 5: csr_spmm_kernel<G, 5, Idx><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, out); break;
+                case 6: csr_spmm_kernel<G, 6, Idx><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, out); break;
+                case 7: csr_spmm_kernel<G, 7, Idx><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, out); break;
+                default: csr_spmm_kernel<G, 8, Idx><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, out); break;
+            }
+        };
         switch (g) {
-            case 1: csr_spmm_kernel<1><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, b, out); break;
-            case 2: csr_spmm_kernel<2><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, b, out); break;
-            case 4: csr_spmm_kernel<4><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, b, out); break;
-            case 8: csr_spmm_kernel<8><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, b, out); break;
-            case 16: csr_spmm_kernel<16><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, b, out); break;
-            default: csr_spmm_kernel<32><<<grid, kT, 0, c.stream>>>(M.csr_rp, ci, M.csr_v, m, W, M.n, b, out); break;
+            case 1: go(std::integral_constant<int, 1>{}); break;
+            case 2: go(std::integral_constant<int, 2>{}); break;
+            case 4: go(std::integral_constant<int, 4>{}); break;
+            case 8: go(std::integral_constant<int, 8>{}); break;
+            case 16: go(std::integral_constant<int, 16>{}); break;
+            default: go(std::integral_constant<int, 32>{}); break;
         }
     });
     MSVD_CUDA(cudaGetLastError());
@@ -353,7 +383,16 @@ int csr_adjoint_parts(Ctx& c, const msvd_matrix& M, Cols Y, int b, double* Gpart
     ProfScope prof(c, kProfGram);
     const int S = csr_parts(c, M);
     dim3 grid(static_cast<unsigned>(ceil_div(M.n, kT / 32)), static_cast<unsigned>(S));
-    csc_gather_kernel<<<grid, kT, 0, c.stream>>>(M.csc_cp, M.csc_ri, M.csc_cv, M.n, Y, b, S, Gpart);
+    switch (b) {
+        case 1: csc_gather_kernel<1><<<grid, kT, 0, c.stream>>>(M.csc_cp, M.csc_ri, M.csc_cv, M.n, Y, S, Gpart); break;
+        case 2: csc_gather_kernel<2><<<grid, kT, 0, c.stream>>>(M.csc_cp, M.csc_ri, M.csc_cv, M.n, Y, S, Gpart); break;
+        case 3: csc_gather_kernel<3><<<grid, kT, 0, c.stream>>>(M.csc_cp, M.csc_ri, M.csc_cv, M.n, Y, S, Gpart); break;
+        case 4: csc_gather_kernel<4><<<grid, kT, 0, c.stream>>>(M.csc_cp, M.csc_ri, M.csc_cv, M.n, Y, S, Gpart); break;
+        case 5: csc_gather_kernel<5><<<grid, kT, 0, c.stream>>>(M.csc_cp, M.csc_ri, M.csc_cv, M.n, Y, S, Gpart); break;
+        case 6: csc_gather_kernel<6><<<grid, kT, 0, c.stream>>>(M.csc_cp, M.csc_ri, M.csc_cv, M.n, Y, S, Gpart); break;
+        case 7: csc_gather_kernel<7><<<grid, kT, 0, c.stream>>>(M.csc_cp, M.csc_ri, M.csc_cv, M.n, Y, S, Gpart); break;
+        default: csc_gather_kernel<8><<<grid, kT, 0, c.stream>>>(M.csc_cp, M.csc_ri, M.csc_cv, M.n, Y, S, Gpart); break;
+    }
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
     return S;

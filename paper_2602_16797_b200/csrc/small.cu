@@ -3,6 +3,7 @@
 // Everything between the two A passes stays on the device: the host only
 // launches and, at check iterations, reads the stop/error words.
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "fold.cuh"
@@ -61,6 +62,107 @@ __global__ void __launch_bounds__(256) tsqr_kernel(TsqrArgs a) {
     for (int i = threadIdx.x; i < a.k * a.k; i += blockDim.x) {
         const int r = i % a.k, cc = i / a.k;
         out[i] = r <= cc ? Rw[0][r + cc * KM] : 0.0;
+    }
+}
+
+// Narrow trial blocks (k <= 8): the CTA's rows in chunks of 512 * RPT, each
+// chunk folded into the CTA's R in ONE Householder step with the whole CTA
+// (every thread holds RPT rows in registers; two fixed-order block
+// reductions per reflector) -- fold_rows' arithmetic with the chunk as the
+// X block, instead of a chain of 32-row warp folds.
+template <int KM, int RPT>
+__global__ void __launch_bounds__(512) tsqr_stacked_kernel(TsqrArgs a) {
+    __shared__ double R[KM * KM];
+    __shared__ double red[2][16][KM + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NW = 16;
+    const int k = a.k;
+    for (int i = threadIdx.x; i < KM * KM; i += blockDim.x) R[i] = 0.0;
+    const int64_t r0 = (a.m * blockIdx.x) / gridDim.x;
+    const int64_t r1 = (a.m * (blockIdx.x + 1)) / gridDim.x;
+    bool finite = true;
+    int buf = 0;
+    auto block_sums = [&](double (&v)[KM], int cnt, double (&out)[KM]) {
+        double(*rb)[KM + 1] = red[buf];
+        buf ^= 1;
+#pragma unroll
+        for (int l = 0; l < KM; ++l)
+            if (l < cnt) {
+                const double t = warp_sum(v[l]);
+                if (lane == 0) rb[warp][l] = t;
+            }
+        __syncthreads();
+#pragma unroll
+        for (int l = 0; l < KM; ++l) {
+            double t = 0.0;
+            if (l < cnt)
+#pragma unroll
+                for (int w = 0; w < NW; ++w) t += rb[w][l];
+            out[l] = t;
+        }
+    };
+    __syncthreads();
+    for (int64_t base = r0; base < r1; base += 512 * RPT) {
+        double x[RPT][KM];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int64_t row = base + threadIdx.x + 512 * i;
+#pragma unroll
+            for (int l = 0; l < KM; ++l) {
+                x[i][l] = (l < k && row < r1) ? a.T.p[l][row] : 0.0;
+                finite = finite && isfinite(x[i][l]);
+            }
+        }
+        for (int j = 0; j < k; ++j) {
+            double v[KM], o[KM];
+#pragma unroll
+            for (int l = 0; l < KM; ++l) v[l] = 0.0;
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) v[0] += x[i][j] * x[i][j];
+            block_sums(v, 1, o);
+            const double rjj = R[j + j * KM];
+            const double nrm2 = rjj * rjj + o[0];
+            if (nrm2 == 0.0) continue;  // svd.cpp:33-36
+            const double xnorm = sqrt(nrm2);
+            const double alpha = rjj >= 0.0 ? -xnorm : xnorm;
+            const double v0 = rjj - alpha;
+            const double beta = -v0 / alpha;
+#pragma unroll
+            for (int l = 0; l < KM; ++l) v[l] = 0.0;
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const double vi = x[i][j] / v0;
+#pragma unroll
+                for (int l = 0; l < KM; ++l)
+                    if (l > j && l < k) v[l] += vi * x[i][l];
+            }
+            block_sums(v, k, o);
+            double sl[KM];
+#pragma unroll
+            for (int l = 0; l < KM; ++l) sl[l] = (l > j && l < k) ? (R[j + l * KM] + o[l]) * beta : 0.0;
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const double vi = x[i][j] / v0;
+#pragma unroll
+                for (int l = 0; l < KM; ++l)
+                    if (l > j && l < k) x[i][l] -= sl[l] * vi;
+                x[i][j] = 0.0;
+            }
+            __syncthreads();  // every thread has read R's row j
+            if (threadIdx.x == 0) {
+                for (int l = j + 1; l < k; ++l) R[j + l * KM] -= sl[l];
+                R[j + j * KM] = alpha;
+            }
+            __syncthreads();
+        }
+    }
+    if (!__all_sync(kFull, finite) && lane == 0 && a.st) {
+        if (atomicCAS(&a.st->err_code, 0, kErrNonfiniteAT) == 0) a.st->err_iter = a.iter;
+    }
+    double* out = a.Rparts + static_cast<size_t>(blockIdx.x) * k * k;
+    for (int i = threadIdx.x; i < k * k; i += blockDim.x) {
+        const int r = i % k, cc = i / k;
+        out[i] = r <= cc ? R[r + cc * KM] : 0.0;
     }
 }
 
@@ -1026,9 +1128,16 @@ void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st,
         MSVD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
         kernel<<<grid, 512, sm, c.stream>>>(a);
     };
+    const bool stacked = !std::getenv("MSVD_TSQR_FOLD");
     switch (km_for(k)) {
-        case 4: tsqr_kernel<4><<<grid, 256, 0, c.stream>>>(a); break;
-        case 8: smem_launch(tsqr_smem_kernel<8>, 8); break;
+        case 4:
+            if (stacked) tsqr_stacked_kernel<4, 8><<<grid, 512, 0, c.stream>>>(a);
+            else tsqr_kernel<4><<<grid, 256, 0, c.stream>>>(a);
+            break;
+        case 8:
+            if (stacked) tsqr_stacked_kernel<8, 4><<<grid, 512, 0, c.stream>>>(a);
+            else smem_launch(tsqr_smem_kernel<8>, 8);
+            break;
         case 16: smem_launch(tsqr_smem_kernel<16>, 16); break;
         default: smem_launch(tsqr_smem_kernel<24>, 24); break;
     }
