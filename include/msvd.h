@@ -307,7 +307,9 @@ int64_t msvd_launch_count(msvd_ctx* ctx);
 /* Per-kernel-class device time with CUDA events on the ctx stream.  Slots:
  * 0 apply (A W), 1 gram (A^T Y), 2 tsqr, 3 rayleigh-ritz, 4 sketch,
  * 5 precond build (SVD), 6 precond apply, 7 cgs2, 8 reduce, 9 control.
- * Enabling resets the accumulators; read synchronizes the stream.          */
+ * enable: 0 off, 1 the A-pass classes only (apply, gram: two events per pass,
+ * negligible overhead), 2 every class.  Enabling resets the accumulators;
+ * read synchronizes the stream.                                             */
 int32_t msvd_ctx_profile(msvd_ctx* ctx, int32_t enable);
 int32_t msvd_ctx_profile_read(msvd_ctx* ctx, double* ms, int64_t* counts, int32_t nslots);
 

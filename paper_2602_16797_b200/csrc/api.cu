@@ -68,7 +68,7 @@ void* Ctx::ensure_scratch(size_t bytes) {
 }
 
 ProfScope::ProfScope(Ctx& ctx, int s) : c(ctx), slot(s) {
-    if (!c.profiling) return;
+    if (!c.profiling || (c.profiling == 1 && slot != kProfApply && slot != kProfGram)) return;
     size_t& used = c.prof_used[slot];
     auto& v = c.prof_ev[slot];
     if (used == v.size()) {
@@ -963,7 +963,7 @@ int32_t msvd_ctx_profile(msvd_ctx* ctx, int32_t enable) {
     return guard([&] {
         need(ctx, "context");
         Ctx& c = ctx->c;
-        c.profiling = enable != 0;
+        c.profiling = enable < 0 ? 0 : (enable > 2 ? 2 : enable);
         for (auto& u : c.prof_used) u = 0;
     });
 }

@@ -277,7 +277,7 @@ struct Ctx {
     void* svd_lw = nullptr;      // cuSOLVER work buffer
     size_t svd_lw_bytes = 0;
     // optional per-kernel-class timing (bench evidence): event pairs per slot
-    bool profiling = false;
+    int profiling = 0;  // 1: the A-pass classes (apply, gram) only; 2: every class
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[kProfSlots];
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_pool;
     size_t prof_used[kProfSlots] = {};

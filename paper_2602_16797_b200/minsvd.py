@@ -304,8 +304,10 @@ class Context:
     PROFILE_SLOTS = ("apply", "gram", "tsqr", "rr", "sketch", "svd", "precond", "cgs2", "reduce", "control")
 
     def profile(self, enable=True):
-        """Per-kernel-class CUDA-event timing on this context's stream."""
-        check(lib().msvd_ctx_profile(self.handle, int(enable)))
+        """Per-kernel-class CUDA-event timing on this context's stream.
+        enable: True / 2 every class, 1 the A-pass classes only (apply, gram),
+        False / 0 off."""
+        check(lib().msvd_ctx_profile(self.handle, 2 if enable is True else int(enable)))
 
     def profile_read(self):
         n = len(self.PROFILE_SLOTS)
