@@ -384,9 +384,13 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
                 const SketchLists L = sketch_prepare(c, ml, M->row0, plan.d, o.zeta, o.seed, step);
                 for (int64_t r = 0; r < ml; r += step) {
                     const int64_t rows = std::min(ml - r, step);
-                    MSVD_CUDA(cudaMemcpy2DAsync(const_cast<double*>(M->A) + r * M->ld, sizeof(double) * M->ld,
-                                                hs->hA + r * hs->ld, sizeof(double) * hs->ld, sizeof(double) * n,
-                                                rows, cudaMemcpyHostToDevice, c.copy_stream));
+                    if (M->ld == n && hs->ld == n)  // contiguous rows: one linear DMA
+                        MSVD_CUDA(cudaMemcpyAsync(const_cast<double*>(M->A) + r * n, hs->hA + r * n,
+                                                  sizeof(double) * n * rows, cudaMemcpyHostToDevice, c.copy_stream));
+                    else
+                        MSVD_CUDA(cudaMemcpy2DAsync(const_cast<double*>(M->A) + r * M->ld, sizeof(double) * M->ld,
+                                                    hs->hA + r * hs->ld, sizeof(double) * hs->ld, sizeof(double) * n,
+                                                    rows, cudaMemcpyHostToDevice, c.copy_stream));
                     MSVD_CUDA(cudaEventRecord(c.copy_ev, c.copy_stream));
                     MSVD_CUDA(cudaStreamWaitEvent(c.stream, c.copy_ev, 0));
                     sketch_rows(c, L, M->A, M->ld, static_cast<int>(n), geom.tma, r / step, SAr, st);

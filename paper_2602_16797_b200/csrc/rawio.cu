@@ -145,8 +145,12 @@ void raw_load_device(Ctx& c, const char* path, int64_t row0, int64_t rows, doubl
             if (std::fread(stage[cur], sizeof(double), static_cast<size_t>(cnt * n), fh.f) !=
                 static_cast<size_t>(cnt * n))
                 fail(MSVD_ERR_IO, p + ": read failed");
-            MSVD_CUDA(cudaMemcpy2DAsync(dA + r * ld, sizeof(double) * ld, stage[cur], sizeof(double) * n,
-                                        sizeof(double) * n, cnt, cudaMemcpyHostToDevice, c.copy_stream));
+            if (ld == n)  // contiguous rows: one linear DMA
+                MSVD_CUDA(cudaMemcpyAsync(dA + r * n, stage[cur], sizeof(double) * n * cnt, cudaMemcpyHostToDevice,
+                                          c.copy_stream));
+            else
+                MSVD_CUDA(cudaMemcpy2DAsync(dA + r * ld, sizeof(double) * ld, stage[cur], sizeof(double) * n,
+                                            sizeof(double) * n, cnt, cudaMemcpyHostToDevice, c.copy_stream));
             MSVD_CUDA(cudaEventRecord(done[cur], c.copy_stream));
         }
         MSVD_CUDA(cudaStreamSynchronize(c.copy_stream));
