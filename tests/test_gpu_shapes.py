@@ -1,0 +1,66 @@
+"""Shape sweep of the device solve against the CPU oracle: odd column counts,
+padded leading dimensions, every block size, explicit sketch sizes, dense and
+CSR operators -- the paths the kernels pick by shape (single-warp one-pass,
+warp-pair one-pass, two-pass, fused and separate TSQR, stacked merges).
+Gates: |dsigma| <= 1e-10 sigma_max and iterations within +-1 of the oracle,
+the subspace angle <= 1e-8 where the oracle converged."""
+import numpy as np
+import pytest
+
+from paper_2602_16797_b200 import problems
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # m, n, b, d, ld_pad
+    (3000, 37, 1, 0, 0), (4000, 64, 1, 256, 1), (5000, 65, 2, 0, 3), (2500, 99, 3, 400, 0),
+    (6000, 120, 4, 0, 2), (3000, 96, 5, 0, 0), (4000, 90, 8, 360, 1), (1000, 250, 1, 0, 0),
+    (2000, 130, 2, 520, 0), (3500, 17, 1, 68, 5),
+    # one-pass shapes: b = 1 with the fused TSQR and the deferred check refresh;
+    # b = 2 at n = 520 through the warp-pair kernel (odd ld)
+    (9000, 600, 1, 0, 0), (6000, 520, 2, 0, 1), (5000, 333, 1, 0, 2),
+]
+
+
+def spectrum(n, seed):
+    rng = np.random.default_rng(seed)
+    s = np.sort(np.logspace(0, -5, n) * (1 + 0.1 * rng.random(n)))[::-1]
+    return s
+
+
+@pytest.mark.parametrize("m,n,b,d,ld_pad", CASES)
+def test_dense_shapes(msvd, cuda, port, m, n, b, d, ld_pad):
+    import torch
+
+    sig = spectrum(n, m + n)
+    a, _ = port.synth_dense(sig, m, 1234 + n)
+    arr = np.zeros((m, n + ld_pad))
+    arr[:, :n] = a
+    dev = torch.from_numpy(arr).to(cuda)[:, :n]
+    opts = msvd.SolverOptions(seed=5, sketch_dim=d if d else -1, tol=1e-11, block_size=b, use_stagnation=False,
+                              record_timing=False, max_iter=120)
+    res = msvd.rlobpcg_block(msvd.DeviceDenseOperator(dev), opts)
+    ref = port.lobpcg_solve(a, opts.to_abi())
+    smax = ref["sigma_max_estimate"]
+    assert np.all(np.abs(res.sigma - ref["sigma"]) <= 1e-10 * smax), (res.sigma, ref["sigma"])
+    assert abs(res.iterations() - ref["iterations"]) <= 1, (res.iterations(), ref["iterations"])
+    if ref["status"] == "converged":
+        vr, vg = ref["v"][:, :1], res.v[:, :1]
+        assert np.linalg.norm(vr - vg @ (vg.T @ vr), 2) <= 1e-8
+
+
+@pytest.mark.parametrize("m,n,b,dens", [(3000, 40, 1, 0.2), (5000, 77, 2, 0.1), (4000, 60, 4, 0.15),
+                                        (2000, 33, 3, 0.5)])
+def test_csr_shapes(msvd, cuda, port, m, n, b, dens):
+    import torch
+
+    rp, ci, v = problems.random_csr(m, n, dens, m + n)
+    op = msvd.DeviceCsrOperator(torch.as_tensor(rp, device=cuda), torch.as_tensor(ci, device=cuda),
+                                torch.as_tensor(v, device=cuda), n)
+    opts = msvd.SolverOptions(seed=3, tol=1e-11, block_size=b, use_stagnation=False, record_timing=False,
+                              max_iter=150)
+    res = msvd.rlobpcg_block(op, opts)
+    ref = port.lobpcg_solve_csr((rp, ci, v, m, n), opts.to_abi())
+    smax = ref["sigma_max_estimate"]
+    assert np.all(np.abs(res.sigma - ref["sigma"]) <= 1e-10 * smax), (res.sigma, ref["sigma"])
+    assert abs(res.iterations() - ref["iterations"]) <= 1, (res.iterations(), ref["iterations"])
