@@ -372,10 +372,10 @@ void csr_apply(Ctx& c, const msvd_matrix& M, const double* W, int b, OutCols out
 
 int csr_parts(const Ctx& c, const msvd_matrix& M) {
     const int64_t n = M.n > 0 ? M.n : 1;
-    const int64_t target = static_cast<int64_t>(c.num_sms) * 64;  // resident warps
+    const int64_t target = static_cast<int64_t>(c.num_sms) * 256;  // 4 waves of resident warps: gathers in flight
     int64_t S = ceil_div(target, n);
     const int64_t mean = M.csr_nnz / n;
-    S = std::min<int64_t>(S, std::max<int64_t>(1, mean / 64));
+    S = std::min<int64_t>(S, std::max<int64_t>(1, mean / 128));
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(S, 64)));
 }
 
