@@ -220,6 +220,32 @@ def test_exact_counts_and_cache_verification(msvd, cuda, port):
     assert ver.record.to_csv() == plain.record.to_csv()
 
 
+def test_one_pass_options_and_counts(msvd, cuda, port):
+    """The one-pass loop with the deferred check refresh under the options
+    that add work inside it (verify_cached_products, store_iterates) and a
+    max_iter that ends on a check iteration: the reference's counters, rows
+    and trail (test_solver.cpp:237-265, solver.cpp:430-436)."""
+    cfg = problems.CONFIGS["c2"].scaled(m=20_000, n=500)
+    sig = cfg.spectrum()
+    a_dev, vmin = problems.make_problem_gpu(cfg.m, cfg.n, sig, device=cuda)
+    a_host = a_dev.cpu().numpy()
+    for max_iter in (51, 50):  # 50: the last iteration is a check (49 % 5 != 0 -> 50 rows)
+        o = msvd.SolverOptions(seed=problems.SOLVER_SEED, sketch_dim=cfg.d, tol=0.0, use_stagnation=False,
+                               record_timing=False, max_iter=max_iter, verify_cached_products=True,
+                               store_iterates=True)
+        res = msvd.rlobpcg_single(msvd.DeviceDenseOperator(a_dev), o)
+        ref = port.lobpcg_solve(a_host, o.to_abi(), want_iterates=True)
+        assert res.status == ref["status"] == "max_iter_reached"
+        assert res.iterations() == ref["iterations"] == max_iter
+        assert res.verify_count == ref["verify_count"] == max_iter // 25
+        assert res.max_cache_drift <= 1e-10 * res.sigma_max_estimate
+        assert [(r.matvecs_a, r.matvecs_at) for r in res.record.rows] == \
+            [(r["matvecs_a"], r["matvecs_at"]) for r in ref["record"]]
+        assert len(res.trail_t) == len(ref["trail_t"]) and len(res.trail_v) == len(ref["trail_v"])
+        smax = ref["sigma_max_estimate"]
+        assert abs(res.sigma[0] - ref["sigma"][0]) <= 1e-10 * smax
+
+
 def test_trial_basis_orthonormal_and_optimal(msvd, cuda, port):
     """test_solver.cpp:267-297"""
     a, _ = _instance(port, 150, 15, geometric_spectrum(15, 1e-4), 9)
