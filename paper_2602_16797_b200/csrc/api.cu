@@ -320,9 +320,9 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     ar.add(&Rres, n * b);
     ar.add(&tmp, n * b);
     ar.add(&Cm, kMaxK * 2 * kMaxB);
-    ar.add(&Gpart, static_cast<size_t>(std::max(geom.grid, gparts)) * (b + 1) * n);
-    ar.add(&Gout, n * (b + 1));
-    ar.add(&nrm, static_cast<size_t>(b + 1) * nblk);
+    ar.add(&Gpart, static_cast<size_t>(std::max(geom.grid, gparts)) * 2 * b * n);
+    ar.add(&Gout, n * 2 * b);
+    ar.add(&nrm, static_cast<size_t>(2 * b) * nblk);
     const int nparts_max = std::max(nparts, geom.grid);
     ar.add(&Rparts, static_cast<size_t>(nparts_max) * kmax * kmax);
     ar.add(&Rall, static_cast<size_t>(ranks) * nparts_max * kmax * kmax);
@@ -485,8 +485,8 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         one_pass = !csr && !(e && std::atoi(e) == 0) && o.check_every > 1 && rows_exact &&
                    apply_gram_supported(c, geom, b, fuse ? &probe : nullptr);
     }
-    // ex != nullptr (one-pass check refresh): the pass also forms A^T ex into
-    // Gout[n : 2n] (b = 1), next to A^T A W
+    // ex != nullptr (one-pass check refresh): the pass also forms A^T E for
+    // E = ex (m x b) into Gout[b n : 2 b n], next to A^T A W
     auto apply_tsqr = [&](Cols Tlead, int nlead, OutCols aw, Cols Tall, int k, int iter,
                           const double* ex = nullptr) -> std::pair<const double*, int> {
         TsqrFuse fz{};
@@ -499,11 +499,11 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         int np = nparts;
         bool fused = false;
         if (ex) {
-            if (launch_apply_ex(c, geom, W, aw, ex, Gpart, fuse ? &fz : nullptr)) np = geom.grid;
+            if (launch_apply_ex(c, geom, W, b, aw, ex, ml, Gpart, fuse ? &fz : nullptr)) np = geom.grid;
             else launch_tsqr(c, Tall, ml, k, Rparts, st, iter);
-            launch_reduce_g(c, Gpart, geom.grid, n, 2, nullptr, st, 0, Gout, nrm, nblk);
-            if (ranks > 1) comm.allreduce_sum(Gout, static_cast<size_t>(2 * n), c.stream);
-            MSVD_CUDA(cudaMemcpyAsync(ZW, Gout, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+            launch_reduce_g(c, Gpart, geom.grid, n, 2 * b, nullptr, st, 0, Gout, nrm, nblk);
+            if (ranks > 1) comm.allreduce_sum(Gout, static_cast<size_t>(2 * b * n), c.stream);
+            MSVD_CUDA(cudaMemcpyAsync(ZW, Gout, sizeof(double) * b * n, cudaMemcpyDeviceToDevice, c.stream));
             if (ranks == 1) return {Rparts, np};
             comm.allgather(Rparts, Rall, static_cast<size_t>(np) * k * k, c.stream);
             return {Rall, np * ranks};
@@ -550,7 +550,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     // pass), the check row is rewritten with the exact residual and the stop
     // rule runs on it (solver.cpp:439).  A stop returns that iterate; the
     // refreshed image A^T A V' feeds the Rayleigh-Ritz step otherwise.
-    const bool fused_check = one_pass && b == 1 && !gate_checks && apply_ex_supported(c, geom) &&
+    const bool fused_check = one_pass && b <= 2 && !gate_checks && apply_ex_supported(c, geom, b) &&
                              !(std::getenv("MSVD_FUSED_CHECK") && std::atoi(std::getenv("MSVD_FUSED_CHECK")) == 0);
     bool pending = false;  // a check row waits for the next pass
     const int* skip_flag = reinterpret_cast<const int*>(reinterpret_cast<unsigned char*>(st) +
@@ -660,8 +660,9 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         if (pending) {
             // the deferred check row i: R = A^T (A V') - theta^2 V' exactly,
             // the image refreshed, then the stop rule (row i, loop counter i-1)
-            launch_reduce_g(c, Gout + n, 1, n, b, Vb[cur], st, 1, Rres, nrm, nblk);
-            MSVD_CUDA(cudaMemcpyAsync(ZVb[cur], Gout + n, sizeof(double) * n, cudaMemcpyDeviceToDevice, c.stream));
+            launch_reduce_g(c, Gout + b * n, 1, n, b, Vb[cur], st, 1, Rres, nrm, nblk);
+            MSVD_CUDA(cudaMemcpyAsync(ZVb[cur], Gout + b * n, sizeof(double) * b * n, cudaMemcpyDeviceToDevice,
+                                      c.stream));
             ca.V = Vb[cur];
             ca.row = i;
             ca.check = 1;

@@ -104,11 +104,12 @@ bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
                   const TsqrFuse* fuse = nullptr, double* gpart = nullptr);
 bool apply_gram_supported(const Ctx& c, const StreamGeom& g, int b, const TsqrFuse* fuse);
 // b = 1: Y = A w and gpart[grid][2][n] = [A^T (A w), A^T e] in one pass (the
-// one-pass solver's check refresh of A^T A V', e = A V'); no fused TSQR
-bool apply_ex_supported(const Ctx& c, const StreamGeom& g);
-// (with `fuse` and e its first trial column the TSQR is folded in too: returns true)
-bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, OutCols out, const double* ex, double* gpart,
-                     const TsqrFuse* fuse = nullptr);
+// one-pass solver's check refresh of A^T A V', e = A V');
+// b = 2: Y = A W and gpart[grid][4][n] = [A^T (A W), A^T E] for E (m x 2, ld ld_ex)
+bool apply_ex_supported(const Ctx& c, const StreamGeom& g, int b);
+// (b = 1 with `fuse` and e its first trial column: the TSQR is folded in too, returns true)
+bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out, const double* ex,
+                     int64_t ld_ex, double* gpart, const TsqrFuse* fuse = nullptr);
 // out[j] = T Cm[:, j] for j < q (m-side recurrence products without A)
 void launch_tcombine(Ctx& c, Cols T, int k, const double* Cm, int q, OutCols out, int64_t m);
 // Gpart[grid][b][n]: A^T Y with Y = T C (gram mode, writes Y cols + extra cols)

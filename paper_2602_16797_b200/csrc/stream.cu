@@ -907,6 +907,179 @@ __global__ void __launch_bounds__(256, 1) apply_pair_kernel(ApplyArgs a) {
     }
 }
 
+// The check-refresh pass for b >= 2: a row is split across a TEAM of T
+// warps (T = 4: a quarter row each), so W, the accumulators of A^T (A W) and
+// of A^T E (E = A V' of the previous check iterate, b columns) and the row
+// values fit in registers.  Chunk c belongs to team c % (8 / T); the quarter
+// dot products meet in shared memory behind a per-team named barrier and are
+// summed in fixed order.  gpart holds [grid][2b][n].
+template <int B, int PL, int T>
+__global__ void __launch_bounds__(256, 1) apply_team_ex_kernel(ApplyArgs a, Cols ex) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int TEAMS = 8 / T;
+    constexpr int BG = 2 * B;
+    const StreamGeom& g = a.g;
+    unsigned char* extra;
+    constexpr size_t kXBytes = sizeof(double) * TEAMS * 2 * T * B;  // [team][buffer][member][B]
+    Pipe p = carve(smem, g, kXBytes, &extra);
+    double* xbuf = reinterpret_cast<double*>(extra);
+    int64_t r_begin, r_end;
+    cta_rows(g.m, r_begin, r_end);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < g.stages; ++s) mbar_init(&p.full[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const int cw = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tm = cw / T, h = cw % T;
+    const int bar = 1 + tm;
+    const int per_team = g.stages / TEAMS;
+    const int64_t nchunks = ceil_div(r_end - r_begin, g.rc);
+    const uint64_t pol = l2_evict_first_policy();
+    auto issue = [&](int64_t c, int s) {
+        const int64_t r0 = r_begin + c * g.rc;
+        const int64_t rc = min(static_cast<int64_t>(g.rc), r_end - r0);
+        const uint32_t bytes = static_cast<uint32_t>(rc * g.ld * 8);
+        mbar_arrive_expect_tx(&p.full[s], bytes);
+        bulk_g2s(p.stage0 + s * p.stage_bytes, g.A + r0 * g.ld, bytes, &p.full[s], pol);
+    };
+    if (h == 0 && lane == 0)
+        for (int j = 0; j < per_team; ++j) {
+            const int64_t c = tm + TEAMS * static_cast<int64_t>(j);
+            if (c < nchunks) issue(c, tm + TEAMS * j);
+        }
+    const int n = g.n;
+    const int npairs = (n + 1) >> 1;
+    const int part = (npairs + T - 1) / T;
+    const int p0 = h * part;
+    const int pend = min(npairs, p0 + part);
+    double w[PL][2][B], ga[PL][2][BG];
+    int off[PL];
+    bool keepy[PL], mine[PL];
+#pragma unroll
+    for (int i = 0; i < PL; ++i) {
+        const int pi = p0 + lane + 32 * i;
+        mine[i] = pi < pend;
+        const int pc = mine[i] ? pi : max(0, min(npairs - 1, pend - 1));
+        off[i] = 2 * pc;
+        keepy[i] = 2 * pc + 1 < n;
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            w[i][0][j] = mine[i] ? a.W[2 * pc + static_cast<int64_t>(j) * n] : 0.0;
+            w[i][1][j] = mine[i] && keepy[i] ? a.W[2 * pc + 1 + static_cast<int64_t>(j) * n] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < BG; ++j) ga[i][0][j] = ga[i][1][j] = 0.0;
+    }
+    // the chunk's E rows, lane l holding rows l and 32 + l, one chunk ahead
+    double exc[2][B], exn[2][B];
+    auto ex_load = [&](int64_t cc) {
+        if (cc >= nchunks) return;
+        const int64_t rr0 = r_begin + cc * g.rc;
+        const int rcc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - rr0));
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            exn[0][j] = lane < rcc ? ex.p[j][rr0 + lane] : 0.0;
+            exn[1][j] = 32 + lane < rcc ? ex.p[j][rr0 + 32 + lane] : 0.0;
+        }
+    };
+#pragma unroll
+    for (int j = 0; j < B; ++j) exn[0][j] = exn[1][j] = 0.0;
+    ex_load(tm);
+    int s = tm, xb = 0;
+    uint32_t ph = 0;
+    for (int64_t c = tm; c < nchunks; c += TEAMS) {
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            exc[0][j] = exn[0][j];
+            exc[1][j] = exn[1][j];
+        }
+        ex_load(c + TEAMS);
+        mbar_wait(&p.full[s], ph);
+        const double* As = reinterpret_cast<const double*>(p.stage0 + s * p.stage_bytes);
+        const int64_t r0 = r_begin + c * g.rc;
+        const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
+        for (int r = 0; r < rc; ++r) {
+            const double* row = As + static_cast<int64_t>(r) * g.ld_s;
+            double2 xr[PL];
+            double acc[B];
+#pragma unroll
+            for (int j = 0; j < B; ++j) acc[j] = 0.0;
+#pragma unroll
+            for (int i = 0; i < PL; ++i) {
+                double2 x = *reinterpret_cast<const double2*>(row + off[i]);
+                x.y = keepy[i] ? x.y : 0.0;  // odd n: the pad column is not A
+                xr[i] = x;
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                    acc[j] = fma(x.x, w[i][0][j], acc[j]);
+                    acc[j] = fma(x.y, w[i][1][j], acc[j]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < B; ++j) acc[j] = warp_sum(acc[j]);
+            double* xs = xbuf + (tm * 2 + xb) * T * B;
+            if (lane == 0)
+#pragma unroll
+                for (int j = 0; j < B; ++j) xs[h * B + j] = acc[j];
+            named_sync(bar, 32 * T);
+            double y[B], e[B];
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                double t = xs[j];
+#pragma unroll
+                for (int q = 1; q < T; ++q) t += xs[q * B + j];  // members in order: the same bits in every warp
+                y[j] = t;
+                e[j] = __shfl_sync(kFull, r < 32 ? exc[0][j] : exc[1][j], r & 31);
+            }
+            xb ^= 1;
+#pragma unroll
+            for (int i = 0; i < PL; ++i)
+#pragma unroll
+                for (int j = 0; j < B; ++j) {
+                    ga[i][0][j] = fma(xr[i].x, y[j], ga[i][0][j]);
+                    ga[i][1][j] = fma(xr[i].y, y[j], ga[i][1][j]);
+                    ga[i][0][B + j] = fma(xr[i].x, e[j], ga[i][0][B + j]);
+                    ga[i][1][B + j] = fma(xr[i].y, e[j], ga[i][1][B + j]);
+                }
+            if (h == 0 && lane < B) {
+                double v = y[0];
+#pragma unroll
+                for (int j = 1; j < B; ++j)
+                    if (lane == j) v = y[j];
+                a.out.p[lane][r0 + r] = v;
+            }
+        }
+        named_sync(bar, 32 * T);  // every member has read the stage: refill it
+        if (h == 0 && lane == 0 && c + g.stages < nchunks) issue(c + g.stages, s);
+        s += TEAMS;
+        if (s >= g.stages) {
+            s -= g.stages;
+            ph ^= 1;
+        }
+    }
+    __syncthreads();
+    double* red = reinterpret_cast<double*>(p.stage0);  // [TEAMS][BG][n]
+#pragma unroll
+    for (int i = 0; i < PL; ++i) {
+        if (!mine[i]) continue;
+        const int c0 = off[i];
+#pragma unroll
+        for (int j = 0; j < BG; ++j) {
+            red[(static_cast<size_t>(tm) * BG + j) * n + c0] = ga[i][0][j];
+            if (keepy[i]) red[(static_cast<size_t>(tm) * BG + j) * n + c0 + 1] = ga[i][1][j];
+        }
+    }
+    __syncthreads();
+    double* gp = a.gpart + static_cast<size_t>(blockIdx.x) * BG * n;
+    for (int i = threadIdx.x; i < BG * n; i += blockDim.x) {
+        double sum = red[i];
+#pragma unroll
+        for (int q = 1; q < TEAMS; ++q) sum += red[static_cast<size_t>(q) * BG * n + i];
+        gp[i] = sum;
+    }
+}
+
 struct GramArgs {
     StreamGeom g;
     Cols T;            // k columns of length m
@@ -1349,16 +1522,55 @@ bool apply_gram_supported(const Ctx& c, const StreamGeom& g, int b, const TsqrFu
 
 // b = 1 pass that also accumulates A^T e for an m-vector e: gpart[grid][2][n]
 // = [A_cta^T (A_cta w), A_cta^T e_cta] (the one-pass check refresh)
-bool apply_ex_supported(const Ctx& c, const StreamGeom& g) { return pair_ok(c, g, 1, true); }
+// team geometry: stages a multiple of the team count
+constexpr int kTeam = 4;
+int team_pl(int n) {
+    const int part = ((n + 1) / 2 + kTeam - 1) / kTeam;
+    const int pl = (part + 31) / 32;
+    return pl <= 4 ? 4 : (pl <= 8 ? 8 : 16);
+}
+StreamGeom team_geom(const Ctx& c, StreamGeom g) {
+    g = pair_geom(c, g);  // 4 * per_pair stages: a multiple of 8 / kTeam = 2 as well
+    return g;
+}
+bool team_ok(const Ctx& c, const StreamGeom& g0, int b) {
+    if (!g0.tma || b != 2 || std::getenv("MSVD_NO_PAIR")) return false;
+    if (b * team_pl(g0.n) > 8) return false;
+    const StreamGeom g = team_geom(c, g0);
+    if (g.stages * g.stage_bytes + bar_bytes(g.stages) + 1024 > c.smem_optin) return false;
+    return sizeof(double) * (8 / kTeam) * 2 * b * g0.n <= static_cast<size_t>(g.stages) * g.stage_bytes;
+}
 
-bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, OutCols out, const double* ex, double* gpart,
-                     const TsqrFuse* fuse) {
-    if (!pair_ok(c, g, 1, true)) fail(MSVD_ERR_INVALID, "msvd: A*W + A^T e pass on an unsupported shape");
+bool apply_ex_supported(const Ctx& c, const StreamGeom& g, int b) {
+    return b == 1 ? pair_ok(c, g, 1, true) : team_ok(c, g, b);
+}
+
+bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out, const double* ex,
+                     int64_t ld_ex, double* gpart, const TsqrFuse* fuse) {
+    if (!apply_ex_supported(c, g, b)) fail(MSVD_ERR_INVALID, "msvd: A*W + A^T e pass on an unsupported shape");
     if (g.m == 0) {
-        MSVD_CUDA(cudaMemsetAsync(gpart, 0, sizeof(double) * g.grid * 2 * g.n, c.stream));
+        MSVD_CUDA(cudaMemsetAsync(gpart, 0, sizeof(double) * g.grid * 2 * b * g.n, c.stream));
         return false;
     }
     ProfScope prof(c, kProfApply);
+    if (b == 2) {
+        ApplyArgs a{team_geom(c, g), W, out, TsqrFuse{}, gpart, nullptr};
+        Cols ec{};
+        for (int j = 0; j < b; ++j) ec.p[j] = ex + j * ld_ex;
+        static bool attr = false;
+        if (!attr) {
+            MSVD_CUDA(cudaFuncSetAttribute(apply_team_ex_kernel<2, 4, kTeam>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(c.smem_optin)));
+            attr = true;
+        }
+        const size_t sm = bar_bytes(a.g.stages) + 128 * ((sizeof(double) * (8 / kTeam) * 2 * kTeam * 2 + 127) / 128) +
+                          a.g.stages * a.g.stage_bytes;
+        apply_team_ex_kernel<2, 4, kTeam><<<a.g.grid, 256, sm, c.stream>>>(a, ec);
+        MSVD_CUDA(cudaGetLastError());
+        ++c.launches;
+        return false;
+    }
     // single-warp form with the fused TSQR when e is its first trial column
     // (the TSQR prefetch brings e's rows) and [8][2][n] fits the stage ring
     if (std::getenv("MSVD_EX_SINGLE") && fuse && fuse->Rparts && fuse->k <= 4 && fuse->k > 1 && fuse->T.p[0] == ex &&
