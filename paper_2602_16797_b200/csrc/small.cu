@@ -113,7 +113,9 @@ __global__ void __launch_bounds__(512) tsqr_stacked_kernel(TsqrArgs a) {
                 finite = finite && isfinite(x[i][l]);
             }
         }
-        for (int j = 0; j < k; ++j) {
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {  // unrolled: x stays in registers (a runtime j would index it in local memory)
+            if (j >= k) break;
             double v[KM], o[KM];
 #pragma unroll
             for (int l = 0; l < KM; ++l) v[l] = 0.0;
