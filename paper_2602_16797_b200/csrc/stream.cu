@@ -913,6 +913,8 @@ __global__ void __launch_bounds__(256, 1) apply_pair_kernel(ApplyArgs a) {
 // values fit in registers.  Chunk c belongs to team c % (8 / T); the quarter
 // dot products meet in shared memory behind a per-team named barrier and are
 // summed in fixed order.  gpart holds [grid][2b][n].
+constexpr int kTeamRows = 4;  // rows per team barrier (= rows per stage)
+
 template <int B, int PL, int T>
 __global__ void __launch_bounds__(256, 1) apply_team_ex_kernel(ApplyArgs a, Cols ex) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -920,7 +922,7 @@ __global__ void __launch_bounds__(256, 1) apply_team_ex_kernel(ApplyArgs a, Cols
     constexpr int BG = 2 * B;
     const StreamGeom& g = a.g;
     unsigned char* extra;
-    constexpr size_t kXBytes = sizeof(double) * TEAMS * 2 * T * B;  // [team][buffer][member][B]
+    constexpr size_t kXBytes = sizeof(double) * TEAMS * 2 * T * kTeamRows * B;  // [team][buffer][member][row][B]
     Pipe p = carve(smem, g, kXBytes, &extra);
     double* xbuf = reinterpret_cast<double*>(extra);
     int64_t r_begin, r_end;
@@ -986,6 +988,7 @@ __global__ void __launch_bounds__(256, 1) apply_team_ex_kernel(ApplyArgs a, Cols
 #pragma unroll
     for (int j = 0; j < B; ++j) exn[0][j] = exn[1][j] = 0.0;
     ex_load(tm);
+    static_assert(kTeamRows == 4, "the transpose-reduce below is written for 4 rows");
     int s = tm, xb = 0;
     uint32_t ph = 0;
     for (int64_t c = tm; c < nchunks; c += TEAMS) {
@@ -999,55 +1002,88 @@ __global__ void __launch_bounds__(256, 1) apply_team_ex_kernel(ApplyArgs a, Cols
         const double* As = reinterpret_cast<const double*>(p.stage0 + s * p.stage_bytes);
         const int64_t r0 = r_begin + c * g.rc;
         const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
-        for (int r = 0; r < rc; ++r) {
-            const double* row = As + static_cast<int64_t>(r) * g.ld_s;
-            double2 xr[PL];
-            double acc[B];
+        for (int r = 0; r < rc; r += kTeamRows) {
+            // sweep 1: this member's quarter-row dot products of kTeamRows rows, lane partials
+            double v[B][kTeamRows];
 #pragma unroll
-            for (int j = 0; j < B; ++j) acc[j] = 0.0;
+            for (int q = 0; q < kTeamRows; ++q) {
 #pragma unroll
-            for (int i = 0; i < PL; ++i) {
-                double2 x = *reinterpret_cast<const double2*>(row + off[i]);
-                x.y = keepy[i] ? x.y : 0.0;  // odd n: the pad column is not A
-                xr[i] = x;
+                for (int j = 0; j < B; ++j) v[j][q] = 0.0;
+                if (r + q < rc) {
+                    const double* row = As + static_cast<int64_t>(r + q) * g.ld_s;
 #pragma unroll
-                for (int j = 0; j < B; ++j) {
-                    acc[j] = fma(x.x, w[i][0][j], acc[j]);
-                    acc[j] = fma(x.y, w[i][1][j], acc[j]);
+                    for (int i = 0; i < PL; ++i) {
+                        double2 x = *reinterpret_cast<const double2*>(row + off[i]);
+                        x.y = keepy[i] ? x.y : 0.0;  // odd n: the pad column is not A
+#pragma unroll
+                        for (int j = 0; j < B; ++j) {
+                            v[j][q] = fma(x.x, w[i][0][j], v[j][q]);
+                            v[j][q] = fma(x.y, w[i][1][j], v[j][q]);
+                        }
+                    }
                 }
             }
-#pragma unroll
-            for (int j = 0; j < B; ++j) acc[j] = warp_sum(acc[j]);
-            double* xs = xbuf + (tm * 2 + xb) * T * B;
-            if (lane == 0)
-#pragma unroll
-                for (int j = 0; j < B; ++j) xs[h * B + j] = acc[j];
-            named_sync(bar, 32 * T);
-            double y[B], e[B];
+            // transpose-reduce: row q = (lane >> 3) & 3 ends in lanes 8q .. 8q+7
+            const bool b4 = lane & 16, b3 = lane & 8;
 #pragma unroll
             for (int j = 0; j < B; ++j) {
-                double t = xs[j];
 #pragma unroll
-                for (int q = 1; q < T; ++q) t += xs[q * B + j];  // members in order: the same bits in every warp
-                y[j] = t;
-                e[j] = __shfl_sync(kFull, r < 32 ? exc[0][j] : exc[1][j], r & 31);
+                for (int t = 0; t < 2; ++t) {
+                    const double send = b4 ? v[j][t] : v[j][t + 2];
+                    const double keep = b4 ? v[j][t + 2] : v[j][t];
+                    v[j][t] = keep + __shfl_xor_sync(kFull, send, 16);
+                }
+                {
+                    const double send = b3 ? v[j][0] : v[j][1];
+                    const double keep = b3 ? v[j][1] : v[j][0];
+                    v[j][0] = keep + __shfl_xor_sync(kFull, send, 8);
+                }
+                v[j][0] += __shfl_xor_sync(kFull, v[j][0], 4);
+                v[j][0] += __shfl_xor_sync(kFull, v[j][0], 2);
+                v[j][0] += __shfl_xor_sync(kFull, v[j][0], 1);
+            }
+            const int qm = (lane >> 3) & 3;
+            double* xs = xbuf + (tm * 2 + xb) * T * kTeamRows * B;  // [member][row][B]
+            if ((lane & 7) == 0)
+#pragma unroll
+                for (int j = 0; j < B; ++j) xs[(h * kTeamRows + qm) * B + j] = v[j][0];
+            named_sync(bar, 32 * T);
+            double ym[B];  // y of row qm: the members' quarters in order, the same bits in every warp
+#pragma unroll
+            for (int j = 0; j < B; ++j) {
+                double t = xs[qm * B + j];
+#pragma unroll
+                for (int mm = 1; mm < T; ++mm) t += xs[(mm * kTeamRows + qm) * B + j];
+                ym[j] = t;
             }
             xb ^= 1;
+            if (h == 0 && (lane & 7) == 0 && r + qm < rc)
 #pragma unroll
-            for (int i = 0; i < PL; ++i)
+                for (int j = 0; j < B; ++j) a.out.p[j][r0 + r + qm] = ym[j];
+            // sweep 2: the accumulators, the rows re-read from the stage
+#pragma unroll
+            for (int q = 0; q < kTeamRows; ++q) {
+                if (r + q >= rc) break;
+                const double* row = As + static_cast<int64_t>(r + q) * g.ld_s;
+                const int rr = r + q;
+                double y[B], e[B];
 #pragma unroll
                 for (int j = 0; j < B; ++j) {
-                    ga[i][0][j] = fma(xr[i].x, y[j], ga[i][0][j]);
-                    ga[i][1][j] = fma(xr[i].y, y[j], ga[i][1][j]);
-                    ga[i][0][B + j] = fma(xr[i].x, e[j], ga[i][0][B + j]);
-                    ga[i][1][B + j] = fma(xr[i].y, e[j], ga[i][1][B + j]);
+                    y[j] = __shfl_sync(kFull, ym[j], 8 * q);
+                    e[j] = __shfl_sync(kFull, rr < 32 ? exc[0][j] : exc[1][j], rr & 31);
                 }
-            if (h == 0 && lane < B) {
-                double v = y[0];
 #pragma unroll
-                for (int j = 1; j < B; ++j)
-                    if (lane == j) v = y[j];
-                a.out.p[lane][r0 + r] = v;
+                for (int i = 0; i < PL; ++i) {
+                    double2 x = *reinterpret_cast<const double2*>(row + off[i]);
+                    x.y = keepy[i] ? x.y : 0.0;
+#pragma unroll
+                    for (int j = 0; j < B; ++j) {
+                        ga[i][0][j] = fma(x.x, y[j], ga[i][0][j]);
+                        ga[i][1][j] = fma(x.y, y[j], ga[i][1][j]);
+                        ga[i][0][B + j] = fma(x.x, e[j], ga[i][0][B + j]);
+                        ga[i][1][B + j] = fma(x.y, e[j], ga[i][1][B + j]);
+                    }
+                }
             }
         }
         named_sync(bar, 32 * T);  // every member has read the stage: refill it
@@ -1529,15 +1565,25 @@ int team_pl(int n) {
     const int pl = (part + 31) / 32;
     return pl <= 4 ? 4 : (pl <= 8 ? 8 : 16);
 }
+// kTeamRows rows per stage (one team barrier per stage), as many stages per
+// team as the shared memory holds
 StreamGeom team_geom(const Ctx& c, StreamGeom g) {
-    g = pair_geom(c, g);  // 4 * per_pair stages: a multiple of 8 / kTeam = 2 as well
+    const int64_t row_bytes = static_cast<int64_t>(g.ld_s) * 8;
+    g.rc = kTeamRows;
+    g.stage_bytes = ((static_cast<size_t>(g.rc) * row_bytes + 127) / 128) * 128;
+    const int64_t xbytes = sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 2;
+    const int64_t avail = static_cast<int64_t>(c.smem_optin) - 2048 - xbytes;
+    const int64_t per_team =
+        std::max<int64_t>(2, std::min<int64_t>(8, avail / ((8 / kTeam) * static_cast<int64_t>(g.stage_bytes))));
+    g.stages = static_cast<int32_t>((8 / kTeam) * per_team);
     return g;
 }
 bool team_ok(const Ctx& c, const StreamGeom& g0, int b) {
     if (!g0.tma || b != 2 || std::getenv("MSVD_NO_PAIR")) return false;
     if (b * team_pl(g0.n) > 8) return false;
     const StreamGeom g = team_geom(c, g0);
-    if (g.stages * g.stage_bytes + bar_bytes(g.stages) + 1024 > c.smem_optin) return false;
+    const size_t xbytes = sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 2;
+    if (g.stages * g.stage_bytes + bar_bytes(g.stages) + xbytes + 1024 > c.smem_optin) return false;
     return sizeof(double) * (8 / kTeam) * 2 * b * g0.n <= static_cast<size_t>(g.stages) * g.stage_bytes;
 }
 
@@ -1564,7 +1610,7 @@ bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, int b, OutCol
                                            static_cast<int>(c.smem_optin)));
             attr = true;
         }
-        const size_t sm = bar_bytes(a.g.stages) + 128 * ((sizeof(double) * (8 / kTeam) * 2 * kTeam * 2 + 127) / 128) +
+        const size_t sm = bar_bytes(a.g.stages) + 128 * ((sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 2 + 127) / 128) +
                           a.g.stages * a.g.stage_bytes;
         apply_team_ex_kernel<2, 4, kTeam><<<a.g.grid, 256, sm, c.stream>>>(a, ec);
         MSVD_CUDA(cudaGetLastError());
