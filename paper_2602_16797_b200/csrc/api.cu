@@ -550,7 +550,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     // pass), the check row is rewritten with the exact residual and the stop
     // rule runs on it (solver.cpp:439).  A stop returns that iterate; the
     // refreshed image A^T A V' feeds the Rayleigh-Ritz step otherwise.
-    const bool fused_check = one_pass && b <= 2 && !gate_checks && apply_ex_supported(c, geom, b) &&
+    const bool fused_check = one_pass && b <= 4 && !gate_checks && apply_ex_supported(c, geom, b) &&
                              !(std::getenv("MSVD_FUSED_CHECK") && std::atoi(std::getenv("MSVD_FUSED_CHECK")) == 0);
     bool pending = false;  // a check row waits for the next pass
     const int* skip_flag = reinterpret_cast<const int*>(reinterpret_cast<unsigned char*>(st) +

@@ -105,7 +105,7 @@ bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
 bool apply_gram_supported(const Ctx& c, const StreamGeom& g, int b, const TsqrFuse* fuse);
 // b = 1: Y = A w and gpart[grid][2][n] = [A^T (A w), A^T e] in one pass (the
 // one-pass solver's check refresh of A^T A V', e = A V');
-// b = 2: Y = A W and gpart[grid][4][n] = [A^T (A W), A^T E] for E (m x 2, ld ld_ex)
+// b = 2..4: Y = A W and gpart[grid][2b][n] = [A^T (A W), A^T E] for E (m x b, ld ld_ex)
 bool apply_ex_supported(const Ctx& c, const StreamGeom& g, int b);
 // (b = 1 with `fuse` and e its first trial column: the TSQR is folded in too, returns true)
 bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out, const double* ex,

@@ -1563,7 +1563,7 @@ constexpr int kTeam = 4;
 int team_pl(int n) {
     const int part = ((n + 1) / 2 + kTeam - 1) / kTeam;
     const int pl = (part + 31) / 32;
-    return pl <= 4 ? 4 : (pl <= 8 ? 8 : 16);
+    return pl <= 2 ? 2 : (pl <= 4 ? 4 : (pl <= 8 ? 8 : 16));
 }
 // kTeamRows rows per stage (one team barrier per stage), as many stages per
 // team as the shared memory holds
@@ -1571,7 +1571,7 @@ StreamGeom team_geom(const Ctx& c, StreamGeom g) {
     const int64_t row_bytes = static_cast<int64_t>(g.ld_s) * 8;
     g.rc = kTeamRows;
     g.stage_bytes = ((static_cast<size_t>(g.rc) * row_bytes + 127) / 128) * 128;
-    const int64_t xbytes = sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 2;
+    const int64_t xbytes = sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 4;  // b <= 4
     const int64_t avail = static_cast<int64_t>(c.smem_optin) - 2048 - xbytes;
     const int64_t per_team =
         std::max<int64_t>(2, std::min<int64_t>(8, avail / ((8 / kTeam) * static_cast<int64_t>(g.stage_bytes))));
@@ -1579,10 +1579,10 @@ StreamGeom team_geom(const Ctx& c, StreamGeom g) {
     return g;
 }
 bool team_ok(const Ctx& c, const StreamGeom& g0, int b) {
-    if (!g0.tma || b != 2 || std::getenv("MSVD_NO_PAIR")) return false;
-    if (b * team_pl(g0.n) > 8) return false;
+    if (!g0.tma || b < 2 || b > 4 || std::getenv("MSVD_NO_PAIR")) return false;
+    if (b * team_pl(g0.n) > 8) return false;  // b = 2 to n = 1024, b = 3, 4 to n = 512
     const StreamGeom g = team_geom(c, g0);
-    const size_t xbytes = sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 2;
+    const size_t xbytes = sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 4;
     if (g.stages * g.stage_bytes + bar_bytes(g.stages) + xbytes + 1024 > c.smem_optin) return false;
     return sizeof(double) * (8 / kTeam) * 2 * b * g0.n <= static_cast<size_t>(g.stages) * g.stage_bytes;
 }
@@ -1599,20 +1599,23 @@ bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, int b, OutCol
         return false;
     }
     ProfScope prof(c, kProfApply);
-    if (b == 2) {
+    if (b >= 2) {
         ApplyArgs a{team_geom(c, g), W, out, TsqrFuse{}, gpart, nullptr};
         Cols ec{};
         for (int j = 0; j < b; ++j) ec.p[j] = ex + j * ld_ex;
-        static bool attr = false;
-        if (!attr) {
-            MSVD_CUDA(cudaFuncSetAttribute(apply_team_ex_kernel<2, 4, kTeam>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(c.smem_optin)));
-            attr = true;
-        }
-        const size_t sm = bar_bytes(a.g.stages) + 128 * ((sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 2 + 127) / 128) +
+        const size_t sm = bar_bytes(a.g.stages) +
+                          128 * ((sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 4 + 127) / 128) +
                           a.g.stages * a.g.stage_bytes;
-        apply_team_ex_kernel<2, 4, kTeam><<<a.g.grid, 256, sm, c.stream>>>(a, ec);
+        auto go = [&](auto kernel) {
+            MSVD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(c.smem_optin)));
+            kernel<<<a.g.grid, 256, sm, c.stream>>>(a, ec);
+        };
+        const int pl = team_pl(g.n);
+        if (b == 2 && pl <= 2) go(apply_team_ex_kernel<2, 2, kTeam>);
+        else if (b == 2) go(apply_team_ex_kernel<2, 4, kTeam>);
+        else if (b == 3) go(apply_team_ex_kernel<3, 2, kTeam>);
+        else go(apply_team_ex_kernel<4, 2, kTeam>);
         MSVD_CUDA(cudaGetLastError());
         ++c.launches;
         return false;
