@@ -19,6 +19,9 @@ CASES = [
     # one-pass shapes: b = 1 with the fused TSQR and the deferred check refresh;
     # b = 2 at n = 520 through the warp-pair kernel (odd ld)
     (9000, 600, 1, 0, 0), (6000, 520, 2, 0, 1), (5000, 333, 1, 0, 2),
+    # the check refresh on the next pass for b = 2..4 (the warp-team kernel: b = 2 at
+    # n = 1000 with a padded ld, b = 3 and 4 at odd n <= 512)
+    (4000, 1000, 2, 0, 2), (3000, 501, 3, 0, 0), (4000, 481, 4, 0, 2),
 ]
 
 
