@@ -11,12 +11,17 @@ library's stream, and an end-to-end number
 through the public host-buffer entry point (msvd_solve_host, pinned A copied
 in every step).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2|c5|...]
     torchrun ... bench.py --gpus N   (row-sharded over NCCL, one rank per GPU)
 
+`--gpus N` without torchrun spawns the N ranks itself and fails if fewer than
+N GPUs are visible.  Every rank generates only its own rows of A
+(problems.make_problem_shard), so the global A is the same at every N.
+
 `--impl reference` times the reference's own CPU solver (oracle/_ref, built
-from the reference's sources; else the oracle port) on a bounded sample of
-the same workload and extrapolates to the full size (see `cpu_baseline`).
+from the reference's sources) on the same bytes: complete solves of the FULL
+configuration for C1/C2/C4 (about a minute each at C2, one thread -- the
+reference has no threading), a bounded, extrapolated sample for C3/C5.
 """
 import argparse
 import json
@@ -46,6 +51,10 @@ def parse():
     p.add_argument("--m", type=int, default=0, help="override rows (debug only; invalidates the metric)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--ref-budget", type=float, default=420.0,
+                   help="--impl reference: stop timing further full solves once this many seconds are spent")
+    p.add_argument("--selftest", action="store_true",
+                   help="launcher/line-format check on CPU (gloo): no solve, no GPU")
     p.add_argument("--workload", default="solve", choices=["solve", "csr", "lanczos"],
                    help="solve: the BASELINE metric (default); csr / lanczos: the SURVEY 8f rows, "
                         "measured on their own lines")
@@ -120,90 +129,178 @@ def dist_env():
     return ws, rank, local
 
 
-def reference_arm(args, cfg):
-    """Reference CPU solver on a bounded sample, extrapolated to the config."""
-    import torch
+def host_cpu():
+    """CPU model and core counts of the box (the reference arm's hardware)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count(), "usable_cpus": len(os.sched_getaffinity(0))}
 
+
+def workload(cfg, m):
+    return {"workload": f"{cfg.name}: m={m} n={cfg.n} b={cfg.b} d={cfg.d} tol={cfg.tol:g} tol-only",
+            "l2": "inputs larger than L2 (A = %.1f GB)" % (8.0 * m * cfg.n / 1e9)}
+
+
+# Configurations whose full-size reference solve fits a bench run (about a
+# minute on one core, SURVEY 8d); C3 (an SVD of 4000 x 2000, about 6 min) and
+# C5 (hours, and 64 GB in host RAM) are timed on a bounded sample instead.
+FULL_REFERENCE = ("c1", "c2", "c4")
+
+
+def reference_solves(cfg, a_host, steps, budget_s, warmup):
+    """Time the reference's own solver (oracle/_ref: minsvd compiled from its
+    sources, one thread -- it has no threading) on the FULL configuration,
+    A column-major in host RAM.  Each step is one complete lobpcg_solve,
+    std::chrono around the call in the harness (steady_clock equivalent)
+    plus the reference's own set-up time record.rows[0].wall_ms
+    (solver.cpp:317-323, :382).  Steps stop early once `budget_s` is spent;
+    the line reports the steps actually run."""
     from oracle import pyoracle
     from paper_2602_16797_b200 import abi, problems
 
-    ws, rank, _ = dist_env()
-    if rank != 0:
-        return None
+    kind = "reference" if pyoracle.available("ref") else "port"
+    orc = pyoracle.load("ref" if kind == "reference" else "port")
+    opts = abi.default_options(seed=problems.SOLVER_SEED, sketch_dim=cfg.d, tol=cfg.tol, block_size=cfg.b,
+                               use_stagnation=0, record_timing=1)
+    c1 = problems.CONFIGS["c1"]
+    if warmup:  # page the library in: C1-size solves (0.1 s each), not the timed workload
+        a1, _ = pyoracle.load("port").synth_dense(c1.spectrum(), c1.m, problems.DATA_SEED)
+        for _ in range(warmup):
+            orc.lobpcg_solve(a1, abi.default_options(seed=7, sketch_dim=c1.d, tol=c1.tol, use_stagnation=0))
+    times, setups, r = [], [], None
+    t_start = time.perf_counter()
+    for k in range(steps):
+        t0 = time.perf_counter()
+        r = orc.lobpcg_solve(a_host, opts)
+        times.append(time.perf_counter() - t0)
+        setups.append(r["record"][0]["wall_ms"] / 1e3)
+        if time.perf_counter() - t_start + times[-1] > budget_s:
+            break
+    return kind, times, setups, r
+
+
+def reference_sample(cfg, steps):
+    """Bounded-sample reference timing for configurations whose full CPU solve
+    does not fit a bench run (C3, C5): the same recipe at m = 2e4 (full n, b,
+    d), extrapolated linearly in m for the sketch and the A passes (the sketch
+    SVD does not depend on m)."""
+    from oracle import pyoracle
+    from paper_2602_16797_b200 import abi, problems
+
     kind = "reference" if pyoracle.available("ref") else "port"
     orc = pyoracle.load("ref" if kind == "reference" else "port")
     m_s = 20_000
     sig = cfg.spectrum()
-    if torch.cuda.is_available():
-        a_dev, _ = problems.make_problem_gpu(m_s, cfg.n, sig)
-        a = a_dev.cpu().numpy()
-        del a_dev
-    else:
-        a, _ = pyoracle.load("port").synth_dense(sig, m_s, problems.DATA_SEED)
-        a = np.ascontiguousarray(a)
-    opts = abi.default_options(seed=problems.SOLVER_SEED, sketch_dim=cfg.d, tol=cfg.tol,
-                               block_size=cfg.b, use_stagnation=0)
-    # per-pass cost at the sample size, to split the m-scaling part
-    acm = np.asfortranarray(a)
-
-    def one():
-        t0 = time.perf_counter()
-        r = orc.lobpcg_solve(acm, opts)
-        t = time.perf_counter() - t0
-        t_sk0 = time.perf_counter()
-        orc.sketch_apply(acm, cfg.d, 4, problems.SOLVER_SEED)
-        t_sk = time.perf_counter() - t_sk0
-        setup = r["record"][0]["wall_ms"] / 1e3
-        iters = r["iterations"]
-        per_pass = (t - setup) / max(1, 2 * iters)
-        scale = cfg.m / m_s
-        # m-proportional parts: sketch, 2 init passes, 2 passes per iteration
-        t_full = t + (scale - 1.0) * (t_sk + per_pass * 2 * (iters + 1))
-        return t_full, t, iters, per_pass
-
-    warm = min(args.warmup, 1)
-    for _ in range(warm):
-        one()
+    a, _ = pyoracle.load("port").synth_fast(sig, m_s, problems.DATA_SEED)
+    opts = abi.default_options(seed=problems.SOLVER_SEED, sketch_dim=cfg.d, tol=cfg.tol, block_size=cfg.b,
+                               use_stagnation=0, record_timing=1)
     vals = []
-    budget = 240.0
-    t_start = time.perf_counter()
-    samples = []
-    for k in range(args.steps):
-        v, t, iters, per_pass = one()
-        vals.append(v)
-        samples.append(t)
-        if time.perf_counter() - t_start > budget and k + 1 < args.steps:
-            break
-    value = float(np.mean(vals))
-    a_gbs = 8.0 * cfg.m * cfg.n / (per_pass * cfg.m / m_s) / 1e9
-    sample = (f"reference lobpcg_solve (single-threaded, {kind}) on the {cfg.name} recipe at m={m_s} "
-              f"(n={cfg.n}, d={cfg.d}, tol {cfg.tol:g}, tol-only), {iters} iterations, {np.mean(samples):.2f} s per "
-              f"sample; extrapolated to m={cfg.m} by scaling the sketch and A passes linearly in m "
-              f"(the sketch SVD is m-independent)")
+    for _ in range(max(1, min(steps, 2))):
+        t0 = time.perf_counter()
+        r = orc.lobpcg_solve(a, opts)
+        t = time.perf_counter() - t0
+        t1 = time.perf_counter()
+        orc.sketch_apply(a, cfg.d, 4, problems.SOLVER_SEED)
+        t_sk = time.perf_counter() - t1
+        setup = r["record"][0]["wall_ms"] / 1e3
+        per_pass = (t - setup) / max(1, 2 * r["iterations"])
+        vals.append(t + (cfg.m / m_s - 1.0) * (t_sk + per_pass * 2 * (r["iterations"] + 1)))
+    sample = (f"{kind} lobpcg_solve (one thread) on the {cfg.name} recipe at m={m_s} (full n={cfg.n}, b={cfg.b}, "
+              f"d={cfg.d}), {r['iterations']} iterations, {t:.1f} s; EXTRAPOLATED to m={cfg.m} linearly in the "
+              f"sketch and the A passes (the full solve does not fit a bench run)")
+    return kind, vals, sample
+
+
+def reference_arm(args, cfg):
+    """`--impl reference`: the reference's own CPU solver on this config, on
+    the box's host cores, on the same bytes our arm solves (generated on the
+    device, transposed once to the reference's column-major DenseMatrix)."""
+    import torch
+
+    from paper_2602_16797_b200 import problems
+
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    sig = cfg.spectrum()
+    m = args.m or cfg.m
+    cpu = host_cpu()
+    if cfg.name in FULL_REFERENCE or args.m:
+        if torch.cuda.is_available():
+            a_dev, _ = problems.make_problem_shard(m, cfg.n, sig, 0, m, device="cuda:0")
+            a = a_dev.t().contiguous().cpu().numpy().T  # column-major
+            del a_dev
+            torch.cuda.empty_cache()
+        else:
+            from oracle import pyoracle
+            a, _ = pyoracle.load("port").synth_fast(sig, m, problems.DATA_SEED)
+        kind, times, setups, r = reference_solves(cfg, a, args.steps, args.ref_budget, args.warmup)
+        value = float(np.mean(times))
+        iters = r["iterations"]
+        per_iter = (value - float(np.mean(setups))) / max(1, iters + 1)
+        a_gbs = 2 * 8.0 * m * cfg.n / per_iter / 1e9
+        sample = (f"{kind} lobpcg_solve on the FULL {cfg.name} configuration (m={m}, n={cfg.n}, b={cfg.b}, "
+                  f"d={cfg.d}, tol {cfg.tol:g}, tol-only), one thread (the reference has no threading), "
+                  f"{len(times)} complete solve(s) of {iters} iterations; set-up (sketch + sketch SVD, "
+                  f"record.rows[0].wall_ms) {np.mean(setups):.1f} s")
+        steps = len(times)
+        extra = {"iterations": iters, "status": r["status"], "sigma": [float(x) for x in r["sigma"]],
+                 "setup_s": float(np.mean(setups)), "steps_requested": args.steps,
+                 "warmup_kind": "C1-size reference solves (library page-in), untimed"}
+    else:
+        kind, times, sample = reference_sample(cfg, args.steps)
+        value = float(np.mean(times))
+        steps = len(times)
+        a_gbs = None
+        extra = {"steps_requested": args.steps, "extrapolated": True}
     line = {
-        "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus, "steps": len(vals),
-        "warmup": warm, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: m={cfg.m} n={cfg.n} b={cfg.b} d={cfg.d} tol={cfg.tol:g}",
-                   "inputs": "host RAM"},
-        "impl": "reference",
-        "a_stream_gbs": a_gbs,
-        "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": kind, "sample": sample},
+        "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U diag(s) V^T, generated on device)",
+        "config": workload(cfg, m), "impl": "reference", "a_stream_gbs": a_gbs,
+        "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": kind, "sample": sample, "host": cpu},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
+    line.update(extra)
     return line
 
 
-def cpu_baseline_quick(cfg):
-    """Reported CPU baseline for our arm (rank 0, N=1): same model as the
-    reference arm with one sample."""
-    class A:
-        warmup = 0
-        steps = 1
-        gpus = 1
-    line = reference_arm(A, cfg)
-    return line["cpu_baseline"] if line else None
+def parity_vs(res, r, b, tol):
+    """The north-star gates of our solve against the reference's on the same
+    bytes (|dsigma| <= 1e-10 sigma_max, sin <= 1e-8 for v_min, +-1 iterations)."""
+    smax = r["sigma_max_estimate"]
+    ds = float(np.max(np.abs(np.asarray(res.sigma) - np.asarray(r["sigma"])))) / smax
+    vr, vg = r["v"][:, 0], res.v[:, 0]
+    sin = float(np.linalg.norm(vr - vg * (vg @ vr)))
+    di = res.iterations() - r["iterations"]
+    return {"dsigma_over_sigma_max": ds, "sin_vmin": sin, "iterations_ours": res.iterations(),
+            "iterations_reference": r["iterations"], "ok": bool(ds <= 1e-10 and sin <= 1e-8 and abs(di) <= 1)}
+
+
+def cpu_baseline_for(args, cfg, a, res):
+    """Reported CPU baseline for our arm (rank 0, N = 1): one reference solve
+    of the same bytes at the full configuration where that fits (C1, C2, C4),
+    with the parity of our answer against it; a bounded sample otherwise."""
+    import torch
+
+    if cfg.name in FULL_REFERENCE or args.m:
+        host = a.t().contiguous().cpu().numpy().T
+        torch.cuda.empty_cache()
+        kind, times, setups, r = reference_solves(cfg, host, 1, 0.0, 0)
+        out = {"value": times[0], "unit": "s", "cores": 1, "kind": kind, "host": host_cpu(),
+               "sample": f"one complete {kind} lobpcg_solve of the same A bytes (full {cfg.name}), one thread; "
+                         f"set-up {setups[0]:.1f} s, {r['iterations']} iterations"}
+        return out, parity_vs(res, r, cfg.b, cfg.tol)
+    kind, vals, sample = reference_sample(cfg, 1)
+    return {"value": vals[0], "unit": "s", "cores": 1, "kind": kind, "sample": sample, "host": host_cpu()}, None
 
 
 def ours(args, cfg):
@@ -215,7 +312,10 @@ def ours(args, cfg):
 
     ws, rank, local = dist_env()
     if ws != args.gpus:
-        args.gpus = ws
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={ws} (launch through torchrun, or run "
+                         f"without WORLD_SIZE and bench.py spawns the ranks)")
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench: rank {rank} needs GPU {local}, only {torch.cuda.device_count()} visible")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
@@ -233,13 +333,11 @@ def ours(args, cfg):
 
     m = args.m or cfg.m
     sig = cfg.spectrum()
-    a_full, vmin = problems.make_problem_gpu(m, cfg.n, sig, device=dev)
     r0, rows = msvd.shard_rows(m, ws, rank)
-    if ws > 1:
-        a = a_full[r0:r0 + rows].clone()
-        del a_full
-    else:
-        a = a_full
+    # each rank generates and orthonormalises only its own rows (the R
+    # factors of the generator's TSQR meet in one allreduce)
+    a, vtrue = problems.make_problem_shard(m, cfg.n, sig, r0, rows,
+                                           (lambda t: dist.all_reduce(t)) if ws > 1 else None, device=dev)
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     op = msvd.DeviceDenseOperator(a, ctx=ctx, row0=r0, m_global=m)
@@ -297,7 +395,7 @@ def ours(args, cfg):
     # iterations)
     init_passes = 2 if prof["gram"][1] / max(1, args.steps) >= max(1, it) else 1
     loop_passes = per_step - init_passes
-    a_gbs_iter = loop_passes * 8.0 * m * cfg.n / (np.median(loop_ms) / 1e3) / 1e9 if it else None
+    a_gbs_iter = loop_passes * 8.0 * rows * cfg.n / (np.median(loop_ms) / 1e3) / 1e9 if it else None
 
     # roofline of the dominant kernel -- the A*W pass, which in one-pass mode
     # also forms A^T A W and folds the TSQR (every iteration), while the
@@ -320,15 +418,17 @@ def ours(args, cfg):
             traffic = json.load(open(tpath)).get(cfg.name, {}).get(dominant + "_kernel")
         except Exception:
             traffic = None
-
+    smax = res.sigma_max_estimate
+    truth = {"sigma_err_over_sigma_max": [float(abs(res.sigma[j] - sig[::-1][j]) / smax) for j in range(cfg.b)],
+             "sin_vmin_vs_truth": float(np.linalg.norm(vtrue[:, -1] - res.v[:, 0] * (res.v[:, 0] @ vtrue[:, -1])))}
 
     line = {
         "metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U diag(s) V^T, generated on device)",
-        "config": {"workload": f"{cfg.name}: m={m} n={cfg.n} b={cfg.b} d={cfg.d} tol={cfg.tol:g} tol-only",
-                   "parallelism": f"row-shard x{ws}", "iterations": it,
-                   "l2": "inputs larger than L2 (A = %.1f GB per rank)" % (8.0 * rows * cfg.n / 1e9)},
+        "config": workload(cfg, m),
+        "parallelism": f"row-shard x{ws} (rows {rows} on rank 0)",
+        "iterations": it, "status": res.status, "sigma": [float(x) for x in res.sigma], "vs_truth": truth,
         "a_stream_gbs_per_iter": a_gbs_iter,
         "a_passes_per_iter": loop_passes / it if it else None,
         "breakdown_ms": {k: round(v, 3) for k, v in res.timings_ms.items()},
@@ -336,7 +436,9 @@ def ours(args, cfg):
         "roofline": {"kernel": kname, "bound": "hbm", "achieved": achieved,
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "bytes_per_launch": bytes_launch, "launches": a_cnt if dominant == "apply" else g_cnt,
+                     "frac_of_8tbs": (achieved / 8000.0) if achieved else None,
+                     "bytes_per_launch": bytes_launch, "per_gpu": True,
+                     "launches": a_cnt if dominant == "apply" else g_cnt,
                      "apply_kernel_achieved": achieved_apply, "gram_kernel_achieved": achieved_gram,
                      "gram_launches": g_cnt},
         "clocks": clk,
@@ -346,7 +448,9 @@ def ours(args, cfg):
         line["e2e"] = e2e(msvd, ctx, a, res, opts, args, cfg, solve)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline_quick(cfg)
+            line["cpu_baseline"], par = cpu_baseline_for(args, cfg, a, res)
+            if par is not None:
+                line["parity_vs_reference"] = par
         except Exception as ex:  # reported, never fatal
             line["cpu_baseline"] = {"value": None, "error": str(ex)}
     if ws > 1:
@@ -456,6 +560,53 @@ def extra_workload(args, cfg):
     return line
 
 
+def spawn_ranks(args):
+    """`--gpus N` outside a torchrun environment: launch the N ranks here
+    (torch.distributed.run, one process per GPU, rendezvous on 127.0.0.1)
+    and return their exit status.  Never downgrades to fewer ranks."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def selftest(args, cfg):
+    """Launcher and line-format check without a GPU (gloo): every rank does a
+    fixed CPU stand-in step; the timing is the max over ranks, as in ours()."""
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, _ = dist_env()
+    if ws != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={ws}")
+    if ws > 1:
+        dist.init_process_group("gloo")
+    x = torch.ones(128, 128, dtype=torch.float64)
+    for _ in range(args.warmup):
+        x @ x
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        x @ x
+    t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item() * 1e3 / args.steps
+    line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "selftest (no solve)", "config": workload(cfg, cfg.m),
+            "parallelism": f"row-shard x{ws}", "selftest": True, "ranks_reported": ws}
+    if ws > 1:
+        dist.destroy_process_group()
+    return line if rank == 0 else None
+
+
 def main():
     args = parse()
     from paper_2602_16797_b200 import problems
@@ -465,11 +616,19 @@ def main():
         print(json.dumps(extra_workload(args, cfg)), flush=True)
         return
     if args.impl == "reference":
-        line = reference_arm(args, cfg)
+        line = reference_arm(args, cfg)  # rank 0 only; the others exit without work
         if line is not None:
             print(json.dumps(line), flush=True)
         return
-    line = ours(args, cfg)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if not args.selftest:
+            import torch
+
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                raise SystemExit(f"bench: --gpus {args.gpus} needs {args.gpus} GPUs, {have} visible")
+        sys.exit(spawn_ranks(args))
+    line = selftest(args, cfg) if args.selftest else ours(args, cfg)
     if line is not None:
         print(json.dumps(line), flush=True)
 

@@ -232,6 +232,13 @@ int32_t msvd_aw_gram(msvd_matrix* mat, const double* dW, int64_t b, double* dAW,
  * already reduced to R: sigma descending, V sign-fixed.                     */
 int32_t msvd_small_svd(msvd_ctx* ctx, const double* dB, int64_t k,
                        double* dSigma, double* dV);
+/* solver.cpp:177-211 check_convergence, evaluated by the device solver's own
+ * stop rule (the control kernel's code) on a HOST history of `len` rows:
+ * flags[4] = {tol_ok, resid_stalled, progress_stalled, stop}.  Throws
+ * (DimensionError) like the reference when i + 1 >= len.                   */
+int32_t msvd_check_convergence(msvd_ctx* ctx, const double* resid_hist, const double* theta_hist,
+                               int64_t len, int32_t i, double sigma1_estimate, double tol,
+                               double factor, int32_t use_stagnation, int32_t* flags);
 
 /* ---- raw binary A interchange -----------------------
  * The dense-matrix counterpart of write_matrix_market_array / read (io.cpp:
@@ -311,6 +318,14 @@ int64_t msvd_launch_count(msvd_ctx* ctx);
  * negligible overhead), 2 every class.  Enabling resets the accumulators;
  * read synchronizes the stream.                                             */
 int32_t msvd_ctx_profile(msvd_ctx* ctx, int32_t enable);
+/* Bit mask of the A-pass kernel variants launched on ctx since the last reset
+ * (test evidence that a shape took the path it is meant to):
+ *   1 apply_rows (producer warp)      2 apply_self (TMA, one warp per row)
+ *   4 apply_pair (warp pair per row)  8 apply_pair EX (b = 1 check refresh)
+ *  16 apply_team_ex (b = 2..4 check refresh)   32 apply ticket (b >= 5)
+ *  64 gram (A^T Y pass)              128 separate TSQR pass
+ * reset != 0 clears the mask after reading it.                             */
+int64_t msvd_ctx_kernel_paths(msvd_ctx* ctx, int32_t reset);
 int32_t msvd_ctx_profile_read(msvd_ctx* ctx, double* ms, int64_t* counts, int32_t nslots);
 
 #ifdef __cplusplus

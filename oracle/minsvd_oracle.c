@@ -37,6 +37,12 @@
 static __thread jmp_buf *g_jmp;
 static __thread char g_msg[512];
 static __thread int g_code;
+/* The input generators (haar_orthonormal, synth, assemble) split their column
+ * loops over OpenMP threads: each output column is still computed by one thread
+ * in the serial operation order, so the bytes do not depend on the thread count
+ * (tests/test_oracle.py pins them to the reference).  Everything else, the
+ * solver included, stays single-threaded like the reference. */
+static __thread int g_par;
 
 typedef struct blk { struct blk *next; void *pad; } blk; /* 16-byte header */
 static __thread blk *g_arena;
@@ -74,6 +80,7 @@ static void arena_release(void) {
     g_arena = NULL;                      \
     g_jmp = &jb__;                       \
     if (setjmp(jb__)) {                  \
+        g_par = 0;                       \
         arena_release();                 \
         g_arena = arena__;               \
         g_jmp = saved__;                 \
@@ -169,6 +176,7 @@ static void matvec_t(mat m, const double *x, double *y) {
 static mat matmul(mat a, mat b) {
     if (a.c != b.r) raise_err(MSVD_ERR_DIMENSION, "matmul: dimension mismatch");
     mat c = mnew(a.r, b.c);
+#pragma omp parallel for schedule(static) if (g_par && a.r * a.c > 65536)
     for (int64_t j = 0; j < b.c; ++j) {
         double *cj = col(c, j);
         for (int64_t k = 0; k < a.c; ++k) {
@@ -222,6 +230,7 @@ static hqr qr_factor(mat a_in) {
         q.beta[k] = -v0 / alpha;
         ck[k] = alpha;
         const double beta = q.beta[k];
+#pragma omp parallel for schedule(static) if (g_par && (m - k) * (n - k) > 65536)
         for (int64_t j = k + 1; j < n; ++j) {
             double *cj = col(w, j);
             double s = cj[k];
@@ -251,6 +260,7 @@ static mat qr_q_times(hqr q, mat b) {
         const double beta = q.beta[k];
         if (beta == 0.0) continue;
         const double *vk = col(q.a, k);
+#pragma omp parallel for schedule(static) if (g_par && (m - k) * y.c > 65536)
         for (int64_t j = 0; j < y.c; ++j) {
             double *cj = col(y, j);
             double s = cj[k];
@@ -1131,14 +1141,17 @@ static mat haar(int64_t m, int64_t n, uint64_t seed) {
 
 int orc_haar_orthonormal(int64_t m, int64_t n, uint64_t seed, double *q) {
     ENTER();
+    g_par = 1;
     mat h = haar(m, n, seed);
     memcpy(q, h.p, sizeof(double) * (size_t)(m * n));
+    g_par = 0;
     LEAVE();
 }
 
 /* synth(explicit_list) dense assembly (matgen.cpp:141-176): A = U diag(s) V^T */
 int orc_synth_dense(const double *sigma, int64_t n, int64_t m, uint64_t seed, double *a_colmajor, double *v_min) {
     ENTER();
+    g_par = 1;
     if (n < 2) raise_err(MSVD_ERR_DIMENSION, "spectrum: need at least two values");
     for (int64_t i = 0; i < n; ++i) {
         if (!(sigma[i] > 0.0)) raise_err(MSVD_ERR_NUMERICAL, "spectrum: values must be strictly positive");
@@ -1155,6 +1168,7 @@ int orc_synth_dense(const double *sigma, int64_t n, int64_t m, uint64_t seed, do
     }
     mat a = matmul(u, transpose(v));
     memcpy(a_colmajor, a.p, sizeof(double) * (size_t)(m * n));
+    g_par = 0;
     LEAVE();
 }
 
@@ -1162,6 +1176,7 @@ int orc_synth_dense(const double *sigma, int64_t n, int64_t m, uint64_t seed, do
  * are assembled directly, since spectrum() rejects them (matgen.cpp:41-47). */
 int orc_assemble_svd(const double *sigma, int64_t n, int64_t m, uint64_t seed, double *a_colmajor, double *v_min) {
     ENTER();
+    g_par = 1;
     if (m < n) raise_err(MSVD_ERR_DIMENSION, "synth: need rows >= columns");
     sm64 ku = sm_keyed(seed, 0x55u), kv = sm_keyed(seed, 0x56u);
     mat u = haar(m, n, sm_u64(&ku));
@@ -1173,6 +1188,109 @@ int orc_assemble_svd(const double *sigma, int64_t n, int64_t m, uint64_t seed, d
     }
     mat a = matmul(u, transpose(v));
     memcpy(a_colmajor, a.p, sizeof(double) * (size_t)(m * n));
+    g_par = 0;
+    LEAVE();
+}
+
+/* ------------------------------------------------ harness-only generator
+ * NOT a reference recipe: a fast, bit-reproducible stand-in for synth() at the
+ * sizes where matgen's serial Householder QR of an m x n Gaussian would take
+ * many minutes (the full-n parity fixtures: C3 at n = 2000, C5 at n = 1000).
+ *
+ *   X  m x n Gaussian, column j from SplitMix64(seed, 0x1000 + j) (rng.hpp)
+ *   G  = X^T X, accumulated over fixed 512-row chunks in chunk order
+ *   R  = chol(G) (upper), so U = X R^{-1} is orthonormal to ~kappa(X)^2 u
+ *        (kappa(X) ~ 1.2-1.6 for the tall Gaussians used here)
+ *   V  = haar_orthonormal(n, n, SplitMix64(seed, 0x56)) (matgen.cpp:126-139)
+ *   A  = X M with M = R^{-1} diag(sigma) V^T, so A = U diag(sigma) V^T
+ *
+ * Every output element is computed by one thread in a fixed operation order
+ * (no FMA: -ffp-contract=off), so the bytes depend only on (sigma, m, seed),
+ * never on the thread count; the fixtures pin them by SHA-256.  Exact zeros
+ * in sigma give exactly zero rows of diag(sigma) V^T, hence an exact
+ * rank deficiency of M up to the rounding of the triangular solve.        */
+static double dot4(const double *a, const double *b, int64_t len) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t i = 0;
+    for (; i + 4 <= len; i += 4) {
+        s0 += a[i] * b[i];
+        s1 += a[i + 1] * b[i + 1];
+        s2 += a[i + 2] * b[i + 2];
+        s3 += a[i + 3] * b[i + 3];
+    }
+    for (; i < len; ++i) s0 += a[i] * b[i];
+    return (s0 + s1) + (s2 + s3);
+}
+
+int orc_synth_fast(const double *sigma, int64_t n, int64_t m, uint64_t seed, double *a_colmajor, double *v_out) {
+    ENTER();
+    g_par = 1;
+    if (n < 1 || m < n) raise_err(MSVD_ERR_DIMENSION, "synth_fast: need rows >= columns >= 1");
+    mat x = mnew(m, n);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t j = 0; j < n; ++j) {
+        sm64 r = sm_keyed(seed, 0x1000u + (uint64_t)j);
+        double *c = col(x, j);
+        for (int64_t i = 0; i < m; ++i) c[i] = sm_gauss(&r);
+    }
+    /* G (upper triangle) = sum over 512-row chunks, in chunk order */
+    mat g = mnew(n, n);
+    const int64_t CH = 512;
+    for (int64_t r0 = 0; r0 < m; r0 += CH) {
+        const int64_t len = (m - r0 < CH) ? m - r0 : CH;
+#pragma omp parallel for schedule(dynamic, 8)
+        for (int64_t q = 0; q < n; ++q) {
+            const double *xq = col(x, q) + r0;
+            for (int64_t p = 0; p <= q; ++p) AT(g, p, q) += dot4(col(x, p) + r0, xq, len);
+        }
+    }
+    /* right-looking Cholesky, R stored transposed (rt(l, k) = R(k, l)) */
+    mat rt = mnew(n, n);
+    for (int64_t k = 0; k < n; ++k) {
+        const double d = AT(g, k, k);
+        if (!(d > 0.0)) raise_err(MSVD_ERR_NUMERICAL, "synth_fast: Gram matrix not positive definite");
+        const double rkk = sqrt(d);
+        AT(rt, k, k) = rkk;
+        for (int64_t j = k + 1; j < n; ++j) AT(rt, j, k) = AT(g, k, j) / rkk;
+        const double *rk = col(rt, k);
+#pragma omp parallel for schedule(static) if ((n - k) * (n - k) > 16384)
+        for (int64_t j = k + 1; j < n; ++j)
+            for (int64_t i = k + 1; i <= j; ++i) AT(g, i, j) -= rk[i] * rk[j];
+    }
+    sm64 kv = sm_keyed(seed, 0x56u);
+    mat v = haar(n, n, sm_u64(&kv));
+    memcpy(v_out, v.p, sizeof(double) * (size_t)(n * n));
+    /* M = R^{-1} diag(sigma) V^T, column by column (back substitution) */
+    mat mm = mnew(n, n);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t j = 0; j < n; ++j) {
+        double *mj = col(mm, j);
+        for (int64_t k = n - 1; k >= 0; --k) {
+            const double *rk = col(rt, k); /* rk[l] = R(k, l) */
+            double s = sigma[k] * AT(v, j, k);
+            for (int64_t l = k + 1; l < n; ++l) s -= rk[l] * mj[l];
+            mj[k] = s / rk[k];
+        }
+    }
+    /* A = X M over 128-row blocks; A(i, j) = sum_k M(k, j) X(i, k), k ascending */
+    const int64_t RB = 128;
+    const int64_t nblk = (m + RB - 1) / RB;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t bi = 0; bi < nblk; ++bi) {
+        const int64_t i0 = bi * RB, len = (m - i0 < RB) ? m - i0 : RB;
+        for (int64_t j = 0; j < n; ++j) {
+            double acc[128];
+            for (int64_t i = 0; i < len; ++i) acc[i] = 0.0;
+            const double *mj = col(mm, j);
+            for (int64_t k = 0; k < n; ++k) {
+                const double c = mj[k];
+                const double *xk = col(x, k) + i0;
+                for (int64_t i = 0; i < len; ++i) acc[i] += c * xk[i];
+            }
+            memcpy(a_colmajor + j * m + i0, acc, sizeof(double) * (size_t)len);
+        }
+    }
+    g_par = 0;
     LEAVE();
 }
 

@@ -181,6 +181,21 @@ class Oracle:
         self._check(f(_p(sigma), n, m, seed, _p(a), _p(vmin)))
         return a, vmin
 
+    def synth_fast(self, sigma, m, seed):
+        """Harness-only generator (port only; minsvd_oracle.c orc_synth_fast):
+        A = U diag(sigma) V^T with U = X R^-1 from a Cholesky QR of a seeded
+        Gaussian X and V = haar_orthonormal(n, n); bit-reproducible and
+        thread-count independent.  Returns (A column-major, V n x n)."""
+        sigma = _f64(sigma)
+        n = sigma.size
+        a = np.empty((m, n), dtype=np.float64, order="F")
+        v = np.empty((n, n), dtype=np.float64, order="F")
+        f = self.lib.orc_synth_fast
+        f.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_int64, C.c_uint64, C.POINTER(C.c_double),
+                      C.POINTER(C.c_double)]
+        self._check(f(_p(sigma), n, m, seed, _p(a), _p(v)))
+        return a, v
+
     def haar_orthonormal(self, m, n, seed):
         q = np.empty((m, n), order="F")
         self._check(self._haar(m, n, seed, _p(q)))

@@ -199,10 +199,25 @@ std::string err_message(const DevState& s) {
     }
 }
 
-DevState read_state(Ctx& c, const DevState* st) {
+DevState read_state_raw(Ctx& c, const DevState* st) {
     DevState h;
     MSVD_CUDA(cudaMemcpyAsync(&h, st, sizeof(DevState), cudaMemcpyDeviceToHost, c.stream));
     MSVD_CUDA(cudaStreamSynchronize(c.stream));
+    return h;
+}
+
+DevState read_state(Ctx& c, const DevState* st) {
+    const DevState h = read_state_raw(c, st);
+    if (h.err_code != kErrNone) fail(MSVD_ERR_NUMERICAL, err_message(h));
+    return h;
+}
+
+// a deferred check row that stops: the speculative work of the next
+// iteration is discarded, so its replacements and errors are too
+DevState stopped_state(DevState h) {
+    h.err_code = h.snap_err_code;
+    h.err_iter = h.snap_err_iter;
+    h.replacements = h.snap_replacements;
     if (h.err_code != kErrNone) fail(MSVD_ERR_NUMERICAL, err_message(h));
     return h;
 }
@@ -550,8 +565,21 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     // pass), the check row is rewritten with the exact residual and the stop
     // rule runs on it (solver.cpp:439).  A stop returns that iterate; the
     // refreshed image A^T A V' feeds the Rayleigh-Ritz step otherwise.
-    const bool fused_check = one_pass && b <= 4 && !gate_checks && apply_ex_supported(c, geom, b) &&
-                             !(std::getenv("MSVD_FUSED_CHECK") && std::atoi(std::getenv("MSVD_FUSED_CHECK")) == 0);
+    bool fused_check = one_pass && b <= 4 && !gate_checks && apply_ex_supported(c, geom, b) &&
+                       !(std::getenv("MSVD_FUSED_CHECK") && std::atoi(std::getenv("MSVD_FUSED_CHECK")) == 0);
+    // One-pass mode and the check refresh decide which collectives run and
+    // their sizes, and each rank derives them from its own geometry (ld
+    // parity, pointer alignment, m_local) and environment: the ranks agree on
+    // the most conservative choice before the first collective of the loop.
+    if (ranks > 1) {
+        double h[2] = {one_pass ? 0.0 : 1.0, fused_check ? 0.0 : 1.0};
+        MSVD_CUDA(cudaMemcpyAsync(tmp, h, sizeof(h), cudaMemcpyHostToDevice, c.stream));
+        comm.allreduce_max(tmp, 2, c.stream);
+        MSVD_CUDA(cudaMemcpyAsync(h, tmp, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+        one_pass = one_pass && h[0] == 0.0;
+        fused_check = fused_check && one_pass && h[1] == 0.0;
+    }
     bool pending = false;  // a check row waits for the next pass
     const int* skip_flag = reinterpret_cast<const int*>(reinterpret_cast<unsigned char*>(st) +
                                                          offsetof(DevState, skip_exact));
@@ -646,11 +674,13 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     int status = 1;
     int last_row = 0;
     int64_t verify_count = 0;
+    bool deferred_stop = false;
     for (int i = 0; i < max_iter; ++i) {
         const bool first = (i == 0);
         const int nx = first ? 0 : b;
         const int k = b + nx + b;
         const int nxt = cur ^ 1;
+        if (pending) launch_snapshot(c, st);
         launch_precond(c, kind, Vcol, Vrow, sig, dinv, n, Rres, b, tmp, W, st, i);
         launch_cgs2(c, W, n, b, cols_n({{Vb[cur], b}, {Xb[cur], nx}}), b + nx, st, i);
         for (int j = 0; j < b; ++j) out.p[j] = AW + static_cast<int64_t>(j) * ml;
@@ -668,11 +698,13 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
             ca.check = 1;
             launch_control(c, ca);
             pending = false;
-            const DevState h = read_state(c, st);
+            const DevState h = read_state_raw(c, st);
             if (h.stop) {
                 status = 0;
+                deferred_stop = true;
                 break;
             }
+            if (h.err_code != kErrNone) fail(MSVD_ERR_NUMERICAL, err_message(h));
         }
         RRArgs ra{};
         ra.Rparts = parts.first;
@@ -764,7 +796,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         }
     }
     MSVD_CUDA(cudaEventRecord(c.ev[4], c.stream));
-    const DevState fin = read_state(c, st);
+    const DevState fin = deferred_stop ? stopped_state(read_state_raw(c, st)) : read_state(c, st);
 
     // ---- results (solver.cpp:469-476): ascending from the smallest ----
     std::vector<double> V(static_cast<size_t>(n) * b);
@@ -963,6 +995,13 @@ int32_t msvd_ctx_synchronize(msvd_ctx* ctx) {
 }
 
 int64_t msvd_launch_count(msvd_ctx* ctx) { return ctx ? ctx->c.launches : -1; }
+
+int64_t msvd_ctx_kernel_paths(msvd_ctx* ctx, int32_t reset) {
+    if (!ctx) return -1;
+    const int64_t p = ctx->c.paths;
+    if (reset) ctx->c.paths = 0;
+    return p;
+}
 
 int32_t msvd_ctx_profile(msvd_ctx* ctx, int32_t enable) {
     return guard([&] {
@@ -1338,6 +1377,32 @@ int32_t msvd_small_svd(msvd_ctx* ctx, const double* dB, int64_t k, double* dSigm
         const DevState h = read_state(c, st);
         if (std::getenv("MSVD_DEBUG_JACOBI")) std::fprintf(stderr, "msvd_small_svd: k=%lld sweeps=%g\n",
                                                          static_cast<long long>(k), h.worst_jacobi);
+    });
+}
+
+int32_t msvd_check_convergence(msvd_ctx* ctx, const double* resid_hist, const double* theta_hist, int64_t len,
+                               int32_t i, double sigma1_estimate, double tol, double factor, int32_t use_stagnation,
+                               int32_t* flags) {
+    return guard([&] {
+        need(ctx, "context");
+        need(flags, "flags");
+        if (i + 1 >= len || i < 0)  // solver.cpp:181-183
+            fail(MSVD_ERR_DIMENSION, "check_convergence: history shorter than the loop counter");
+        need(resid_hist, "resid_hist");
+        need(theta_hist, "theta_hist");
+        Ctx& c = ctx->c;
+        set_device(c);
+        double* d = nullptr;
+        MSVD_CUDA(cudaMalloc(&d, sizeof(double) * 2 * len + sizeof(int) * 4));
+        MSVD_CUDA(cudaMemcpyAsync(d, resid_hist, sizeof(double) * len, cudaMemcpyHostToDevice, c.stream));
+        MSVD_CUDA(cudaMemcpyAsync(d + len, theta_hist, sizeof(double) * len, cudaMemcpyHostToDevice, c.stream));
+        int* df = reinterpret_cast<int*>(d + 2 * len);
+        launch_stop_rule(c, d, d + len, i, sigma1_estimate, tol, factor, use_stagnation, df);
+        int hf[4];
+        MSVD_CUDA(cudaMemcpyAsync(hf, df, sizeof(hf), cudaMemcpyDeviceToHost, c.stream));
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+        MSVD_CUDA(cudaFree(d));
+        for (int k = 0; k < 4; ++k) flags[k] = hf[k];
     });
 }
 

@@ -416,8 +416,7 @@ void csr_sketch(Ctx& c, const msvd_matrix& M, int64_t d, int zeta, uint64_t seed
     const size_t smem = sizeof(double) * n * warps;
     with_idx(M, [&](auto* ci) {
         auto kern = csr_sketch_kernel<std::remove_const_t<std::remove_pointer_t<decltype(ci)>>>;
-        if (smem > 48 * 1024)
-            MSVD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        if (smem > 48 * 1024) optin_smem(c, kern);
         kern<<<static_cast<unsigned>(ceil_div(d, warps)), 32 * warps, smem, c.stream>>>(M.csr_rp, ci, M.csr_v, n, d,
                                                                                         L.offs, L.vals, L.val, SA);
     });

@@ -431,9 +431,7 @@ void lanczos_run(Ctx& c, const msvd_matrix& M, int iters, const double* v0h, con
     double coeff = a1;
 
     const size_t bis_smem = sizeof(double) * 2 * static_cast<size_t>(N2);
-    if (bis_smem > 48 * 1024)
-        MSVD_CUDA(cudaFuncSetAttribute(bidiag_min_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(bis_smem)));
+    if (bis_smem > 48 * 1024) optin_smem(c, bidiag_min_kernel);
     for (int j = 1; j <= iters; ++j) {
         // w = A^T u_{j-1} - alpha_{j-1} v_{j-1}, reorthogonalized against V
         Cols T{};

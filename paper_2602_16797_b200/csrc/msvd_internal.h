@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "msvd.h"
@@ -55,6 +56,12 @@ struct DevState {
     double worst_jacobi;
     int32_t skip_exact;     // one-pass check gate: 1 = the images' residual decides (far from tol)
     int32_t pad_;
+    // taken before the speculative work a deferred check row runs ahead of its
+    // stop test (precond, cgs2 and the next pass of iteration i + 1): a stop
+    // there reports the state the reference stops with
+    int32_t snap_err_code;
+    int32_t snap_err_iter;
+    int64_t snap_replacements;
 };
 
 // column-pointer bundles passed by value to kernels
@@ -88,6 +95,9 @@ struct StreamGeom {
 };
 
 struct Ctx;
+
+enum KernelPath : int64_t { kPathRows = 1, kPathSelf = 2, kPathPair = 4, kPathPairEx = 8, kPathTeamEx = 16,
+                            kPathTicket = 32, kPathGram = 64, kPathTsqr = 128 };
 
 enum ProfSlot { kProfApply = 0, kProfGram, kProfTsqr, kProfRR, kProfSketch, kProfSvd, kProfPrecond, kProfCgs2,
                 kProfReduce, kProfControl, kProfSlots };
@@ -173,6 +183,11 @@ void launch_precond(Ctx& c, int kind, const double* Vcol, const double* Vrow, co
                     DevState* st, int iter);
 void launch_cgs2(Ctx& c, double* W, int64_t n, int b, Cols basis, int nb, DevState* st, int iter);
 void launch_state_init(Ctx& c, DevState* st, uint64_t seed);
+void launch_snapshot(Ctx& c, DevState* st);
+// the control kernel's stop rule on a given history (flags: tol_ok,
+// resid_stalled, progress_stalled, stop; device memory)
+void launch_stop_rule(Ctx& c, const double* rh, const double* th, int i, double sigma1, double tol, double factor,
+                      int use_stag, int* flags);  // snap_* <- err_code, err_iter, replacements
 void launch_drift(Ctx& c, const double* fresh, const double* cached, int64_t count, DevState* st,
                   double limit, int iter);
 void launch_colnorms(Ctx& c, const StreamGeom& g, double* part, double* out);
@@ -282,7 +297,21 @@ struct Ctx {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_ev[kProfSlots];
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_pool;
     size_t prof_used[kProfSlots] = {};
+    // A-pass kernel variants launched (msvd_ctx_kernel_paths bits)
+    int64_t paths = 0;
+    // kernels already opted in to the device's full dynamic shared memory
+    std::unordered_set<const void*> smem_attr;
 };
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device-context setting:
+// opt each kernel in once per Ctx (a Ctx is bound to one device), never
+// through process-wide flags (several devices / FakeComm threads per process)
+template <class K>
+inline void optin_smem(Ctx& c, K* kernel) {
+    if (c.smem_attr.insert(reinterpret_cast<const void*>(kernel)).second)
+        MSVD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(c.smem_optin)));
+}
 
 // RAII: events around the launches of one kernel class when profiling
 struct ProfScope {

@@ -738,6 +738,34 @@ __global__ void gate_kernel(const double* nrm_part, int nblk, int b, DevState* s
     st->skip_exact = best > thresh ? 1 : 0;
 }
 
+// the stop rule (solver.cpp:177-211) for loop counter i: flags = {tol_ok,
+// resid_stalled, progress_stalled, stop}
+__device__ void stop_rule(const double* rh, const double* th, int i, double sigma1, double tol, double factor,
+                          int use_stag, int flags[4]) {
+    const bool tol_ok = rh[i + 1] <= sigma1 * sigma1 * tol;
+    bool rs = false, ps = false, stop = tol_ok;
+    if (use_stag) {
+        if (i >= 4) rs = factor * rh[i + 1] >= rh[i - 4];
+        if (i >= 9) {
+            const double dn = th[i] > 0.0 ? th[i] : 1.0;
+            const double dt = th[i - 4] > 0.0 ? th[i - 4] : 1.0;
+            const double recent = (th[i - 4] - th[i + 1]) / dn;
+            const double earlier = (th[i - 9] - th[i - 4]) / dt;
+            ps = factor * recent >= earlier;
+        }
+        stop = tol_ok && rs && ps;
+    }
+    flags[0] = tol_ok;
+    flags[1] = rs;
+    flags[2] = ps;
+    flags[3] = stop;
+}
+
+__global__ void stop_rule_kernel(const double* rh, const double* th, int i, double sigma1, double tol,
+                                 double factor, int use_stag, int* flags) {
+    stop_rule(rh, th, i, sigma1, tol, factor, use_stag, flags);
+}
+
 // record row + stop rule (solver.cpp:376-397, :177-211)
 __global__ void __launch_bounds__(256) control_kernel(ControlArgs a) {
     __shared__ double red[8];
@@ -785,24 +813,9 @@ __global__ void __launch_bounds__(256) control_kernel(ControlArgs a) {
     a.rh[a.row] = resid_s;
     a.th[a.row] = st->theta[0];
     if (a.check) {
-        const int i = a.row - 1;
-        const double* rh = a.rh;
-        const double* th = a.th;
-        const bool tol_ok = rh[i + 1] <= a.sigma1 * a.sigma1 * a.tol;
-        bool stop = tol_ok;
-        if (a.use_stag) {
-            bool rs = false, ps = false;
-            if (i >= 4) rs = a.factor * rh[i + 1] >= rh[i - 4];
-            if (i >= 9) {
-                const double dn = th[i] > 0.0 ? th[i] : 1.0;
-                const double dt = th[i - 4] > 0.0 ? th[i - 4] : 1.0;
-                const double recent = (th[i - 4] - th[i + 1]) / dn;
-                const double earlier = (th[i - 9] - th[i - 4]) / dt;
-                ps = a.factor * recent >= earlier;
-            }
-            stop = tol_ok && rs && ps;
-        }
-        st->stop = stop ? 1 : 0;
+        int f[4];
+        stop_rule(a.rh, a.th, a.row - 1, a.sigma1, a.tol, a.factor, a.use_stag, f);
+        st->stop = f[3];
     }
 }
 
@@ -1017,6 +1030,15 @@ __global__ void state_init_kernel(DevState* st, uint64_t seed) {
     st->max_drift = 0.0;
     st->worst_jacobi = 0.0;
     for (int j = 0; j < kMaxB; ++j) st->theta[j] = 0.0;
+    st->snap_err_code = 0;
+    st->snap_err_iter = -1;
+    st->snap_replacements = 0;
+}
+
+__global__ void snapshot_kernel(DevState* st) {
+    st->snap_err_code = st->err_code;
+    st->snap_err_iter = st->err_iter;
+    st->snap_replacements = st->replacements;
 }
 
 __global__ void drift_kernel(const double* fresh, const double* cached, int64_t count, DevState* st) {
@@ -1111,7 +1133,7 @@ void rr_launch(Ctx& c, const RRArgs& a) {
     const size_t stacked = sizeof(double) * (static_cast<size_t>(a.nparts) * a.k * (KM + 1) + 2 * 17 * (KM + 1));
     if (KM <= 8 && sm + stacked <= c.smem_optin) sm += stacked;  // room for the stacked-QR merge
     if (KM == 16) sm = c.smem_optin;                             // the stacked merge in groups of parts
-    MSVD_CUDA(cudaFuncSetAttribute(rr_kernel<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+    optin_smem(c, rr_kernel<KM>);
     rr_kernel<KM><<<1, 512, sm, c.stream>>>(a);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
@@ -1127,7 +1149,7 @@ void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st,
     const int grid = tsqr_parts(c);
     auto smem_launch = [&](auto kernel, int km) {
         const size_t sm = sizeof(double) * 16 * (km * km + 32 * (km + 1));
-        MSVD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+        optin_smem(c, kernel);
         kernel<<<grid, 512, sm, c.stream>>>(a);
     };
     const bool stacked = !std::getenv("MSVD_TSQR_FOLD");
@@ -1145,6 +1167,7 @@ void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st,
     }
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
+    c.paths |= kPathTsqr;
 }
 
 template <int B>
@@ -1263,6 +1286,19 @@ void launch_cgs2(Ctx& c, double* W, int64_t n, int b, Cols basis, int nb, DevSta
 
 void launch_state_init(Ctx& c, DevState* st, uint64_t seed) {
     state_init_kernel<<<1, 1, 0, c.stream>>>(st, seed);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void launch_stop_rule(Ctx& c, const double* rh, const double* th, int i, double sigma1, double tol, double factor,
+                      int use_stag, int* flags) {
+    stop_rule_kernel<<<1, 1, 0, c.stream>>>(rh, th, i, sigma1, tol, factor, use_stag, flags);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+}
+
+void launch_snapshot(Ctx& c, DevState* st) {
+    snapshot_kernel<<<1, 1, 0, c.stream>>>(st);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
 }

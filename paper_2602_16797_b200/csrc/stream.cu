@@ -1319,28 +1319,18 @@ size_t gram_smem(const StreamGeom& g, int B) {
 
 template <int B, int PL, int KM, bool GR, bool EX = false>
 void apply_rows_b(Ctx& c, const ApplyArgs& a) {
-    static bool attr = false;
-    if (!attr) {
-        MSVD_CUDA(cudaFuncSetAttribute(apply_rows_kernel<B, PL, KM, GR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(c.smem_optin)));
-        attr = true;
-    }
+    optin_smem(c, apply_rows_kernel<B, PL, KM, GR>);
     // self-fed form: faster for the one-pass and wider blocks; the producer
     // form stays ahead for the plain b = 1 pass (measured, C2)
     const bool self = a.g.tma && !std::getenv("MSVD_APPLY_PRODUCER") && (GR || B > 1 || std::getenv("MSVD_APPLY_SELF"));
     if (self) {
-        static bool attr2 = false;
-        if (!attr2) {
-            MSVD_CUDA(cudaFuncSetAttribute(apply_self_kernel<B, PL, KM, GR, EX>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(c.smem_optin)));
-            attr2 = true;
-        }
+        optin_smem(c, apply_self_kernel<B, PL, KM, GR, EX>);
         const size_t tsqr = KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM + 2 * kRowsFused * KM) : 0;
         const size_t sm = bar_bytes(a.g.stages) + ((tsqr + 127) / 128) * 128 + a.g.stages * a.g.stage_bytes;
         apply_self_kernel<B, PL, KM, GR, EX><<<a.g.grid, 256, sm, c.stream>>>(a);
         MSVD_CUDA(cudaGetLastError());
         ++c.launches;
+        c.paths |= kPathSelf;
         return;
     }
     const size_t tsqr = (KM > 0 ? sizeof(double) * 8 * (KM * KM + 32 * KM + 2 * kRowsFused * KM) : 0) +
@@ -1349,6 +1339,7 @@ void apply_rows_b(Ctx& c, const ApplyArgs& a) {
     apply_rows_kernel<B, PL, KM, GR><<<a.g.grid, 32 + kConsumers, sm, c.stream>>>(a);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
+    c.paths |= kPathRows;
 }
 
 // dispatch on the fused-TSQR width (KM = k rounded up to 4/8/16)
@@ -1445,16 +1436,12 @@ bool pair_ok(const Ctx& c, const StreamGeom& g0, int b, bool ex) {
 
 template <int B, int PL, bool EX = false>
 void apply_pair_b(Ctx& c, const ApplyArgs& a) {
-    static bool attr = false;
-    if (!attr) {
-        MSVD_CUDA(cudaFuncSetAttribute(apply_pair_kernel<B, PL, EX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(c.smem_optin)));
-        attr = true;
-    }
+    optin_smem(c, apply_pair_kernel<B, PL, EX>);
     const size_t sm = bar_bytes(a.g.stages) + 128 * ((sizeof(double) * 16 * B + 127) / 128) + a.g.stages * a.g.stage_bytes;
     apply_pair_kernel<B, PL, EX><<<a.g.grid, 256, sm, c.stream>>>(a);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
+    c.paths |= EX ? kPathPairEx : kPathPair;
 }
 
 void launch_pair(Ctx& c, const ApplyArgs& a0, int b) {
@@ -1499,29 +1486,21 @@ bool try_apply_rows(Ctx& c, const ApplyArgs& a0, int b) {
 template <int B>
 void apply_b(Ctx& c, const ApplyArgs& a) {
     const size_t sm = apply_smem(a.g);
-    static bool attr = false;
-    if (!attr) {
-        MSVD_CUDA(cudaFuncSetAttribute(apply_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(c.smem_optin)));
-        attr = true;
-    }
+    optin_smem(c, apply_kernel<B>);
     apply_kernel<B><<<a.g.grid, 32 + kConsumers, sm, c.stream>>>(a);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
+    c.paths |= kPathTicket;
 }
 
 template <int B>
 void gram_b(Ctx& c, const GramArgs& a) {
     const size_t sm = gram_smem(a.g, B);
-    static bool attr = false;
-    if (!attr) {
-        MSVD_CUDA(cudaFuncSetAttribute(gram_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(c.smem_optin)));
-        attr = true;
-    }
+    optin_smem(c, gram_kernel<B>);
     gram_kernel<B><<<a.g.grid, 64 + kConsumers, sm, c.stream>>>(a);
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
+    c.paths |= kPathGram;
 }
 
 }  // namespace
@@ -1607,8 +1586,7 @@ bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, int b, OutCol
                           128 * ((sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 4 + 127) / 128) +
                           a.g.stages * a.g.stage_bytes;
         auto go = [&](auto kernel) {
-            MSVD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(c.smem_optin)));
+            optin_smem(c, kernel);
             kernel<<<a.g.grid, 256, sm, c.stream>>>(a, ec);
         };
         const int pl = team_pl(g.n);
@@ -1618,6 +1596,7 @@ bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, int b, OutCol
         else go(apply_team_ex_kernel<4, 2, kTeam>);
         MSVD_CUDA(cudaGetLastError());
         ++c.launches;
+        c.paths |= kPathTeamEx;
         return false;
     }
     // single-warp form with the fused TSQR when e is its first trial column

@@ -108,6 +108,7 @@ def _declare(lib):
         "msvd_aw_tsqr": (i32, [vp, vp, i64, vp, i64, vp, vp]),
         "msvd_aw_gram": (i32, [vp, vp, i64, vp, vp]),
         "msvd_small_svd": (i32, [vp, vp, i64, vp, vp]),
+        "msvd_check_convergence": (i32, [vp, P(d), P(d), i64, i32, d, d, d, i32, P(i32)]),
         "msvd_raw_write": (i32, [C.c_char_p, vp, i64, i64, i64]),
         "msvd_raw_info": (i32, [C.c_char_p, P(i64), P(i64)]),
         "msvd_raw_read_rows": (i32, [C.c_char_p, i64, i64, vp, i64]),
@@ -121,6 +122,7 @@ def _declare(lib):
         "msvd_launch_count": (i64, [vp]),
         "msvd_abi_sizes": (None, [P(i64), i32]),
         "msvd_ctx_profile": (i32, [vp, i32]),
+        "msvd_ctx_kernel_paths": (i64, [vp, i32]),
         "msvd_ctx_profile_read": (i32, [vp, P(d), P(i64), i32]),
     }
     for name, (res, args) in sig.items():
@@ -137,7 +139,8 @@ EXPORTED = (
     "msvd_matrix_detach msvd_csr_attach msvd_apply msvd_apply_adjoint msvd_column_norms msvd_build_sparsestack msvd_sketch "
     "msvd_precond_build msvd_precond_apply msvd_tsqr_r msvd_gram_apply msvd_aw_tsqr msvd_aw_gram msvd_small_svd "
     "msvd_raw_write msvd_raw_info msvd_raw_read_rows msvd_raw_load_device msvd_lanczos_gk msvd_lobpcg_solve msvd_rlobpcg_single "
-    "msvd_rlobpcg_block msvd_solve_host msvd_launch_count msvd_abi_sizes msvd_ctx_profile msvd_ctx_profile_read"
+    "msvd_rlobpcg_block msvd_solve_host msvd_launch_count msvd_abi_sizes msvd_ctx_profile msvd_ctx_profile_read "
+    "msvd_ctx_kernel_paths msvd_check_convergence"
 ).split()
 
 
@@ -300,6 +303,14 @@ class Context:
 
     def launch_count(self):
         return lib().msvd_launch_count(self.handle)
+
+    PATHS = ("rows", "self", "pair", "pair_ex", "team_ex", "ticket", "gram", "tsqr")
+
+    def kernel_paths(self, reset=True):
+        """Names of the A-pass kernel variants launched since the last reset
+        (msvd_ctx_kernel_paths)."""
+        mask = lib().msvd_ctx_kernel_paths(self.handle, int(bool(reset)))
+        return {name for i, name in enumerate(self.PATHS) if mask >> i & 1}
 
     PROFILE_SLOTS = ("apply", "gram", "tsqr", "rr", "sketch", "svd", "precond", "cgs2", "reduce", "control")
 
@@ -796,6 +807,30 @@ def solve_host(a_host, opts=None, truth=None, ctx=None, row0=0, m_global=None, k
                                 C.byref(t) if t is not None else None, C.byref(bufs.res)))
     del keep
     return bufs.result(truth is not None)
+
+
+@dataclass
+class StopDecision:
+    """solver.hpp:145-155"""
+
+    tol_ok: bool = False
+    resid_stalled: bool = False
+    progress_stalled: bool = False
+    stop: bool = False
+
+
+def check_convergence(resid_hist, theta_hist, i, sigma1_estimate, tol, factor=1.1, use_stagnation=True, ctx=None):
+    """solver.cpp:177-211, evaluated by the device solver's stop rule (the
+    control kernel's code) on a host history (msvd_check_convergence)."""
+    ctx = ctx or default_context(0)
+    rh = np.ascontiguousarray(resid_hist, dtype=np.float64)
+    th = np.ascontiguousarray(theta_hist, dtype=np.float64)
+    n = min(rh.size, th.size)
+    flags = (C.c_int32 * 4)()
+    check(lib().msvd_check_convergence(ctx.handle, rh.ctypes.data_as(C.POINTER(C.c_double)),
+                                       th.ctypes.data_as(C.POINTER(C.c_double)), n, int(i), float(sigma1_estimate),
+                                       float(tol), float(factor), int(bool(use_stagnation)), flags))
+    return StopDecision(*(bool(x) for x in flags))
 
 
 def validate_options(m, n, opts: SolverOptions, kind=abi.PRECOND_RANDOMIZED):

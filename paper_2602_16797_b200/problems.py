@@ -138,6 +138,70 @@ def make_problem_gpu(m, n, sigma, seed=DATA_SEED, device="cuda:0", block_rows=2_
     return out, vmin
 
 
+def _block_seed(seed, i):
+    """Per-block generator seed (a SplitMix64 step, rng.hpp:18-19 style)."""
+    z = (seed + 0x9E3779B97F4A7C15 * (i + 1)) & 0xFFFFFFFFFFFFFFFF
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+    return (z ^ (z >> 31)) & 0x7FFFFFFFFFFFFFFF
+
+
+def make_problem_shard(m, n, sigma, r0, rows, allreduce=None, seed=DATA_SEED, device="cuda:0",
+                       block_rows=500_000):
+    """Rows [r0, r0 + rows) of A = U diag(sigma) V^T, generated and
+    orthonormalised shard by shard on the device (BASELINE configs[4]).
+
+    U is the sign-fixed Q of an m x n Gaussian whose nb = m // block_rows
+    fixed row blocks (boundaries i m / nb) draw from their own seeded generators, orthonormalised as a
+    two-level TSQR: each block's local QR, then the QR of the stacked R
+    factors (the same matgen.cpp:126-139 recipe, R_jj > 0).  Every rank
+    factors only the blocks its rows touch; the R factors meet through
+    `allreduce` (a sum over ranks of the [blocks * n, n] stack, each block's
+    R contributed by the rank holding its first row; None on one rank).  The
+    global A is therefore the same for every rank count.  Returns (A_local
+    row-major, V) with V the n x n right factor."""
+    import torch
+
+    gen = torch.Generator(device=device)
+    gen.manual_seed(int(seed))
+    v = _haar_gpu(torch, n, n, gen, device)
+    nb = max(1, m // block_rows)  # blocks [i m / nb, (i + 1) m / nb): each >= block_rows rows
+    bound = [i * m // nb for i in range(nb + 1)]
+    touch = [i for i in range(nb) if bound[i] < r0 + rows and bound[i + 1] > r0]
+    first, last = (touch[0], touch[-1]) if touch else (0, -1)
+    rstack = torch.zeros(nb * n, n, dtype=torch.float64, device=device)
+    a = torch.empty(rows, n, dtype=torch.float64, device=device)  # holds the local Q rows first
+    for i in range(first, last + 1):
+        b0, b1 = bound[i], bound[i + 1]
+        g = torch.Generator(device=device)
+        g.manual_seed(_block_seed(int(seed), i))
+        x = torch.randn(b1 - b0, n, dtype=torch.float64, device=device, generator=g)
+        q, r = torch.linalg.qr(x)
+        del x
+        lo, hi = max(b0, r0), min(b1, r0 + rows)
+        a[lo - r0:hi - r0] = q[lo - b0:hi - b0]
+        del q
+        if r0 <= b0 < r0 + rows:  # this rank holds the block's first row
+            rstack[i * n:(i + 1) * n] = r
+    if allreduce is not None:
+        allreduce(rstack)
+    q2, r2 = torch.linalg.qr(rstack)
+    del rstack
+    s = torch.sign(torch.diagonal(r2))
+    s[s == 0] = 1.0
+    q2 *= s
+    sig = torch.as_tensor(np.asarray(sigma, dtype=np.float64), device=device)
+    m2 = sig[:, None] * v.t()  # diag(sigma) V^T
+    for i in range(first, last + 1):
+        lo, hi = max(bound[i], r0), min(bound[i + 1], r0 + rows)
+        m3 = q2[i * n:(i + 1) * n] @ m2  # U rows = Q_i Q2_i, so A rows = Q_i (Q2_i diag(sigma) V^T)
+        step = 1 << 18
+        for c0 in range(lo - r0, hi - r0, step):
+            c1 = min(hi - r0, c0 + step)
+            a[c0:c1] = a[c0:c1] @ m3
+    return a, v.cpu().numpy()
+
+
 def random_csr(m, n, density, seed, decay=1e-4):
     """A seeded sparse test operator for the CSR path (no BASELINE config is
     sparse): each row holds ~density*n distinct columns drawn uniformly,

@@ -134,3 +134,86 @@ def test_two_rank_gloo_protocol_matches_oracle(port):
         assert abs(sigma[0] - ref["sigma"][0]) <= 1e-10 * smax
         vr = ref["v"][:, 0]
         assert np.linalg.norm(vr - v[:, 0] * (v[:, 0] @ vr)) <= 1e-8
+
+
+# ---------------------------------------------------------------- bench launcher
+def test_bench_spawns_ranks_itself():
+    """`bench.py --gpus 2` outside torchrun launches two ranks (gloo selftest:
+    no GPU needed) and rank 0 prints one line for the whole job."""
+    import json
+    import subprocess
+    import sys
+
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--selftest", "--steps", "2",
+                          "--warmup", "3"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["ranks_reported"] == 2 and d["steps"] == 2 and d["warmup"] == 3
+    for key in ("metric", "value", "unit", "ms_per_step", "higher_is_better", "scaling", "config"):
+        assert key in d
+
+
+def test_bench_refuses_missing_gpus():
+    """Never a silent downgrade: --gpus 2 without two visible GPUs fails."""
+    import subprocess
+    import sys
+
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                         capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode != 0 and "needs 2 GPUs" in (out.stderr + out.stdout)
+
+
+# ------------------------------------------------- shard-by-shard generator
+def _gen_worker(rank, world, port_no, m, n, q):
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, ROOT)
+    from paper_2602_16797_b200 import problems
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        r0, r1 = (m * rank) // world, (m * (rank + 1)) // world
+        a, _ = problems.make_problem_shard(m, n, problems.spectrum("c5", n), r0, r1 - r0,
+                                           lambda t: dist.all_reduce(t), device="cpu", block_rows=450)
+        q.put((rank, r0, a.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shard_generator_independent_of_rank_count(world):
+    """BASELINE configs[4]: U generated and orthonormalised shard by shard
+    (two-level TSQR across ranks); the global A is the same for every rank
+    count, and U diag(sigma) V^T has the requested spectrum."""
+    import torch.multiprocessing as mp
+
+    from paper_2602_16797_b200 import problems
+
+    m, n = 3100, 24  # 6 generator blocks that straddle the rank boundaries
+    sig = problems.spectrum("c5", n)
+    whole, v = problems.make_problem_shard(m, n, sig, 0, m, None, device="cpu", block_rows=450)
+    whole = whole.numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = free_port()
+    procs = [ctx.Process(target=_gen_worker, args=(r, world, port_no, m, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = sorted([q.get(timeout=240) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    glued = np.vstack([p[2] for p in parts])
+    assert glued.shape == (m, n)
+    assert np.max(np.abs(glued - whole)) <= 1e-13 * np.max(np.abs(whole))
+    s = np.linalg.svd(whole, compute_uv=False)
+    assert np.max(np.abs(s - sig)) <= 1e-13
+    assert np.linalg.norm(whole @ v[:, -1]) <= 1e-13 + sig[-1] * 1.0001
