@@ -313,13 +313,14 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     DevState* st;
     msvd_record_row* rows;
     double *rh, *th, *Vcol, *Vrow, *sig, *AVb[2], *AXb[2], *AW, *Vb[2], *Xb[2], *W, *Rres, *tmp, *Cm, *Gpart,
-        *Gout, *nrm, *Rparts, *Rall, *tv, *dinv, *cpart, *fresh, *ZVb[2], *ZXb[2], *ZW;
+        *Gout, *nrm, *Rparts, *Rall, *tv, *dinv, *cpart, *fresh, *ZVb[2], *ZXb[2], *ZW, *V0b;
     ar.add(&st, 1);
     ar.add(&rows, max_iter + 2);
     ar.add(&rh, max_iter + 2);
     ar.add(&th, max_iter + 2);
     ar.add(&Vcol, n * n);
     ar.add(&Vrow, n * n);
+    ar.add(&V0b, n * b);
     ar.add(&sig, n);
     for (int i = 0; i < 2; ++i) {
         ar.add(&AVb[i], ml * b);
@@ -355,6 +356,11 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     // ---- prepare (solver.cpp:128-145) ----
     double sigma1 = 0.0;
     int64_t nfloor = 0;
+    // Cholesky-QR route (csrc/precond_chol.cu): P = R^-1 with sigma~_1 and V0
+    // from block iterations, where no sigma~ can reach the floor and the
+    // caller did not ask for the factors Vt / sigma~ themselves
+    bool chol_route = false;
+    const bool root = ranks == 1 || comm.rank() == 0;  // rank 0 factors, the others receive
     {
         double* SA = nullptr;
         int64_t sa_rows = 0;
@@ -425,23 +431,31 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
                 for (double v : h)
                     if (!std::isfinite(v)) fail(MSVD_ERR_NUMERICAL, "DenseOperator: non-finite entry");
             }
-            precond_build_dev(c, SA, sa_rows, n, Vcol, Vrow, sig, &sigma1, &nfloor, b + 8);
+            if (root) {
+                const char* pe = std::getenv("MSVD_PRECOND");
+                const bool want_factors = res->vtilde || res->sigma_tilde;
+                if (!want_factors && !(pe && std::string(pe) == "svd"))
+                    chol_route = precond_build_chol(c, SA, sa_rows, n, b, Vcol, Vrow, sig, V0b, &sigma1, o.seed);
+                if (!chol_route) precond_build_dev(c, SA, sa_rows, n, Vcol, Vrow, sig, &sigma1, &nfloor, b + 8);
+            }
         } catch (...) {
             if (plan.skip) cudaFree(SA);
             throw;
         }
         if (plan.skip) MSVD_CUDA(cudaFree(SA));
         if (ranks > 1) {  // every rank uses rank 0's factorization bit for bit
-            comm.bcast(Vcol, static_cast<size_t>(n * n), 0, c.stream);
-            comm.bcast(Vrow, static_cast<size_t>(n * n), 0, c.stream);
-            comm.bcast(sig, static_cast<size_t>(n), 0, c.stream);
-            double hs[2] = {sigma1, static_cast<double>(nfloor)};
+            double hs[3] = {sigma1, static_cast<double>(nfloor), chol_route ? 1.0 : 0.0};
             MSVD_CUDA(cudaMemcpyAsync(tmp, hs, sizeof(hs), cudaMemcpyHostToDevice, c.stream));
-            comm.bcast(tmp, 2, 0, c.stream);
+            comm.bcast(tmp, 3, 0, c.stream);
             MSVD_CUDA(cudaMemcpyAsync(hs, tmp, sizeof(hs), cudaMemcpyDeviceToHost, c.stream));
             MSVD_CUDA(cudaStreamSynchronize(c.stream));
             sigma1 = hs[0];
             nfloor = static_cast<int64_t>(hs[1]);
+            chol_route = hs[2] != 0.0;
+            comm.bcast(Vcol, static_cast<size_t>(n * n), 0, c.stream);
+            comm.bcast(Vrow, static_cast<size_t>(n * n), 0, c.stream);
+            comm.bcast(sig, static_cast<size_t>(n), 0, c.stream);
+            if (chol_route) comm.bcast(V0b, static_cast<size_t>(n * b), 0, c.stream);
         }
     }
     MSVD_CUDA(cudaEventRecord(c.ev[2], c.stream));
@@ -619,7 +633,10 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     };
 
     // ---- initial block and Rayleigh-Ritz (solver.cpp:349-371) ----
-    launch_copy_cols(c, Vcol, n, n - b, n, b, W);  // sketch_and_solve_init: last b columns
+    // sketch_and_solve_init: the last b columns of Vt (precond.cpp:50-57)
+    if (chol_route) c.paths |= kPathCholPrecond;
+    if (chol_route) launch_copy_cols(c, V0b, n, 0, n, b, W);
+    else launch_copy_cols(c, Vcol, n, n - b, n, b, W);
     OutCols out{};
     for (int j = 0; j < b; ++j) out.p[j] = AW + static_cast<int64_t>(j) * ml;
     {

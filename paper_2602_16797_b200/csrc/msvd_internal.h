@@ -97,7 +97,7 @@ struct StreamGeom {
 struct Ctx;
 
 enum KernelPath : int64_t { kPathRows = 1, kPathSelf = 2, kPathPair = 4, kPathPairEx = 8, kPathTeamEx = 16,
-                            kPathTicket = 32, kPathGram = 64, kPathTsqr = 128 };
+                            kPathTicket = 32, kPathGram = 64, kPathTsqr = 128, kPathCholPrecond = 256 };
 
 enum ProfSlot { kProfApply = 0, kProfGram, kProfTsqr, kProfRR, kProfSketch, kProfSvd, kProfPrecond, kProfCgs2,
                 kProfReduce, kProfControl, kProfSlots };
@@ -224,6 +224,11 @@ void sketch_finish(Ctx& c, const double* SAr, int64_t d, int64_t n, double* SA);
 // when the fast polar SVD is used (the solver passes b + 8)
 void precond_build_dev(Ctx& c, const double* SA, int64_t rows, int64_t n, double* Vcol,
                        double* Vrow, double* sig, double* sigma_max, int64_t* nfloor, int tail_hint = 8);
+// Cholesky-QR route (precond_chol.cu): Vcol / Vrow = R^-1 of the sketch, sig = 1,
+// V0 (n x b) = the b smallest right singular vectors (Vt's last b columns),
+// sigma_max = sigma~_1.  false (nothing usable written): take the SVD route
+bool precond_build_chol(Ctx& c, const double* SA, int64_t rows, int64_t n, int b, double* Vcol, double* Vrow,
+                        double* sig, double* V0, double* sigma_max, uint64_t seed);
 
 // ---- operator kinds --------------------------------------------------------
 enum MatKind { kMatDense = 0, kMatCsr = 1 };

@@ -1,0 +1,356 @@
+// Randomized preconditioner without the n x n SVD (precond.cpp:11-36).
+//
+// The solver applies P P^T r = Vt diag(sigma~^-2) Vt^T r (precond.cpp:38-48).
+// With a square orthogonal Vt (d >= n) that is (SA^T SA)^-1 r exactly, as
+// long as no sigma~ was raised to the sqrt(n) u sigma~_1 floor
+// (precond.cpp:26-34).  So where the floor cannot fire, the preconditioner is
+// R^-1 R^-T r for the R of a QR of the sketch, and the SVD is needed only for
+// the three things the solve reads from it besides P:
+//   * sigma~_1 (the stop rule's scale, solver.cpp:183-184),
+//   * the start block V0 = Vt(:, n-b : n-1) (precond.cpp:50-57),
+//   * the floor count (0 here, by the test below).
+//
+// Here, all on the device with DMMA GEMMs (cuBLAS) and small cuSOLVER
+// Choleskys instead of the 10 ms cuSOLVER syevd of the SVD route:
+//   1. R = CholeskyQR2(SA): G = SA^T SA, R1 = chol(G), Q = SA R1^-1,
+//      R2 = chol(Q^T Q), R = R2 R1 -- backward stable like the reference's
+//      Householder QR (svd.cpp:21-55) while kappa(SA) < ~1e7 (the first
+//      Cholesky fails, or the route is refused, beyond that);
+//   2. R^-1 by a triangular solve; stored where the SVD route keeps Vt
+//      (column- and row-major) with sigma = 1, so the iteration's
+//      preconditioner kernels are unchanged: w = R^-1 (R^-T r);
+//   3. sigma~_1: block power iteration on R^T R (four products per
+//      Householder orthonormalization), then Rayleigh-Ritz through the
+//      one-sided Jacobi of the small R factor of R X (svd.cpp:99-150);
+//   4. V0: block inverse iteration with (R^T R)^-1 = R^-1 R^-T (Householder
+//      orthonormalization, robust for any conditioning), Rayleigh-Ritz the
+//      same way, signed like svd.cpp:232-248.  The Ritz residuals must reach
+//      the accuracy of the reference's Jacobi (~u sigma~_1^2) and sigma~_n
+//      must sit 1e3 above the floor; otherwise the caller takes the SVD route.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "msvd_internal.h"
+
+namespace msvd {
+namespace {
+
+#define MSVD_BLAS(x)                                                                                   \
+    do {                                                                                               \
+        cublasStatus_t bs__ = (x);                                                                     \
+        if (bs__ != CUBLAS_STATUS_SUCCESS)                                                             \
+            fail(MSVD_ERR_CUDA, std::string("cuBLAS failure ") + std::to_string(bs__) + " in " #x);    \
+    } while (0)
+#define MSVD_SOLVER(x)                                                                                 \
+    do {                                                                                               \
+        cusolverStatus_t ss__ = (x);                                                                   \
+        if (ss__ != CUSOLVER_STATUS_SUCCESS)                                                           \
+            fail(MSVD_ERR_CUDA, std::string("cuSOLVER failure ") + std::to_string(ss__) + " in " #x); \
+    } while (0)
+
+constexpr double kEps = 2.220446049250313e-16;
+
+// M (n x n, col-major): entries below the diagonal set to zero
+__global__ void zero_lower_kernel(double* M, int64_t n) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n * n) return;
+    if (i % n > i / n) M[i] = 0.0;
+}
+// M (n x n, col-major, upper triangle valid) -> full symmetric, scaled by 1 / s[0]
+__global__ void sym_fill_scale_kernel(double* M, int64_t n, const double* s) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n * n) return;
+    const int64_t r = i % n, c = i / n;
+    const double inv = 1.0 / s[0];
+    M[i] = (r <= c ? M[i] : M[c + r * n]) * inv;
+}
+__global__ void eye_kernel(double* M, int64_t n) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n * n) M[i] = (i % n == i / n) ? 1.0 : 0.0;
+}
+__global__ void fill_kernel(double* p, int64_t count, double v) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < count) p[i] = v;
+}
+// row-major copy of a col-major square matrix
+__global__ void transpose_kernel(const double* A, int64_t n, double* out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < n * n) out[(i / n) + (i % n) * n] = A[i];
+}
+// max over the diagonal (one CTA)
+__global__ void max_diag_kernel(const double* M, int64_t n, double* out) {
+    __shared__ double red[32];
+    double v = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v = fmax(v, M[i + i * n]);
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+        out[0] = m > 0.0 ? m : 1.0;
+    }
+}
+// deterministic start block: SplitMix64 (rng.hpp) uniform in [-1, 1), keyed per entry
+__global__ void start_block_kernel(double* X, int64_t count, uint64_t seed) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= count) return;
+    uint64_t z = seed + 0x9E3779B97F4A7C15ULL * static_cast<uint64_t>(i + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    X[i] = static_cast<double>(z >> 11) * 0x1.0p-52 - 1.0;
+}
+// V0(:, j) = (X W)(:, p - b + j), signed so the first largest-magnitude entry
+// is positive (svd.cpp:232-248); one CTA per output column
+__global__ void ritz_cols_kernel(const double* X, int64_t n, int p, const double* W, int b, double* V0) {
+    const int j = blockIdx.x;
+    const double* w = W + static_cast<int64_t>(p - b + j) * p;
+    __shared__ double bv[32];
+    __shared__ int64_t bi[32];
+    double amax = -1.0;
+    int64_t imax = 0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        double s = 0.0;
+        for (int q = 0; q < p; ++q) s += X[i + q * n] * w[q];
+        V0[i + static_cast<int64_t>(j) * n] = s;
+        if (fabs(s) > amax) {
+            amax = fabs(s);
+            imax = i;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, amax, o);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, imax, o);
+        if (ov > amax || (ov == amax && oi < imax)) {
+            amax = ov;
+            imax = oi;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        bv[threadIdx.x >> 5] = amax;
+        bi[threadIdx.x >> 5] = imax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w2 = 1; w2 < static_cast<int>(blockDim.x >> 5); ++w2)
+            if (bv[w2] > bv[0] || (bv[w2] == bv[0] && bi[w2] < bi[0])) {
+                bv[0] = bv[w2];
+                bi[0] = bi[w2];
+            }
+    }
+    __syncthreads();
+    const double s = V0[bi[0] + static_cast<int64_t>(j) * n] < 0.0 ? -1.0 : 1.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) V0[i + static_cast<int64_t>(j) * n] *= s;
+}
+// out[j] = || Y(:, j) - s_j^2 V(:, j) ||_2 for j < b (one CTA per column):
+// the Ritz residuals of (s_j, V(:, j)) with Y = R^T R V
+__global__ void resid_kernel(const double* Y, const double* V, const double* sg, int p, int b, int64_t n,
+                             double* out) {
+    const int j = blockIdx.x;
+    const double s = sg[p - b + j];
+    __shared__ double red[32];
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double d = Y[i + static_cast<int64_t>(j) * n] - s * s * V[i + static_cast<int64_t>(j) * n];
+        acc += d * d;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+        out[j] = sqrt(t);
+    }
+}
+
+unsigned blocks(int64_t count) { return static_cast<unsigned>(ceil_div(count, 256)); }
+
+}  // namespace
+
+bool precond_build_chol(Ctx& c, const double* SA, int64_t rows, int64_t n, int b, double* Vcol, double* Vrow,
+                        double* sig, double* V0, double* sigma_max, uint64_t seed) {
+    if (n < 2 || rows < n || b < 1 || b > kMaxB || 3 * b > n) return false;
+    ProfScope prof(c, kProfSvd);
+    if (!c.blas) {
+        MSVD_BLAS(cublasCreate(&c.blas));
+        MSVD_BLAS(cublasSetPointerMode(c.blas, CUBLAS_POINTER_MODE_HOST));
+    }
+    if (!c.solver) MSVD_SOLVER(cusolverDnCreate(&c.solver));
+    MSVD_BLAS(cublasSetStream(c.blas, c.stream));
+    MSVD_SOLVER(cusolverDnSetStream(c.solver, c.stream));
+    const int in = static_cast<int>(n), ir = static_cast<int>(rows);
+    const int p = static_cast<int>(std::min<int64_t>(n, std::min(24, b + 22)));  // block width (small_svd: <= 24)
+    const int ps = static_cast<int>(std::min<int64_t>(n, 24));                    // sigma~_1 block
+    const int64_t nn = n * n;
+
+    // ctx-owned workspace (shared with the SVD route):
+    // Q (rows x n) | G | R1 | R | Gi (n x n each) | X | Y | Z (n x p) | H (p x p) | small
+    const size_t need = sizeof(double) * (static_cast<size_t>(rows) * n + 4 * nn + 3 * n * 24 + 2 * 24 * 24 + 256) +
+                        sizeof(DevState) + sizeof(int) * 16 + 1024;
+    if (need > c.svd_ws_bytes) {
+        if (c.svd_ws) MSVD_CUDA(cudaFree(c.svd_ws));
+        c.svd_ws = nullptr;
+        MSVD_CUDA(cudaMalloc(&c.svd_ws, need));
+        c.svd_ws_bytes = need;
+    }
+    double* Q = static_cast<double*>(c.svd_ws);
+    double* G = Q + static_cast<size_t>(rows) * n;
+    double* R1 = G + nn;
+    double* R = R1 + nn;
+    double* Gi = R + nn;
+    double* X = Gi + nn;
+    double* Y = X + n * 24;
+    double* Z = Y + n * 24;
+    double* H = Z + n * 24;
+    double* W = H + 24 * 24;
+    double* small = W + 24 * 24;  // sg[24] | scale[2] | resid[8] | tau[24] | sg1[24]
+    double* sg = small;
+    double* scale = sg + 24;
+    double* resid = scale + 2;
+    double* tau = resid + 8;
+    double* sg1 = tau + 24;
+    DevState* st = reinterpret_cast<DevState*>(small + 256);
+    int* info = reinterpret_cast<int*>(st + 1);
+    MSVD_CUDA(cudaMemsetAsync(st, 0, sizeof(DevState), c.stream));
+    MSVD_CUDA(cudaMemsetAsync(info, 0, sizeof(int) * 16, c.stream));
+
+    int lw_n = 0, lw_p = 0, lq = 0, lo = 0;
+    MSVD_SOLVER(cusolverDnDpotrf_bufferSize(c.solver, CUBLAS_FILL_MODE_UPPER, in, G, in, &lw_n));
+    MSVD_SOLVER(cusolverDnDpotrf_bufferSize(c.solver, CUBLAS_FILL_MODE_UPPER, 24, H, 24, &lw_p));
+    MSVD_SOLVER(cusolverDnDgeqrf_bufferSize(c.solver, in, 24, X, in, &lq));
+    MSVD_SOLVER(cusolverDnDorgqr_bufferSize(c.solver, in, 24, 24, X, in, tau, &lo));
+    const int lwork = std::max(std::max(lw_n, lw_p), std::max(lq, lo)) + 1;
+    if (sizeof(double) * lwork > c.svd_lw_bytes) {
+        if (c.svd_lw) MSVD_CUDA(cudaFree(c.svd_lw));
+        c.svd_lw = nullptr;
+        MSVD_CUDA(cudaMalloc(&c.svd_lw, sizeof(double) * lwork));
+        c.svd_lw_bytes = sizeof(double) * lwork;
+    }
+    double* lw = static_cast<double*>(c.svd_lw);
+    const double one = 1.0, zero = 0.0;
+    auto gemm = [&](cublasOperation_t ta, cublasOperation_t tb, int mm, int nc, int kk, const double* A, int lda,
+                    const double* Bm, int ldb, double* C, int ldc) {
+        MSVD_BLAS(cublasDgemm(c.blas, ta, tb, mm, nc, kk, &one, A, lda, Bm, ldb, &zero, C, ldc));
+    };
+    auto potrf = [&](double* M, int k, int ld, int* inf) {
+        MSVD_SOLVER(cusolverDnDpotrf(c.solver, CUBLAS_FILL_MODE_UPPER, k, M, ld, lw, lwork, inf));
+    };
+    // ---- 1. R = CholeskyQR2(SA) ------------------------------------------
+    MSVD_BLAS(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, in, ir, &one, SA, ir, &zero, R1, in));
+    potrf(R1, in, in, info + 0);
+    MSVD_CUDA(cudaMemcpyAsync(Q, SA, sizeof(double) * rows * n, cudaMemcpyDeviceToDevice, c.stream));
+    MSVD_BLAS(cublasDtrsm(c.blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ir,
+                          in, &one, R1, in, Q, ir));
+    MSVD_BLAS(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, in, ir, &one, Q, ir, &zero, G, in));
+    potrf(G, in, in, info + 1);
+    zero_lower_kernel<<<blocks(nn), 256, 0, c.stream>>>(R1, n);
+    MSVD_BLAS(cublasDtrmm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, in, in,
+                          &one, G, in, R1, in, R, in));  // R = R2 R1 (upper)
+    // ---- 2. R^-1 in the preconditioner slots, sigma = 1 ------------------
+    eye_kernel<<<blocks(nn), 256, 0, c.stream>>>(Vcol, n);
+    MSVD_BLAS(cublasDtrsm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, in, in,
+                          &one, R, in, Vcol, in));
+    transpose_kernel<<<blocks(nn), 256, 0, c.stream>>>(Vcol, n, Vrow);
+    fill_kernel<<<blocks(n), 256, 0, c.stream>>>(sig, n, 1.0);
+    c.launches += 4;
+
+    // Rayleigh-Ritz of the n x k block Xb through R: the small R factor of R Xb
+    // (Householder) and its one-sided Jacobi SVD -> sgo (descending), W
+    auto ritz = [&](const double* Xb, int k, double* sgo) {
+        MSVD_BLAS(cublasDtrmm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, in,
+                              k, &one, R, in, Xb, in, Z, in));
+        MSVD_SOLVER(cusolverDnDgeqrf(c.solver, in, k, Z, in, tau, lw, lwork, info + 4));
+        MSVD_CUDA(cudaMemsetAsync(H, 0, sizeof(double) * k * k, c.stream));
+        MSVD_CUDA(cudaMemcpy2DAsync(H, sizeof(double) * k, Z, sizeof(double) * n, sizeof(double) * k, k,
+                                    cudaMemcpyDeviceToDevice, c.stream));
+        zero_lower_kernel<<<blocks(k * k), 256, 0, c.stream>>>(H, k);
+        ++c.launches;
+        launch_small_svd(c, H, k, sgo, W, st);
+    };
+    auto read = [&](const double* src, int count) {
+        std::vector<double> h(count);
+        MSVD_CUDA(cudaMemcpyAsync(h.data(), src, sizeof(double) * count, cudaMemcpyDeviceToHost, c.stream));
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+        return h;
+    };
+    auto infos_ok = [&]() {
+        int hi[8];
+        MSVD_CUDA(cudaMemcpyAsync(hi, info, sizeof(hi), cudaMemcpyDeviceToHost, c.stream));
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+        for (int k = 0; k < 8; ++k)
+            if (hi[k] != 0) return false;
+        return true;
+    };
+    if (!infos_ok()) return false;  // the sketch is too ill-conditioned for Cholesky QR: SVD route
+
+    // ---- 3. sigma~_1: block power iteration on R^T R ---------------------
+    MSVD_BLAS(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, in, in, &one, R, in, &zero, G, in));
+    max_diag_kernel<<<1, 256, 0, c.stream>>>(G, n, scale);
+    sym_fill_scale_kernel<<<blocks(nn), 256, 0, c.stream>>>(G, n, scale);  // spectrum in [~1, n]
+    start_block_kernel<<<blocks(n * ps), 256, 0, c.stream>>>(X, n * ps, seed ^ 0x5349474D41ULL);
+    c.launches += 3;
+    double s1 = 0.0;
+    for (int round = 0; round < 40; ++round) {
+        for (int q = 0; q < 2; ++q) {  // (R^T R)^4 between Householder orthonormalizations
+            gemm(CUBLAS_OP_N, CUBLAS_OP_N, in, ps, in, G, in, X, in, Y, in);
+            gemm(CUBLAS_OP_N, CUBLAS_OP_N, in, ps, in, G, in, Y, in, X, in);
+        }
+        MSVD_SOLVER(cusolverDnDgeqrf(c.solver, in, ps, X, in, tau, lw, lwork, info + 2));
+        MSVD_SOLVER(cusolverDnDorgqr(c.solver, in, ps, ps, X, in, tau, lw, lwork, info + 2));
+        if (round >= 5 && round % 3 == 2) {
+            ritz(X, ps, sg1);
+            const double s = read(sg1, 1)[0];
+            const bool done = std::fabs(s - s1) <= 2.0 * kEps * s;
+            s1 = s;
+            if (done) break;
+        }
+    }
+    if (!infos_ok() || !(s1 > 0.0)) return false;
+
+    // ---- 4. V0: block inverse iteration with R^-1 R^-T ---------------------
+    MSVD_BLAS(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, in, in, &one, Vcol, in, &zero, Gi, in));
+    max_diag_kernel<<<1, 256, 0, c.stream>>>(Gi, n, scale + 1);
+    sym_fill_scale_kernel<<<blocks(nn), 256, 0, c.stream>>>(Gi, n, scale + 1);
+    start_block_kernel<<<blocks(n * p), 256, 0, c.stream>>>(X, n * p, seed ^ 0x56304254ULL);
+    c.launches += 3;
+    const double floor = std::sqrt(static_cast<double>(n)) * kEps * s1;  // precond.cpp:26-34
+    bool converged = false;
+    double smin = 0.0;
+    for (int round = 0; round < 60 && !converged; ++round) {
+        gemm(CUBLAS_OP_N, CUBLAS_OP_N, in, p, in, Gi, in, X, in, Y, in);
+        MSVD_SOLVER(cusolverDnDgeqrf(c.solver, in, p, Y, in, tau, lw, lwork, info + 3));
+        MSVD_SOLVER(cusolverDnDorgqr(c.solver, in, p, p, Y, in, tau, lw, lwork, info + 3));
+        std::swap(X, Y);
+        if (round >= 2 && round % 3 == 2) {
+            ritz(X, p, sg);
+            // Ritz vectors of the b smallest, their residuals against R^T R
+            ritz_cols_kernel<<<b, 256, 0, c.stream>>>(X, n, p, W, b, V0);
+            MSVD_BLAS(cublasDtrmm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
+                                  in, b, &one, R, in, V0, in, Z, in));
+            MSVD_BLAS(cublasDtrmm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
+                                  in, b, &one, R, in, Z, in, Y, in));
+            resid_kernel<<<b, 256, 0, c.stream>>>(Y, V0, sg, p, b, n, resid);
+            c.launches += 2;
+            const std::vector<double> r = read(resid, b);
+            smin = read(sg + p - 1, 1)[0];
+            converged = true;
+            for (int j = 0; j < b; ++j)
+                if (!(r[j] <= 64.0 * kEps * s1 * s1)) converged = false;  // the Jacobi SVD's accuracy
+        }
+    }
+    if (!converged || !infos_ok() || !(smin >= 1e3 * floor)) return false;
+    DevState h;
+    MSVD_CUDA(cudaMemcpyAsync(&h, st, sizeof(DevState), cudaMemcpyDeviceToHost, c.stream));
+    MSVD_CUDA(cudaStreamSynchronize(c.stream));
+    if (h.err_code) return false;
+    *sigma_max = s1;
+    return true;
+}
+
+}  // namespace msvd
