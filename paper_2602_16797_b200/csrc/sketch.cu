@@ -370,15 +370,12 @@ void sketch_dev(Ctx& c, const StreamGeom& g, int64_t row0, int64_t d, int zeta, 
         ++c.launches;
         return;
     }
-    const char* ce = std::getenv("MSVD_SKETCH_CPL");
-    const int cpl = ce ? std::atoi(ce) : 2;  // measured (C2): 32*2 columns x 8 entries in flight per warp
-    const int slice = 32 * cpl;
+    // measured (C2): 32 * 2 columns x 8 entries in flight per warp (the 1-, 4-
+    // and 8-pair variants were slower and spilled; removed)
+    const int slice = 64;
     const unsigned grid = static_cast<unsigned>(ceil_div(d, 8));
     for (int c0 = 0; c0 < g.n; c0 += slice) {
-        if (cpl == 1) gather_slice_kernel<1, 16><<<grid, 256, 0, c.stream>>>(g.A, g.ld, g.n, d, L.offs, L.vals, L.val, SA, st, c0);
-        else if (cpl == 2) gather_slice_kernel<2, 8><<<grid, 256, 0, c.stream>>>(g.A, g.ld, g.n, d, L.offs, L.vals, L.val, SA, st, c0);
-        else if (cpl == 8) gather_slice_kernel<8, 2><<<grid, 256, 0, c.stream>>>(g.A, g.ld, g.n, d, L.offs, L.vals, L.val, SA, st, c0);
-        else gather_slice_kernel<4, 4><<<grid, 256, 0, c.stream>>>(g.A, g.ld, g.n, d, L.offs, L.vals, L.val, SA, st, c0);
+        gather_slice_kernel<2, 8><<<grid, 256, 0, c.stream>>>(g.A, g.ld, g.n, d, L.offs, L.vals, L.val, SA, st, c0);
         MSVD_CUDA(cudaGetLastError());
         ++c.launches;
     }
