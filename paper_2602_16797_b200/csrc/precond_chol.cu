@@ -29,6 +29,7 @@
 //      must sit 1e3 above the floor; otherwise the caller takes the SVD route.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -60,13 +61,13 @@ __global__ void zero_lower_kernel(double* M, int64_t n) {
     if (i >= n * n) return;
     if (i % n > i / n) M[i] = 0.0;
 }
-// M (n x n, col-major, upper triangle valid) -> full symmetric, scaled by 1 / s[0]
-__global__ void sym_fill_scale_kernel(double* M, int64_t n, const double* s) {
+// out (n x n, col-major) = the full symmetric matrix whose upper triangle is
+// M's, scaled by 1 / s[0] (out of place: no thread reads what another writes)
+__global__ void sym_fill_scale_kernel(const double* M, int64_t n, const double* s, double* out) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= n * n) return;
     const int64_t r = i % n, c = i / n;
-    const double inv = 1.0 / s[0];
-    M[i] = (r <= c ? M[i] : M[c + r * n]) * inv;
+    out[i] = (r <= c ? M[i] : M[c + r * n]) * (1.0 / s[0]);
 }
 __global__ void eye_kernel(double* M, int64_t n) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -182,10 +183,17 @@ bool precond_build_chol(Ctx& c, const double* SA, int64_t rows, int64_t n, int b
         MSVD_BLAS(cublasSetPointerMode(c.blas, CUBLAS_POINTER_MODE_HOST));
     }
     if (!c.solver) MSVD_SOLVER(cusolverDnCreate(&c.solver));
+    const bool timed = std::getenv("MSVD_DEBUG_CHOL") != nullptr;
+    cudaEvent_t ev_start = nullptr;
+    if (timed) {
+        MSVD_CUDA(cudaEventCreate(&ev_start));
+        MSVD_CUDA(cudaEventRecord(ev_start, c.stream));
+    }
     MSVD_BLAS(cublasSetStream(c.blas, c.stream));
     MSVD_SOLVER(cusolverDnSetStream(c.solver, c.stream));
     const int in = static_cast<int>(n), ir = static_cast<int>(rows);
-    const int p = static_cast<int>(std::min<int64_t>(n, std::min(24, b + 22)));  // block width (small_svd: <= 24)
+    // block widths (small_svd: <= 24): V0 for b = 1 needs only a small guard block
+    const int p = static_cast<int>(std::min<int64_t>(n, b == 1 ? 12 : std::min(24, b + 22)));
     const int ps = static_cast<int>(std::min<int64_t>(n, 24));                    // sigma~_1 block
     const int64_t nn = n * n;
 
@@ -241,21 +249,49 @@ bool precond_build_chol(Ctx& c, const double* SA, int64_t rows, int64_t n, int b
     auto potrf = [&](double* M, int k, int ld, int* inf) {
         MSVD_SOLVER(cusolverDnDpotrf(c.solver, CUBLAS_FILL_MODE_UPPER, k, M, ld, lw, lwork, inf));
     };
+    std::vector<cudaEvent_t> marks;
+    auto mark = [&]() {
+        if (!timed) return;
+        cudaEvent_t e;
+        MSVD_CUDA(cudaEventCreate(&e));
+        MSVD_CUDA(cudaEventRecord(e, c.stream));
+        marks.push_back(e);
+    };
     // ---- 1. R = CholeskyQR2(SA) ------------------------------------------
+    mark();
     MSVD_BLAS(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, in, ir, &one, SA, ir, &zero, R1, in));
+    mark();
     potrf(R1, in, in, info + 0);
+    mark();
     MSVD_CUDA(cudaMemcpyAsync(Q, SA, sizeof(double) * rows * n, cudaMemcpyDeviceToDevice, c.stream));
     MSVD_BLAS(cublasDtrsm(c.blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ir,
                           in, &one, R1, in, Q, ir));
+    mark();
     MSVD_BLAS(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, in, ir, &one, Q, ir, &zero, G, in));
+    mark();
     potrf(G, in, in, info + 1);
+    mark();
     zero_lower_kernel<<<blocks(nn), 256, 0, c.stream>>>(R1, n);
     MSVD_BLAS(cublasDtrmm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, in, in,
                           &one, G, in, R1, in, R, in));  // R = R2 R1 (upper)
+    mark();
     // ---- 2. R^-1 in the preconditioner slots, sigma = 1 ------------------
     eye_kernel<<<blocks(nn), 256, 0, c.stream>>>(Vcol, n);
     MSVD_BLAS(cublasDtrsm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, in, in,
                           &one, R, in, Vcol, in));
+    mark();
+    if (timed) {
+        MSVD_CUDA(cudaEventSynchronize(marks.back()));
+        std::fprintf(stderr, "msvd chol route stage 1:");
+        const char* names[] = {"syrk", "potrf", "trsm", "syrk", "potrf", "trmm", "inverse"};
+        for (size_t k = 1; k < marks.size(); ++k) {
+            float t = 0.0f;
+            MSVD_CUDA(cudaEventElapsedTime(&t, marks[k - 1], marks[k]));
+            std::fprintf(stderr, " %s %.3f", names[k - 1], t);
+        }
+        std::fprintf(stderr, " ms\n");
+        for (auto e : marks) cudaEventDestroy(e);
+    }
     transpose_kernel<<<blocks(nn), 256, 0, c.stream>>>(Vcol, n, Vrow);
     fill_kernel<<<blocks(n), 256, 0, c.stream>>>(sig, n, 1.0);
     c.launches += 4;
@@ -289,60 +325,112 @@ bool precond_build_chol(Ctx& c, const double* SA, int64_t rows, int64_t n, int b
     };
     if (!infos_ok()) return false;  // the sketch is too ill-conditioned for Cholesky QR: SVD route
 
-    // ---- 3. sigma~_1: block power iteration on R^T R ---------------------
-    MSVD_BLAS(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, in, in, &one, R, in, &zero, G, in));
-    max_diag_kernel<<<1, 256, 0, c.stream>>>(G, n, scale);
-    sym_fill_scale_kernel<<<blocks(nn), 256, 0, c.stream>>>(G, n, scale);  // spectrum in [~1, n]
+    const bool debug = timed;
+    cudaEvent_t evs[4] = {};
+    if (debug) {
+        for (auto& e : evs) MSVD_CUDA(cudaEventCreate(&e));
+        MSVD_CUDA(cudaEventRecord(evs[0], c.stream));
+        MSVD_CUDA(cudaEventSynchronize(evs[0]));
+        float t0 = 0.0f;
+        MSVD_CUDA(cudaEventElapsedTime(&t0, ev_start, evs[0]));
+        std::fprintf(stderr, "msvd chol route: Cholesky QR2 + R^-1 %.3f ms\n", t0);
+        cudaEventDestroy(ev_start);
+    }
+    // M^8 of a symmetric n x n M (three DMMA GEMMs), into dst; tmp: n x n scratch
+    auto pow8 = [&](const double* M, double* tmp, double* dst) {
+        gemm(CUBLAS_OP_N, CUBLAS_OP_N, in, in, in, M, in, M, in, tmp, in);      // M^2
+        gemm(CUBLAS_OP_N, CUBLAS_OP_N, in, in, in, tmp, in, tmp, in, dst, in);  // M^4
+        gemm(CUBLAS_OP_N, CUBLAS_OP_N, in, in, in, dst, in, dst, in, tmp, in);  // M^8
+        MSVD_CUDA(cudaMemcpyAsync(dst, tmp, sizeof(double) * nn, cudaMemcpyDeviceToDevice, c.stream));
+    };
+    auto orth = [&](double* Xb, int k, int* inf) {  // Householder: robust for any conditioning
+        MSVD_SOLVER(cusolverDnDgeqrf(c.solver, in, k, Xb, in, tau, lw, lwork, inf));
+        MSVD_SOLVER(cusolverDnDorgqr(c.solver, in, k, k, Xb, in, tau, lw, lwork, inf));
+    };
+
+    // ---- 3. sigma~_1: block power iteration on (R^T R)^32 ------------------
+    // Gs = R^T R / max diag (spectrum in [1, n]: no overflow in the powers);
+    // only the top Ritz value is read, so the block may collapse towards the
+    // top vector between orthonormalizations
+    MSVD_BLAS(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, in, in, &one, R, in, &zero, R1, in));
+    max_diag_kernel<<<1, 256, 0, c.stream>>>(R1, n, scale);
+    sym_fill_scale_kernel<<<blocks(nn), 256, 0, c.stream>>>(R1, n, scale, G);
     start_block_kernel<<<blocks(n * ps), 256, 0, c.stream>>>(X, n * ps, seed ^ 0x5349474D41ULL);
     c.launches += 3;
+    pow8(G, R1, Gi);  // Gi := Gs^8 (Gi is rebuilt for step 4)
     double s1 = 0.0;
-    for (int round = 0; round < 40; ++round) {
-        for (int q = 0; q < 2; ++q) {  // (R^T R)^4 between Householder orthonormalizations
-            gemm(CUBLAS_OP_N, CUBLAS_OP_N, in, ps, in, G, in, X, in, Y, in);
-            gemm(CUBLAS_OP_N, CUBLAS_OP_N, in, ps, in, G, in, Y, in, X, in);
+    bool s1_done = false;
+    for (int round = 0; round < 8 && !s1_done; ++round) {
+        for (int q = 0; q < 2; ++q) {
+            gemm(CUBLAS_OP_N, CUBLAS_OP_N, in, ps, in, Gi, in, X, in, Y, in);
+            gemm(CUBLAS_OP_N, CUBLAS_OP_N, in, ps, in, Gi, in, Y, in, X, in);
         }
-        MSVD_SOLVER(cusolverDnDgeqrf(c.solver, in, ps, X, in, tau, lw, lwork, info + 2));
-        MSVD_SOLVER(cusolverDnDorgqr(c.solver, in, ps, ps, X, in, tau, lw, lwork, info + 2));
-        if (round >= 5 && round % 3 == 2) {
-            ritz(X, ps, sg1);
-            const double s = read(sg1, 1)[0];
-            const bool done = std::fabs(s - s1) <= 2.0 * kEps * s;
-            s1 = s;
-            if (done) break;
-        }
+        orth(X, ps, info + 2);
+        ritz(X, ps, sg1);
+        const double s = read(sg1, 1)[0];
+        s1_done = round > 0 && std::fabs(s - s1) <= 2.0 * kEps * s;
+        s1 = s;
     }
-    if (!infos_ok() || !(s1 > 0.0)) return false;
+    if (debug) MSVD_CUDA(cudaEventRecord(evs[1], c.stream));
+    if (!s1_done || !infos_ok() || !(s1 > 0.0)) return false;
 
-    // ---- 4. V0: block inverse iteration with R^-1 R^-T ---------------------
-    MSVD_BLAS(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, in, in, &one, Vcol, in, &zero, Gi, in));
-    max_diag_kernel<<<1, 256, 0, c.stream>>>(Gi, n, scale + 1);
-    sym_fill_scale_kernel<<<blocks(nn), 256, 0, c.stream>>>(Gi, n, scale + 1);
+    // ---- 4. V0: block inverse iteration with (R^T R)^-1 = R^-1 R^-T --------
+    MSVD_BLAS(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, in, in, &one, Vcol, in, &zero, R1, in));
+    max_diag_kernel<<<1, 256, 0, c.stream>>>(R1, n, scale + 1);
+    sym_fill_scale_kernel<<<blocks(nn), 256, 0, c.stream>>>(R1, n, scale + 1, Gi);
     start_block_kernel<<<blocks(n * p), 256, 0, c.stream>>>(X, n * p, seed ^ 0x56304254ULL);
     c.launches += 3;
+    // b = 1: only the dominant direction of Gi is wanted, so it is applied as
+    // Gi^8 (four times per orthonormalization).  b > 1: every wanted direction
+    // must keep its precision, so K products of Gi per orthonormalization with
+    // (theta_1 / theta_b)^K <= 1e6, from the Ritz values of the first round.
+    const bool single = b == 1;
+    if (single) pow8(Gi, R1, G);  // G := Gi^8 (G is free after step 3)
+    const double* M = single ? G : Gi;
     const double floor = std::sqrt(static_cast<double>(n)) * kEps * s1;  // precond.cpp:26-34
     bool converged = false;
     double smin = 0.0;
-    for (int round = 0; round < 60 && !converged; ++round) {
-        gemm(CUBLAS_OP_N, CUBLAS_OP_N, in, p, in, Gi, in, X, in, Y, in);
-        MSVD_SOLVER(cusolverDnDgeqrf(c.solver, in, p, Y, in, tau, lw, lwork, info + 3));
-        MSVD_SOLVER(cusolverDnDorgqr(c.solver, in, p, p, Y, in, tau, lw, lwork, info + 3));
-        std::swap(X, Y);
-        if (round >= 2 && round % 3 == 2) {
-            ritz(X, p, sg);
-            // Ritz vectors of the b smallest, their residuals against R^T R
-            ritz_cols_kernel<<<b, 256, 0, c.stream>>>(X, n, p, W, b, V0);
-            MSVD_BLAS(cublasDtrmm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT,
-                                  in, b, &one, R, in, V0, in, Z, in));
-            MSVD_BLAS(cublasDtrmm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
-                                  in, b, &one, R, in, Z, in, Y, in));
-            resid_kernel<<<b, 256, 0, c.stream>>>(Y, V0, sg, p, b, n, resid);
-            c.launches += 2;
-            const std::vector<double> r = read(resid, b);
-            smin = read(sg + p - 1, 1)[0];
-            converged = true;
-            for (int j = 0; j < b; ++j)
-                if (!(r[j] <= 64.0 * kEps * s1 * s1)) converged = false;  // the Jacobi SVD's accuracy
+    int K = single ? 4 : 1;
+    for (int round = 0; round < 16 && !converged; ++round) {
+        for (int q = 0; q < K; ++q) {
+            gemm(CUBLAS_OP_N, CUBLAS_OP_N, in, p, in, M, in, X, in, Y, in);
+            std::swap(X, Y);
         }
+        orth(X, p, info + 3);
+        ritz(X, p, sg);
+        // Ritz vectors of the b smallest, their residuals against R^T R
+        ritz_cols_kernel<<<b, 256, 0, c.stream>>>(X, n, p, W, b, V0);
+        MSVD_BLAS(cublasDtrmm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, in,
+                              b, &one, R, in, V0, in, Z, in));
+        MSVD_BLAS(cublasDtrmm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, in,
+                              b, &one, R, in, Z, in, Y, in));
+        resid_kernel<<<b, 256, 0, c.stream>>>(Y, V0, sg, p, b, n, resid);
+        c.launches += 2;
+        const std::vector<double> r = read(resid, b);
+        const std::vector<double> th = read(sg, p);  // descending
+        smin = th[p - 1];
+        converged = true;
+        for (int j = 0; j < b; ++j)
+            if (!(r[j] <= 64.0 * kEps * s1 * s1)) converged = false;  // the Jacobi SVD's accuracy
+        if (converged || single) continue;
+        // block: products needed for 1e-10 of the rest of the block, at the
+        // per-product rate (sigma_(b) / sigma_(p))^2 (an upper bound); give up
+        // (SVD route) when that cannot finish within the round budget
+        const double rate = (th[p - b] / th[0]) * (th[p - b] / th[0]);
+        const double spread2 = (th[p - b] / th[p - 1]) * (th[p - b] / th[p - 1]);
+        K = spread2 > 1.0 ? std::max(1, std::min(8, static_cast<int>(6.0 / std::log10(spread2)))) : 8;
+        const double need = rate < 1.0 ? 10.0 / -std::log10(rate) : 1e9;
+        if (need / K > 16 - round - 1) break;
+    }
+    if (debug) {
+        MSVD_CUDA(cudaEventRecord(evs[2], c.stream));
+        MSVD_CUDA(cudaEventSynchronize(evs[2]));
+        float t1 = 0.0f, t2 = 0.0f;
+        MSVD_CUDA(cudaEventElapsedTime(&t1, evs[0], evs[1]));
+        MSVD_CUDA(cudaEventElapsedTime(&t2, evs[1], evs[2]));
+        std::fprintf(stderr, "msvd chol route: sigma1 %.3f ms, V0 %.3f ms (converged %d, K %d)\n", t1, t2,
+                     static_cast<int>(converged), K);
+        for (auto& e : evs) cudaEventDestroy(e);
     }
     if (!converged || !infos_ok() || !(smin >= 1e3 * floor)) return false;
     DevState h;

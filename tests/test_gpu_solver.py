@@ -420,7 +420,7 @@ def test_solve_host_chunked_sketch_bit_identical(msvd, cuda, port, monkeypatch):
     ref = gpu_solve(msvd, to_device(a, cuda), opts)
     for mb in ("1", "3"):
         monkeypatch.setenv("MSVD_SKETCH_CHUNK_MB", mb)  # C1: 8 and 3 chunks
-        r = msvd.solve_host(np.ascontiguousarray(a), opts, want_precond=True)
+        r = msvd.solve_host(np.ascontiguousarray(a), opts)
         assert r.record.to_csv() == ref.record.to_csv()
         assert np.array_equal(r.v, ref.v)
 
