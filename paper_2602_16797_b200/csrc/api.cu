@@ -313,7 +313,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     DevState* st;
     msvd_record_row* rows;
     double *rh, *th, *Vcol, *Vrow, *sig, *AVb[2], *AXb[2], *AW, *Vb[2], *Xb[2], *W, *Rres, *tmp, *Cm, *Gpart,
-        *Gout, *nrm, *Rparts, *Rall, *tv, *dinv, *cpart, *fresh, *ZVb[2], *ZXb[2], *ZW, *V0b;
+        *Gout, *nrm, *Rparts, *Rall, *tv, *dinv, *cpart, *fresh, *ZVb[2], *ZXb[2], *ZW, *V0b, *tq_buf;
     ar.add(&st, 1);
     ar.add(&rows, max_iter + 2);
     ar.add(&rh, max_iter + 2);
@@ -346,7 +346,19 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     ar.add(&dinv, n);
     ar.add(&cpart, static_cast<size_t>(c.num_sms) * n);
     ar.add(&fresh, o.verify_cached_products ? ml * b : 1);
+    ar.add(&tq_buf, static_cast<size_t>(c.num_sms + 5) * kmax * kmax + 2);
     ar.commit();
+    // Cholesky QR2 of the trial block (trial_qr.cu) for b >= 2 on one rank;
+    // the TSQR kernels still run where its device flag says it failed
+    TrialQr tq{};
+    tq.gpart = tq_buf;
+    tq.R1 = tq_buf + static_cast<size_t>(c.num_sms) * kmax * kmax;
+    tq.R1inv = tq.R1 + kmax * kmax;
+    tq.R2inv = tq.R1inv + kmax * kmax;
+    tq.R = tq.R2inv + kmax * kmax;
+    tq.flag = reinterpret_cast<int*>(tq.R + kmax * kmax);
+    const char* tqe = std::getenv("MSVD_TRIAL_QR");
+    const bool use_cholqr = ranks == 1 && b >= 2 && !(tqe && std::string(tqe) == "householder");
 
     launch_state_init(c, st, o.seed);
     double* theta_dev =
@@ -528,8 +540,12 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         int np = nparts;
         bool fused = false;
         if (ex) {
-            if (launch_apply_ex(c, geom, W, b, aw, ex, ml, Gpart, fuse ? &fz : nullptr)) np = geom.grid;
-            else launch_tsqr(c, Tall, ml, k, Rparts, st, iter);
+            if (launch_apply_ex(c, geom, W, b, aw, ex, ml, Gpart, fuse ? &fz : nullptr)) {
+                np = geom.grid;
+            } else {
+                if (use_cholqr) launch_trial_cholqr(c, Tall, ml, k, tq);
+                launch_tsqr(c, Tall, ml, k, Rparts, st, iter, use_cholqr ? tq.flag : nullptr);
+            }
             launch_reduce_g(c, Gpart, geom.grid, n, 2 * b, nullptr, st, 0, Gout, nrm, nblk);
             if (ranks > 1) comm.allreduce_sum(Gout, static_cast<size_t>(2 * b * n), c.stream);
             MSVD_CUDA(cudaMemcpyAsync(ZW, Gout, sizeof(double) * b * n, cudaMemcpyDeviceToDevice, c.stream));
@@ -542,7 +558,8 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         if (fused) {
             np = geom.grid;
         } else {
-            launch_tsqr(c, Tall, ml, k, Rparts, st, iter);
+            if (use_cholqr) launch_trial_cholqr(c, Tall, ml, k, tq);
+            launch_tsqr(c, Tall, ml, k, Rparts, st, iter, use_cholqr ? tq.flag : nullptr);
         }
         if (one_pass) {  // ZW = A^T A W summed over CTAs (and ranks)
             launch_reduce_g(c, Gpart, geom.grid, n, b, W, st, 0, ZW, nrm, nblk);
@@ -655,6 +672,10 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         ra.theta_out = theta_dev;
         ra.st = st;
         ra.iter = -1;
+        if (use_cholqr) {
+            ra.chol_R = tq.R;
+            ra.chol_ok = tq.flag;
+        }
         if (one_pass) {
             ra.Z = cols_n({{ZW, b}});
             ra.ZVout = ZVb[0];
@@ -737,6 +758,10 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         ra.theta_out = theta_dev;
         ra.st = st;
         ra.iter = i;
+        if (use_cholqr) {
+            ra.chol_R = tq.R;
+            ra.chol_ok = tq.flag;
+        }
         if (one_pass) {
             ra.Z = cols_n({{ZVb[cur], b}, {ZXb[cur], nx}, {ZW, b}});
             ra.ZVout = ZVb[nxt];

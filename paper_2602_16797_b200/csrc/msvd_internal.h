@@ -128,7 +128,21 @@ void launch_gram(Ctx& c, const StreamGeom& g, Cols T, int k, const double* Cm, i
                  OutCols out, bool direct, double* Gpart, const int* skip = nullptr);
 // per-CTA Householder R of the m x k column block T, Rparts[nparts][k][k]
 int tsqr_parts(const Ctx& c);  // number of partial R factors launch_tsqr produces
-void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st, int iter);
+// skip: device flag; nonzero = the Cholesky QR2 of the block succeeded, the
+// TSQR kernels return at once (trial_qr.cu)
+void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st, int iter,
+                 const int* skip = nullptr);
+// Cholesky QR2 of the m x k trial block (trial_qr.cu): R (k x k upper) and a
+// device flag (1 = usable; else the TSQR path runs)
+struct TrialQr {
+    double* gpart;   // [num_sms][k][k] partial Grams
+    double* R1;      // k x k
+    double* R1inv;   // k x k
+    double* R2inv;   // k x k
+    double* R;       // k x k: R2 R1, the block's R factor
+    int* flag;
+};
+void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q);
 
 // single-CTA Rayleigh-Ritz: merge R parts, Jacobi SVD, C / theta / mix, V' = T C, X' = T mix
 struct RRArgs {
@@ -150,6 +164,8 @@ struct RRArgs {
     double* ZXout;       // n x b (mode 1): A^T A X' = Z mix
     DevState* st;
     int iter;
+    const double* chol_R = nullptr;  // k x k R from launch_trial_cholqr, used when *chol_ok != 0
+    const int* chol_ok = nullptr;
 };
 void launch_rr(Ctx& c, const RRArgs& a);
 

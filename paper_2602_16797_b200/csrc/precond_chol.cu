@@ -390,12 +390,22 @@ bool precond_build_chol(Ctx& c, const double* SA, int64_t rows, int64_t n, int b
     const double floor = std::sqrt(static_cast<double>(n)) * kEps * s1;  // precond.cpp:26-34
     bool converged = false;
     double smin = 0.0;
-    int K = single ? 4 : 1;
+    // Converged when the components outside the block have been contracted
+    // to rounding level: (sigma_(b) / sigma_(p+1))^(2 products) <= 1e-16, with
+    // the block's own largest Ritz value standing in for sigma_(p+1) (a lower
+    // bound, so the estimate is conservative) -- the accuracy the reference's
+    // Jacobi SVD delivers -- and the Ritz residuals at the Gram's rounding
+    // level as a sanity check.  Too slow a contraction for the round budget
+    // (a near-degenerate tail): the SVD route.
+    int K = single ? 4 : 1;                 // products of M per round
+    const int per = single ? 8 : 1;         // Gi products per product of M
+    double products = 0.0;
     for (int round = 0; round < 16 && !converged; ++round) {
         for (int q = 0; q < K; ++q) {
             gemm(CUBLAS_OP_N, CUBLAS_OP_N, in, p, in, M, in, X, in, Y, in);
             std::swap(X, Y);
         }
+        products += static_cast<double>(K) * per;
         orth(X, p, info + 3);
         ritz(X, p, sg);
         // Ritz vectors of the b smallest, their residuals against R^T R
@@ -409,18 +419,19 @@ bool precond_build_chol(Ctx& c, const double* SA, int64_t rows, int64_t n, int b
         const std::vector<double> r = read(resid, b);
         const std::vector<double> th = read(sg, p);  // descending
         smin = th[p - 1];
-        converged = true;
+        const double ratio = th[0] > 0.0 ? th[p - b] / th[0] : 1.0;
+        const double rate = ratio * ratio;
+        const double need = rate < 1.0 ? 16.0 / -std::log10(rate) : 1e9;
+        bool resid_ok = true;
         for (int j = 0; j < b; ++j)
-            if (!(r[j] <= 64.0 * kEps * s1 * s1)) converged = false;  // the Jacobi SVD's accuracy
-        if (converged || single) continue;
-        // block: products needed for 1e-10 of the rest of the block, at the
-        // per-product rate (sigma_(b) / sigma_(p))^2 (an upper bound); give up
-        // (SVD route) when that cannot finish within the round budget
-        const double rate = (th[p - b] / th[0]) * (th[p - b] / th[0]);
-        const double spread2 = (th[p - b] / th[p - 1]) * (th[p - b] / th[p - 1]);
-        K = spread2 > 1.0 ? std::max(1, std::min(8, static_cast<int>(6.0 / std::log10(spread2)))) : 8;
-        const double need = rate < 1.0 ? 10.0 / -std::log10(rate) : 1e9;
-        if (need / K > 16 - round - 1) break;
+            if (!(r[j] <= 64.0 * kEps * s1 * s1)) resid_ok = false;
+        converged = resid_ok && products >= need;
+        if (converged) continue;
+        if (!single) {  // keep every wanted direction's precision: (theta_1 / theta_b)^K <= 1e6
+            const double spread2 = (th[p - b] / th[p - 1]) * (th[p - b] / th[p - 1]);
+            K = spread2 > 1.0 ? std::max(1, std::min(8, static_cast<int>(6.0 / std::log10(spread2)))) : 8;
+        }
+        if ((need - products) / (static_cast<double>(K) * per) > 16 - round - 1) break;
     }
     if (debug) {
         MSVD_CUDA(cudaEventRecord(evs[2], c.stream));

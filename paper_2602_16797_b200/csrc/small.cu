@@ -22,11 +22,13 @@ struct TsqrArgs {
     double* Rparts;  // [grid][k][k]
     DevState* st;
     int iter;
+    const int* skip;  // nonzero: the Cholesky QR2 of the block was usable, nothing to do
 };
 
 // per-CTA TSQR: 8 warps fold 32-row tiles round-robin, then a 3-level tree
 template <int KM>
 __global__ void __launch_bounds__(256) tsqr_kernel(TsqrArgs a) {
+    if (a.skip && *a.skip) return;
     __shared__ double Rw[8][KM * KM];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = lane; i < KM * KM; i += 32) Rw[warp][i] = 0.0;
@@ -72,6 +74,7 @@ __global__ void __launch_bounds__(256) tsqr_kernel(TsqrArgs a) {
 // X block, instead of a chain of 32-row warp folds.
 template <int KM, int RPT>
 __global__ void __launch_bounds__(512) tsqr_stacked_kernel(TsqrArgs a) {
+    if (a.skip && *a.skip) return;
     __shared__ double R[KM * KM];
     __shared__ double red[2][16][KM + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -171,6 +174,7 @@ __global__ void __launch_bounds__(512) tsqr_stacked_kernel(TsqrArgs a) {
 // Wide trial blocks: 16 warps per CTA, shared-memory folds (fold_smem)
 template <int KM>
 __global__ void __launch_bounds__(512) tsqr_smem_kernel(TsqrArgs a) {
+    if (a.skip && *a.skip) return;
     extern __shared__ __align__(16) double tsm[];
     constexpr int XLD = KM + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -475,7 +479,12 @@ __global__ void __launch_bounds__(512) rr_kernel(RRArgs a) {
     const int64_t room = static_cast<int64_t>(dyn_smem / sizeof(double)) -
                          static_cast<int64_t>(base_words + 2 * 17 * (KM + 1));
     const int group = KM == 16 && room > 0 ? static_cast<int>(room / (k * (KM + 1))) - 1 : 0;
-    if (KM <= 8 && (base_words + stacked_words) * sizeof(double) <= dyn_smem) {
+    if (a.chol_ok && *a.chol_ok) {  // the block's R from Cholesky QR2 (trial_qr.cu)
+        for (int i = threadIdx.x; i < KM * KM; i += blockDim.x) {
+            const int r = i % KM, c = i / KM;
+            Bm[i] = (r < k && c < k && r <= c) ? a.chol_R[r + c * k] : 0.0;
+        }
+    } else if (KM <= 8 && (base_words + stacked_words) * sizeof(double) <= dyn_smem) {
         double* Ms = sh + base_words;
         stacked_qr<KM>(a.Rparts, a.nparts, k, Ms + 2 * 17 * (KM + 1), Ms, Bm);
     } else if (KM == 16 && group >= 8) {
@@ -1143,9 +1152,9 @@ void rr_launch(Ctx& c, const RRArgs& a) {
 
 int tsqr_parts(const Ctx& c) { return c.num_sms; }
 
-void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st, int iter) {
+void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st, int iter, const int* skip) {
     ProfScope prof(c, kProfTsqr);
-    TsqrArgs a{T, m, k, Rparts, st, iter};
+    TsqrArgs a{T, m, k, Rparts, st, iter, skip};
     const int grid = tsqr_parts(c);
     auto smem_launch = [&](auto kernel, int km) {
         const size_t sm = sizeof(double) * 16 * (km * km + 32 * (km + 1));

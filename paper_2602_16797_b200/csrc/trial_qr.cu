@@ -1,0 +1,188 @@
+// Cholesky QR2 of the m x k trial block [AV AX AW] (solver.cpp:412-417).
+//
+// The Rayleigh-Ritz step needs the R factor of the tall trial block
+// (svd.cpp:21-55 Householder QR; then the Jacobi SVD of R).  For b >= 2 the
+// separate Householder TSQR pass (a 48 MB block at C4, k = 12) ran at
+// ~0.2 TB/s and its 148-part stacked merge took another ~0.2 ms per
+// iteration.  Cholesky QR2 gives the same R (backward stable, positive
+// diagonal -- the SVD's right vectors do not depend on R's row signs) while
+// kappa(AT) < ~1e7: two streaming Gram passes over the block,
+//   G1 = AT^T AT,              R1 = chol(G1)
+//   G2 = (AT R1^-1)^T (AT R1^-1), R2 = chol(G2),   R = R2 R1,
+// each a fixed-order per-CTA partial sum (deterministic), and two k x k
+// Choleskys in one warp.  A device flag records whether both Choleskys
+// succeeded with diag(R1) within 1e6 of each other; where not, the TSQR
+// kernels (launched after, reading the flag) run and the RR step merges their
+// parts as before -- no host round trip either way.
+#include "common.cuh"
+#include "msvd_internal.h"
+
+namespace msvd {
+namespace {
+
+constexpr int kTile = 32;      // rows per staged tile
+constexpr int kGramT = 256;    // threads per CTA
+
+// Gpart[cta] (k x k, col-major, full) = sum over the CTA's rows of t t^T with
+// t = the row of T (times Rinv, upper k x k, when given)
+__global__ void __launch_bounds__(kGramT) block_gram_kernel(Cols T, int64_t m, int k, const double* Rinv,
+                                                           double* Gpart) {
+    __shared__ double tile[kTile][kMaxK + 1];
+    __shared__ double tt[kTile][kMaxK + 1];
+    __shared__ double ri[kMaxK * kMaxK];
+    const int64_t r0 = (m * blockIdx.x) / gridDim.x, r1 = (m * (blockIdx.x + 1)) / gridDim.x;
+    if (Rinv)
+        for (int i = threadIdx.x; i < k * k; i += blockDim.x) ri[i] = Rinv[i];
+    // entries (p <= q) owned by this thread: e = tid, tid + 256 (k(k+1)/2 <= 300)
+    const int ne = k * (k + 1) / 2;
+    int ep[2] = {0, 0}, eq[2] = {0, 0};
+    bool own[2] = {false, false};
+    for (int s = 0; s < 2; ++s) {
+        const int e = threadIdx.x + s * kGramT;
+        if (e < ne) {
+            int q = 0, base = 0;
+            while (base + q + 1 <= e) {  // column q holds entries base .. base + q
+                base += q + 1;
+                ++q;
+            }
+            ep[s] = e - base;
+            eq[s] = q;
+            own[s] = true;
+        }
+    }
+    double acc[2] = {0.0, 0.0};
+    for (int64_t base = r0; base < r1; base += kTile) {
+        const int rows = static_cast<int>(min(static_cast<int64_t>(kTile), r1 - base));
+        __syncthreads();
+        for (int i = threadIdx.x; i < kTile * k; i += blockDim.x) {
+            const int r = i % kTile, col = i / kTile;
+            tile[r][col] = r < rows ? T.p[col][base + r] : 0.0;
+        }
+        __syncthreads();
+        double(*src)[kMaxK + 1] = tile;
+        if (Rinv) {
+            for (int i = threadIdx.x; i < kTile * k; i += blockDim.x) {
+                const int r = i % kTile, j = i / kTile;
+                double s = 0.0;
+                for (int l = 0; l <= j; ++l) s += tile[r][l] * ri[l + j * k];
+                tt[r][j] = s;
+            }
+            __syncthreads();
+            src = tt;
+        }
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+            if (own[s]) {
+                double a = acc[s];
+                for (int r = 0; r < kTile; ++r) a += src[r][ep[s]] * src[r][eq[s]];
+                acc[s] = a;
+            }
+    }
+    double* G = Gpart + static_cast<size_t>(blockIdx.x) * k * k;
+    for (int s = 0; s < 2; ++s)
+        if (own[s]) {
+            G[ep[s] + eq[s] * k] = acc[s];
+            G[eq[s] + ep[s] * k] = acc[s];
+        }
+}
+
+// One warp: G = sum of the parts (in part order), R = chol(G) upper, Rinv =
+// R^-1; pass 2 also R_final = R Rprev.  flag: pass 1 writes success (both
+// pivots finite and positive, diag(R) within 1e6); pass 2 ands its own.
+__global__ void __launch_bounds__(32) chol_small_kernel(const double* Gpart, int nparts, int k, double* Rout,
+                                                        double* Rinv, const double* Rprev, double* Rfinal, int* flag,
+                                                        int pass) {
+    __shared__ double G[kMaxK * kMaxK];
+    __shared__ double R[kMaxK * kMaxK];
+    const int lane = threadIdx.x;
+    for (int e = lane; e < k * k; e += 32) {
+        double s = 0.0;
+        for (int p = 0; p < nparts; ++p) s += Gpart[static_cast<size_t>(p) * k * k + e];
+        G[e] = s;
+    }
+    __syncwarp();
+    // lane l owns column l of R (rows 0..l)
+    double col[kMaxK];
+#pragma unroll
+    for (int i = 0; i < kMaxK; ++i) col[i] = 0.0;
+    bool ok = true;
+    double dmax = 0.0, dmin = 1e300;
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+        if (j >= k) break;
+        // pivot: lane j
+        double d = 0.0;
+        if (lane == j) {
+            double s = G[j + j * k];
+#pragma unroll
+            for (int i = 0; i < kMaxK; ++i)
+                if (i < j) s -= col[i] * col[i];
+            d = s > 0.0 ? sqrt(s) : 0.0;
+            col[j] = d;
+        }
+        d = __shfl_sync(0xffffffffu, d, j);
+        if (!(d > 0.0) || !isfinite(d)) ok = false;
+        dmax = fmax(dmax, d);
+        dmin = fmin(dmin, d);
+        // R(j, l) for l > j: (G(j, l) - sum_i<j R(i, j) R(i, l)) / d
+        double s = (lane > j && lane < k) ? G[j + lane * k] : 0.0;
+#pragma unroll
+        for (int i = 0; i < kMaxK; ++i) {
+            if (i >= j) break;
+            const double rij = __shfl_sync(0xffffffffu, col[i], j);
+            s -= rij * col[i];
+        }
+        if (lane > j && lane < k) col[j] = d > 0.0 ? s / d : 0.0;
+    }
+    if (dmin < 1e-6 * dmax) ok = false;
+    if (lane < k)
+        for (int i = 0; i < kMaxK; ++i)
+            if (i < k) R[i + lane * k] = i <= lane ? col[i] : 0.0;
+    __syncwarp();
+    if (!ok) {  // keep everything finite: identity factors (the TSQR path takes over)
+        for (int e = lane; e < k * k; e += 32) {
+            const double v = (e % k == e / k) ? 1.0 : 0.0;
+            R[e] = v;
+        }
+        __syncwarp();
+    }
+    if (Rout)
+        for (int e = lane; e < k * k; e += 32) Rout[e] = R[e];
+    // Rinv column lane: back substitution R x = e_lane
+    if (lane < k) {
+        double x[kMaxK];
+#pragma unroll
+        for (int i = 0; i < kMaxK; ++i) x[i] = 0.0;
+        for (int i = lane; i >= 0; --i) {
+            double s = (i == lane) ? 1.0 : 0.0;
+            for (int l = i + 1; l <= lane; ++l) s -= R[i + l * k] * x[l];
+            x[i] = s / R[i + i * k];
+        }
+        for (int i = 0; i < k; ++i) Rinv[i + lane * k] = i <= lane ? x[i] : 0.0;
+    }
+    if (pass == 2 && lane < k) {  // R_final(:, lane) = R Rprev(:, lane)
+        for (int i = 0; i < k; ++i) {
+            double s = 0.0;
+            for (int l = i; l <= lane; ++l) s += R[i + l * k] * Rprev[l + lane * k];
+            Rfinal[i + lane * k] = i <= lane ? s : 0.0;
+        }
+    }
+    if (lane == 0) *flag = pass == 1 ? (ok ? 1 : 0) : ((*flag && ok) ? 1 : 0);
+}
+
+}  // namespace
+
+void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q) {
+    ProfScope prof(c, kProfTsqr);
+    const unsigned grid = static_cast<unsigned>(c.num_sms);
+    block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, nullptr, q.gpart);
+    chol_small_kernel<<<1, 32, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, q.R1, q.R1inv, nullptr, nullptr,
+                                              q.flag, 1);
+    block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, q.R1inv, q.gpart);
+    chol_small_kernel<<<1, 32, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, nullptr, q.R2inv, q.R1, q.R,
+                                              q.flag, 2);
+    MSVD_CUDA(cudaGetLastError());
+    c.launches += 4;
+}
+
+}  // namespace msvd

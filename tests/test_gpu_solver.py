@@ -250,18 +250,24 @@ def test_one_pass_stagnation_mode(msvd, cuda, port):
     """The default stop rule (stagnation, solver.cpp:177-211) on a one-pass
     shape: the deferred check rows are rewritten with exact residuals before
     the rule reads them and the row 5 back.  The stop row at the roundoff
-    floor is chaotic in the reference itself: the window and the
-    answer are gated, as in test_c1_stagnation_mode."""
+    floor is chaotic in the reference itself: it is gated by the
+    reference's own spread under 1-ulp perturbations of A (as in
+    tests/test_gpu_default_mode.py), widened by two check periods because
+    the device's floor noise is not the reference's; the answer is gated
+    exactly."""
+    from test_gpu_default_mode import spread
+
     cfg = problems.CONFIGS["c2"].scaled(m=30_000, n=500)
     sig = cfg.spectrum()
     a_dev, vmin = problems.make_problem_gpu(cfg.m, cfg.n, sig, device=cuda)
     o = msvd.SolverOptions(seed=problems.SOLVER_SEED, sketch_dim=cfg.d, tol=cfg.tol, record_timing=False)
     res = msvd.rlobpcg_single(msvd.DeviceDenseOperator(a_dev), o)
-    ref = port.lobpcg_solve(a_dev.cpu().numpy(), o.to_abi())
+    ref, lo, hi, its = spread(port, a_dev.cpu().numpy(), o)
+    print(f"[stagnation, one-pass] device {res.iterations()} iterations; reference spread {its}")
     smax = ref["sigma_max_estimate"]
     assert res.status == ref["status"] == "converged"
     assert (res.iterations() - 1) % o.check_every == 0
-    assert abs(res.iterations() - ref["iterations"]) <= 4 * o.check_every
+    assert lo - 2 * o.check_every <= res.iterations() <= hi + 2 * o.check_every, (res.iterations(), its)
     assert abs(res.sigma[0] - ref["sigma"][0]) <= SIGMA_TOL * smax
     assert subspace_sin(ref["v"], res.v) <= ANGLE_TOL
 
