@@ -285,6 +285,18 @@ struct HostSource {
     int64_t ld;
 };
 
+// Cholesky QR2 of the trial block (trial_qr.cu): b >= 3 on one rank, unless
+// MSVD_TRIAL_QR = householder.  Measured: it pays where the TSQR's merge of
+// k x k parts is the cost (C4, k = 12: 10.5 -> 7.7 ms of loop at m = 6e4);
+// for b = 2 (k = 6) the stacked TSQR is already cheap (C5: no gain), and C5's
+// second target is roundoff-chaotic, so b = 2 keeps the
+// reference's Householder arithmetic.
+bool use_cholqr_req(int b, int ranks) {
+    const char* e = std::getenv("MSVD_TRIAL_QR");
+    if (e && std::string(e) == "cholqr") return ranks == 1 && b >= 2;
+    return ranks == 1 && b >= 3 && !(e && std::string(e) == "householder");
+}
+
 void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_result* res,
            const HostSource* hs = nullptr) {
     Ctx& c = M->ctx->c;
@@ -357,8 +369,9 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     tq.R2inv = tq.R1inv + kmax * kmax;
     tq.R = tq.R2inv + kmax * kmax;
     tq.flag = reinterpret_cast<int*>(tq.R + kmax * kmax);
-    const char* tqe = std::getenv("MSVD_TRIAL_QR");
-    const bool use_cholqr = ranks == 1 && b >= 2 && !(tqe && std::string(tqe) == "householder");
+    tq.disabled = tq.flag + 1;
+    if (use_cholqr_req(b, ranks)) MSVD_CUDA(cudaMemsetAsync(tq.flag, 0, 2 * sizeof(int), c.stream));
+    const bool use_cholqr = use_cholqr_req(b, ranks);
 
     launch_state_init(c, st, o.seed);
     double* theta_dev =

@@ -141,6 +141,7 @@ struct TrialQr {
     double* R2inv;   // k x k
     double* R;       // k x k: R2 R1, the block's R factor
     int* flag;
+    int* disabled;   // sticky: set when a block failed; zeroed at solve start
 };
 void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q);
 

@@ -232,14 +232,9 @@ __global__ void __launch_bounds__(256, 4) gather_slice_kernel(const double* __re
     for (int q = 0; q < kSliceCPL; ++q) acc[q] = 0.0;
     bool finite = true;
     int64_t e = e0;
-    // lane u < U holds entry e + u of the NEXT batch: the (sketch row, source
-    // row) list is prefetched one batch ahead, so only the A loads are on a
-    // batch's critical path
-    uint32_t next = (lane < kSliceU && e + lane < e1) ? vals[e + lane] : 0u;
     for (; e + kSliceU <= e1; e += kSliceU) {
-        // the row indices of this batch are broadcast from the lanes that hold them
-        const uint32_t mine = next;
-        next = (lane < kSliceU && e + kSliceU + lane < e1) ? vals[e + kSliceU + lane] : 0u;
+        // lane u < U fetches entry e+u; the row indices are then broadcast
+        const uint32_t mine = lane < kSliceU ? vals[e + lane] : 0u;
         double x[kSliceU][kSliceCPL];
         double sv[kSliceU];
 #pragma unroll

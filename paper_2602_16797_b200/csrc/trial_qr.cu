@@ -26,7 +26,8 @@ constexpr int kGramT = 256;    // threads per CTA
 // Gpart[cta] (k x k, col-major, full) = sum over the CTA's rows of t t^T with
 // t = the row of T (times Rinv, upper k x k, when given)
 __global__ void __launch_bounds__(kGramT) block_gram_kernel(Cols T, int64_t m, int k, const double* Rinv,
-                                                           double* Gpart) {
+                                                           double* Gpart, const int* disabled) {
+    if (*disabled) return;
     __shared__ double tile[kTile][kMaxK + 1];
     __shared__ double tt[kTile][kMaxK + 1];
     __shared__ double ri[kMaxK * kMaxK];
@@ -91,7 +92,11 @@ __global__ void __launch_bounds__(kGramT) block_gram_kernel(Cols T, int64_t m, i
 // pivots finite and positive, diag(R) within 1e6); pass 2 ands its own.
 __global__ void __launch_bounds__(32) chol_small_kernel(const double* Gpart, int nparts, int k, double* Rout,
                                                         double* Rinv, const double* Rprev, double* Rfinal, int* flag,
-                                                        int pass) {
+                                                        int pass, int* disabled) {
+    if (*disabled) {  // an earlier iteration's block was too ill-conditioned: TSQR from here on
+        if (threadIdx.x == 0) *flag = 0;
+        return;
+    }
     __shared__ double G[kMaxK * kMaxK];
     __shared__ double R[kMaxK * kMaxK];
     const int lane = threadIdx.x;
@@ -167,7 +172,12 @@ __global__ void __launch_bounds__(32) chol_small_kernel(const double* Gpart, int
             Rfinal[i + lane * k] = i <= lane ? s : 0.0;
         }
     }
-    if (lane == 0) *flag = pass == 1 ? (ok ? 1 : 0) : ((*flag && ok) ? 1 : 0);
+    if (lane == 0) {
+        *flag = pass == 1 ? (ok ? 1 : 0) : ((*flag && ok) ? 1 : 0);
+        // sticky: once a trial block needs the TSQR, the later ones (whose
+        // conditioning only grows as the iteration converges) skip straight to it
+        if (pass == 2 && !*flag) *disabled = 1;
+    }
 }
 
 }  // namespace
@@ -175,12 +185,12 @@ __global__ void __launch_bounds__(32) chol_small_kernel(const double* Gpart, int
 void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q) {
     ProfScope prof(c, kProfTsqr);
     const unsigned grid = static_cast<unsigned>(c.num_sms);
-    block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, nullptr, q.gpart);
+    block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, nullptr, q.gpart, q.disabled);
     chol_small_kernel<<<1, 32, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, q.R1, q.R1inv, nullptr, nullptr,
-                                              q.flag, 1);
-    block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, q.R1inv, q.gpart);
+                                              q.flag, 1, q.disabled);
+    block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, q.R1inv, q.gpart, q.disabled);
     chol_small_kernel<<<1, 32, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, nullptr, q.R2inv, q.R1, q.R,
-                                              q.flag, 2);
+                                              q.flag, 2, q.disabled);
     MSVD_CUDA(cudaGetLastError());
     c.launches += 4;
 }

@@ -88,6 +88,7 @@ def test_trial_block_cholqr_matches_tsqr(msvd, cuda, name, shape, monkeypatch):
     opts = msvd.SolverOptions(seed=problems.SOLVER_SEED, sketch_dim=cfg.d, tol=cfg.tol, block_size=cfg.b,
                               use_stagnation=False, record_timing=False)
     op = msvd.DeviceDenseOperator(a_dev)
+    monkeypatch.setenv("MSVD_TRIAL_QR", "cholqr")  # default only for b >= 3 (api.cu use_cholqr_req)
     fast = msvd.rlobpcg_block(op, opts)
     monkeypatch.setenv("MSVD_TRIAL_QR", "householder")
     ref = msvd.rlobpcg_block(op, opts)

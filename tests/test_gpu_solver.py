@@ -123,8 +123,11 @@ def test_config_shape_parity(msvd, cuda, port, name):
         assert abs(res.iterations() - ref["iterations"]) <= 1
     elif name == "c5":
         # v_{n-1} is roundoff-chaotic in the reference itself:
-        # gate sigma_n, sigma_{n-1} and v_min only
-        assert_parity(res, ref, 2, gate_vectors=[0])
+        # gate sigma_n, sigma_{n-1} and v_min only; the iteration count with
+        # the near-tie rule of tests/_parity.py (the second target's residual
+        # sits at the threshold for many check rows)
+        from _parity import assert_parity as assert_parity_tie
+        assert_parity_tie(res, ref, 2, cfg.tol, gate_vectors=[0], label="c5 shape")
     else:
         assert_parity(res, ref, cfg.b)
     del torch
