@@ -18,6 +18,7 @@
 // stream_ticket.cu (stream_impl.cuh).
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include "stream_impl.cuh"
 
@@ -233,6 +234,14 @@ bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
     ProfScope prof(c, kProfApply);
     TsqrFuse none{};
     if (try_apply_rows(c, ApplyArgs{g, W, out, fuse ? *fuse : none, gpart, nullptr}, b)) return fuse != nullptr;
+    // one-pass, b = 3, 4: a team of four warps per row, four rows per barrier
+    // (MSVD_ONEPASS_KERNEL = pair | team overrides the choice, for measurement)
+    const char* ok_env = std::getenv("MSVD_ONEPASS_KERNEL");
+    const bool want_team = ok_env ? std::string(ok_env) == "team" : b >= 3;
+    if (gpart && want_team && team_ok(c, g, b)) {
+        launch_team(c, ApplyArgs{team_geom(c, g), W, out, none, gpart, nullptr}, b);
+        return false;
+    }
     if (gpart && pair_ok(c, g, b, false)) {  // one-pass, rows split over warp pairs (no fused TSQR)
         launch_pair(c, ApplyArgs{g, W, out, none, gpart, nullptr}, b);
         return false;

@@ -159,6 +159,7 @@ bool try_apply_rows(Ctx& c, const ApplyArgs& a0, int b);
 void launch_pair(Ctx& c, const ApplyArgs& a0, int b);
 void launch_pair_ex(Ctx& c, const ApplyArgs& a);
 void launch_team_ex(Ctx& c, const ApplyArgs& a, Cols ex, int b);
+void launch_team(Ctx& c, const ApplyArgs& a, int b);  // the plain one-pass pass in the team form
 // stream_ticket.cu: the ticket A*W pass (any b <= 8) and the K2 gram pass
 void launch_ticket(Ctx& c, const ApplyArgs& a, int b);
 void launch_gram_b(Ctx& c, const GramArgs& a, int b);

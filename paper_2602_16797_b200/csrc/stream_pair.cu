@@ -195,11 +195,14 @@ __global__ void __launch_bounds__(256, 1) apply_pair_kernel(ApplyArgs a) {
 // dot products meet in shared memory behind a per-team named barrier and are
 // summed in fixed order.  gpart holds [grid][2b][n].
 
-template <int B, int PL, int T>
+// EX = false: the plain one-pass pass (A W and A^T (A W)) in the same
+// four-rows-per-barrier form, for b = 3, 4 where the warp-pair kernel's
+// per-row barrier and butterflies cap it at ~0.55 of the HBM roofline (C4).
+template <int B, int PL, int T, bool EX = true>
 __global__ void __launch_bounds__(256, 1) apply_team_ex_kernel(ApplyArgs a, Cols ex) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int TEAMS = 8 / T;
-    constexpr int BG = 2 * B;
+    constexpr int BG = EX ? 2 * B : B;
     const StreamGeom& g = a.g;
     unsigned char* extra;
     constexpr size_t kXBytes = sizeof(double) * TEAMS * 2 * T * kTeamRows * B;  // [team][buffer][member][row][B]
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(256, 1) apply_team_ex_kernel(ApplyArgs a, Cols
     // the chunk's E rows, lane l holding rows l and 32 + l, one chunk ahead
     double exc[2][B], exn[2][B];
     auto ex_load = [&](int64_t cc) {
-        if (cc >= nchunks) return;
+        if (!EX || cc >= nchunks) return;
         const int64_t rr0 = r_begin + cc * g.rc;
         const int rcc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - rr0));
 #pragma unroll
@@ -350,7 +353,7 @@ __global__ void __launch_bounds__(256, 1) apply_team_ex_kernel(ApplyArgs a, Cols
 #pragma unroll
                 for (int j = 0; j < B; ++j) {
                     y[j] = __shfl_sync(kFull, ym[j], 8 * q);
-                    e[j] = __shfl_sync(kFull, rr < 32 ? exc[0][j] : exc[1][j], rr & 31);
+                    e[j] = EX ? __shfl_sync(kFull, rr < 32 ? exc[0][j] : exc[1][j], rr & 31) : 0.0;
                 }
 #pragma unroll
                 for (int i = 0; i < PL; ++i) {
@@ -360,8 +363,10 @@ __global__ void __launch_bounds__(256, 1) apply_team_ex_kernel(ApplyArgs a, Cols
                     for (int j = 0; j < B; ++j) {
                         ga[i][0][j] = fma(x.x, y[j], ga[i][0][j]);
                         ga[i][1][j] = fma(x.y, y[j], ga[i][1][j]);
-                        ga[i][0][B + j] = fma(x.x, e[j], ga[i][0][B + j]);
-                        ga[i][1][B + j] = fma(x.y, e[j], ga[i][1][B + j]);
+                        if constexpr (EX) {
+                            ga[i][0][B + j] = fma(x.x, e[j], ga[i][0][B + j]);
+                            ga[i][1][B + j] = fma(x.y, e[j], ga[i][1][B + j]);
+                        }
                     }
                 }
             }
@@ -430,6 +435,24 @@ void launch_pair_ex(Ctx& c, const ApplyArgs& a) {
         case 8: apply_pair_b<1, 8, true>(c, a); break;
         default: fail(MSVD_ERR_INVALID, "msvd: A*W + A^T e pass on an unsupported shape");
     }
+}
+
+void launch_team(Ctx& c, const ApplyArgs& a, int b) {
+    const size_t sm = bar_bytes(a.g.stages) +
+                      128 * ((sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 4 + 127) / 128) +
+                      a.g.stages * a.g.stage_bytes;
+    auto go = [&](auto kernel) {
+        optin_smem(c, kernel);
+        kernel<<<a.g.grid, 256, sm, c.stream>>>(a, Cols{});
+    };
+    const int pl = team_pl(a.g.n);
+    if (b == 2 && pl <= 2) go(apply_team_ex_kernel<2, 2, kTeam, false>);
+    else if (b == 2) go(apply_team_ex_kernel<2, 4, kTeam, false>);
+    else if (b == 3) go(apply_team_ex_kernel<3, 2, kTeam, false>);
+    else go(apply_team_ex_kernel<4, 2, kTeam, false>);
+    MSVD_CUDA(cudaGetLastError());
+    ++c.launches;
+    c.paths |= kPathTeam;
 }
 
 void launch_team_ex(Ctx& c, const ApplyArgs& a, Cols ec, int b) {
