@@ -358,13 +358,13 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     ar.add(&dinv, n);
     ar.add(&cpart, static_cast<size_t>(c.num_sms) * n);
     ar.add(&fresh, o.verify_cached_products ? ml * b : 1);
-    ar.add(&tq_buf, static_cast<size_t>(c.num_sms + 5) * kmax * kmax + 2);
+    ar.add(&tq_buf, static_cast<size_t>(4 * c.num_sms + 5) * kmax * kmax + 2);
     ar.commit();
     // Cholesky QR2 of the trial block (trial_qr.cu) for b >= 2 on one rank;
     // the TSQR kernels still run where its device flag says it failed
     TrialQr tq{};
     tq.gpart = tq_buf;
-    tq.R1 = tq_buf + static_cast<size_t>(c.num_sms) * kmax * kmax;
+    tq.R1 = tq_buf + static_cast<size_t>(4 * c.num_sms) * kmax * kmax;  // after [4 num_sms][k][k] parts
     tq.R1inv = tq.R1 + kmax * kmax;
     tq.R2inv = tq.R1inv + kmax * kmax;
     tq.R = tq.R2inv + kmax * kmax;

@@ -136,7 +136,7 @@ void launch_tsqr(Ctx& c, Cols T, int64_t m, int k, double* Rparts, DevState* st,
 // Cholesky QR2 of the m x k trial block (trial_qr.cu): R (k x k upper) and a
 // device flag (1 = usable; else the TSQR path runs)
 struct TrialQr {
-    double* gpart;   // [num_sms][k][k] partial Grams
+    double* gpart;   // [4 num_sms][k][k] partial Grams
     double* R1;      // k x k
     double* R1inv;   // k x k
     double* R2inv;   // k x k

@@ -31,6 +31,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -234,6 +235,39 @@ __global__ void __launch_bounds__(1024) unit_step_kernel(const double* Y, double
     }
 }
 
+// E = sym(G) - I from G's upper triangle, and X0 = up(E) (strict upper E,
+// half the diagonal); emax: max |E_ij| (one CTA reduction via atomicMax on
+// the bit pattern of a non-negative double)
+__global__ void near_id_init_kernel(const double* G, int64_t n, double* E, double* X,
+                                    unsigned long long* emax_bits) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    double a = 0.0;
+    if (i < n * n) {
+        const int64_t r = i % n, c = i / n;
+        const double g = r <= c ? G[r + c * n] : G[c + r * n];
+        const double e = g - (r == c ? 1.0 : 0.0);
+        E[i] = e;
+        X[i] = r < c ? e : (r == c ? 0.5 * e : 0.0);
+        a = fabs(e);
+    }
+    for (int o = 16; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(emax_bits, static_cast<unsigned long long>(__double_as_longlong(a)));
+}
+// X = up(E - S) with S = X^T X (upper triangle valid)
+__global__ void near_id_step_kernel(const double* E, const double* S, int64_t n, double* X) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n * n) return;
+    const int64_t r = i % n, c = i / n;
+    X[i] = r < c ? E[i] - S[i] : (r == c ? 0.5 * (E[i] - S[i]) : 0.0);
+}
+// out = I + s * M (M upper; lower of out zero)
+__global__ void id_plus_kernel(const double* M, int64_t n, double s, double* out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n * n) return;
+    const int64_t r = i % n, c = i / n;
+    out[i] = r <= c ? (r == c ? 1.0 : 0.0) + s * M[i] : 0.0;
+}
+
 unsigned blocks(int64_t count) { return static_cast<unsigned>(ceil_div(count, 256)); }
 
 }  // namespace
@@ -336,7 +370,45 @@ bool precond_build_chol(Ctx& c, const double* SA, int64_t rows, int64_t n, int b
     mark();
     MSVD_BLAS(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, in, ir, &one, Q, ir, &zero, Gi, in));
     mark();
-    chol_inverse(c, Gi, n, R2, R2inv, cws, info + 6);
+    // Q^T Q = I + E with |E| ~ kappa(SA)^2 u: its Cholesky factor I + X by the
+    // fixed point X = up(E - X^T X) (each step a DMMA SYRK), its inverse by
+    // Horner's Neumann series -- a few GEMMs instead of potrf's panel loop.
+    // |E| > 0.05: potrf (chol_inverse)
+    bool near_id = false;
+    if (!std::getenv("MSVD_CHOL2_POTRF")) {
+        double* E = cws;
+        double* Xn = cws + nn;
+        double* S = cws + 2 * nn;
+        unsigned long long* ebits = reinterpret_cast<unsigned long long*>(resid);
+        MSVD_CUDA(cudaMemsetAsync(ebits, 0, sizeof(unsigned long long), c.stream));
+        near_id_init_kernel<<<blocks(nn), 256, 0, c.stream>>>(Gi, n, E, Xn, ebits);
+        ++c.launches;
+        unsigned long long hb = 0;
+        MSVD_CUDA(cudaMemcpyAsync(&hb, ebits, sizeof(hb), cudaMemcpyDeviceToHost, c.stream));
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+        double emax;
+        std::memcpy(&emax, &hb, sizeof(emax));
+        if (emax > 0.0 && emax <= 0.05) {
+            const int iters = std::min(24, static_cast<int>(std::ceil(17.0 / -std::log10(emax))) + 1);
+            for (int k = 0; k < iters; ++k) {
+                MSVD_BLAS(cublasDsyrk(c.blas, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, in, in, &one, Xn, in, &zero, S, in));
+                near_id_step_kernel<<<blocks(nn), 256, 0, c.stream>>>(E, S, n, Xn);
+            }
+            id_plus_kernel<<<blocks(nn), 256, 0, c.stream>>>(Xn, n, 1.0, R2);  // R2 = I + X
+            // R2^-1 = I - X + X^2 - ... : Y <- I - X Y, Y_0 = I
+            id_plus_kernel<<<blocks(nn), 256, 0, c.stream>>>(Xn, n, -1.0, R2inv);
+            for (int k = 1; k < iters; ++k) {
+                MSVD_BLAS(cublasDtrmm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N,
+                                      CUBLAS_DIAG_NON_UNIT, in, in, &one, Xn, in, R2inv, in, S, in));
+                id_plus_kernel<<<blocks(nn), 256, 0, c.stream>>>(S, n, -1.0, R2inv);
+            }
+            c.launches += 2 + 2 * iters;
+            const int one_i = 1;
+            MSVD_CUDA(cudaMemcpyAsync(info + 6, &one_i, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+            near_id = true;
+        }
+    }
+    if (!near_id) chol_inverse(c, Gi, n, R2, R2inv, cws, info + 6);
     mark();
     MSVD_BLAS(cublasDtrmm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, in, in,
                           &one, R2, in, G, in, R, in));  // R = R2 R1 (upper)

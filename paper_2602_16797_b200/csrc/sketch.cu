@@ -272,70 +272,6 @@ __global__ void __launch_bounds__(256, 4) gather_slice_kernel(const double* __re
     if (!__all_sync(0xffffffffu, finite) && lane == 0 && st) atomicCAS(&st->err_code, 0, kErrNonfiniteA);
 }
 
-// Asynchronous form of the column-slice gather (64 columns, one warp per
-// sketch row): each lane copies its 16 bytes of an entry's row slice
-// straight into a per-warp shared-memory ring with cp.async, DEPTH batches of
-// U entries ahead of the sums, so the loads in flight do not hold registers
-// and the row-list reads are off the critical path.  Same per-element
-// sequential __dmul_rn/__dadd_rn sums as gather_slice_kernel -> same bits.
-// Persistent: one CTA per SM, warps stride over sketch rows.  Needs even ld
-// (16-byte aligned row slices).
-template <int U, int DEPTH>
-__global__ void __launch_bounds__(256, 1) gather_async_kernel(const double* __restrict__ A, int64_t ld, int n,
-                                                              int64_t d, const int64_t* __restrict__ offs,
-                                                              const uint32_t* __restrict__ vals, double val,
-                                                              double* __restrict__ SA, DevState* st, int c0) {
-    extern __shared__ __align__(16) double ring[];  // [8 warps][DEPTH][U][64] + signs [8][DEPTH][U]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* my = ring + static_cast<size_t>(warp) * DEPTH * U * 64;
-    double* sgn = ring + static_cast<size_t>(8) * DEPTH * U * 64 + static_cast<size_t>(warp) * DEPTH * U;
-    const int col = c0 + 2 * lane;
-    const int bytes = col + 1 < n ? 16 : (col < n ? 8 : 0);
-    bool finite = true;
-    for (int64_t s = static_cast<int64_t>(blockIdx.x) * 8 + warp; s < d; s += static_cast<int64_t>(gridDim.x) * 8) {
-        const int64_t e0 = offs[s], e1 = offs[s + 1];
-        const int64_t nb = (e1 - e0 + U - 1) / U;
-        auto issue = [&](int64_t b) {
-            const int stg = static_cast<int>(b % DEPTH);
-            const int64_t e = e0 + b * U;
-            const int cnt = static_cast<int>(min(static_cast<int64_t>(U), e1 - e));
-            const uint32_t mine = lane < cnt ? vals[e + lane] : 0u;
-            if (lane < U) sgn[stg * U + lane] = (mine >> 31) ? -val : val;
-            for (int u = 0; u < cnt; ++u) {
-                const uint32_t v = __shfl_sync(0xffffffffu, mine, u);
-                const double* src = A + static_cast<int64_t>(v & 0x7fffffffu) * ld + (bytes ? col : c0);
-                cp_async16_zfill(my + (stg * U + u) * 64 + 2 * lane, src, bytes);
-            }
-        };
-        double acc0 = 0.0, acc1 = 0.0;
-        for (int64_t b = 0; b < DEPTH - 1; ++b) {
-            if (b < nb) issue(b);
-            cp_async_commit();
-        }
-        for (int64_t b = 0; b < nb; ++b) {
-            if (b + DEPTH - 1 < nb) issue(b + DEPTH - 1);
-            cp_async_commit();
-            cp_async_wait<DEPTH - 1>();
-            __syncwarp();
-            const int stg = static_cast<int>(b % DEPTH);
-            const int cnt = static_cast<int>(min(static_cast<int64_t>(U), e1 - (e0 + b * U)));
-            for (int u = 0; u < cnt; ++u) {
-                const double sv = sgn[stg * U + u];
-                const double2 x = *reinterpret_cast<const double2*>(my + (stg * U + u) * 64 + 2 * lane);
-                acc0 = __dadd_rn(acc0, __dmul_rn(sv, x.x));
-                acc1 = __dadd_rn(acc1, __dmul_rn(sv, x.y));
-                finite = finite && isfinite(x.x) && isfinite(x.y);
-            }
-            __syncwarp();  // the stage is refilled by the next issue
-        }
-        cp_async_wait<0>();
-        __syncwarp();
-        if (col < n) SA[s + static_cast<int64_t>(col) * d] = acc0;
-        if (col + 1 < n) SA[s + static_cast<int64_t>(col + 1) * d] = acc1;
-    }
-    if (!__all_sync(0xffffffffu, finite) && lane == 0 && st) atomicCAS(&st->err_code, 0, kErrNonfiniteA);
-}
-
 }  // namespace
 
 void build_sparsestack_dev(Ctx& c, int64_t d, int64_t m, int zeta, uint64_t seed, uint32_t* pos, int8_t* sgn) {
@@ -434,20 +370,10 @@ void sketch_dev(Ctx& c, const StreamGeom& g, int64_t row0, int64_t d, int zeta, 
         ++c.launches;
         return;
     }
-    if (g.tma && std::getenv("MSVD_SKETCH_ASYNC")) {  // opt-in while measured
-        constexpr int U = 8, DEPTH = 6;
-        const size_t smem = sizeof(double) * (8 * DEPTH * U * 64 + 8 * DEPTH * U);
-        optin_smem(c, gather_async_kernel<U, DEPTH>);
-        for (int c0 = 0; c0 < g.n; c0 += 64) {
-            gather_async_kernel<U, DEPTH><<<static_cast<unsigned>(c.num_sms), 256, smem, c.stream>>>(
-                g.A, g.ld, g.n, d, L.offs, L.vals, L.val, SA, st, c0);
-            MSVD_CUDA(cudaGetLastError());
-            ++c.launches;
-        }
-        return;
-    }
     // measured (C2): 32 * 2 columns x 8 entries in flight per warp (the 1-, 4-
-    // and 8-pair variants were slower and spilled; removed)
+    // and 8-pair variants were slower and spilled; a cp.async form landing the
+    // rows in a per-warp shared-memory ring, 6 x 8 entries ahead, took 8.0 ms
+    // instead of 3.9: removed)
     const int slice = 64;
     const unsigned grid = static_cast<unsigned>(ceil_div(d, 8));
     for (int c0 = 0; c0 < g.n; c0 += slice) {

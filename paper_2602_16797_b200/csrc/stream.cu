@@ -234,10 +234,12 @@ bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
     ProfScope prof(c, kProfApply);
     TsqrFuse none{};
     if (try_apply_rows(c, ApplyArgs{g, W, out, fuse ? *fuse : none, gpart, nullptr}, b)) return fuse != nullptr;
-    // one-pass, b = 3, 4: a team of four warps per row, four rows per barrier
-    // (MSVD_ONEPASS_KERNEL = pair | team overrides the choice, for measurement)
+    // one-pass in the team form (four warps per row, four rows per barrier):
+    // opt-in, MSVD_ONEPASS_KERNEL = team.  Measured at C4 (b = 4, n = 500) it
+    // is slower than the warp-pair kernel (13.8 vs 12.9 ms of passes), and equal
+    // at C5 (b = 2)
     const char* ok_env = std::getenv("MSVD_ONEPASS_KERNEL");
-    const bool want_team = ok_env ? std::string(ok_env) == "team" : b >= 3;
+    const bool want_team = ok_env && std::string(ok_env) == "team";
     if (gpart && want_team && team_ok(c, g, b)) {
         launch_team(c, ApplyArgs{team_geom(c, g), W, out, none, gpart, nullptr}, b);
         return false;

@@ -20,71 +20,92 @@
 namespace msvd {
 namespace {
 
-constexpr int kTile = 32;      // rows per staged tile
-constexpr int kGramT = 256;    // threads per CTA
+constexpr int kGramT = 128;    // threads per CTA (4 warps; static shared memory)
+constexpr int kGramW = kGramT / 32;
+constexpr int kMaxEnt = (kMaxK * (kMaxK + 1) / 2 + 31) / 32;  // Gram entries per lane (<= 10)
 
 // Gpart[cta] (k x k, col-major, full) = sum over the CTA's rows of t t^T with
-// t = the row of T (times Rinv, upper k x k, when given)
+// t = the row of T (times Rinv, upper k x k, when given).  Each warp streams
+// its own contiguous rows in 32-row tiles with no CTA barrier: lane = row for
+// the loads (coalesced per column) and the R^-1 transform, then the tile goes
+// through the warp's shared-memory slot and lane e sums the Gram entries e,
+// e + 32, ... over the tile's rows; the 8 warp partials are added in warp
+// order at the end (deterministic).  Four CTAs per SM.
 __global__ void __launch_bounds__(kGramT) block_gram_kernel(Cols T, int64_t m, int k, const double* Rinv,
                                                            double* Gpart, const int* disabled) {
     if (*disabled) return;
-    __shared__ double tile[kTile][kMaxK + 1];
-    __shared__ double tt[kTile][kMaxK + 1];
+    __shared__ double tile[kGramW][32][kMaxK + 1];
     __shared__ double ri[kMaxK * kMaxK];
-    const int64_t r0 = (m * blockIdx.x) / gridDim.x, r1 = (m * (blockIdx.x + 1)) / gridDim.x;
+    __shared__ double wsum[kGramW][kMaxK * (kMaxK + 1) / 2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (Rinv)
         for (int i = threadIdx.x; i < k * k; i += blockDim.x) ri[i] = Rinv[i];
-    // entries (p <= q) owned by this thread: e = tid, tid + 256 (k(k+1)/2 <= 300)
+    __syncthreads();
+    const int64_t gw = static_cast<int64_t>(blockIdx.x) * kGramW + warp, nw = static_cast<int64_t>(gridDim.x) * kGramW;
+    const int64_t r0 = (m * gw) / nw, r1 = (m * (gw + 1)) / nw;
     const int ne = k * (k + 1) / 2;
-    int ep[2] = {0, 0}, eq[2] = {0, 0};
-    bool own[2] = {false, false};
-    for (int s = 0; s < 2; ++s) {
-        const int e = threadIdx.x + s * kGramT;
-        if (e < ne) {
-            int q = 0, base = 0;
+    int ep[kMaxEnt], eq[kMaxEnt];
+#pragma unroll
+    for (int s = 0; s < kMaxEnt; ++s) {
+        const int e = lane + 32 * s;
+        int q = 0, base = 0;
+        if (e < ne)
             while (base + q + 1 <= e) {  // column q holds entries base .. base + q
                 base += q + 1;
                 ++q;
             }
-            ep[s] = e - base;
-            eq[s] = q;
-            own[s] = true;
-        }
+        ep[s] = e < ne ? e - base : 0;
+        eq[s] = e < ne ? q : 0;
     }
-    double acc[2] = {0.0, 0.0};
-    for (int64_t base = r0; base < r1; base += kTile) {
-        const int rows = static_cast<int>(min(static_cast<int64_t>(kTile), r1 - base));
-        __syncthreads();
-        for (int i = threadIdx.x; i < kTile * k; i += blockDim.x) {
-            const int r = i % kTile, col = i / kTile;
-            tile[r][col] = r < rows ? T.p[col][base + r] : 0.0;
-        }
-        __syncthreads();
-        double(*src)[kMaxK + 1] = tile;
+    double acc[kMaxEnt];
+#pragma unroll
+    for (int s = 0; s < kMaxEnt; ++s) acc[s] = 0.0;
+    double(*tl)[kMaxK + 1] = tile[warp];
+    for (int64_t base = r0; base < r1; base += 32) {
+        const int64_t r = base + lane;
+        double t[kMaxK];
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j) t[j] = (j < k && r < r1) ? T.p[j][r] : 0.0;
         if (Rinv) {
-            for (int i = threadIdx.x; i < kTile * k; i += blockDim.x) {
-                const int r = i % kTile, j = i / kTile;
-                double s = 0.0;
-                for (int l = 0; l <= j; ++l) s += tile[r][l] * ri[l + j * k];
-                tt[r][j] = s;
+#pragma unroll
+            for (int j = kMaxK - 1; j >= 0; --j) {  // t <- t R^-1 (upper): column j uses t[0..j]
+                if (j >= k) continue;
+                double sj = 0.0;
+#pragma unroll
+                for (int l = 0; l <= j; ++l) sj += t[l] * ri[l + j * k];
+                t[j] = sj;
             }
-            __syncthreads();
-            src = tt;
         }
 #pragma unroll
-        for (int s = 0; s < 2; ++s)
-            if (own[s]) {
-                double a = acc[s];
-                for (int r = 0; r < kTile; ++r) a += src[r][ep[s]] * src[r][eq[s]];
-                acc[s] = a;
-            }
-    }
-    double* G = Gpart + static_cast<size_t>(blockIdx.x) * k * k;
-    for (int s = 0; s < 2; ++s)
-        if (own[s]) {
-            G[ep[s] + eq[s] * k] = acc[s];
-            G[eq[s] + ep[s] * k] = acc[s];
+        for (int j = 0; j < kMaxK; ++j)
+            if (j < k) tl[lane][j] = t[j];
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < kMaxEnt; ++s) {
+            if (lane + 32 * s >= ne) break;
+            double a = acc[s];
+            for (int rr = 0; rr < 32; ++rr) a += tl[rr][ep[s]] * tl[rr][eq[s]];
+            acc[s] = a;
         }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int s = 0; s < kMaxEnt; ++s)
+        if (lane + 32 * s < ne) wsum[warp][lane + 32 * s] = acc[s];
+    __syncthreads();
+    double* G = Gpart + static_cast<size_t>(blockIdx.x) * k * k;
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+        double v = wsum[0][e];
+        for (int w = 1; w < kGramW; ++w) v += wsum[w][e];
+        int q = 0, base = 0;
+        while (base + q + 1 <= e) {
+            base += q + 1;
+            ++q;
+        }
+        const int p0 = e - base;
+        G[p0 + q * k] = v;
+        G[q + p0 * k] = v;
+    }
 }
 
 // One warp: G = sum of the parts (in part order), R = chol(G) upper, Rinv =
@@ -184,7 +205,7 @@ __global__ void __launch_bounds__(32) chol_small_kernel(const double* Gpart, int
 
 void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q) {
     ProfScope prof(c, kProfTsqr);
-    const unsigned grid = static_cast<unsigned>(c.num_sms);
+    const unsigned grid = static_cast<unsigned>(c.num_sms) * 4;
     block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, nullptr, q.gpart, q.disabled);
     chol_small_kernel<<<1, 32, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, q.R1, q.R1inv, nullptr, nullptr,
                                               q.flag, 1, q.disabled);

@@ -1,0 +1,103 @@
+"""Race and ordering stress for the hand-rolled synchronization.
+
+compute-sanitizer is closed on this GPU pool (profiles/round2_compute_sanitizer_closed.txt),
+so the TMA/mbarrier stage rings, the per-pair / per-team named barriers and the
+fixed-order reductions are stressed here instead: every pass variant runs many
+times on inputs large enough that each CTA's stage ring wraps hundreds of times
+(the mbarrier parity must never run ahead -- the ABA bug fixed in round 1), at
+several stage geometries, and must give the SAME BITS every time and agree
+with a torch fp64 reference.  A race or a missed barrier shows up as a
+run-to-run difference or a wrong value.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+REPEATS = 12
+
+
+def _ptr(t):
+    import ctypes as C
+
+    return C.c_void_p(t.data_ptr())
+
+
+@pytest.mark.parametrize("b,n,env", [
+    (1, 1000, {}),                                  # apply_self (one-pass, TMA) at C2's n
+    (1, 1000, {"MSVD_ROWS_STAGE_KB": "16"}),
+    (2, 1000, {}),                                  # warp-pair one-pass
+    (2, 1000, {"MSVD_PAIR_STAGE_KB": "16"}),
+    (4, 500, {}),                                   # warp-pair one-pass at b = 4
+    (4, 500, {"MSVD_ONEPASS_KERNEL": "team"}),      # the team form (opt-in)
+    (3, 501, {}),
+])
+def test_one_pass_pass_repeatable(msvd, cuda, b, n, env, monkeypatch):
+    """msvd_aw_gram: AW = A W and Z = A^T A W from one sweep."""
+    import torch
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    m = 300_000 if n <= 600 else 150_000
+    ldp = n + (n & 1)  # even leading dimension: the TMA row stream
+    g = torch.Generator(device=cuda).manual_seed(n + b)
+    full = torch.randn(m, ldp, dtype=torch.float64, device=cuda, generator=g)
+    a = full[:, :n]
+    w = torch.randn(n, b, dtype=torch.float64, device=cuda, generator=g)
+    op = msvd.DeviceDenseOperator(a)
+    op.ctx.kernel_paths(reset=True)
+    aw0, z0 = op.aw_gram(w)
+    paths = op.ctx.kernel_paths()
+    for _ in range(REPEATS):
+        aw, z = op.aw_gram(w)
+        assert torch.equal(aw, aw0) and torch.equal(z, z0), paths
+    aw_ref = a @ w
+    z_ref = a.t() @ aw_ref
+    assert torch.allclose(aw0, aw_ref, rtol=0, atol=1e-10 * aw_ref.abs().max().item())
+    assert torch.allclose(z0, z_ref, rtol=0, atol=1e-10 * z_ref.abs().max().item())
+    print(f"[b={b} n={n} {env}] paths {sorted(paths)}: {REPEATS + 1} identical runs")
+
+
+@pytest.mark.parametrize("b,n,env", [(1, 1000, {}), (1, 999, {}), (5, 2000, {}), (8, 700, {}),
+                                     (1, 1000, {"MSVD_STAGE_KB": "8"})])
+def test_apply_and_gram_repeatable(msvd, cuda, b, n, env, monkeypatch):
+    """The plain A W pass (producer-warp rows kernel, ticket kernel) and the
+    K2 gram pass, odd and even leading dimensions."""
+    import torch
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    m = 120_000
+    g = torch.Generator(device=cuda).manual_seed(3 * n + b)
+    a = torch.randn(m, n, dtype=torch.float64, device=cuda, generator=g)
+    w = torch.randn(n, b, dtype=torch.float64, device=cuda, generator=g)
+    y = torch.randn(m, b, dtype=torch.float64, device=cuda, generator=g)
+    op = msvd.DeviceDenseOperator(a)
+    y0 = op.apply_block(w).clone()
+    x0 = op.apply_adjoint_block(y).clone()
+    for _ in range(REPEATS):
+        assert torch.equal(op.apply_block(w), y0)
+        assert torch.equal(op.apply_adjoint_block(y), x0)
+    assert torch.allclose(y0, a @ w, rtol=0, atol=1e-10 * (a @ w).abs().max().item())
+    xr = a.t() @ y
+    assert torch.allclose(x0, xr, rtol=0, atol=1e-10 * xr.abs().max().item())
+
+
+@pytest.mark.parametrize("name,shape", [("c2", dict(m=60_000, n=1000)), ("c5", dict(m=60_000, n=1000)),
+                                        ("c4", dict(m=60_000, n=500))])
+def test_whole_solve_repeatable(msvd, cuda, name, shape):
+    """Complete solves (the one-pass loop with the check refresh -- the
+    pair-EX and team-EX passes --, the trial-block QR, the preconditioner
+    route): the same record and vectors, bit for bit, on every repeat."""
+    from paper_2602_16797_b200 import problems
+
+    cfg = problems.CONFIGS[name].scaled(**shape)
+    a, _ = problems.make_problem_gpu(cfg.m, cfg.n, cfg.spectrum(), device=cuda)
+    opts = msvd.SolverOptions(seed=problems.SOLVER_SEED, sketch_dim=cfg.d, tol=cfg.tol, block_size=cfg.b,
+                              use_stagnation=False, record_timing=False, max_iter=40)
+    op = msvd.DeviceDenseOperator(a)
+    r0 = msvd.rlobpcg_block(op, opts)
+    for _ in range(3):
+        r = msvd.rlobpcg_block(op, opts)
+        assert r.record.to_csv() == r0.record.to_csv()
+        assert np.array_equal(r.v, r0.v) and np.array_equal(r.sigma, r0.sigma)

@@ -64,23 +64,6 @@ def test_sketch_bit_exact(msvd, cuda, port, m, n, d, zeta, ld_pad):
     assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("m,n,d", [(20_000, 1000, 4000), (5000, 130, 520), (3000, 65, 260)])
-def test_sketch_async_gather_bit_exact(msvd, cuda, port, m, n, d, monkeypatch):
-    """The cp.async column-slice gather (MSVD_SKETCH_ASYNC) gives the same
-    bits as the reference's sketch_apply, like the register gather."""
-    import torch
-
-    rng = np.random.default_rng(m + 7 * n)
-    a = _rand(rng, m, n)
-    dev = torch.from_numpy(a).to(cuda)
-    op = msvd.DeviceDenseOperator(dev)
-    want = port.sketch_apply(a, d, 4, 99)
-    monkeypatch.setenv("MSVD_SKETCH_ASYNC", "1")
-    sa = torch.empty((n, d), dtype=torch.float64, device=cuda)
-    msvd.check(msvd.lib().msvd_sketch(op.handle, d, 4, 99, _ptr(sa)))
-    assert np.array_equal(sa.cpu().numpy().T, want)
-
-
 def test_sketch_rejects_nonfinite(msvd, cuda):
     import torch
 
