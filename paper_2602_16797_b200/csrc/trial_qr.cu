@@ -108,93 +108,93 @@ __global__ void __launch_bounds__(kGramT) block_gram_kernel(Cols T, int64_t m, i
     }
 }
 
-// One warp: G = sum of the parts (in part order), R = chol(G) upper, Rinv =
-// R^-1; pass 2 also R_final = R Rprev.  flag: pass 1 writes success (both
-// pivots finite and positive, diag(R) within 1e6); pass 2 ands its own.
-__global__ void __launch_bounds__(32) chol_small_kernel(const double* Gpart, int nparts, int k, double* Rout,
-                                                        double* Rinv, const double* Rprev, double* Rfinal, int* flag,
-                                                        int pass, int* disabled) {
+// G = sum of the parts (in part order; a thread per entry), R = chol(G)
+// upper (warp 0, lane = column), Rinv = R^-1 (lane = column, back
+// substitution through shared memory); pass 2 also R_final = R Rprev.
+// flag: pass 1 writes success (pivots finite and positive, diag(R) within
+// 1e6); pass 2 ands its own.
+__global__ void __launch_bounds__(256) chol_small_kernel(const double* Gpart, int nparts, int k, double* Rout,
+                                                         double* Rinv, const double* Rprev, double* Rfinal,
+                                                         int* flag, int pass, int* disabled) {
     if (*disabled) {  // an earlier iteration's block was too ill-conditioned: TSQR from here on
         if (threadIdx.x == 0) *flag = 0;
         return;
     }
     __shared__ double G[kMaxK * kMaxK];
     __shared__ double R[kMaxK * kMaxK];
-    const int lane = threadIdx.x;
-    for (int e = lane; e < k * k; e += 32) {
+    __shared__ double X[kMaxK * kMaxK];
+    __shared__ int ok_s;
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
         double s = 0.0;
         for (int p = 0; p < nparts; ++p) s += Gpart[static_cast<size_t>(p) * k * k + e];
         G[e] = s;
     }
-    __syncwarp();
-    // lane l owns column l of R (rows 0..l)
-    double col[kMaxK];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+        // lane l owns column l of R (rows 0..l)
+        double col[kMaxK];
 #pragma unroll
-    for (int i = 0; i < kMaxK; ++i) col[i] = 0.0;
-    bool ok = true;
-    double dmax = 0.0, dmin = 1e300;
+        for (int i = 0; i < kMaxK; ++i) col[i] = 0.0;
+        bool ok = true;
+        double dmax = 0.0, dmin = 1e300;
 #pragma unroll
-    for (int j = 0; j < kMaxK; ++j) {
-        if (j >= k) break;
-        // pivot: lane j
-        double d = 0.0;
-        if (lane == j) {
-            double s = G[j + j * k];
+        for (int j = 0; j < kMaxK; ++j) {
+            if (j >= k) break;
+            double d = 0.0;
+            if (lane == j) {
+                double s = G[j + j * k];
+#pragma unroll
+                for (int i = 0; i < kMaxK; ++i)
+                    if (i < j) s -= col[i] * col[i];
+                d = s > 0.0 ? sqrt(s) : 0.0;
+                col[j] = d;
+            }
+            d = __shfl_sync(0xffffffffu, d, j);
+            if (!(d > 0.0) || !isfinite(d)) ok = false;
+            dmax = fmax(dmax, d);
+            dmin = fmin(dmin, d);
+            // R(j, l) for l > j: (G(j, l) - sum_i<j R(i, j) R(i, l)) / d
+            double s = (lane > j && lane < k) ? G[j + lane * k] : 0.0;
+#pragma unroll
+            for (int i = 0; i < kMaxK; ++i) {
+                if (i >= j) break;
+                const double rij = __shfl_sync(0xffffffffu, col[i], j);
+                s -= rij * col[i];
+            }
+            if (lane > j && lane < k) col[j] = d > 0.0 ? s / d : 0.0;
+        }
+        if (dmin < 1e-6 * dmax) ok = false;
+        if (lane < k)
 #pragma unroll
             for (int i = 0; i < kMaxK; ++i)
-                if (i < j) s -= col[i] * col[i];
-            d = s > 0.0 ? sqrt(s) : 0.0;
-            col[j] = d;
-        }
-        d = __shfl_sync(0xffffffffu, d, j);
-        if (!(d > 0.0) || !isfinite(d)) ok = false;
-        dmax = fmax(dmax, d);
-        dmin = fmin(dmin, d);
-        // R(j, l) for l > j: (G(j, l) - sum_i<j R(i, j) R(i, l)) / d
-        double s = (lane > j && lane < k) ? G[j + lane * k] : 0.0;
-#pragma unroll
-        for (int i = 0; i < kMaxK; ++i) {
-            if (i >= j) break;
-            const double rij = __shfl_sync(0xffffffffu, col[i], j);
-            s -= rij * col[i];
-        }
-        if (lane > j && lane < k) col[j] = d > 0.0 ? s / d : 0.0;
+                if (i < k) R[i + lane * k] = (ok ? (i <= lane ? col[i] : 0.0) : (i == lane ? 1.0 : 0.0));
+        if (lane == 0) ok_s = ok ? 1 : 0;  // not ok: identity factors keep everything finite
     }
-    if (dmin < 1e-6 * dmax) ok = false;
-    if (lane < k)
-        for (int i = 0; i < kMaxK; ++i)
-            if (i < k) R[i + lane * k] = i <= lane ? col[i] : 0.0;
-    __syncwarp();
-    if (!ok) {  // keep everything finite: identity factors (the TSQR path takes over)
-        for (int e = lane; e < k * k; e += 32) {
-            const double v = (e % k == e / k) ? 1.0 : 0.0;
-            R[e] = v;
-        }
-        __syncwarp();
-    }
+    __syncthreads();
     if (Rout)
-        for (int e = lane; e < k * k; e += 32) Rout[e] = R[e];
-    // Rinv column lane: back substitution R x = e_lane
-    if (lane < k) {
-        double x[kMaxK];
-#pragma unroll
-        for (int i = 0; i < kMaxK; ++i) x[i] = 0.0;
-        for (int i = lane; i >= 0; --i) {
-            double s = (i == lane) ? 1.0 : 0.0;
-            for (int l = i + 1; l <= lane; ++l) s -= R[i + l * k] * x[l];
-            x[i] = s / R[i + i * k];
+        for (int e = threadIdx.x; e < k * k; e += blockDim.x) Rout[e] = R[e];
+    // Rinv column c = threadIdx.x: back substitution R x = e_c, x kept in X (shared)
+    if (threadIdx.x < k) {
+        const int cidx = threadIdx.x;
+        for (int i = k - 1; i >= 0; --i) {
+            double s = (i == cidx) ? 1.0 : 0.0;
+            if (i <= cidx)
+                for (int l = i + 1; l <= cidx; ++l) s -= R[i + l * k] * X[l + cidx * k];
+            X[i + cidx * k] = i <= cidx ? s / R[i + i * k] : 0.0;
         }
-        for (int i = 0; i < k; ++i) Rinv[i + lane * k] = i <= lane ? x[i] : 0.0;
     }
-    if (pass == 2 && lane < k) {  // R_final(:, lane) = R Rprev(:, lane)
-        for (int i = 0; i < k; ++i) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) Rinv[e] = X[e];
+    if (pass == 2)  // R_final = R Rprev (both upper)
+        for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+            const int i = e % k, c = e / k;
             double s = 0.0;
-            for (int l = i; l <= lane; ++l) s += R[i + l * k] * Rprev[l + lane * k];
-            Rfinal[i + lane * k] = i <= lane ? s : 0.0;
+            for (int l = i; l <= c; ++l) s += R[i + l * k] * Rprev[l + c * k];
+            Rfinal[e] = i <= c ? s : 0.0;
         }
-    }
-    if (lane == 0) {
-        *flag = pass == 1 ? (ok ? 1 : 0) : ((*flag && ok) ? 1 : 0);
+    if (threadIdx.x == 0) {
+        *flag = pass == 1 ? ok_s : ((*flag && ok_s) ? 1 : 0);
         // sticky: once a trial block needs the TSQR, the later ones (whose
         // conditioning only grows as the iteration converges) skip straight to it
         if (pass == 2 && !*flag) *disabled = 1;
@@ -207,11 +207,11 @@ void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q) {
     ProfScope prof(c, kProfTsqr);
     const unsigned grid = static_cast<unsigned>(c.num_sms) * 4;
     block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, nullptr, q.gpart, q.disabled);
-    chol_small_kernel<<<1, 32, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, q.R1, q.R1inv, nullptr, nullptr,
-                                              q.flag, 1, q.disabled);
+    chol_small_kernel<<<1, 256, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, q.R1, q.R1inv, nullptr, nullptr,
+                                               q.flag, 1, q.disabled);
     block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, q.R1inv, q.gpart, q.disabled);
-    chol_small_kernel<<<1, 32, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, nullptr, q.R2inv, q.R1, q.R,
-                                              q.flag, 2, q.disabled);
+    chol_small_kernel<<<1, 256, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, nullptr, q.R2inv, q.R1, q.R,
+                                               q.flag, 2, q.disabled);
     MSVD_CUDA(cudaGetLastError());
     c.launches += 4;
 }
