@@ -140,31 +140,34 @@ bool pair_ok(const Ctx& c, const StreamGeom& g0, int b, bool ex) {
 // b = 1 pass that also accumulates A^T e for an m-vector e: gpart[grid][2][n]
 // = [A_cta^T (A_cta w), A_cta^T e_cta] (the one-pass check refresh)
 // team geometry: stages a multiple of the team count
-int team_pl(int n) {
-    const int part = ((n + 1) / 2 + kTeam - 1) / kTeam;
+int team_pl(int n, int T) {
+    const int part = ((n + 1) / 2 + T - 1) / T;
     const int pl = (part + 31) / 32;
     return pl <= 2 ? 2 : (pl <= 4 ? 4 : (pl <= 8 ? 8 : 16));
 }
 // kTeamRows rows per stage (one team barrier per stage), as many stages per
-// team as the shared memory holds
-StreamGeom team_geom(const Ctx& c, StreamGeom g) {
+// team as the shared memory holds; 8 / T teams per CTA
+StreamGeom team_geom(const Ctx& c, StreamGeom g, int T) {
     const int64_t row_bytes = static_cast<int64_t>(g.ld_s) * 8;
+    const int teams = 8 / T;
     g.rc = kTeamRows;
     g.stage_bytes = ((static_cast<size_t>(g.rc) * row_bytes + 127) / 128) * 128;
-    const int64_t xbytes = sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 4;  // b <= 4
+    const int64_t xbytes = sizeof(double) * 2 * 8 * kTeamRows * 4;  // [team][buffer][member][row][b <= 4]
     const int64_t avail = static_cast<int64_t>(c.smem_optin) - 2048 - xbytes;
     const int64_t per_team =
-        std::max<int64_t>(2, std::min<int64_t>(8, avail / ((8 / kTeam) * static_cast<int64_t>(g.stage_bytes))));
-    g.stages = static_cast<int32_t>((8 / kTeam) * per_team);
+        std::max<int64_t>(2, std::min<int64_t>(8, avail / (teams * static_cast<int64_t>(g.stage_bytes))));
+    g.stages = static_cast<int32_t>(teams * per_team);
     return g;
 }
-bool team_ok(const Ctx& c, const StreamGeom& g0, int b) {
+// T = 4 (quarter rows) carries the check refresh's 2b accumulators; T = 2
+// (half rows) the plain one-pass pass's b
+bool team_ok(const Ctx& c, const StreamGeom& g0, int b, int T) {
     if (!g0.tma || b < 2 || b > 4 || std::getenv("MSVD_NO_PAIR")) return false;
-    if (b * team_pl(g0.n) > 8) return false;  // b = 2 to n = 1024, b = 3, 4 to n = 512
-    const StreamGeom g = team_geom(c, g0);
-    const size_t xbytes = sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 4;
+    if (b * team_pl(g0.n, T) > (T == 4 ? 8 : 16)) return false;
+    const StreamGeom g = team_geom(c, g0, T);
+    const size_t xbytes = sizeof(double) * 2 * 8 * kTeamRows * 4;
     if (g.stages * g.stage_bytes + bar_bytes(g.stages) + xbytes + 1024 > c.smem_optin) return false;
-    return sizeof(double) * (8 / kTeam) * 2 * b * g0.n <= static_cast<size_t>(g.stages) * g.stage_bytes;
+    return sizeof(double) * (8 / T) * (T == 4 ? 2 : 1) * b * g0.n <= static_cast<size_t>(g.stages) * g.stage_bytes;
 }
 
 
@@ -203,7 +206,7 @@ bool apply_gram_supported(const Ctx& c, const StreamGeom& g, int b, const TsqrFu
 }
 
 bool apply_ex_supported(const Ctx& c, const StreamGeom& g, int b) {
-    return b == 1 ? pair_ok(c, g, 1, true) : team_ok(c, g, b);
+    return b == 1 ? pair_ok(c, g, 1, true) : team_ok(c, g, b, kTeam);
 }
 
 bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out, const double* ex,
@@ -217,7 +220,7 @@ bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, int b, OutCol
     if (b >= 2) {
         Cols ec{};
         for (int j = 0; j < b; ++j) ec.p[j] = ex + j * ld_ex;
-        launch_team_ex(c, ApplyArgs{team_geom(c, g), W, out, TsqrFuse{}, gpart, nullptr}, ec, b);
+        launch_team_ex(c, ApplyArgs{team_geom(c, g, kTeam), W, out, TsqrFuse{}, gpart, nullptr}, ec, b);
         return false;
     }
     (void)fuse;  // the b = 1 refresh pass runs the TSQR separately
@@ -234,14 +237,15 @@ bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
     ProfScope prof(c, kProfApply);
     TsqrFuse none{};
     if (try_apply_rows(c, ApplyArgs{g, W, out, fuse ? *fuse : none, gpart, nullptr}, b)) return fuse != nullptr;
-    // one-pass in the team form (four warps per row, four rows per barrier):
-    // opt-in, MSVD_ONEPASS_KERNEL = team.  Measured at C4 (b = 4, n = 500) it
-    // is slower than the warp-pair kernel (13.8 vs 12.9 ms of passes), and equal
-    // at C5 (b = 2)
+    // one-pass in the team form, four rows per barrier and one
+    // transpose-reduce per four rows (MSVD_ONEPASS_KERNEL = pair | team4 |
+    // team2 for measurement).  team4 (quarter rows) measured slower than the
+    // warp-pair kernel at C4 (13.8 vs 12.9 ms of passes) and equal at C5
     const char* ok_env = std::getenv("MSVD_ONEPASS_KERNEL");
-    const bool want_team = ok_env && std::string(ok_env) == "team";
-    if (gpart && want_team && team_ok(c, g, b)) {
-        launch_team(c, ApplyArgs{team_geom(c, g), W, out, none, gpart, nullptr}, b);
+    const std::string okk = ok_env ? ok_env : "";
+    const int team_t = okk == "team4" ? 4 : (okk == "team2" ? 2 : 0);
+    if (gpart && team_t && team_ok(c, g, b, team_t)) {
+        launch_team(c, ApplyArgs{team_geom(c, g, team_t), W, out, none, gpart, nullptr}, b, team_t);
         return false;
     }
     if (gpart && pair_ok(c, g, b, false)) {  // one-pass, rows split over warp pairs (no fused TSQR)

@@ -147,9 +147,9 @@ bool rows_ok(const Ctx& c, const StreamGeom& g0, int b, const TsqrFuse* ts, bool
 int pair_pl(int n);
 StreamGeom pair_geom(const Ctx& c, StreamGeom g);
 bool pair_ok(const Ctx& c, const StreamGeom& g0, int b, bool ex);
-int team_pl(int n);
-StreamGeom team_geom(const Ctx& c, StreamGeom g);
-bool team_ok(const Ctx& c, const StreamGeom& g0, int b);
+int team_pl(int n, int T = kTeam);
+StreamGeom team_geom(const Ctx& c, StreamGeom g, int T = kTeam);
+bool team_ok(const Ctx& c, const StreamGeom& g0, int b, int T = kTeam);
 
 // ---- kernel-family launchers ---------------------------------------------
 // stream_rows.cu: true if launched (the fused TSQR, when requested, too)
@@ -159,7 +159,7 @@ bool try_apply_rows(Ctx& c, const ApplyArgs& a0, int b);
 void launch_pair(Ctx& c, const ApplyArgs& a0, int b);
 void launch_pair_ex(Ctx& c, const ApplyArgs& a);
 void launch_team_ex(Ctx& c, const ApplyArgs& a, Cols ex, int b);
-void launch_team(Ctx& c, const ApplyArgs& a, int b);  // the plain one-pass pass in the team form
+void launch_team(Ctx& c, const ApplyArgs& a, int b, int T);  // the plain one-pass pass in the team form
 // stream_ticket.cu: the ticket A*W pass (any b <= 8) and the K2 gram pass
 void launch_ticket(Ctx& c, const ApplyArgs& a, int b);
 void launch_gram_b(Ctx& c, const GramArgs& a, int b);

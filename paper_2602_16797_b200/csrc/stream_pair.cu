@@ -437,27 +437,32 @@ void launch_pair_ex(Ctx& c, const ApplyArgs& a) {
     }
 }
 
-void launch_team(Ctx& c, const ApplyArgs& a, int b) {
-    const size_t sm = bar_bytes(a.g.stages) +
-                      128 * ((sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 4 + 127) / 128) +
+void launch_team(Ctx& c, const ApplyArgs& a, int b, int T) {
+    const size_t sm = bar_bytes(a.g.stages) + 128 * ((sizeof(double) * 2 * 8 * kTeamRows * 4 + 127) / 128) +
                       a.g.stages * a.g.stage_bytes;
     auto go = [&](auto kernel) {
         optin_smem(c, kernel);
         kernel<<<a.g.grid, 256, sm, c.stream>>>(a, Cols{});
     };
-    const int pl = team_pl(a.g.n);
-    if (b == 2 && pl <= 2) go(apply_team_ex_kernel<2, 2, kTeam, false>);
-    else if (b == 2) go(apply_team_ex_kernel<2, 4, kTeam, false>);
-    else if (b == 3) go(apply_team_ex_kernel<3, 2, kTeam, false>);
-    else go(apply_team_ex_kernel<4, 2, kTeam, false>);
+    const int pl = team_pl(a.g.n, T);
+    if (T == 4) {
+        if (b == 2 && pl <= 2) go(apply_team_ex_kernel<2, 2, 4, false>);
+        else if (b == 2) go(apply_team_ex_kernel<2, 4, 4, false>);
+        else if (b == 3) go(apply_team_ex_kernel<3, 2, 4, false>);
+        else go(apply_team_ex_kernel<4, 2, 4, false>);
+    } else {
+        if (b == 2 && pl <= 4) go(apply_team_ex_kernel<2, 4, 2, false>);
+        else if (b == 2) go(apply_team_ex_kernel<2, 8, 2, false>);
+        else if (b == 3) go(apply_team_ex_kernel<3, 4, 2, false>);
+        else go(apply_team_ex_kernel<4, 4, 2, false>);
+    }
     MSVD_CUDA(cudaGetLastError());
     ++c.launches;
     c.paths |= kPathTeam;
 }
 
 void launch_team_ex(Ctx& c, const ApplyArgs& a, Cols ec, int b) {
-    const size_t sm = bar_bytes(a.g.stages) +
-                      128 * ((sizeof(double) * (8 / kTeam) * 2 * kTeam * kTeamRows * 4 + 127) / 128) +
+    const size_t sm = bar_bytes(a.g.stages) + 128 * ((sizeof(double) * 2 * 8 * kTeamRows * 4 + 127) / 128) +
                       a.g.stages * a.g.stage_bytes;
     auto go = [&](auto kernel) {
         optin_smem(c, kernel);

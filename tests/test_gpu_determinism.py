@@ -29,7 +29,9 @@ def _ptr(t):
     (2, 1000, {}),                                  # warp-pair one-pass
     (2, 1000, {"MSVD_PAIR_STAGE_KB": "16"}),
     (4, 500, {}),                                   # warp-pair one-pass at b = 4
-    (4, 500, {"MSVD_ONEPASS_KERNEL": "team"}),      # the team form (opt-in)
+    (4, 500, {"MSVD_ONEPASS_KERNEL": "team4"}),     # the team forms: quarter rows
+    (4, 500, {"MSVD_ONEPASS_KERNEL": "team2"}),     # half rows, four rows per barrier
+    (2, 1000, {"MSVD_ONEPASS_KERNEL": "team2"}),
     (3, 501, {}),
 ])
 def test_one_pass_pass_repeatable(msvd, cuda, b, n, env, monkeypatch):
