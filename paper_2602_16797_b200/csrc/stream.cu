@@ -237,12 +237,15 @@ bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
     ProfScope prof(c, kProfApply);
     TsqrFuse none{};
     if (try_apply_rows(c, ApplyArgs{g, W, out, fuse ? *fuse : none, gpart, nullptr}, b)) return fuse != nullptr;
-    // one-pass in the team form, four rows per barrier and one
-    // transpose-reduce per four rows (MSVD_ONEPASS_KERNEL = pair | team4 |
-    // team2 for measurement).  team4 (quarter rows) measured slower than the
-    // warp-pair kernel at C4 (13.8 vs 12.9 ms of passes) and equal at C5
+    // one-pass in the team form: four rows per barrier and one
+    // transpose-reduce per four rows.  b >= 3: half rows (T = 2), measured at
+    // C4 (b = 4, n = 500) 10.2 ms of passes against 12.8 for the warp-pair
+    // kernel's row-at-a-time barrier and butterflies (0.69 vs 0.55 of the copy
+    // peak; the plain passes alone 5.7 TB/s); quarter rows (T = 4) were slower
+    // (13.8), and at b = 2 (C5) the pair kernel stays ahead (877 vs 890 ms).
+    // MSVD_ONEPASS_KERNEL = pair | team2 | team4 overrides, for measurement.
     const char* ok_env = std::getenv("MSVD_ONEPASS_KERNEL");
-    const std::string okk = ok_env ? ok_env : "";
+    const std::string okk = ok_env ? ok_env : (b >= 3 ? "team2" : "pair");
     const int team_t = okk == "team4" ? 4 : (okk == "team2" ? 2 : 0);
     if (gpart && team_t && team_ok(c, g, b, team_t)) {
         launch_team(c, ApplyArgs{team_geom(c, g, team_t), W, out, none, gpart, nullptr}, b, team_t);

@@ -28,7 +28,8 @@ def _ptr(t):
     (1, 1000, {"MSVD_ROWS_STAGE_KB": "16"}),
     (2, 1000, {}),                                  # warp-pair one-pass
     (2, 1000, {"MSVD_PAIR_STAGE_KB": "16"}),
-    (4, 500, {}),                                   # warp-pair one-pass at b = 4
+    (4, 500, {}),                                   # team (half rows) one-pass at b = 4
+    (4, 500, {"MSVD_ONEPASS_KERNEL": "pair"}),      # the warp-pair kernel at b = 4
     (4, 500, {"MSVD_ONEPASS_KERNEL": "team4"}),     # the team forms: quarter rows
     (4, 500, {"MSVD_ONEPASS_KERNEL": "team2"}),     # half rows, four rows per barrier
     (2, 1000, {"MSVD_ONEPASS_KERNEL": "team2"}),

@@ -31,8 +31,8 @@ CASES = [
 ]
 
 # kernel variants each team case must reach (msvd_ctx_kernel_paths)
-EXPECT_PATHS = {(4000, 1000, 2): {"team_ex"}, (3000, 501, 3): {"team_ex"}, (4000, 481, 4): {"team_ex"},
-                (3000, 511, 4): {"team_ex"}, (9000, 600, 1): {"pair_ex"}, (6000, 520, 2): {"pair"}}
+EXPECT_PATHS = {(4000, 1000, 2): {"team_ex"}, (3000, 501, 3): {"team_ex", "team"}, (4000, 481, 4): {"team_ex", "team"},
+                (3000, 511, 4): {"team_ex", "team"}, (9000, 600, 1): {"pair_ex"}, (6000, 520, 2): {"pair"}}
 
 
 def spectrum(n, seed):
