@@ -210,66 +210,90 @@ __global__ void __launch_bounds__(kGatherT) gather_kernel(const double* A, int64
 // same pace, so the zeta readers of each A row-slice meet it in L2 within a
 // short window: A comes from HBM once instead of zeta times.  Same per-column
 // sequential __dmul_rn/__dadd_rn sums as gather_kernel -> the same bits.
-template <int kSliceCPL, int kSliceU>
-__global__ void __launch_bounds__(256, 4) gather_slice_kernel(const double* __restrict__ A, int64_t ld, int n,
-                                                           int64_t d, const int64_t* __restrict__ offs,
-                                                           const uint32_t* __restrict__ vals, double val,
-                                                           double* __restrict__ SA, DevState* st, int c0) {
+constexpr int kIdxCap = 1024;  // list entries staged per warp (4 KB)
+
+// Per entry and lane the inner loop is: the row index from a broadcast
+// shared-memory read (four entries per 16-byte read), one IMAD.WIDE per column
+// for the address (ld * 8 < 2^32, checked by the caller), the sign folded into
+// the high word of val, two loads, two mul + add.  The compiler's 64-bit
+// index arithmetic and shuffles had made it ~35 instructions per entry, and
+// the kernel issue-bound (ncu: one issue every 1.9 cycles per scheduler).
+template <int kU, int kMinB>
+__global__ void __launch_bounds__(256, kMinB) gather_slice_kernel(const double* __restrict__ A, uint32_t ld8, int n,
+                                                                 int64_t d, const int64_t* __restrict__ offs,
+                                                                 const uint32_t* __restrict__ vals, double val,
+                                                                 double* __restrict__ SA, DevState* st, int c0) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t s = static_cast<int64_t>(blockIdx.x) * 8 + warp;
     if (s >= d) return;
     const int64_t e0 = offs[s], e1 = offs[s + 1];
-    int col[kSliceCPL];
-    bool in[kSliceCPL];
+    // the lane's two columns (clamped to n - 1: loaded, result dropped)
+    const int colA = c0 + lane, colB = c0 + lane + 32;
+    const bool inA = colA < n, inB = colB < n;
+    const char* baseA = reinterpret_cast<const char*>(A + (inA ? colA : n - 1));
+    const char* baseB = reinterpret_cast<const char*>(A + (inB ? colB : n - 1));
+    const uint64_t vbits = static_cast<uint64_t>(__double_as_longlong(val));
+    double accA = 0.0, accB = 0.0;
+    // a non-finite entry of A makes its sums non-finite (sv = +-zeta^-1/2 is
+    // never 0), so the operator's finite check (operator.cpp:33-35) looks at
+    // the sums at the end and rescans elements only when one is not finite
+    // the warp's (source row, sign) list is staged in shared memory a piece at
+    // a time (one coalesced copy), so a batch's row indices come from shared
+    // memory and only the A loads are on its critical path
+    extern __shared__ __align__(16) uint32_t sidx_all[];  // [8 warps][kIdxCap]
+    uint32_t* sidx = sidx_all + warp * kIdxCap;
+    for (int64_t pb = e0; pb < e1; pb += kIdxCap) {
+        const int cnt = static_cast<int>(min(static_cast<int64_t>(kIdxCap), e1 - pb));
+        __syncwarp();
+        for (int i = lane; i < cnt; i += 32) sidx[i] = vals[pb + i];
+        __syncwarp();
+        int e = 0;
+        for (; e + kU <= cnt; e += kU) {
+            uint32_t v[kU];
 #pragma unroll
-    for (int q = 0; q < kSliceCPL; ++q) {
-        col[q] = c0 + lane + 32 * q;
-        in[q] = col[q] < n;
-        if (!in[q]) col[q] = n - 1;  // clamped load, result dropped
-    }
-    double acc[kSliceCPL];
-#pragma unroll
-    for (int q = 0; q < kSliceCPL; ++q) acc[q] = 0.0;
-    bool finite = true;
-    int64_t e = e0;
-    for (; e + kSliceU <= e1; e += kSliceU) {
-        // lane u < U fetches entry e+u; the row indices are then broadcast
-        const uint32_t mine = lane < kSliceU ? vals[e + lane] : 0u;
-        double x[kSliceU][kSliceCPL];
-        double sv[kSliceU];
-#pragma unroll
-        for (int u = 0; u < kSliceU; ++u) {
-            const uint32_t v = __shfl_sync(0xffffffffu, mine, u);
-            const int64_t r = v & 0x7fffffffu;
-            sv[u] = (v >> 31) ? -val : val;
-            const double* row = A + r * ld;
-#pragma unroll
-            for (int q = 0; q < kSliceCPL; ++q) x[u][q] = row[col[q]];
-        }
-#pragma unroll
-        for (int u = 0; u < kSliceU; ++u)
-#pragma unroll
-            for (int q = 0; q < kSliceCPL; ++q) {
-                acc[q] = __dadd_rn(acc[q], __dmul_rn(sv[u], x[u][q]));
-                finite = finite && isfinite(x[u][q]);
+            for (int u = 0; u < kU; u += 4) {
+                const uint4 q4 = *reinterpret_cast<const uint4*>(sidx + e + u);
+                v[u] = q4.x;
+                v[u + 1] = q4.y;
+                v[u + 2] = q4.z;
+                v[u + 3] = q4.w;
             }
-    }
-    for (; e < e1; ++e) {
-        const uint32_t v = vals[e];
-        const int64_t r = v & 0x7fffffffu;
-        const double svv = (v >> 31) ? -val : val;
-        const double* row = A + r * ld;
+            double xa[kU], xb[kU];
 #pragma unroll
-        for (int q = 0; q < kSliceCPL; ++q) {
-            const double xv = row[col[q]];
-            acc[q] = __dadd_rn(acc[q], __dmul_rn(svv, xv));
-            finite = finite && isfinite(xv);
+            for (int u = 0; u < kU; ++u) {
+                const uint64_t off = static_cast<uint64_t>(v[u] & 0x7fffffffu) * ld8;
+                xa[u] = __ldg(reinterpret_cast<const double*>(baseA + off));
+                xb[u] = __ldg(reinterpret_cast<const double*>(baseB + off));
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const double sv = __longlong_as_double(
+                    static_cast<long long>(vbits ^ (static_cast<uint64_t>(v[u] & 0x80000000u) << 32)));
+                accA = __dadd_rn(accA, __dmul_rn(sv, xa[u]));
+                accB = __dadd_rn(accB, __dmul_rn(sv, xb[u]));
+            }
+        }
+        for (; e < cnt; ++e) {
+            const uint32_t vv = sidx[e];
+            const uint64_t off = static_cast<uint64_t>(vv & 0x7fffffffu) * ld8;
+            const double sv =
+                __longlong_as_double(static_cast<long long>(vbits ^ (static_cast<uint64_t>(vv & 0x80000000u) << 32)));
+            accA = __dadd_rn(accA, __dmul_rn(sv, __ldg(reinterpret_cast<const double*>(baseA + off))));
+            accB = __dadd_rn(accB, __dmul_rn(sv, __ldg(reinterpret_cast<const double*>(baseB + off))));
         }
     }
-#pragma unroll
-    for (int q = 0; q < kSliceCPL; ++q)
-        if (in[q]) SA[s + static_cast<int64_t>(col[q]) * d] = acc[q];
-    if (!__all_sync(0xffffffffu, finite) && lane == 0 && st) atomicCAS(&st->err_code, 0, kErrNonfiniteA);
+    if (inA) SA[s + static_cast<int64_t>(colA) * d] = accA;
+    if (inB) SA[s + static_cast<int64_t>(colB) * d] = accB;
+    if (__all_sync(0xffffffffu, isfinite(accA) && isfinite(accB))) return;
+    // a non-finite sum: an element is non-finite, or finite ones overflowed
+    // (not an error of A) -- rescan this warp's elements to tell which
+    bool bad = false;
+    for (int64_t e = e0; e < e1; ++e) {
+        const uint64_t off = static_cast<uint64_t>(vals[e] & 0x7fffffffu) * ld8;
+        bad = bad || !isfinite(*reinterpret_cast<const double*>(baseA + off)) ||
+              !isfinite(*reinterpret_cast<const double*>(baseB + off));
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0 && st) atomicCAS(&st->err_code, 0, kErrNonfiniteA);
 }
 
 }  // namespace
@@ -363,21 +387,27 @@ void sketch_dev(Ctx& c, const StreamGeom& g, int64_t row0, int64_t d, int zeta, 
         return;
     }
     const SketchLists L = sketch_prepare(c, g.m, row0, d, zeta, seed, g.m);  // one chunk
-    if (std::getenv("MSVD_SKETCH_GATHER")) {  // one launch, A read zeta times
+    // one launch, A read zeta times (also for a row stride of 2^29 or more
+    // doubles, which the slice form's 32-bit byte offsets do not cover)
+    if (std::getenv("MSVD_SKETCH_GATHER") || g.ld * 8 > static_cast<int64_t>(UINT32_MAX)) {
         gather_kernel<<<static_cast<unsigned>(d), kGatherT, 0, c.stream>>>(g.A, g.ld, g.n, d, L.offs, L.vals, L.val,
                                                                            SA, st, g.tma);
         MSVD_CUDA(cudaGetLastError());
         ++c.launches;
         return;
     }
-    // measured (C2): 32 * 2 columns x 8 entries in flight per warp (the 1-, 4-
-    // and 8-pair variants were slower and spilled; a cp.async form landing the
-    // rows in a per-warp shared-memory ring, 6 x 8 entries ahead, took 8.0 ms
-    // instead of 3.9: removed)
+    // measured (C2, 16 slices): 2.5 ms with 2 columns x 8 entries in flight
+    // per lane and 4 CTAs per SM (every warp of a slice resident).  Slower,
+    // and removed: 16 entries in flight or 3 CTAs per SM (a second wave;
+    // 3.9 / 4.7 ms), L2 prefetch of the rows 16-32 entries ahead (3.7 ms), a
+    // cp.async ring of rows in shared memory (8.0 ms), and pacing the warps so
+    // the zeta readers of a row-slice meet in L2 (DRAM 1.77x -> 1.18x the
+    // algorithmic bytes, but 2.5 -> 8.9 ms: the fast warps idle)
     const int slice = 64;
     const unsigned grid = static_cast<unsigned>(ceil_div(d, 8));
     for (int c0 = 0; c0 < g.n; c0 += slice) {
-        gather_slice_kernel<2, 8><<<grid, 256, 0, c.stream>>>(g.A, g.ld, g.n, d, L.offs, L.vals, L.val, SA, st, c0);
+        gather_slice_kernel<8, 4><<<grid, 256, sizeof(uint32_t) * 8 * kIdxCap, c.stream>>>(
+            g.A, static_cast<uint32_t>(g.ld * 8), g.n, d, L.offs, L.vals, L.val, SA, st, c0);
         MSVD_CUDA(cudaGetLastError());
         ++c.launches;
     }

@@ -23,13 +23,14 @@ namespace {
 constexpr int kGramT = 128;    // threads per CTA (4 warps; static shared memory)
 constexpr int kGramW = kGramT / 32;
 constexpr int kMaxEnt = (kMaxK * (kMaxK + 1) / 2 + 31) / 32;  // Gram entries per lane (<= 10)
+constexpr int kCholT = 512;    // chol_small_kernel threads
 
 // Gpart[cta] (k x k, col-major, full) = sum over the CTA's rows of t t^T with
 // t = the row of T (times Rinv, upper k x k, when given).  Each warp streams
 // its own contiguous rows in 32-row tiles with no CTA barrier: lane = row for
 // the loads (coalesced per column) and the R^-1 transform, then the tile goes
 // through the warp's shared-memory slot and lane e sums the Gram entries e,
-// e + 32, ... over the tile's rows; the 8 warp partials are added in warp
+// e + 32, ... over the tile's rows; the 4 warp partials are added in warp
 // order at the end (deterministic).  Four CTAs per SM.
 __global__ void __launch_bounds__(kGramT) block_gram_kernel(Cols T, int64_t m, int k, const double* Rinv,
                                                            double* Gpart, const int* disabled) {
@@ -108,14 +109,14 @@ __global__ void __launch_bounds__(kGramT) block_gram_kernel(Cols T, int64_t m, i
     }
 }
 
-// G = sum of the parts (in part order; a thread per entry), R = chol(G)
+// G = sum of the parts (fixed order, below), R = chol(G)
 // upper (warp 0, lane = column), Rinv = R^-1 (lane = column, back
 // substitution through shared memory); pass 2 also R_final = R Rprev.
 // flag: pass 1 writes success (pivots finite and positive, diag(R) within
 // 1e6); pass 2 ands its own.
-__global__ void __launch_bounds__(256) chol_small_kernel(const double* Gpart, int nparts, int k, double* Rout,
-                                                         double* Rinv, const double* Rprev, double* Rfinal,
-                                                         int* flag, int pass, int* disabled) {
+__global__ void __launch_bounds__(kCholT) chol_small_kernel(const double* Gpart, int nparts, int k, double* Rout,
+                                                            double* Rinv, const double* Rprev, double* Rfinal,
+                                                            int* flag, int pass, int* disabled) {
     if (*disabled) {  // an earlier iteration's block was too ill-conditioned: TSQR from here on
         if (threadIdx.x == 0) *flag = 0;
         return;
@@ -124,10 +125,46 @@ __global__ void __launch_bounds__(256) chol_small_kernel(const double* Gpart, in
     __shared__ double R[kMaxK * kMaxK];
     __shared__ double X[kMaxK * kMaxK];
     __shared__ int ok_s;
-    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-        double s = 0.0;
-        for (int p = 0; p < nparts; ++p) s += Gpart[static_cast<size_t>(p) * k * k + e];
-        G[e] = s;
+    // G = sum of the parts: a warp per upper entry (four entries at a time,
+    // independent loads in flight), lane l adds parts l, l + 32, ... in order,
+    // then a fixed butterfly -- deterministic, and ~nparts / 32 dependent
+    // loads per lane instead of nparts (a thread per entry took ~70 us at
+    // 592 parts)
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        const int ne = k * (k + 1) / 2;
+        const size_t kk = static_cast<size_t>(k) * k;
+        for (int e0 = warp; e0 < ne; e0 += 4 * nw) {
+            int pq[4][2];
+            double acc[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * nw;
+                int q = 0, base = 0;
+                if (e < ne)
+                    while (base + q + 1 <= e) {  // column q holds entries base .. base + q
+                        base += q + 1;
+                        ++q;
+                    }
+                pq[u][0] = e < ne ? e - base : -1;
+                pq[u][1] = q;
+                acc[u] = 0.0;
+            }
+            for (int p = lane; p < nparts; p += 32) {
+                const double* Gp = Gpart + p * kk;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (pq[u][0] >= 0) acc[u] += Gp[pq[u][0] + pq[u][1] * k];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double t = warp_sum(acc[u]);
+                if (lane == 0 && pq[u][0] >= 0) {
+                    G[pq[u][0] + pq[u][1] * k] = t;
+                    G[pq[u][1] + pq[u][0] * k] = t;
+                }
+            }
+        }
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -207,10 +244,10 @@ void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q) {
     ProfScope prof(c, kProfTsqr);
     const unsigned grid = static_cast<unsigned>(c.num_sms) * 4;
     block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, nullptr, q.gpart, q.disabled);
-    chol_small_kernel<<<1, 256, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, q.R1, q.R1inv, nullptr, nullptr,
+    chol_small_kernel<<<1, kCholT, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, q.R1, q.R1inv, nullptr, nullptr,
                                                q.flag, 1, q.disabled);
     block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, q.R1inv, q.gpart, q.disabled);
-    chol_small_kernel<<<1, 256, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, nullptr, q.R2inv, q.R1, q.R,
+    chol_small_kernel<<<1, kCholT, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, nullptr, q.R2inv, q.R1, q.R,
                                                q.flag, 2, q.disabled);
     MSVD_CUDA(cudaGetLastError());
     c.launches += 4;

@@ -75,6 +75,43 @@ def test_sketch_rejects_nonfinite(msvd, cuda):
         msvd.check(msvd.lib().msvd_sketch(op.handle, 80, 4, 1, _ptr(sa)))
 
 
+def test_sketch_overflow_is_not_a_nonfinite_a(msvd, cuda, port):
+    """Finite entries whose sums overflow are not an error of A (the check is
+    on A's elements, operator.cpp:33-35): SA carries the infinities, the same
+    ones sketch_apply computes."""
+    import torch
+
+    rng = np.random.default_rng(5)
+    a = rng.choice([-1.0, 1.0], size=(4000, 70)) * 1.5e308
+    dev = torch.from_numpy(a).to(cuda)
+    op = msvd.DeviceDenseOperator(dev)
+    sa = torch.empty((70, 100), dtype=torch.float64, device=cuda)
+    msvd.check(msvd.lib().msvd_sketch(op.handle, 100, 4, 3, _ptr(sa)))
+    got = sa.cpu().numpy().T
+    with np.errstate(over="ignore", invalid="ignore"):
+        want = port.sketch_apply(a, 100, 4, 3)
+    assert not np.all(np.isfinite(want))
+    assert np.array_equal(got, want, equal_nan=True)
+
+
+@pytest.mark.parametrize("env", [{}, {"MSVD_SKETCH_GATHER": "1"}])
+def test_sketch_variants_bit_exact(msvd, cuda, port, env, monkeypatch):
+    """The slice gather (entry batches, a ragged tail per list) and the
+    one-launch gather: the same bits."""
+    import torch
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(11)
+    m, n, d = 30_000, 150, 600
+    a = _rand(rng, m, n)
+    dev = torch.from_numpy(a).to(cuda)
+    op = msvd.DeviceDenseOperator(dev)
+    sa = torch.empty((n, d), dtype=torch.float64, device=cuda)
+    msvd.check(msvd.lib().msvd_sketch(op.handle, d, 4, 99, _ptr(sa)))
+    assert np.array_equal(sa.cpu().numpy().T, port.sketch_apply(a, d, 4, 99))
+
+
 # ------------------------------------------------------- A passes (K2 / K3)
 @pytest.mark.parametrize("m,n,b", [(1, 1, 1), (7, 3, 1), (1000, 100, 1), (4097, 257, 3), (20_000, 1000, 2),
                                    (10_000, 2000, 5), (12_345, 500, 4), (3000, 2048, 8), (50, 1999, 6)])
