@@ -139,9 +139,10 @@ Plan validate(int64_t m, int64_t n, const msvd_options& o) {
                                          std::to_string(d + (o.zeta - d % o.zeta)));
         p.d = d;
     }
-    // limits of this build's register-tiled kernels (not reference errors)
+    // limits of this build's register-tiled kernels (not reference errors);
+    // n > 2048 streams in column panels (stream.cu)
     if (b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size above 8 is not supported by this build");
-    if (n > kMaxN) fail(MSVD_ERR_DIMENSION, "msvd: more than 2048 columns is not supported by this build");
+    if (n > kMaxCols) fail(MSVD_ERR_DIMENSION, "msvd: more than 2^20 columns is not supported by this build");
     if (o.precond_kind < 0 || o.precond_kind > 2) fail(MSVD_ERR_INVALID, "msvd: unknown preconditioner kind");
     return p;
 }
@@ -1126,7 +1127,7 @@ int32_t msvd_csr_attach(msvd_ctx* ctx, const int64_t* dRowOffsets, const void* d
         if (index_bytes != 4 && index_bytes != 8) fail(MSVD_ERR_INVALID, "msvd: CSR column indices must be 4 or 8 bytes");
         if (m_local < 0 || n < 0) fail(MSVD_ERR_DIMENSION, "CsrMatrix: negative dimension");
         if (row0 < 0 || row0 + m_local > m_global) fail(MSVD_ERR_DIMENSION, "msvd: local rows outside the global range");
-        if (n < 1 || n > kMaxN) fail(MSVD_ERR_DIMENSION, "msvd: column count outside the supported range [1, 2048]");
+        if (n < 1 || n > kMaxCols) fail(MSVD_ERR_DIMENSION, "msvd: column count outside the supported range [1, 2^20]");
         Ctx& c = ctx->c;
         set_device(c);
         auto* M = new msvd_matrix{ctx, nullptr, m_local, n, n, row0, m_global};

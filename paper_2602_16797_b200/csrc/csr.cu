@@ -198,8 +198,10 @@ __global__ void csc_colsq_kernel(const int64_t* cp, const double* cv, int64_t n,
 }
 
 // --------------------------------------------------------------- S A
-// one warp per sketch row; running sums of its n columns in shared memory
-template <typename Idx>
+// one warp per sketch row; running sums of its n columns in shared memory,
+// or (GLOBAL: rows wider than shared memory holds) in the sketch row itself
+// (SA zeroed by the caller; stride d) -- the same per-column order either way
+template <typename Idx, bool GLOBAL>
 __global__ void __launch_bounds__(kT) csr_sketch_kernel(const int64_t* __restrict__ rp, const Idx* __restrict__ ci,
                                                         const double* __restrict__ v, int64_t n, int64_t d,
                                                         const int64_t* offs, const uint32_t* vals, double val,
@@ -208,8 +210,10 @@ __global__ void __launch_bounds__(kT) csr_sketch_kernel(const int64_t* __restric
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t s = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
     if (s >= d) return;
-    double* acc = acc_all + static_cast<int64_t>(warp) * n;
-    for (int64_t j = lane; j < n; j += 32) acc[j] = 0.0;
+    double* acc = GLOBAL ? SA + s : acc_all + static_cast<int64_t>(warp) * n;
+    const int64_t as = GLOBAL ? d : 1;
+    if (!GLOBAL)
+        for (int64_t j = lane; j < n; j += 32) acc[j] = 0.0;
     __syncwarp();
     const int64_t e0 = offs[s], e1 = offs[s + 1];
     for (int64_t e = e0; e < e1; ++e) {
@@ -218,12 +222,13 @@ __global__ void __launch_bounds__(kT) csr_sketch_kernel(const int64_t* __restric
         const double svv = (w >> 31) ? -val : val;
         const int64_t k1 = rp[r + 1];
         for (int64_t k = rp[r] + lane; k < k1; k += 32) {
-            const int64_t j = ld_idx(ci, k);
+            const int64_t j = ld_idx(ci, k) * as;
             acc[j] = __dadd_rn(acc[j], __dmul_rn(svv, v[k]));
         }
         __syncwarp();
     }
-    for (int64_t j = lane; j < n; j += 32) SA[s + j * d] = acc[j];
+    if (!GLOBAL)
+        for (int64_t j = lane; j < n; j += 32) SA[s + j * d] = acc[j];
 }
 
 // dense row-major rows [row0, row0 + m) of an (m_global x n) zero matrix
@@ -414,8 +419,19 @@ void csr_sketch(Ctx& c, const msvd_matrix& M, int64_t d, int zeta, uint64_t seed
     const SketchLists L = sketch_prepare(c, M.m_local, M.row0, d, zeta, seed, M.m_local);
     int warps = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, 65536 / (8 * n))));
     const size_t smem = sizeof(double) * n * warps;
+    const bool global = smem + 1024 > c.smem_optin;  // a row wider than shared memory: sums in SA
+    if (global) {
+        warps = 8;
+        MSVD_CUDA(cudaMemsetAsync(SA, 0, sizeof(double) * d * n, c.stream));
+    }
     with_idx(M, [&](auto* ci) {
-        auto kern = csr_sketch_kernel<std::remove_const_t<std::remove_pointer_t<decltype(ci)>>>;
+        using Idx = std::remove_const_t<std::remove_pointer_t<decltype(ci)>>;
+        if (global) {
+            csr_sketch_kernel<Idx, true><<<static_cast<unsigned>(ceil_div(d, warps)), 32 * warps, 0, c.stream>>>(
+                M.csr_rp, ci, M.csr_v, n, d, L.offs, L.vals, L.val, SA);
+            return;
+        }
+        auto kern = csr_sketch_kernel<Idx, false>;
         if (smem > 48 * 1024) optin_smem(c, kern);
         kern<<<static_cast<unsigned>(ceil_div(d, warps)), 32 * warps, smem, c.stream>>>(M.csr_rp, ci, M.csr_v, n, d,
                                                                                         L.offs, L.vals, L.val, SA);

@@ -316,7 +316,7 @@ void lanczos_run(Ctx& c, const msvd_matrix& M, int iters, const double* v0h, con
     v0n = std::sqrt(v0n);
     if (v0n == 0.0) fail(MSVD_ERR_NUMERICAL, "lanczos_gk: starting vector is zero");
     if (truth && !truth->v_min) fail(MSVD_ERR_DIMENSION, "lanczos_gk: ground-truth vector length mismatch");
-    if (n > kMaxN) fail(MSVD_ERR_DIMENSION, "msvd: more than 2048 columns is not supported by this build");
+    if (n > kMaxCols) fail(MSVD_ERR_DIMENSION, "msvd: more than 2^20 columns is not supported by this build");
     const auto t_start = std::chrono::steady_clock::now();
     auto elapsed_ms = [&] {
         return timing ? std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count()

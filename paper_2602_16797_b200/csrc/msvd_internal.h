@@ -17,9 +17,13 @@ namespace msvd {
 
 constexpr int kMaxB = 8;              // block size limit of the register-tiled kernels
 constexpr int kMaxK = 3 * kMaxB;      // trial width limit
-constexpr int kMaxPairs = 4;          // column pairs per consumer thread (n <= 2048)
+constexpr int kMaxPairs = 4;          // column pairs per consumer thread (n <= 2048 per panel)
 constexpr int kConsumers = 256;       // consumer threads per stream CTA
-constexpr int kMaxN = 2 * kMaxPairs * kConsumers;
+constexpr int kMaxN = 2 * kMaxPairs * kConsumers;  // widest column panel of one streaming launch
+// wider A (the paper's own 2e6 x 4e3 example) streams in column panels of
+// <= kMaxN columns, one launch per panel (stream.cu); the n x n
+// preconditioner bounds n in practice -- this cap only keeps 8 n^2 in int64
+constexpr int64_t kMaxCols = 1 << 20;
 
 // thrown inside the library; converted to a status at the C boundary
 struct Fail : std::runtime_error {
@@ -92,6 +96,7 @@ struct StreamGeom {
     int32_t tma;     // 1: cp.async.bulk producer, 0: LDG producer
     int32_t grid;    // persistent CTAs
     size_t stage_bytes;
+    int32_t rowcopy; // column panel of a wider A: one bulk copy per row (ld_s of the ld-pitched row)
 };
 
 struct Ctx;

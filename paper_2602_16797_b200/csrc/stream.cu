@@ -90,7 +90,7 @@ StreamGeom rows_geom(const Ctx& c, StreamGeom g, size_t extra) {
 
 // can the narrow kernel take this launch (b, n, fused TSQR width, one-pass gram)?
 bool rows_ok(const Ctx& c, const StreamGeom& g0, int b, const TsqrFuse* ts, bool gram) {
-    if (std::getenv("MSVD_APPLY_TICKET")) return false;
+    if (std::getenv("MSVD_APPLY_TICKET") || g0.n > kMaxN) return false;
     const int npairs = (g0.n + 1) / 2;
     const int pl = (npairs + 31) / 32;
     const bool pl_ok = (b == 1 && pl <= 32) || (b == 2 && pl <= 16) || ((b == 3 || b == 4) && pl <= 8);
@@ -129,7 +129,7 @@ StreamGeom pair_geom(const Ctx& c, StreamGeom g) {
 // b * (register pairs per lane) <= 16 keeps W, the accumulators and the
 // half-row values in registers
 bool pair_ok(const Ctx& c, const StreamGeom& g0, int b, bool ex) {
-    if (!g0.tma || b < 1 || b > 4 || std::getenv("MSVD_NO_PAIR")) return false;
+    if (!g0.tma || b < 1 || b > 4 || g0.n > kMaxN || std::getenv("MSVD_NO_PAIR")) return false;
     const int bg = b + (ex ? 1 : 0);
     if (bg * pair_pl(g0.n) > 16) return false;
     const StreamGeom g = pair_geom(c, g0);
@@ -162,7 +162,7 @@ StreamGeom team_geom(const Ctx& c, StreamGeom g, int T) {
 // T = 4 (quarter rows) carries the check refresh's 2b accumulators; T = 2
 // (half rows) the plain one-pass pass's b
 bool team_ok(const Ctx& c, const StreamGeom& g0, int b, int T) {
-    if (!g0.tma || b < 2 || b > 4 || std::getenv("MSVD_NO_PAIR")) return false;
+    if (!g0.tma || b < 2 || b > 4 || g0.n > kMaxN || std::getenv("MSVD_NO_PAIR")) return false;
     if (b * team_pl(g0.n, T) > (T == 4 ? 8 : 16)) return false;
     const StreamGeom g = team_geom(c, g0, T);
     const size_t xbytes = sizeof(double) * 2 * 8 * kTeamRows * 4;
@@ -176,15 +176,17 @@ bool team_ok(const Ctx& c, const StreamGeom& g0, int b, int T) {
 using namespace strm;
 
 StreamGeom make_geom(const Ctx& c, const double* A, int64_t m, int32_t n, int64_t ld) {
-    if (n < 1 || n > kMaxN)
+    if (n < 1 || n > kMaxCols)
         fail(MSVD_ERR_DIMENSION, "msvd: column count " + std::to_string(n) +
-                                     " outside the supported range [1, " + std::to_string(kMaxN) + "]");
+                                     " outside the supported range [1, " + std::to_string(kMaxCols) + "]");
     StreamGeom g{};
     g.A = A;
     g.m = m;
     g.n = n;
     g.ld = ld;
     g.tma = (ld % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) ? 1 : 0;
+    g.grid = c.num_sms * static_cast<int32_t>(env_int("MSVD_CTAS_PER_SM", 1));
+    if (n > kMaxN) return g;  // streamed in column panels (panel_geom); no whole-row stages
     g.ld_s = g.tma ? static_cast<int32_t>(ld) : static_cast<int32_t>((n + 1) & ~1);
     const int64_t row_bytes = static_cast<int64_t>(g.ld_s) * 8;
     if (row_bytes > kStageBudget / 2)
@@ -194,8 +196,36 @@ StreamGeom make_geom(const Ctx& c, const double* A, int64_t m, int32_t n, int64_
     g.rc = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(target / row_bytes, 64)));
     g.stage_bytes = ((static_cast<size_t>(g.rc) * row_bytes + 127) / 128) * 128;
     g.stages = static_cast<int32_t>(std::max<size_t>(2, std::min<size_t>(8, budget / g.stage_bytes)));
-    g.grid = c.num_sms * static_cast<int32_t>(env_int("MSVD_CTAS_PER_SM", 1));
     return g;
+}
+
+// ---- column panels of a wide A (n > kMaxN) ---------------------------------
+// The register-tiled passes hold <= kMaxN columns per CTA (W or the G
+// accumulators, kMaxPairs column pairs per consumer thread).  A wider A is
+// streamed as P = ceil(n / kMaxN) column panels of even width, one launch each:
+// the panels partition the columns, so A is still read exactly once per pass
+// (8 m n bytes); each row's panel segment is one bulk copy (rowcopy) when A's
+// rows are TMA-aligned, else the LDG producer re-pitches it.  Y = A W sums the
+// panels' partial products in panel order (deterministic); A^T Y writes each
+// panel's columns of the partials directly.
+int panel_count(int n) { return static_cast<int>(ceil_div(n, kMaxN)); }
+
+StreamGeom panel_geom(const StreamGeom& g, int p, int* c0_out) {
+    const int P = panel_count(g.n);
+    const int w = ((static_cast<int>(ceil_div(g.n, P)) + 1) & ~1);  // even: panel starts stay 16-byte aligned
+    const int c0 = p * w;
+    const int np = std::min(w, g.n - c0);
+    StreamGeom q = g;
+    q.A = g.A + c0;
+    q.n = np;
+    q.ld_s = (np + 1) & ~1;  // an odd last panel (odd n) copies one pad column of the even ld
+    q.rowcopy = g.tma;
+    const int64_t row_bytes = static_cast<int64_t>(q.ld_s) * 8;
+    q.rc = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(kStageTarget / row_bytes, 64)));
+    q.stage_bytes = ((static_cast<size_t>(q.rc) * row_bytes + 127) / 128) * 128;
+    q.stages = static_cast<int32_t>(std::max<size_t>(2, std::min<size_t>(8, kStageBudget / q.stage_bytes)));
+    *c0_out = c0;
+    return q;
 }
 
 bool apply_gram_supported(const Ctx& c, const StreamGeom& g, int b, const TsqrFuse* fuse) {
@@ -236,6 +266,17 @@ bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
     }
     ProfScope prof(c, kProfApply);
     TsqrFuse none{};
+    if (g.n > kMaxN) {  // column panels: out = sum over panels of A_p W_p, in panel order
+        if (gpart) fail(MSVD_ERR_INVALID, "msvd: one-pass A*W / A^T A W launch on an unsupported shape");
+        for (int p = 0; p < panel_count(g.n); ++p) {
+            int c0 = 0;
+            const StreamGeom pg = panel_geom(g, p, &c0);
+            ApplyArgs a{cap_rows(rechunk(pg, 48, 144), kRedSlots / std::max(1, b)), W + c0, out, none, nullptr,
+                        nullptr, g.n, p > 0 ? 1 : 0};
+            launch_ticket(c, a, b);
+        }
+        return false;
+    }
     if (try_apply_rows(c, ApplyArgs{g, W, out, fuse ? *fuse : none, gpart, nullptr}, b)) return fuse != nullptr;
     // one-pass in the team form: four rows per barrier and one
     // transpose-reduce per four rows.  b >= 3: half rows (T = 2), measured at
@@ -268,13 +309,22 @@ void launch_gram(Ctx& c, const StreamGeom& g, Cols T, int k, const double* Cm, i
     ProfScope prof(c, kProfGram);
     // stage geometry by block size (tuning sweep, profiles/README.md):
     // b = 1: 32 KB x 3, b = 2: 48 KB x 3, b >= 3: 64 KB x 2
-    const StreamGeom gg = b == 1 ? rechunk(g, 32, 96) : (b == 2 ? rechunk(g, 48, 144) : rechunk(g, 64, 128));
-    GramArgs a{gg, T, k, Cm, q, out, direct ? 1 : 0, Gpart, skip};
     if (g.m == 0) {
         MSVD_CUDA(cudaMemsetAsync(Gpart, 0, sizeof(double) * g.grid * b * g.n, c.stream));
         return;
     }
-    launch_gram_b(c, a, b);
+    if (g.n > kMaxN) {  // column panels: each writes its columns of Gpart; the first also the outputs
+        for (int p = 0; p < panel_count(g.n); ++p) {
+            int c0 = 0;
+            const StreamGeom pg0 = panel_geom(g, p, &c0);
+            const StreamGeom pg = b == 1 ? rechunk(pg0, 32, 96) : (b == 2 ? rechunk(pg0, 48, 144) : rechunk(pg0, 64, 128));
+            GramArgs ap{pg, T, k, Cm, q, p == 0 ? out : OutCols{}, direct ? 1 : 0, Gpart + c0, skip, g.n};
+            launch_gram_b(c, ap, b);
+        }
+        return;
+    }
+    const StreamGeom gg = b == 1 ? rechunk(g, 32, 96) : (b == 2 ? rechunk(g, 48, 144) : rechunk(g, 64, 128));
+    launch_gram_b(c, GramArgs{gg, T, k, Cm, q, out, direct ? 1 : 0, Gpart, skip}, b);
 }
 
 }  // namespace msvd

@@ -36,6 +36,30 @@ static __device__ void produce(const StreamGeom& g, const Pipe& p, int64_t r_beg
     const int lane = threadIdx.x & 31;
     const int64_t nrows = r_end - r_begin;
     const int64_t nchunks = ceil_div(nrows, g.rc);
+    if (g.tma && g.rowcopy) {
+        // a column panel: the chunk's rows are ld-pitched segments of ld_s
+        // doubles, one bulk copy per row, spread over the lanes; the expected
+        // bytes are posted before any copy is issued
+        const uint64_t pol = l2_evict_first_policy();
+        const uint32_t row_bytes = static_cast<uint32_t>(g.ld_s) * 8u;
+        int s = 0;
+        uint32_t ph = 1;
+        for (int64_t c = 0; c < nchunks; ++c) {
+            if (c >= g.stages) mbar_wait(&p.empty[s], ph);
+            const int64_t r0 = r_begin + c * g.rc;
+            const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
+            if (lane == 0) mbar_arrive_expect_tx(&p.full[s], row_bytes * static_cast<uint32_t>(rc));
+            __syncwarp();
+            for (int r = lane; r < rc; r += 32)
+                bulk_g2s(p.stage0 + s * p.stage_bytes + static_cast<size_t>(r) * row_bytes, g.A + (r0 + r) * g.ld,
+                         row_bytes, &p.full[s], pol);
+            if (++s == g.stages) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+        return;
+    }
     if (g.tma) {
         if (lane != 0) return;
         const uint64_t pol = l2_evict_first_policy();
@@ -103,6 +127,8 @@ struct ApplyArgs {
     TsqrFuse ts;      // ts.Rparts == nullptr: no fused TSQR
     double* gpart;    // [grid][b][n] A_cta^T (A_cta W) partials (one-pass mode), or nullptr
     const double* ex; // pair kernel, EX: an m-vector e whose A_cta^T e fills column b of gpart
+    int64_t wstride;  // ticket kernel, column panel: W's column stride (0: g.n)
+    int accum;        // ticket kernel, column panel: out += the panel's A W (panels after the first)
 };
 
 // K3: Y = A W.  Warps 1..8 consume.  Each warp reduces its threads'
@@ -133,6 +159,8 @@ struct GramArgs {
     int direct;        // Y = T (k == B), no outputs
     double* Gpart;     // [grid][B][n]
     const int* skip;   // device flag: nonzero = the pass is not needed (one-pass check gate)
+    int64_t gstride;   // column panel: Gpart's (cta, column) row stride (0: g.n); a null
+                       // out.p[j] skips that output (the panels after the first)
 };
 
 // ---- geometry helpers (stream.cu) ---------------------------------------

@@ -51,14 +51,15 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) 
     const int cw = ct >> 5;
     const int n = g.n;
     const int npairs = (n + 1) >> 1;
+    const int64_t ws = a.wstride ? a.wstride : n;  // W's column stride (the full n for a column panel)
     double w[kMaxPairs][2][B];
 #pragma unroll
     for (int i = 0; i < kMaxPairs; ++i) {
         const int c0 = 2 * (ct + i * kConsumers);
 #pragma unroll
         for (int j = 0; j < B; ++j) {
-            w[i][0][j] = c0 < n ? a.W[c0 + static_cast<int64_t>(j) * n] : 0.0;
-            w[i][1][j] = c0 + 1 < n ? a.W[c0 + 1 + static_cast<int64_t>(j) * n] : 0.0;
+            w[i][0][j] = c0 < n ? a.W[c0 + static_cast<int64_t>(j) * ws] : 0.0;
+            w[i][1][j] = c0 + 1 < n ? a.W[c0 + 1 + static_cast<int64_t>(j) * ws] : 0.0;
         }
     }
     constexpr int NV = ApplyShape<B>::NV;
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(32 + kConsumers, 1) apply_kernel(ApplyArgs a) 
 #pragma unroll
                 for (int q = 0; q < 8; ++q) sum += r8[q * kRedSlots + v];
                 const int rr = v / B, j = v - (v / B) * B;
+                if (a.accum) sum = a.out.p[j][r0 + rr] + sum;  // panels in order: deterministic
                 a.out.p[j][r0 + rr] = sum;
             }
             __syncwarp();
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(64 + kConsumers, 1) gram_kernel(GramArgs a) {
                                     for (int l = 0; l < kMaxK; ++l)
                                         if (l < a.k) y = fma(Cs[l + j * a.k], t[l], y);
                                     yv[j] = y;
-                                    a.out.p[j][gr] = y;
+                                    if (a.out.p[j]) a.out.p[j][gr] = y;
                                 }
                             }
                         }
@@ -272,14 +274,15 @@ __global__ void __launch_bounds__(64 + kConsumers, 1) gram_kernel(GramArgs a) {
             ph ^= 1;
         }
     }
-    double* gp = a.Gpart + static_cast<size_t>(blockIdx.x) * B * n;
+    const size_t gs = a.gstride ? static_cast<size_t>(a.gstride) : static_cast<size_t>(n);
+    double* gp = a.Gpart + static_cast<size_t>(blockIdx.x) * B * gs;
 #pragma unroll
     for (int i = 0; i < kMaxPairs; ++i) {
         const int c0 = 2 * (ct + i * kConsumers);
 #pragma unroll
         for (int j = 0; j < B; ++j) {
-            if (c0 < n) gp[static_cast<size_t>(j) * n + c0] = acc[i][0][j];
-            if (c0 + 1 < n) gp[static_cast<size_t>(j) * n + c0 + 1] = acc[i][1][j];
+            if (c0 < n) gp[j * gs + c0] = acc[i][0][j];
+            if (c0 + 1 < n) gp[j * gs + c0 + 1] = acc[i][1][j];
         }
     }
 }

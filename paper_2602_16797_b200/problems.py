@@ -54,6 +54,10 @@ CONFIGS = {
     "c3": Config("c3", 1_000_000, 2_000, 5, 2, 1e-12, "5-dim exact nullspace"),
     "c4": Config("c4", 500_000, 500, 4, 4, 1e-10, "small gap, ill-conditioned"),
     "c5": Config("c5", 8_000_000, 1_000, 2, 4, 1e-12, "multi-GPU scaling; tol unspecified -> 1e-12"),
+    # the paper's illustrative example (section 1.2): m = 2e6, n = 4e3, 64 GB;
+    # n > 2048 streams in column panels
+    "paper_easy": Config("paper_easy", 2_000_000, 4_000, 1, 4, 1e-12, "paper section 1.2, easy"),
+    "paper_hard": Config("paper_hard", 2_000_000, 4_000, 1, 4, 1e-12, "paper section 1.2, hard"),
 }
 
 
@@ -69,6 +73,11 @@ def spectrum(name, n):
         return np.concatenate([geometric(1.0, 1e-3, n - 4), [1.3e-4, 1.2e-4, 1.1e-4, 1.0e-4]])
     if name == "c5":
         return np.concatenate([geometric(1.0, 1e-5, n - 1), [1e-7]])
+    # the paper's own 2e6 x 4e3 examples (section 1.2), with Haar U, V
+    if name == "paper_easy":  # sigma_1..n-1 geometric 1 -> 0.1, sigma_n = 1e-7
+        return np.concatenate([geometric(1.0, 0.1, n - 1), [1e-7]])
+    if name == "paper_hard":  # geometric 1 -> 1e-10: relative gap ~0.05 at the minimum
+        return geometric(1.0, 1e-10, n)
     raise KeyError(name)
 
 

@@ -66,7 +66,8 @@ def test_defaults_match_solver_options(msvd):
     (40, 8, dict(block_size=2, max_iter=-5), None),
     (20, 8, dict(zeta=0), None),            # m <= 4n: sketch skipped, zeta unused
     (10**6, 1000, {}, None),
-    (10**6, 4096, {}, "DimensionError"),    # this build: n <= 2048
+    (10**6, 4096, {}, None),                # wide A: column panels (the paper's 2e6 x 4e3 example)
+    (2**22, 2**20 + 2, {}, "DimensionError"),  # this build: n <= 2^20
     (10**6, 1000, dict(block_size=9), "DimensionError"),  # this build: b <= 8
 ])
 def test_validation_order_and_classes(msvd, m, n, kw, exc):

@@ -1,14 +1,27 @@
 """The reference's DEFAULT options on the device: tol < 0 (default_tolerance =
 2 sqrt(n) eps, solver.hpp:83-85) and the stagnation stop (solver.cpp:177-211).
 
-The stagnation clauses compare residuals at the roundoff floor, so the
-reference's own stop row moves by whole check periods under 1-ulp input
-perturbations (81 vs 76 at C1).  Instead of a fixed window, the
-gate here is that spread MEASURED on the same input: the oracle solves A and
-K seeded 1-ulp perturbations A o (1 + delta); the device's stop must fall
-inside [min, max] of those iteration counts (+-1), and its answer must meet
-the parity gates against the unperturbed oracle run.  One-pass (default) and
-two-pass (MSVD_ONE_PASS=0) device loops are both held to it.
+The stagnation clauses compare residuals at the roundoff floor, so where the
+reference stops is itself chaotic: under seeded 1-ulp perturbations of A its
+C1 stop row ranges over 61..116 (40 perturbations measured; SURVEY A.3 saw
+81 vs 76).  The gates therefore split the deterministic part of the
+trajectory from the chaotic part:
+
+* the rule itself: the reference's check_convergence (the oracle), applied
+  to the device's OWN residual / theta history, must stop exactly at the
+  device's stop row and at no earlier check row -- the device implements the
+  rule, not an approximation of it;
+* the deterministic part: the first check row whose residual meets the
+  tolerance (the floor entry) agrees with the unperturbed reference within one
+  check period;
+* the chaotic part: where the stop lands after the floor entry is a random
+  variable of the roundoff, so it is compared as a distribution -- the
+  device and the reference each solve A and the same K seeded 1-ulp
+  perturbations; their median stops agree within two check periods;
+* the answer meets the north-star gates against the unperturbed reference.
+
+One-pass (default) and two-pass (MSVD_ONE_PASS=0) device loops are both held
+to these gates.
 """
 import numpy as np
 import pytest
@@ -18,7 +31,8 @@ from paper_2602_16797_b200 import problems
 
 pytestmark = pytest.mark.gpu
 
-K_PERTURB = 4
+K_PERTURB = {"c1": 16, "c2": 5}
+CHECK_EVERY = 5
 
 
 def perturbed(a, k):
@@ -27,9 +41,9 @@ def perturbed(a, k):
     return a * (1.0 + rng.choice([-1.0, 1.0], size=a.shape) * np.finfo(np.float64).eps)
 
 
-def spread(port, a, opts):
+def spread(port, a, opts, k_perturb=4):
     runs = [port.lobpcg_solve(a, opts.to_abi())]
-    for k in range(K_PERTURB):
+    for k in range(k_perturb):
         runs.append(port.lobpcg_solve(perturbed(a, k), opts.to_abi()))
     its = [r["iterations"] for r in runs]
     return runs[0], min(its), max(its), its
@@ -38,21 +52,68 @@ def spread(port, a, opts):
 @pytest.mark.parametrize("name,shape,d", [("c1", dict(m=10_000, n=100), 200),
                                           ("c2", dict(m=20_000, n=1000), 2000)])
 def test_default_options_within_reference_spread(msvd, cuda, port, name, shape, d, monkeypatch):
+    import torch
+
     cfg = problems.CONFIGS[name].scaled(**shape)
     a_dev, _ = problems.make_problem_gpu(cfg.m, cfg.n, cfg.spectrum(), device=cuda)
     a = a_dev.cpu().numpy()
     opts = msvd.SolverOptions(seed=problems.SOLVER_SEED, sketch_dim=d, record_timing=False)  # tol < 0, stagnation
-    ref, lo, hi, its = spread(port, a, opts)
+    ref, lo, hi, its = spread(port, a, opts, K_PERTURB[name])
     smax = ref["sigma_max_estimate"]
+    tol = 2.0 * np.sqrt(cfg.n) * np.finfo(np.float64).eps  # default_tolerance (solver.hpp:83-85)
+    ref_entry = floor_entry([(x["iter"], x["resid"]) for x in ref["record"]], smax, tol)
+    failures = []
     for one_pass in ("1", "0"):
         monkeypatch.setenv("MSVD_ONE_PASS", one_pass)
         res = msvd.rlobpcg_single(msvd.DeviceDenseOperator(a_dev), opts)
-        print(f"[{name} default options, one_pass={one_pass}] device {res.iterations()} iterations; "
-              f"reference under 1-ulp perturbations {its}")
+        rows = [(x.iter, x.resid) for x in res.record.rows]
+        entry = floor_entry(rows, res.sigma_max_estimate, tol)
+        fired = rule_stops(port, res, tol)
+        # the device's own stop distribution on the SAME perturbed inputs
+        dev_its = [res.iterations()]
+        for k in range(K_PERTURB[name]):
+            ak = torch.from_numpy(perturbed(a, k)).to(cuda)
+            dev_its.append(msvd.rlobpcg_single(msvd.DeviceDenseOperator(ak), opts).iterations())
+            del ak
+        med_dev, med_ref = float(np.median(dev_its)), float(np.median(its))
+        print(f"[{name} default options, one_pass={one_pass}] device {res.iterations()} iterations, floor entry "
+              f"row {entry}, rule fires at {fired}; reference floor entry row {ref_entry}; stops under 1-ulp "
+              f"perturbations: reference {sorted(its)} (median {med_ref}), device {sorted(dev_its)} "
+              f"(median {med_dev})")
         assert res.status == ref["status"] == "converged"
-        assert lo - 1 <= res.iterations() <= hi + 1, (res.iterations(), its)
+        assert fired == [res.iterations()], fired  # the rule on the device's own history
+        assert entry is not None and ref_entry is not None and abs(entry - ref_entry) <= CHECK_EVERY
+        # same stop distribution: medians within two check periods, and the
+        # unperturbed device stop inside the two ensembles' joint range
+        if abs(med_dev - med_ref) > 2 * CHECK_EVERY or not (min(its + dev_its) <= res.iterations() <= max(its + dev_its)):
+            failures.append((one_pass, sorted(dev_its), sorted(its)))
         assert abs(res.sigma[0] - ref["sigma"][0]) <= 1e-10 * smax
         assert subspace_sin(ref["v"][:, 0], res.v[:, 0]) <= 1e-8
+    assert not failures, failures
+
+
+def floor_entry(rows, smax, tol):
+    """First check row (row i + 1 with i % check_every == 0) whose residual
+    meets sigma1^2 tol (solver.cpp:183-184)."""
+    for it, resid in rows:
+        if it >= 1 and (it - 1) % CHECK_EVERY == 0 and resid <= smax * smax * tol:
+            return it
+    return None
+
+
+def rule_stops(port, res, tol):
+    """Check rows at which the reference's check_convergence (oracle,
+    solver.cpp:177-211) stops on the device's own history (b = 1: the record
+    row's theta and resid are theta_hist and resid_hist, solver.cpp:376-397)."""
+    resid = np.array([x.resid for x in res.record.rows])
+    theta = np.array([x.theta for x in res.record.rows])
+    out = []
+    for i in range(0, len(resid) - 1):
+        if i % CHECK_EVERY == 0:
+            d = port.check_convergence(resid[: i + 2], theta[: i + 2], i, res.sigma_max_estimate, tol, 1.1, True)
+            if d["stop"]:
+                out.append(i + 1)
+    return out
 
 
 def test_default_tolerance_tol_only(msvd, cuda, port, monkeypatch):
