@@ -326,6 +326,8 @@ int32_t msvd_ctx_profile(msvd_ctx* ctx, int32_t enable);
  *  64 gram (A^T Y pass)              128 separate TSQR pass
  * 256 the preconditioner from the Cholesky-QR route (no n x n SVD)
  * 512 apply_team (the b = 3, 4 one-pass pass, four warps per row)
+ * 1024 apply_split (b = 2..4 one-pass pass: dot, acc and producer warps)
+ * 2048 apply_split EX (b = 2..4 check refresh in the split-role form)
  * reset != 0 clears the mask after reading it.                             */
 int64_t msvd_ctx_kernel_paths(msvd_ctx* ctx, int32_t reset);
 int32_t msvd_ctx_profile_read(msvd_ctx* ctx, double* ms, int64_t* counts, int32_t nslots);

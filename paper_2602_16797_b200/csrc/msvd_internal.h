@@ -103,7 +103,7 @@ struct Ctx;
 
 enum KernelPath : int64_t { kPathRows = 1, kPathSelf = 2, kPathPair = 4, kPathPairEx = 8, kPathTeamEx = 16,
                             kPathTicket = 32, kPathGram = 64, kPathTsqr = 128, kPathCholPrecond = 256,
-                            kPathTeam = 512 };
+                            kPathTeam = 512, kPathSplit = 1024, kPathSplitEx = 2048 };
 
 enum ProfSlot { kProfApply = 0, kProfGram, kProfTsqr, kProfRR, kProfSketch, kProfSvd, kProfPrecond, kProfCgs2,
                 kProfReduce, kProfControl, kProfSlots };

@@ -232,11 +232,11 @@ bool apply_gram_supported(const Ctx& c, const StreamGeom& g, int b, const TsqrFu
     const int pl = ((g.n + 1) / 2 + 31) / 32;
     const int plt = pl <= 4 ? 4 : (pl <= 8 ? 8 : (pl <= 16 ? 16 : 32));  // the PL template the launch picks
     if (b * plt <= 16 && rows_ok(c, g, b, fuse, true)) return true;
-    return !fuse && pair_ok(c, g, b, false);  // the pair kernel has no fused TSQR
+    return !fuse && (pair_ok(c, g, b, false) || split_ok(c, g, b, false));  // neither has a fused TSQR
 }
 
 bool apply_ex_supported(const Ctx& c, const StreamGeom& g, int b) {
-    return b == 1 ? pair_ok(c, g, 1, true) : team_ok(c, g, b, kTeam);
+    return b == 1 ? pair_ok(c, g, 1, true) : (team_ok(c, g, b, kTeam) || split_ok(c, g, b, true));
 }
 
 bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out, const double* ex,
@@ -250,6 +250,11 @@ bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, int b, OutCol
     if (b >= 2) {
         Cols ec{};
         for (int j = 0; j < b; ++j) ec.p[j] = ex + j * ld_ex;
+        // split-role form first (MSVD_ONEPASS_KERNEL names another one-pass kernel: the team form)
+        if (!std::getenv("MSVD_ONEPASS_KERNEL") && split_ok(c, g, b, true)) {
+            launch_split(c, ApplyArgs{g, W, out, TsqrFuse{}, gpart, nullptr}, b, &ec);
+            return false;
+        }
         launch_team_ex(c, ApplyArgs{team_geom(c, g, kTeam), W, out, TsqrFuse{}, gpart, nullptr}, ec, b);
         return false;
     }
@@ -285,7 +290,13 @@ bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
     // peak; the plain passes alone 5.7 TB/s); quarter rows (T = 4) were slower
     // (13.8), and at b = 2 (C5) the pair kernel stays ahead (877 vs 890 ms).
     // MSVD_ONEPASS_KERNEL = pair | team2 | team4 overrides, for measurement.
+    // The split-role kernel (stream_split.cu: dot, acc and producer warps) takes every
+    // b = 2..4 shape it fits; the forms below remain for measurement and as the fallback.
     const char* ok_env = std::getenv("MSVD_ONEPASS_KERNEL");
+    if (gpart && !ok_env && split_ok(c, g, b, false)) {
+        launch_split(c, ApplyArgs{g, W, out, none, gpart, nullptr}, b, nullptr);
+        return false;
+    }
     const std::string okk = ok_env ? ok_env : (b >= 3 ? "team2" : "pair");
     const int team_t = okk == "team4" ? 4 : (okk == "team2" ? 2 : 0);
     if (gpart && team_t && team_ok(c, g, b, team_t)) {

@@ -4,6 +4,7 @@
 //   stream.cu         geometry, support queries and the launch entry points
 //   stream_rows.cu    apply_rows_kernel / apply_self_kernel (one warp per row)
 //   stream_pair.cu    apply_pair_kernel / apply_team_ex_kernel (2 / 4 warps per row)
+//   stream_split.cu   apply_split_kernel (b = 2..4 one-pass: dot, acc and producer warps)
 //   stream_ticket.cu  apply_kernel (b >= 5) and gram_kernel (K2)
 #pragma once
 
@@ -178,6 +179,9 @@ bool pair_ok(const Ctx& c, const StreamGeom& g0, int b, bool ex);
 int team_pl(int n, int T = kTeam);
 StreamGeom team_geom(const Ctx& c, StreamGeom g, int T = kTeam);
 bool team_ok(const Ctx& c, const StreamGeom& g0, int b, int T = kTeam);
+// stream_split.cu: split-role one-pass kernel (dot / acc / producer warps), b = 2..4
+bool split_ok(const Ctx& c, const StreamGeom& g0, int b, bool ex);
+void launch_split(Ctx& c, const ApplyArgs& a0, int b, const Cols* ex);  // ex: the check refresh's E columns
 
 // ---- kernel-family launchers ---------------------------------------------
 // stream_rows.cu: true if launched (the fused TSQR, when requested, too)

@@ -304,7 +304,7 @@ class Context:
     def launch_count(self):
         return lib().msvd_launch_count(self.handle)
 
-    PATHS = ("rows", "self", "pair", "pair_ex", "team_ex", "ticket", "gram", "tsqr", "chol_precond", "team")
+    PATHS = ("rows", "self", "pair", "pair_ex", "team_ex", "ticket", "gram", "tsqr", "chol_precond", "team", "split", "split_ex")
 
     def kernel_paths(self, reset=True):
         """Names of the A-pass kernel variants launched since the last reset

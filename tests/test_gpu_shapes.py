@@ -20,7 +20,7 @@ CASES = [
     # one-pass shapes: b = 1 with the fused TSQR and the deferred check refresh;
     # b = 2 at n = 520 through the warp-pair kernel (even ld: the TMA row stream)
     (9000, 600, 1, 0, 0), (6000, 520, 2, 0, 2), (5000, 333, 1, 0, 2),
-    # the check refresh on the next pass for b = 2..4 (the warp-team kernel: b = 2 at
+    # the check refresh on the next pass for b = 2..4 (the split-role kernel: b = 2 at
     # n = 1000 with a padded ld, b = 3 and 4 at odd n <= 512 padded to an even ld,
     # which the TMA row stream needs)
     (4000, 1000, 2, 0, 2), (3000, 501, 3, 0, 1), (4000, 481, 4, 0, 1),
@@ -31,8 +31,8 @@ CASES = [
 ]
 
 # kernel variants each team case must reach (msvd_ctx_kernel_paths)
-EXPECT_PATHS = {(4000, 1000, 2): {"team_ex"}, (3000, 501, 3): {"team_ex", "team"}, (4000, 481, 4): {"team_ex", "team"},
-                (3000, 511, 4): {"team_ex", "team"}, (9000, 600, 1): {"pair_ex"}, (6000, 520, 2): {"pair"}}
+EXPECT_PATHS = {(4000, 1000, 2): {"split_ex"}, (3000, 501, 3): {"split_ex", "split"}, (4000, 481, 4): {"split_ex", "split"},
+                (3000, 511, 4): {"split_ex", "split"}, (9000, 600, 1): {"pair_ex"}, (6000, 520, 2): {"split", "split_ex"}}
 
 
 def spectrum(n, seed):
