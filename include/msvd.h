@@ -228,6 +228,13 @@ int32_t msvd_aw_tsqr(msvd_matrix* mat, const double* dW, int64_t b,
  *   worth) it makes the two passes instead.                                 */
 int32_t msvd_aw_gram(msvd_matrix* mat, const double* dW, int64_t b, double* dAW,
                      double* dZ);
+/* msvd_aw_gram_ex -- the one-pass check refresh (solver.cpp:439 evaluated on
+ *   the next pass): dAW = A dW, dZ (n x b) = A^T (A dW) and dZE (n x b) =
+ *   A^T dE for dE (m_local x b, col-major; the solver passes E = A V' of the
+ *   previous check iterate), all from ONE pass over A, summed over ranks.
+ *   MSVD_ERR_INVALID where the shape has no such kernel (b > 4, wide n).    */
+int32_t msvd_aw_gram_ex(msvd_matrix* mat, const double* dW, int64_t b, const double* dE,
+                        double* dAW, double* dZ, double* dZE);
 /* svd.cpp:180-252 dense_svd(B, false) of a small square dB (k x k, k<=32)
  * already reduced to R: sigma descending, V sign-fixed.                     */
 int32_t msvd_small_svd(msvd_ctx* ctx, const double* dB, int64_t k,
@@ -322,10 +329,10 @@ int32_t msvd_ctx_profile(msvd_ctx* ctx, int32_t enable);
  * (test evidence that a shape took the path it is meant to):
  *   1 apply_rows (producer warp)      2 apply_self (TMA, one warp per row)
  *   4 apply_pair (warp pair per row)  8 apply_pair EX (b = 1 check refresh)
- *  16 apply_team_ex (b = 2..4 check refresh)   32 apply ticket (b >= 5)
+ *  16 (retired: the four-warp team check refresh)   32 apply ticket (b >= 5)
  *  64 gram (A^T Y pass)              128 separate TSQR pass
  * 256 the preconditioner from the Cholesky-QR route (no n x n SVD)
- * 512 apply_team (the b = 3, 4 one-pass pass, four warps per row)
+ * 512 (retired: the team one-pass pass)
  * 1024 apply_split (b = 2..4 one-pass pass: dot, acc and producer warps)
  * 2048 apply_split EX (b = 2..4 check refresh in the split-role form)
  * reset != 0 clears the mask after reading it.                             */

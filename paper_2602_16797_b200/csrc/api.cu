@@ -542,6 +542,13 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     }
     // ex != nullptr (one-pass check refresh): the pass also forms A^T E for
     // E = ex (m x b) into Gout[b n : 2 b n], next to A^T A W
+    // trial-block Cholesky QR2 in one-pass mode: pass 1's Gram is S^T Z from the n-side basis S
+    // = [V X W] and its carried images Z = A^T A S (set by the caller before each pass; ZW is
+    // reduced first), so the m x k block is swept once, not twice.  MSVD_TRIAL_IMAGE_GRAM = 0
+    // sweeps twice.
+    Cols imgS{}, imgZ{};
+    const bool image_gram = one_pass && !(std::getenv("MSVD_TRIAL_IMAGE_GRAM") &&
+                                          std::atoi(std::getenv("MSVD_TRIAL_IMAGE_GRAM")) == 0);
     auto apply_tsqr = [&](Cols Tlead, int nlead, OutCols aw, Cols Tall, int k, int iter,
                           const double* ex = nullptr) -> std::pair<const double*, int> {
         TsqrFuse fz{};
@@ -554,30 +561,29 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         int np = nparts;
         bool fused = false;
         if (ex) {
-            if (launch_apply_ex(c, geom, W, b, aw, ex, ml, Gpart, fuse ? &fz : nullptr)) {
-                np = geom.grid;
-            } else {
-                if (use_cholqr) launch_trial_cholqr(c, Tall, ml, k, tq);
-                launch_tsqr(c, Tall, ml, k, Rparts, st, iter, use_cholqr ? tq.flag : nullptr);
-            }
+            const bool exfused = launch_apply_ex(c, geom, W, b, aw, ex, ml, Gpart, fuse ? &fz : nullptr);
+            if (exfused) np = geom.grid;
             launch_reduce_g(c, Gpart, geom.grid, n, 2 * b, nullptr, st, 0, Gout, nrm, nblk);
             if (ranks > 1) comm.allreduce_sum(Gout, static_cast<size_t>(2 * b * n), c.stream);
             MSVD_CUDA(cudaMemcpyAsync(ZW, Gout, sizeof(double) * b * n, cudaMemcpyDeviceToDevice, c.stream));
+            if (!exfused) {
+                if (use_cholqr) launch_trial_cholqr(c, Tall, ml, k, tq, image_gram ? &imgS : nullptr, &imgZ, n);
+                launch_tsqr(c, Tall, ml, k, Rparts, st, iter, use_cholqr ? tq.flag : nullptr);
+            }
             if (ranks == 1) return {Rparts, np};
             comm.allgather(Rparts, Rall, static_cast<size_t>(np) * k * k, c.stream);
             return {Rall, np * ranks};
         }
         if (csr) csr_apply(c, *M, W, b, aw);
         else fused = launch_apply(c, geom, W, b, aw, fuse ? &fz : nullptr, one_pass ? Gpart : nullptr);
-        if (fused) {
-            np = geom.grid;
-        } else {
-            if (use_cholqr) launch_trial_cholqr(c, Tall, ml, k, tq);
-            launch_tsqr(c, Tall, ml, k, Rparts, st, iter, use_cholqr ? tq.flag : nullptr);
-        }
+        if (fused) np = geom.grid;
         if (one_pass) {  // ZW = A^T A W summed over CTAs (and ranks)
             launch_reduce_g(c, Gpart, geom.grid, n, b, W, st, 0, ZW, nrm, nblk);
             if (ranks > 1) comm.allreduce_sum(ZW, static_cast<size_t>(n * b), c.stream);
+        }
+        if (!fused) {
+            if (use_cholqr) launch_trial_cholqr(c, Tall, ml, k, tq, image_gram ? &imgS : nullptr, &imgZ, n);
+            launch_tsqr(c, Tall, ml, k, Rparts, st, iter, use_cholqr ? tq.flag : nullptr);
         }
         if (ranks == 1) return {Rparts, np};
         comm.allgather(Rparts, Rall, static_cast<size_t>(np) * k * k, c.stream);
@@ -671,6 +677,8 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     OutCols out{};
     for (int j = 0; j < b; ++j) out.p[j] = AW + static_cast<int64_t>(j) * ml;
     {
+        imgS = cols_n({{W, b}});
+        imgZ = cols_n({{ZW, b}});
         auto parts = apply_tsqr(Cols{}, 0, out, cols_m({{AW, b}}), b, -1);
         RRArgs ra{};
         ra.Rparts = parts.first;
@@ -737,6 +745,10 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         launch_cgs2(c, W, n, b, cols_n({{Vb[cur], b}, {Xb[cur], nx}}), b + nx, st, i);
         for (int j = 0; j < b; ++j) out.p[j] = AW + static_cast<int64_t>(j) * ml;
         const Cols Tm = cols_m({{AVb[cur], b}, {AXb[cur], nx}, {AW, b}});
+        if (one_pass) {
+            imgS = cols_n({{Vb[cur], b}, {Xb[cur], nx}, {W, b}});
+            imgZ = cols_n({{ZVb[cur], b}, {ZXb[cur], nx}, {ZW, b}});
+        }
         auto parts = apply_tsqr(cols_m({{AVb[cur], b}, {AXb[cur], nx}}), b + nx, out, Tm, k, i,
                                 pending ? AVb[cur] : nullptr);
         if (pending) {
@@ -1417,6 +1429,32 @@ int32_t msvd_aw_gram(msvd_matrix* M, const double* dW, int64_t b, double* dAW, d
         }
         launch_reduce_g(c, s, np, n, static_cast<int>(b), nullptr, nullptr, 0, dZ, s + gp, nblk);
         c.comm->allreduce_sum(dZ, static_cast<size_t>(n * b), c.stream);
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+    });
+}
+
+int32_t msvd_aw_gram_ex(msvd_matrix* M, const double* dW, int64_t b, const double* dE, double* dAW, double* dZ,
+                        double* dZE) {
+    return guard([&] {
+        need(M, "matrix");
+        Ctx& c = M->ctx->c;
+        set_device(c);
+        if (b < 1 || b > kMaxB) fail(MSVD_ERR_DIMENSION, "msvd: block size must lie in [1, 8]");
+        const int64_t n = M->n, ml = M->m_local;
+        const StreamGeom g = geom_of(c, *M);
+        if (M->kind != kMatDense || b > 4 || !apply_ex_supported(c, g, static_cast<int>(b)))
+            fail(MSVD_ERR_INVALID, "msvd: A*W + A^T e pass on an unsupported shape");
+        const int nblk = static_cast<int>(ceil_div(n, 64));  // reduce_g column blocks
+        const size_t gp = static_cast<size_t>(g.grid) * 2 * b * n;
+        double* s = static_cast<double*>(c.ensure_scratch(sizeof(double) * (gp + 2 * b * n + static_cast<size_t>(2 * b) * nblk)));
+        double* gout = s + gp;
+        OutCols out{};
+        for (int j = 0; j < b; ++j) out.p[j] = dAW + j * ml;
+        launch_apply_ex(c, g, dW, static_cast<int>(b), out, dE, ml, s, nullptr);
+        launch_reduce_g(c, s, g.grid, n, static_cast<int>(2 * b), nullptr, nullptr, 0, gout, gout + 2 * b * n, nblk);
+        c.comm->allreduce_sum(gout, static_cast<size_t>(2 * b * n), c.stream);
+        MSVD_CUDA(cudaMemcpyAsync(dZ, gout, sizeof(double) * b * n, cudaMemcpyDeviceToDevice, c.stream));
+        MSVD_CUDA(cudaMemcpyAsync(dZE, gout + b * n, sizeof(double) * b * n, cudaMemcpyDeviceToDevice, c.stream));
         MSVD_CUDA(cudaStreamSynchronize(c.stream));
     });
 }

@@ -149,7 +149,10 @@ struct TrialQr {
     int* flag;
     int* disabled;   // sticky: set when a block failed; zeroed at solve start
 };
-void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q);
+// S, Z (n-side trial basis and its images A^T A S, k columns each): pass 1's Gram from
+// S^T Z instead of a sweep of the block (one-pass mode); nullptr: two sweeps
+void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q, const Cols* S = nullptr,
+                         const Cols* Z = nullptr, int64_t n = 0);
 
 // single-CTA Rayleigh-Ritz: merge R parts, Jacobi SVD, C / theta / mix, V' = T C, X' = T mix
 struct RRArgs {

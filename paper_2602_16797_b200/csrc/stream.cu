@@ -129,45 +129,12 @@ StreamGeom pair_geom(const Ctx& c, StreamGeom g) {
 // b * (register pairs per lane) <= 16 keeps W, the accumulators and the
 // half-row values in registers
 bool pair_ok(const Ctx& c, const StreamGeom& g0, int b, bool ex) {
-    if (!g0.tma || b < 1 || b > 4 || g0.n > kMaxN || std::getenv("MSVD_NO_PAIR")) return false;
+    if (!g0.tma || b != 1 || g0.n > kMaxN || std::getenv("MSVD_NO_PAIR")) return false;
     const int bg = b + (ex ? 1 : 0);
     if (bg * pair_pl(g0.n) > 16) return false;
     const StreamGeom g = pair_geom(c, g0);
     if (g.stages * g.stage_bytes + bar_bytes(g.stages) + 1024 > c.smem_optin) return false;
     return sizeof(double) * 4 * bg * g0.n <= static_cast<size_t>(g.stages) * g.stage_bytes;
-}
-
-// b = 1 pass that also accumulates A^T e for an m-vector e: gpart[grid][2][n]
-// = [A_cta^T (A_cta w), A_cta^T e_cta] (the one-pass check refresh)
-// team geometry: stages a multiple of the team count
-int team_pl(int n, int T) {
-    const int part = ((n + 1) / 2 + T - 1) / T;
-    const int pl = (part + 31) / 32;
-    return pl <= 2 ? 2 : (pl <= 4 ? 4 : (pl <= 8 ? 8 : 16));
-}
-// kTeamRows rows per stage (one team barrier per stage), as many stages per
-// team as the shared memory holds; 8 / T teams per CTA
-StreamGeom team_geom(const Ctx& c, StreamGeom g, int T) {
-    const int64_t row_bytes = static_cast<int64_t>(g.ld_s) * 8;
-    const int teams = 8 / T;
-    g.rc = kTeamRows;
-    g.stage_bytes = ((static_cast<size_t>(g.rc) * row_bytes + 127) / 128) * 128;
-    const int64_t xbytes = sizeof(double) * 2 * 8 * kTeamRows * 4;  // [team][buffer][member][row][b <= 4]
-    const int64_t avail = static_cast<int64_t>(c.smem_optin) - 2048 - xbytes;
-    const int64_t per_team =
-        std::max<int64_t>(2, std::min<int64_t>(8, avail / (teams * static_cast<int64_t>(g.stage_bytes))));
-    g.stages = static_cast<int32_t>(teams * per_team);
-    return g;
-}
-// T = 4 (quarter rows) carries the check refresh's 2b accumulators; T = 2
-// (half rows) the plain one-pass pass's b
-bool team_ok(const Ctx& c, const StreamGeom& g0, int b, int T) {
-    if (!g0.tma || b < 2 || b > 4 || g0.n > kMaxN || std::getenv("MSVD_NO_PAIR")) return false;
-    if (b * team_pl(g0.n, T) > (T == 4 ? 8 : 16)) return false;
-    const StreamGeom g = team_geom(c, g0, T);
-    const size_t xbytes = sizeof(double) * 2 * 8 * kTeamRows * 4;
-    if (g.stages * g.stage_bytes + bar_bytes(g.stages) + xbytes + 1024 > c.smem_optin) return false;
-    return sizeof(double) * (8 / T) * (T == 4 ? 2 : 1) * b * g0.n <= static_cast<size_t>(g.stages) * g.stage_bytes;
 }
 
 
@@ -236,7 +203,7 @@ bool apply_gram_supported(const Ctx& c, const StreamGeom& g, int b, const TsqrFu
 }
 
 bool apply_ex_supported(const Ctx& c, const StreamGeom& g, int b) {
-    return b == 1 ? pair_ok(c, g, 1, true) : (team_ok(c, g, b, kTeam) || split_ok(c, g, b, true));
+    return b == 1 ? pair_ok(c, g, 1, true) : split_ok(c, g, b, true);
 }
 
 bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols out, const double* ex,
@@ -250,12 +217,7 @@ bool launch_apply_ex(Ctx& c, const StreamGeom& g, const double* W, int b, OutCol
     if (b >= 2) {
         Cols ec{};
         for (int j = 0; j < b; ++j) ec.p[j] = ex + j * ld_ex;
-        // split-role form first (MSVD_ONEPASS_KERNEL names another one-pass kernel: the team form)
-        if (!std::getenv("MSVD_ONEPASS_KERNEL") && split_ok(c, g, b, true)) {
-            launch_split(c, ApplyArgs{g, W, out, TsqrFuse{}, gpart, nullptr}, b, &ec);
-            return false;
-        }
-        launch_team_ex(c, ApplyArgs{team_geom(c, g, kTeam), W, out, TsqrFuse{}, gpart, nullptr}, ec, b);
+        launch_split(c, ApplyArgs{g, W, out, TsqrFuse{}, gpart, nullptr}, b, &ec);
         return false;
     }
     (void)fuse;  // the b = 1 refresh pass runs the TSQR separately
@@ -283,27 +245,15 @@ bool launch_apply(Ctx& c, const StreamGeom& g, const double* W, int b, OutCols o
         return false;
     }
     if (try_apply_rows(c, ApplyArgs{g, W, out, fuse ? *fuse : none, gpart, nullptr}, b)) return fuse != nullptr;
-    // one-pass in the team form: four rows per barrier and one
-    // transpose-reduce per four rows.  b >= 3: half rows (T = 2), measured at
-    // C4 (b = 4, n = 500) 10.2 ms of passes against 12.8 for the warp-pair
-    // kernel's row-at-a-time barrier and butterflies (0.69 vs 0.55 of the copy
-    // peak; the plain passes alone 5.7 TB/s); quarter rows (T = 4) were slower
-    // (13.8), and at b = 2 (C5) the pair kernel stays ahead (877 vs 890 ms).
-    // MSVD_ONEPASS_KERNEL = pair | team2 | team4 overrides, for measurement.
-    // The split-role kernel (stream_split.cu: dot, acc and producer warps) takes every
-    // b = 2..4 shape it fits; the forms below remain for measurement and as the fallback.
-    const char* ok_env = std::getenv("MSVD_ONEPASS_KERNEL");
-    if (gpart && !ok_env && split_ok(c, g, b, false)) {
+    // b = 2..4: the split-role kernel (stream_split.cu: dot and acc warps).  It replaced the
+    // warp-pair and team forms (one warp set doing both halves of the work behind a barrier
+    // per row or per four rows): b = 4, n = 500 plain pass 6.6 TB/s against 5.7 (team) and
+    // 3.9 (pair), check refresh 5.2 against 2.6; b = 2, n = 1000 7.1 against 6.8 (pair).
+    if (gpart && split_ok(c, g, b, false)) {
         launch_split(c, ApplyArgs{g, W, out, none, gpart, nullptr}, b, nullptr);
         return false;
     }
-    const std::string okk = ok_env ? ok_env : (b >= 3 ? "team2" : "pair");
-    const int team_t = okk == "team4" ? 4 : (okk == "team2" ? 2 : 0);
-    if (gpart && team_t && team_ok(c, g, b, team_t)) {
-        launch_team(c, ApplyArgs{team_geom(c, g, team_t), W, out, none, gpart, nullptr}, b, team_t);
-        return false;
-    }
-    if (gpart && pair_ok(c, g, b, false)) {  // one-pass, rows split over warp pairs (no fused TSQR)
+    if (gpart && pair_ok(c, g, b, false)) {  // b = 1, wide rows: split over warp pairs (no fused TSQR)
         launch_pair(c, ApplyArgs{g, W, out, none, gpart, nullptr}, b);
         return false;
     }

@@ -3,7 +3,7 @@
 // parallel:
 //   stream.cu         geometry, support queries and the launch entry points
 //   stream_rows.cu    apply_rows_kernel / apply_self_kernel (one warp per row)
-//   stream_pair.cu    apply_pair_kernel / apply_team_ex_kernel (2 / 4 warps per row)
+//   stream_pair.cu    apply_pair_kernel (b = 1: a warp pair per row; the b = 1 check refresh)
 //   stream_split.cu   apply_split_kernel (b = 2..4 one-pass: dot, acc and producer warps)
 //   stream_ticket.cu  apply_kernel (b >= 5) and gram_kernel (K2)
 #pragma once
@@ -147,8 +147,6 @@ struct ApplyShape {
 
 
 constexpr int kRowsFused = 4;  // rows per chunk supported by the fused TSQR prefetch
-constexpr int kTeamRows = 4;  // rows per team barrier (= rows per stage)
-constexpr int kTeam = 4;      // warps per team (check-refresh pass, b >= 2)
 
 struct GramArgs {
     StreamGeom g;
@@ -176,9 +174,6 @@ bool rows_ok(const Ctx& c, const StreamGeom& g0, int b, const TsqrFuse* ts, bool
 int pair_pl(int n);
 StreamGeom pair_geom(const Ctx& c, StreamGeom g);
 bool pair_ok(const Ctx& c, const StreamGeom& g0, int b, bool ex);
-int team_pl(int n, int T = kTeam);
-StreamGeom team_geom(const Ctx& c, StreamGeom g, int T = kTeam);
-bool team_ok(const Ctx& c, const StreamGeom& g0, int b, int T = kTeam);
 // stream_split.cu: split-role one-pass kernel (dot / acc / producer warps), b = 2..4
 bool split_ok(const Ctx& c, const StreamGeom& g0, int b, bool ex);
 void launch_split(Ctx& c, const ApplyArgs& a0, int b, const Cols* ex);  // ex: the check refresh's E columns
@@ -186,12 +181,10 @@ void launch_split(Ctx& c, const ApplyArgs& a0, int b, const Cols* ex);  // ex: t
 // ---- kernel-family launchers ---------------------------------------------
 // stream_rows.cu: true if launched (the fused TSQR, when requested, too)
 bool try_apply_rows(Ctx& c, const ApplyArgs& a0, int b);
-// stream_pair.cu: one-pass pass with rows split over warp pairs; the b = 1
-// check-refresh pass (EX); the b = 2..4 check-refresh team pass
+// stream_pair.cu: b = 1 one-pass pass with rows split over warp pairs; the b = 1
+// check-refresh pass (EX)
 void launch_pair(Ctx& c, const ApplyArgs& a0, int b);
 void launch_pair_ex(Ctx& c, const ApplyArgs& a);
-void launch_team_ex(Ctx& c, const ApplyArgs& a, Cols ex, int b);
-void launch_team(Ctx& c, const ApplyArgs& a, int b, int T);  // the plain one-pass pass in the team form
 // stream_ticket.cu: the ticket A*W pass (any b <= 8) and the K2 gram pass
 void launch_ticket(Ctx& c, const ApplyArgs& a, int b);
 void launch_gram_b(Ctx& c, const GramArgs& a, int b);

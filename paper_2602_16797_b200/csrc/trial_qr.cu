@@ -109,63 +109,12 @@ __global__ void __launch_bounds__(kGramT) block_gram_kernel(Cols T, int64_t m, i
     }
 }
 
-// G = sum of the parts (fixed order, below), R = chol(G)
-// upper (warp 0, lane = column), Rinv = R^-1 (lane = column, back
-// substitution through shared memory); pass 2 also R_final = R Rprev.
-// flag: pass 1 writes success (pivots finite and positive, diag(R) within
-// 1e6); pass 2 ands its own.
-__global__ void __launch_bounds__(kCholT) chol_small_kernel(const double* Gpart, int nparts, int k, double* Rout,
-                                                            double* Rinv, const double* Rprev, double* Rfinal,
-                                                            int* flag, int pass, int* disabled) {
-    if (*disabled) {  // an earlier iteration's block was too ill-conditioned: TSQR from here on
-        if (threadIdx.x == 0) *flag = 0;
-        return;
-    }
-    __shared__ double G[kMaxK * kMaxK];
-    __shared__ double R[kMaxK * kMaxK];
-    __shared__ double X[kMaxK * kMaxK];
-    __shared__ int ok_s;
-    // G = sum of the parts: a warp per upper entry (four entries at a time,
-    // independent loads in flight), lane l adds parts l, l + 32, ... in order,
-    // then a fixed butterfly -- deterministic, and ~nparts / 32 dependent
-    // loads per lane instead of nparts (a thread per entry took ~70 us at
-    // 592 parts)
-    {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-        const int ne = k * (k + 1) / 2;
-        const size_t kk = static_cast<size_t>(k) * k;
-        for (int e0 = warp; e0 < ne; e0 += 4 * nw) {
-            int pq[4][2];
-            double acc[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = e0 + u * nw;
-                int q = 0, base = 0;
-                if (e < ne)
-                    while (base + q + 1 <= e) {  // column q holds entries base .. base + q
-                        base += q + 1;
-                        ++q;
-                    }
-                pq[u][0] = e < ne ? e - base : -1;
-                pq[u][1] = q;
-                acc[u] = 0.0;
-            }
-            for (int p = lane; p < nparts; p += 32) {
-                const double* Gp = Gpart + p * kk;
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (pq[u][0] >= 0) acc[u] += Gp[pq[u][0] + pq[u][1] * k];
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const double t = warp_sum(acc[u]);
-                if (lane == 0 && pq[u][0] >= 0) {
-                    G[pq[u][0] + pq[u][1] * k] = t;
-                    G[pq[u][1] + pq[u][0] * k] = t;
-                }
-            }
-        }
-    }
+// R = chol(G) upper (warp 0, lane = column), Rinv = R^-1 (thread = column, back
+// substitution through shared memory); pass 2 also R_final = R Rprev.  flag: pass 1
+// writes success (pivots finite and positive, diag(R) within 1e6); pass 2 ands its own.
+__device__ void chol_tail(double* G, double* R, double* X, int* ok_sp, int k, double* Rout, double* Rinv,
+                          const double* Rprev, double* Rfinal, int* flag, int pass, int* disabled) {
+    int& ok_s = *ok_sp;
     __syncthreads();
     const int lane = threadIdx.x & 31;
     if (threadIdx.x < 32) {
@@ -238,19 +187,129 @@ __global__ void __launch_bounds__(kCholT) chol_small_kernel(const double* Gpart,
     }
 }
 
+// G = sum of the parts (fixed order, below), R = chol(G)
+// upper (warp 0, lane = column), Rinv = R^-1 (lane = column, back
+// substitution through shared memory); pass 2 also R_final = R Rprev.
+// flag: pass 1 writes success (pivots finite and positive, diag(R) within
+// 1e6); pass 2 ands its own.
+__global__ void __launch_bounds__(kCholT) chol_small_kernel(const double* Gpart, int nparts, int k, double* Rout,
+                                                            double* Rinv, const double* Rprev, double* Rfinal,
+                                                            int* flag, int pass, int* disabled) {
+    if (*disabled) {  // an earlier iteration's block was too ill-conditioned: TSQR from here on
+        if (threadIdx.x == 0) *flag = 0;
+        return;
+    }
+    __shared__ double G[kMaxK * kMaxK];
+    __shared__ double R[kMaxK * kMaxK];
+    __shared__ double X[kMaxK * kMaxK];
+    __shared__ int ok_s;
+    // G = sum of the parts: a warp per upper entry (four entries at a time,
+    // independent loads in flight), lane l adds parts l, l + 32, ... in order,
+    // then a fixed butterfly -- deterministic, and ~nparts / 32 dependent
+    // loads per lane instead of nparts (a thread per entry took ~70 us at
+    // 592 parts)
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        const int ne = k * (k + 1) / 2;
+        const size_t kk = static_cast<size_t>(k) * k;
+        for (int e0 = warp; e0 < ne; e0 += 4 * nw) {
+            int pq[4][2];
+            double acc[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * nw;
+                int q = 0, base = 0;
+                if (e < ne)
+                    while (base + q + 1 <= e) {  // column q holds entries base .. base + q
+                        base += q + 1;
+                        ++q;
+                    }
+                pq[u][0] = e < ne ? e - base : -1;
+                pq[u][1] = q;
+                acc[u] = 0.0;
+            }
+            for (int p = lane; p < nparts; p += 32) {
+                const double* Gp = Gpart + p * kk;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (pq[u][0] >= 0) acc[u] += Gp[pq[u][0] + pq[u][1] * k];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double t = warp_sum(acc[u]);
+                if (lane == 0 && pq[u][0] >= 0) {
+                    G[pq[u][0] + pq[u][1] * k] = t;
+                    G[pq[u][1] + pq[u][0] * k] = t;
+                }
+            }
+        }
+    }
+    chol_tail(G, R, X, &ok_s, k, Rout, Rinv, Rprev, Rfinal, flag, pass, disabled);
+}
+
+// Pass 1 without a pass over the block: in one-pass mode the solver carries the images
+// Z = A^T A [V X W] next to S = [V X W], and T^T T = S^T (A^T A S) = S^T Z -- k (k + 1) / 2
+// dot products of length n instead of a sweep of the m x k block.  The block's columns are
+// recurrence products (AV' = T C next to V' = S C), so S^T Z equals T^T T to the
+// recurrences' rounding; it only has to make T R1^-1 well conditioned: pass 2 measures
+// (T R1^-1)^T (T R1^-1) from the block itself.  A warp per entry (i <= j): lanes stride the
+// n entries, fixed butterfly -- deterministic.
+__global__ void __launch_bounds__(kCholT) image_chol_kernel(Cols S, Cols Z, int64_t n, int k, double* Rout,
+                                                            double* Rinv, int* flag, int* disabled) {
+    if (*disabled) {
+        if (threadIdx.x == 0) *flag = 0;
+        return;
+    }
+    __shared__ double G[kMaxK * kMaxK];
+    __shared__ double R[kMaxK * kMaxK];
+    __shared__ double X[kMaxK * kMaxK];
+    __shared__ int ok_s;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int ne = k * (k + 1) / 2;
+    for (int e = warp; e < ne; e += nw) {
+        int q = 0, base = 0;
+        while (base + q + 1 <= e) {  // column q holds entries base .. base + q
+            base += q + 1;
+            ++q;
+        }
+        const int pi = e - base;
+        const double* sp = S.p[pi];
+        const double* zq = Z.p[q];
+        double a0 = 0.0, a1 = 0.0;
+        int64_t i = lane;
+        for (; i + 32 < n; i += 64) {
+            a0 = fma(sp[i], zq[i], a0);
+            a1 = fma(sp[i + 32], zq[i + 32], a1);
+        }
+        if (i < n) a0 = fma(sp[i], zq[i], a0);
+        const double t = warp_sum(a0 + a1);
+        if (lane == 0) {
+            G[pi + q * k] = t;
+            G[q + pi * k] = t;
+        }
+    }
+    chol_tail(G, R, X, &ok_s, k, Rout, Rinv, nullptr, nullptr, flag, 1, disabled);
+}
+
 }  // namespace
 
-void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q) {
+void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q, const Cols* S, const Cols* Z, int64_t n) {
     ProfScope prof(c, kProfTsqr);
     const unsigned grid = static_cast<unsigned>(c.num_sms) * 4;
-    block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, nullptr, q.gpart, q.disabled);
-    chol_small_kernel<<<1, kCholT, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, q.R1, q.R1inv, nullptr, nullptr,
-                                               q.flag, 1, q.disabled);
+    if (S && Z) {
+        image_chol_kernel<<<1, kCholT, 0, c.stream>>>(*S, *Z, n, k, q.R1, q.R1inv, q.flag, q.disabled);
+        c.launches += 1;
+    } else {
+        block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, nullptr, q.gpart, q.disabled);
+        chol_small_kernel<<<1, kCholT, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, q.R1, q.R1inv, nullptr,
+                                                   nullptr, q.flag, 1, q.disabled);
+        c.launches += 2;
+    }
     block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, q.R1inv, q.gpart, q.disabled);
     chol_small_kernel<<<1, kCholT, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, nullptr, q.R2inv, q.R1, q.R,
                                                q.flag, 2, q.disabled);
     MSVD_CUDA(cudaGetLastError());
-    c.launches += 4;
+    c.launches += 2;
 }
 
 }  // namespace msvd

@@ -107,6 +107,7 @@ def _declare(lib):
         "msvd_gram_apply": (i32, [vp, vp, i64, vp, i64, i64, vp, vp]),
         "msvd_aw_tsqr": (i32, [vp, vp, i64, vp, i64, vp, vp]),
         "msvd_aw_gram": (i32, [vp, vp, i64, vp, vp]),
+        "msvd_aw_gram_ex": (i32, [vp, vp, i64, vp, vp, vp, vp]),
         "msvd_small_svd": (i32, [vp, vp, i64, vp, vp]),
         "msvd_check_convergence": (i32, [vp, P(d), P(d), i64, i32, d, d, d, i32, P(i32)]),
         "msvd_raw_write": (i32, [C.c_char_p, vp, i64, i64, i64]),
@@ -137,7 +138,7 @@ EXPORTED = (
     "msvd_validate_options msvd_shard_rows msvd_get_nccl_unique_id msvd_fake_group_create "
     "msvd_fake_group_destroy msvd_ctx_create msvd_ctx_destroy msvd_ctx_synchronize msvd_matrix_attach "
     "msvd_matrix_detach msvd_csr_attach msvd_apply msvd_apply_adjoint msvd_column_norms msvd_build_sparsestack msvd_sketch "
-    "msvd_precond_build msvd_precond_apply msvd_tsqr_r msvd_gram_apply msvd_aw_tsqr msvd_aw_gram msvd_small_svd "
+    "msvd_precond_build msvd_precond_apply msvd_tsqr_r msvd_gram_apply msvd_aw_tsqr msvd_aw_gram msvd_aw_gram_ex msvd_small_svd "
     "msvd_raw_write msvd_raw_info msvd_raw_read_rows msvd_raw_load_device msvd_lanczos_gk msvd_lobpcg_solve msvd_rlobpcg_single "
     "msvd_rlobpcg_block msvd_solve_host msvd_launch_count msvd_abi_sizes msvd_ctx_profile msvd_ctx_profile_read "
     "msvd_ctx_kernel_paths msvd_check_convergence"
@@ -503,6 +504,20 @@ class DeviceDenseOperator:
         check(lib().msvd_aw_gram(self.handle, C.c_void_p(wt.data_ptr()), b, C.c_void_p(aw.data_ptr()),
                                  C.c_void_p(z.data_ptr())))
         return aw.t(), z.t()
+
+    def aw_gram_ex(self, w, e):
+        """One pass (the check refresh): AW = A W, Z = A^T A W and ZE = A^T E."""
+        torch = _torch()
+        wt, b = self._cm(w, self.n)
+        et, be = self._cm(e, self.m_local)
+        if be != b:
+            raise DimensionError("aw_gram_ex: E must have as many columns as W")
+        aw = torch.empty((b, self.m_local), dtype=torch.float64, device=self.device)
+        z = torch.empty((b, self.n), dtype=torch.float64, device=self.device)
+        ze = torch.empty((b, self.n), dtype=torch.float64, device=self.device)
+        check(lib().msvd_aw_gram_ex(self.handle, C.c_void_p(wt.data_ptr()), b, C.c_void_p(et.data_ptr()),
+                                    C.c_void_p(aw.data_ptr()), C.c_void_p(z.data_ptr()), C.c_void_p(ze.data_ptr())))
+        return aw.t(), z.t(), ze.t()
 
     def apply(self, x):
         return self.apply_block(x)[:, 0]

@@ -1,20 +1,13 @@
 """GPU micro-benchmark of the b >= 2 one-pass pass kernels (msvd_aw_gram):
-the split-role kernel against the warp-pair / team forms, with the results
+the split-role kernel (plain pass and check refresh), with the results
 compared bit for bit across repeats and against torch fp64.
     python scripts/bench_split.py [b n m]"""
 import os
 import subprocess
 import sys
 
-CASES = [(4, 500, 500_000), (2, 1000, 1_000_000), (3, 500, 500_000), (2, 512, 500_000), (4, 128, 1_000_000)]
-ENVS = [
-    {"MSVD_NO_SPLIT": "1"},
-    {},
-    {"MSVD_SPLIT_STAGE_KB": "32"},
-    {"MSVD_SPLIT_GROUPS": "3"},
-    {"MSVD_SPLIT_GROUPS": "3", "MSVD_SPLIT_STAGE_KB": "32"},
-    {"MSVD_SPLIT_STAGE_KB": "32", "MSVD_SPLIT_DEPTH": "1"},
-]
+CASES = [(4, 500, 500_000), (2, 1000, 1_000_000), (3, 500, 500_000)]
+ENVS = [{}, {"MSVD_SPLIT_GROUPS": "4", "MSVD_SPLIT_STAGE_KB": "16"}]
 
 
 def child(b, n, m):
@@ -47,6 +40,21 @@ def child(b, n, m):
     per = ms / cnt
     print(f"b={b} n={n} m={m} paths={paths} {per:.4f} ms/launch = {8e-6 * m * n / per:.0f} GB/s  "
           f"err aw {e1:.1e} z {e2:.1e} repeatable={same}", flush=True)
+    # the check-refresh pass (EX): also A^T E
+    e = torch.randn(m, b, dtype=torch.float64, device=dev, generator=g)
+    op.ctx.profile(0)
+    op.ctx.kernel_paths(reset=True)
+    awx, zx, zex = op.aw_gram_ex(w, e)
+    paths = sorted(op.ctx.kernel_paths())
+    ze_ref = a.t() @ e
+    e3 = (zex - ze_ref).abs().max().item() / ze_ref.abs().max().item()
+    e4 = (zx - z_ref).abs().max().item() / z_ref.abs().max().item()
+    op.ctx.profile(1)
+    for _ in range(10):
+        op.aw_gram_ex(w, e)
+    ms, cnt = op.ctx.profile_read()["apply"]
+    per = ms / cnt
+    print(f"   EX  paths={paths} {per:.4f} ms/launch = {8e-6 * m * n / per:.0f} GB/s  err z {e4:.1e} ze {e3:.1e}", flush=True)
 
 
 if __name__ == "__main__":

@@ -6,7 +6,7 @@ one tool per gpurun call (profiling guide):
 
 Covers the hand-rolled synchronization: the TMA/mbarrier stage rings of the
 one-pass passes (b = 1 self-fed + fused TSQR, the warp-pair b = 1 check
-refresh), the four-warp team pass and the trial-block Cholesky QR2 (b = 4),
+refresh), the split-role pass and the trial-block Cholesky QR2 (b = 4),
 the ticket pass and the K2 gram pass (b = 5), the Cholesky-QR preconditioner
 route and the SVD route, the sketch gather.  Shapes are C1 (BASELINE
 configs[0], full size) and scaled C4 / C3 recipes; each solve is checked

@@ -1,7 +1,7 @@
 """Race and ordering stress for the hand-rolled synchronization.
 
 compute-sanitizer is closed on this GPU pool (profiles/round2_compute_sanitizer_closed.txt),
-so the TMA/mbarrier stage rings, the per-pair / per-team named barriers and the
+so the TMA/mbarrier stage rings, the per-pair named barriers, the split-role kernel's mbarriers and tickets and the
 fixed-order reductions are stressed here instead: every pass variant runs many
 times on inputs large enough that each CTA's stage ring wraps hundreds of times
 (the mbarrier parity must never run ahead -- the ABA bug fixed in round 1), at
@@ -26,14 +26,13 @@ def _ptr(t):
 @pytest.mark.parametrize("b,n,env", [
     (1, 1000, {}),                                  # apply_self (one-pass, TMA) at C2's n
     (1, 1000, {"MSVD_ROWS_STAGE_KB": "16"}),
-    (2, 1000, {}),                                  # warp-pair one-pass
-    (2, 1000, {"MSVD_PAIR_STAGE_KB": "16"}),
-    (4, 500, {}),                                   # team (half rows) one-pass at b = 4
-    (4, 500, {"MSVD_ONEPASS_KERNEL": "pair"}),      # the warp-pair kernel at b = 4
-    (4, 500, {"MSVD_ONEPASS_KERNEL": "team4"}),     # the team forms: quarter rows
-    (4, 500, {"MSVD_ONEPASS_KERNEL": "team2"}),     # half rows, four rows per barrier
-    (2, 1000, {"MSVD_ONEPASS_KERNEL": "team2"}),
-    (3, 501, {}),
+    (2, 1000, {}),                                  # split-role one-pass (dot / acc warps)
+    (2, 1000, {"MSVD_SPLIT_STAGE_KB": "16"}),
+    (4, 500, {}),
+    (4, 500, {"MSVD_SPLIT_GROUPS": "4"}),           # four groups (16 warps)
+    (4, 500, {"MSVD_SPLIT_STAGE_KB": "16", "MSVD_SPLIT_DEPTH": "2"}),
+    (3, 501, {}), (2, 700, {}), (4, 300, {}),
+    (1, 2000, {}),                                  # b = 1, wide rows: the warp-pair kernel
 ])
 def test_one_pass_pass_repeatable(msvd, cuda, b, n, env, monkeypatch):
     """msvd_aw_gram: AW = A W and Z = A^T A W from one sweep."""
@@ -59,6 +58,42 @@ def test_one_pass_pass_repeatable(msvd, cuda, b, n, env, monkeypatch):
     assert torch.allclose(aw0, aw_ref, rtol=0, atol=1e-10 * aw_ref.abs().max().item())
     assert torch.allclose(z0, z_ref, rtol=0, atol=1e-10 * z_ref.abs().max().item())
     print(f"[b={b} n={n} {env}] paths {sorted(paths)}: {REPEATS + 1} identical runs")
+
+
+@pytest.mark.parametrize("b,n,env", [
+    (1, 1000, {}),                                  # warp-pair EX (b = 1)
+    (2, 1000, {}), (3, 501, {}), (4, 500, {}),      # split-role EX
+    (2, 130, {}), (4, 120, {}),                     # narrow rows: one column pair per lane
+    (4, 500, {"MSVD_SPLIT_STAGE_KB": "16"}),
+])
+def test_check_refresh_pass_repeatable(msvd, cuda, b, n, env, monkeypatch):
+    """msvd_aw_gram_ex: AW = A W, Z = A^T A W and ZE = A^T E from one sweep."""
+    import torch
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    m = 200_003 if n <= 600 else 100_001
+    ldp = n + (n & 1)  # even leading dimension: the TMA row stream
+    g = torch.Generator(device=cuda).manual_seed(7 * n + b)
+    full = torch.randn(m, ldp, dtype=torch.float64, device=cuda, generator=g)
+    a = full[:, :n]
+    w = torch.randn(n, b, dtype=torch.float64, device=cuda, generator=g)
+    e = torch.randn(m, b, dtype=torch.float64, device=cuda, generator=g)
+    op = msvd.DeviceDenseOperator(a)
+    op.ctx.kernel_paths(reset=True)
+    aw0, z0, ze0 = op.aw_gram_ex(w, e)
+    paths = op.ctx.kernel_paths()
+    for _ in range(REPEATS):
+        aw, z, ze = op.aw_gram_ex(w, e)
+        assert torch.equal(aw, aw0) and torch.equal(z, z0) and torch.equal(ze, ze0), paths
+    aw_ref = a @ w
+    z_ref = a.t() @ aw_ref
+    ze_ref = a.t() @ e
+    assert torch.allclose(aw0, aw_ref, rtol=0, atol=1e-10 * aw_ref.abs().max().item())
+    assert torch.allclose(z0, z_ref, rtol=0, atol=1e-10 * z_ref.abs().max().item())
+    assert torch.allclose(ze0, ze_ref, rtol=0, atol=1e-10 * ze_ref.abs().max().item())
+    # the same A W and A^T A W bits as the plain one-pass pass of the same kernel family
+    print(f"[check refresh b={b} n={n} {env}] paths {sorted(paths)}: {REPEATS + 1} identical runs")
 
 
 @pytest.mark.parametrize("b,n,env", [(1, 1000, {}), (1, 999, {}), (5, 2000, {}), (8, 700, {}),
@@ -90,7 +125,7 @@ def test_apply_and_gram_repeatable(msvd, cuda, b, n, env, monkeypatch):
                                         ("c4", dict(m=60_000, n=500))])
 def test_whole_solve_repeatable(msvd, cuda, name, shape):
     """Complete solves (the one-pass loop with the check refresh -- the
-    pair-EX and team-EX passes --, the trial-block QR, the preconditioner
+    pair-EX and split-EX passes --, the trial-block QR, the preconditioner
     route): the same record and vectors, bit for bit, on every repeat."""
     from paper_2602_16797_b200 import problems
 
