@@ -286,16 +286,17 @@ struct HostSource {
     int64_t ld;
 };
 
-// Cholesky QR2 of the trial block (trial_qr.cu): b >= 3 on one rank, unless
+// Cholesky QR2 of the trial block (trial_qr.cu): b >= 2 on one rank, unless
 // MSVD_TRIAL_QR = householder.  Measured: it pays where the TSQR's merge of
-// k x k parts is the cost (C4, k = 12: 10.5 -> 7.7 ms of loop at m = 6e4);
-// for b = 2 (k = 6) the stacked TSQR is already cheap (C5: no gain), and C5's
-// second target is roundoff-chaotic, so b = 2 keeps the
-// reference's Householder arithmetic.
+// k x k parts is the cost (C4, k = 12: 10.5 -> 7.7 ms of loop at m = 6e4).
+// b = 2 (k = 6) joined in round 2, once pass 1's Gram came from the carried
+// images and the block's Gram pass kept its sums in registers: C5's TSQR +
+// Rayleigh-Ritz merge 50.7 -> 16.9 ms per solve, the same iteration counts on
+// every b = 2 parity case (C5's roundoff-chaotic second target included:
+// tests/test_gpu_true_shapes.py).  b = 1 keeps the TSQR fused into the pass.
 bool use_cholqr_req(int b, int ranks) {
     const char* e = std::getenv("MSVD_TRIAL_QR");
-    if (e && std::string(e) == "cholqr") return ranks == 1 && b >= 2;
-    return ranks == 1 && b >= 3 && !(e && std::string(e) == "householder");
+    return ranks == 1 && b >= 2 && !(e && std::string(e) == "householder");
 }
 
 void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_result* res,

@@ -109,6 +109,97 @@ __global__ void __launch_bounds__(kGramT) block_gram_kernel(Cols T, int64_t m, i
     }
 }
 
+// Register form of the block Gram for k <= 12 (b <= 4): lane = row; the row's k values are
+// transformed by R^-1 in registers and its outer product t t^T goes into k (k + 1) / 2
+// per-thread accumulators -- no shared-memory tile, no per-entry row loops (the kernel
+// above spends two shared loads per multiply-add and ran at ~1 TB/s).  The lanes' sums are
+// reduced once at the end: a fixed butterfly per entry, the 4 warps in order (deterministic).
+// K > 8: the k (k + 1) / 2 accumulators do not fit one thread (78 doubles at k = 12), so the
+// warp takes 16 rows at a time and its two half-warps own the entries of columns
+// [0, KH) and [KH, K) of the same rows (both halves load and transform the same 16 rows:
+// the same addresses, one transaction).
+template <int K>
+__global__ void __launch_bounds__(kGramT) block_gram_reg_kernel(Cols T, int64_t m, const double* Rinv, double* Gpart,
+                                                               const int* disabled) {
+    if (*disabled) return;
+    constexpr int NE = K * (K + 1) / 2;
+    constexpr bool kHalves = K > 8;
+    constexpr int KH = kHalves ? (K * 7 + 9) / 10 : K;     // columns [0, KH) hold about half the entries
+    constexpr int NE0 = KH * (KH + 1) / 2;                  // entries of the first half
+    constexpr int NA = kHalves ? (NE0 > NE - NE0 ? NE0 : NE - NE0) : NE;  // accumulators per thread
+    constexpr int ROWS = kHalves ? 16 : 32;
+    __shared__ double ri[K * K];
+    __shared__ double wsum[kGramW][NE];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (Rinv)
+        for (int i = threadIdx.x; i < K * K; i += blockDim.x) ri[i] = Rinv[i];
+    __syncthreads();
+    const int64_t gw = static_cast<int64_t>(blockIdx.x) * kGramW + warp, nw = static_cast<int64_t>(gridDim.x) * kGramW;
+    const int64_t r0 = (m * gw) / nw, r1 = (m * (gw + 1)) / nw;
+    const bool upper = kHalves && lane >= 16;
+    // (volatile: R^-1 is re-read from shared memory per tile; hoisted into registers its
+    // k (k + 1) / 2 entries would crowd out the accumulators)
+    const volatile double* riv = ri;
+    double acc[NA];
+#pragma unroll
+    for (int e = 0; e < NA; ++e) acc[e] = 0.0;
+#pragma unroll 1
+    for (int64_t base = r0; base < r1; base += ROWS) {
+        const int64_t r = base + (lane & (ROWS - 1));
+        double t[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) t[j] = r < r1 ? T.p[j][r] : 0.0;
+        if (Rinv) {
+#pragma unroll
+            for (int j = K - 1; j >= 0; --j) {  // t <- t R^-1 (upper): column j uses t[0..j]
+                double sj = 0.0;
+#pragma unroll
+                for (int l = 0; l <= j; ++l) sj += t[l] * riv[l + j * K];
+                t[j] = sj;
+            }
+        }
+        if (!upper) {
+#pragma unroll
+            for (int q = 0; q < KH; ++q)
+#pragma unroll
+                for (int pp = 0; pp <= q; ++pp) acc[q * (q + 1) / 2 + pp] = fma(t[pp], t[q], acc[q * (q + 1) / 2 + pp]);
+        } else {
+#pragma unroll
+            for (int q = KH; q < K; ++q)
+#pragma unroll
+                for (int pp = 0; pp <= q; ++pp)
+                    acc[q * (q + 1) / 2 + pp - NE0] = fma(t[pp], t[q], acc[q * (q + 1) / 2 + pp - NE0]);
+        }
+    }
+    // lanes' sums: a fixed butterfly within each 16- or 32-lane owner set
+#pragma unroll
+    for (int e = 0; e < NA; ++e) {
+        double v = acc[e];
+#pragma unroll
+        for (int o = ROWS / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        if (!kHalves) {
+            if (lane == 0) wsum[warp][e] = v;
+        } else {
+            if (lane == 0 && e < NE0) wsum[warp][e] = v;
+            if (lane == 16 && e < NE - NE0) wsum[warp][NE0 + e] = v;
+        }
+    }
+    __syncthreads();
+    double* G = Gpart + static_cast<size_t>(blockIdx.x) * K * K;
+    for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+        double v = wsum[0][e];
+        for (int w = 1; w < kGramW; ++w) v += wsum[w][e];
+        int q = 0, base = 0;
+        while (base + q + 1 <= e) {  // column q holds entries base .. base + q
+            base += q + 1;
+            ++q;
+        }
+        const int p0 = e - base;
+        G[p0 + q * K] = v;
+        G[q + p0 * K] = v;
+    }
+}
+
 // R = chol(G) upper (warp 0, lane = column), Rinv = R^-1 (thread = column, back
 // substitution through shared memory); pass 2 also R_final = R Rprev.  flag: pass 1
 // writes success (pivots finite and positive, diag(R) within 1e6); pass 2 ands its own.
@@ -296,16 +387,29 @@ __global__ void __launch_bounds__(kCholT) image_chol_kernel(Cols S, Cols Z, int6
 void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q, const Cols* S, const Cols* Z, int64_t n) {
     ProfScope prof(c, kProfTsqr);
     const unsigned grid = static_cast<unsigned>(c.num_sms) * 4;
+    // the block's Gram (of T Rinv when given): register form for the trial widths of b <= 4
+    auto gram = [&](const double* Rinv) {
+        switch (k) {
+            case 2: block_gram_reg_kernel<2><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 3: block_gram_reg_kernel<3><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 4: block_gram_reg_kernel<4><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 6: block_gram_reg_kernel<6><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 8: block_gram_reg_kernel<8><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 9: block_gram_reg_kernel<9><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 12: block_gram_reg_kernel<12><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            default: block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, Rinv, q.gpart, q.disabled); break;
+        }
+    };
     if (S && Z) {
         image_chol_kernel<<<1, kCholT, 0, c.stream>>>(*S, *Z, n, k, q.R1, q.R1inv, q.flag, q.disabled);
         c.launches += 1;
     } else {
-        block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, nullptr, q.gpart, q.disabled);
+        gram(nullptr);
         chol_small_kernel<<<1, kCholT, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, q.R1, q.R1inv, nullptr,
                                                    nullptr, q.flag, 1, q.disabled);
         c.launches += 2;
     }
-    block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, q.R1inv, q.gpart, q.disabled);
+    gram(q.R1inv);
     chol_small_kernel<<<1, kCholT, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, nullptr, q.R2inv, q.R1, q.R,
                                                q.flag, 2, q.disabled);
     MSVD_CUDA(cudaGetLastError());
