@@ -22,6 +22,8 @@ namespace {
 
 constexpr int kGramT = 128;    // threads per CTA (4 warps; static shared memory)
 constexpr int kGramW = kGramT / 32;
+constexpr int kGramRegT = 512;  // block_gram_reg_kernel: 16 warps, one CTA per SM -> num_sms parts
+constexpr int kGramRegW = kGramRegT / 32;
 constexpr int kMaxEnt = (kMaxK * (kMaxK + 1) / 2 + 31) / 32;  // Gram entries per lane (<= 10)
 constexpr int kCholT = 512;    // chol_small_kernel threads
 
@@ -119,7 +121,7 @@ __global__ void __launch_bounds__(kGramT) block_gram_kernel(Cols T, int64_t m, i
 // [0, KH) and [KH, K) of the same rows (both halves load and transform the same 16 rows:
 // the same addresses, one transaction).
 template <int K>
-__global__ void __launch_bounds__(kGramT) block_gram_reg_kernel(Cols T, int64_t m, const double* Rinv, double* Gpart,
+__global__ void __launch_bounds__(kGramRegT) block_gram_reg_kernel(Cols T, int64_t m, const double* Rinv, double* Gpart,
                                                                const int* disabled) {
     if (*disabled) return;
     constexpr int NE = K * (K + 1) / 2;
@@ -129,12 +131,12 @@ __global__ void __launch_bounds__(kGramT) block_gram_reg_kernel(Cols T, int64_t 
     constexpr int NA = kHalves ? (NE0 > NE - NE0 ? NE0 : NE - NE0) : NE;  // accumulators per thread
     constexpr int ROWS = kHalves ? 16 : 32;
     __shared__ double ri[K * K];
-    __shared__ double wsum[kGramW][NE];
+    __shared__ double wsum[kGramRegW][NE];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (Rinv)
         for (int i = threadIdx.x; i < K * K; i += blockDim.x) ri[i] = Rinv[i];
     __syncthreads();
-    const int64_t gw = static_cast<int64_t>(blockIdx.x) * kGramW + warp, nw = static_cast<int64_t>(gridDim.x) * kGramW;
+    const int64_t gw = static_cast<int64_t>(blockIdx.x) * kGramRegW + warp, nw = static_cast<int64_t>(gridDim.x) * kGramRegW;
     const int64_t r0 = (m * gw) / nw, r1 = (m * (gw + 1)) / nw;
     const bool upper = kHalves && lane >= 16;
     // (volatile: R^-1 is re-read from shared memory per tile; hoisted into registers its
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(kGramT) block_gram_reg_kernel(Cols T, int64_t 
     double* G = Gpart + static_cast<size_t>(blockIdx.x) * K * K;
     for (int e = threadIdx.x; e < NE; e += blockDim.x) {
         double v = wsum[0][e];
-        for (int w = 1; w < kGramW; ++w) v += wsum[w][e];
+        for (int w = 1; w < kGramRegW; ++w) v += wsum[w][e];
         int q = 0, base = 0;
         while (base + q + 1 <= e) {  // column q holds entries base .. base + q
             base += q + 1;
@@ -294,45 +296,43 @@ __global__ void __launch_bounds__(kCholT) chol_small_kernel(const double* Gpart,
     __shared__ double R[kMaxK * kMaxK];
     __shared__ double X[kMaxK * kMaxK];
     __shared__ int ok_s;
-    // G = sum of the parts: a warp per upper entry (four entries at a time,
-    // independent loads in flight), lane l adds parts l, l + 32, ... in order,
-    // then a fixed butterfly -- deterministic, and ~nparts / 32 dependent
-    // loads per lane instead of nparts (a thread per entry took ~70 us at
-    // 592 parts)
+    // G = sum of the parts (fixed order): entry e is summed by NG threads, thread g
+    // taking parts g, g + NG, ... with eight independent loads in flight, then the NG
+    // partial sums in order -- deterministic, and a few dependent load rounds instead of
+    // nparts / 32 per entry (26 us of the kernel's 46 at 592 parts)
     {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        __shared__ double part[kCholT];
         const int ne = k * (k + 1) / 2;
         const size_t kk = static_cast<size_t>(k) * k;
-        for (int e0 = warp; e0 < ne; e0 += 4 * nw) {
-            int pq[4][2];
-            double acc[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = e0 + u * nw;
-                int q = 0, base = 0;
-                if (e < ne)
-                    while (base + q + 1 <= e) {  // column q holds entries base .. base + q
-                        base += q + 1;
-                        ++q;
-                    }
-                pq[u][0] = e < ne ? e - base : -1;
-                pq[u][1] = q;
-                acc[u] = 0.0;
+        const int NG = max(1, static_cast<int>(blockDim.x) / ne);
+        const int e = threadIdx.x / NG, g = threadIdx.x % NG;
+        int pq0 = 0, pq1 = 0;
+        double sum = 0.0;
+        if (e < ne) {
+            int q = 0, base = 0;
+            while (base + q + 1 <= e) {  // column q holds entries base .. base + q
+                base += q + 1;
+                ++q;
             }
-            for (int p = lane; p < nparts; p += 32) {
-                const double* Gp = Gpart + p * kk;
+            pq0 = e - base;
+            pq1 = q;
+            const double* Ge = Gpart + pq0 + static_cast<size_t>(pq1) * k;
+            double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            int p = g;
+            for (; p + 7 * NG < nparts; p += 8 * NG) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (pq[u][0] >= 0) acc[u] += Gp[pq[u][0] + pq[u][1] * k];
+                for (int u = 0; u < 8; ++u) a[u] += Ge[static_cast<size_t>(p + u * NG) * kk];
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const double t = warp_sum(acc[u]);
-                if (lane == 0 && pq[u][0] >= 0) {
-                    G[pq[u][0] + pq[u][1] * k] = t;
-                    G[pq[u][1] + pq[u][0] * k] = t;
-                }
-            }
+            for (; p < nparts; p += NG) a[0] += Ge[static_cast<size_t>(p) * kk];
+            sum = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+        }
+        part[threadIdx.x] = sum;
+        __syncthreads();
+        if (e < ne && g == 0) {
+            double t = part[threadIdx.x];
+            for (int u = 1; u < NG; ++u) t += part[threadIdx.x + u];
+            G[pq0 + pq1 * k] = t;
+            G[pq1 + pq0 * k] = t;
         }
     }
     chol_tail(G, R, X, &ok_s, k, Rout, Rinv, Rprev, Rfinal, flag, pass, disabled);
@@ -366,14 +366,16 @@ __global__ void __launch_bounds__(kCholT) image_chol_kernel(Cols S, Cols Z, int6
         const int pi = e - base;
         const double* sp = S.p[pi];
         const double* zq = Z.p[q];
-        double a0 = 0.0, a1 = 0.0;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;  // eight loads in flight per lane
         int64_t i = lane;
-        for (; i + 32 < n; i += 64) {
+        for (; i + 96 < n; i += 128) {
             a0 = fma(sp[i], zq[i], a0);
             a1 = fma(sp[i + 32], zq[i + 32], a1);
+            a2 = fma(sp[i + 64], zq[i + 64], a2);
+            a3 = fma(sp[i + 96], zq[i + 96], a3);
         }
-        if (i < n) a0 = fma(sp[i], zq[i], a0);
-        const double t = warp_sum(a0 + a1);
+        for (; i < n; i += 32) a0 = fma(sp[i], zq[i], a0);
+        const double t = warp_sum((a0 + a1) + (a2 + a3));
         if (lane == 0) {
             G[pi + q * k] = t;
             G[q + pi * k] = t;
@@ -388,15 +390,18 @@ void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q, const Col
     ProfScope prof(c, kProfTsqr);
     const unsigned grid = static_cast<unsigned>(c.num_sms) * 4;
     // the block's Gram (of T Rinv when given): register form for the trial widths of b <= 4
+    const unsigned rgrid = static_cast<unsigned>(c.num_sms);
+    const bool reg = k == 2 || k == 3 || k == 4 || k == 6 || k == 8 || k == 9 || k == 12;
+    const int parts = static_cast<int>(reg ? rgrid : grid);
     auto gram = [&](const double* Rinv) {
         switch (k) {
-            case 2: block_gram_reg_kernel<2><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
-            case 3: block_gram_reg_kernel<3><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
-            case 4: block_gram_reg_kernel<4><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
-            case 6: block_gram_reg_kernel<6><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
-            case 8: block_gram_reg_kernel<8><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
-            case 9: block_gram_reg_kernel<9><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
-            case 12: block_gram_reg_kernel<12><<<grid, kGramT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 2: block_gram_reg_kernel<2><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 3: block_gram_reg_kernel<3><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 4: block_gram_reg_kernel<4><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 6: block_gram_reg_kernel<6><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 8: block_gram_reg_kernel<8><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 9: block_gram_reg_kernel<9><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 12: block_gram_reg_kernel<12><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
             default: block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, Rinv, q.gpart, q.disabled); break;
         }
     };
@@ -405,12 +410,12 @@ void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q, const Col
         c.launches += 1;
     } else {
         gram(nullptr);
-        chol_small_kernel<<<1, kCholT, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, q.R1, q.R1inv, nullptr,
+        chol_small_kernel<<<1, kCholT, 0, c.stream>>>(q.gpart, parts, k, q.R1, q.R1inv, nullptr,
                                                    nullptr, q.flag, 1, q.disabled);
         c.launches += 2;
     }
     gram(q.R1inv);
-    chol_small_kernel<<<1, kCholT, 0, c.stream>>>(q.gpart, static_cast<int>(grid), k, nullptr, q.R2inv, q.R1, q.R,
+    chol_small_kernel<<<1, kCholT, 0, c.stream>>>(q.gpart, parts, k, nullptr, q.R2inv, q.R1, q.R,
                                                q.flag, 2, q.disabled);
     MSVD_CUDA(cudaGetLastError());
     c.launches += 2;
