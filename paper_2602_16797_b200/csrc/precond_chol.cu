@@ -169,6 +169,79 @@ __global__ void coldiff_kernel(const double* A, const double* B, int64_t n, doub
     }
 }
 
+// Householder QR of a tall panel X (n x k, k <= 24, ld = n) held in shared memory by ONE
+// CTA (cuSOLVER's geqrf + orgqr cost 0.3-0.5 ms per n x 24 panel in small latency-bound
+// kernels; the block iterations below orthonormalize a panel per round).  Reflector j is
+// formed by warp 0 (v stored below the diagonal, v_j = 1 implied, tau[j]); warp w then
+// updates column j + 1 + w, ... -- one block barrier per phase.  Rout (k x k, ld k, upper;
+// may be null): the R factor.  formQ: X <- Q (n x k), LAPACK dorg2r's in-place backward
+// accumulation.  Zero columns keep tau = 0 (H = I), like dlarfg.
+__global__ void __launch_bounds__(1024) panel_qr_kernel(double* X, int n, int k, double* Rout, int formQ) {
+    extern __shared__ __align__(16) double pq[];  // [k][n] columns, then tau[k]
+    double* tau = pq + static_cast<size_t>(k) * n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int i = threadIdx.x; i < n * k; i += blockDim.x) pq[i] = X[i];
+    __syncthreads();
+    for (int j = 0; j < k; ++j) {
+        double* cj = pq + static_cast<size_t>(j) * n;
+        if (warp == 0) {
+            double ss = 0.0;
+            for (int i = j + 1 + lane; i < n; i += 32) ss = fma(cj[i], cj[i], ss);
+            ss = warp_sum(ss);
+            const double alpha = cj[j];
+            double t = 0.0, scale = 0.0, beta = alpha;
+            if (ss != 0.0) {
+                const double nrm = sqrt(alpha * alpha + ss);
+                beta = alpha >= 0.0 ? -nrm : nrm;
+                t = (beta - alpha) / beta;
+                scale = 1.0 / (alpha - beta);
+            }
+            __syncwarp();
+            for (int i = j + 1 + lane; i < n; i += 32) cj[i] *= scale;
+            if (lane == 0) {
+                cj[j] = beta;
+                tau[j] = t;
+            }
+        }
+        __syncthreads();
+        const double t = tau[j];
+        if (t != 0.0)
+            for (int l = j + 1 + warp; l < k; l += nw) {  // H_j applied to column l
+                double* cl = pq + static_cast<size_t>(l) * n;
+                double w = lane == 0 ? cl[j] : 0.0;
+                for (int i = j + 1 + lane; i < n; i += 32) w = fma(cj[i], cl[i], w);
+                w = warp_sum(w) * t;
+                if (lane == 0) cl[j] -= w;
+                for (int i = j + 1 + lane; i < n; i += 32) cl[i] = fma(-w, cj[i], cl[i]);
+            }
+        __syncthreads();
+    }
+    if (Rout)
+        for (int i = threadIdx.x; i < k * k; i += blockDim.x) {
+            const int r = i % k, c = i / k;
+            Rout[i] = r <= c ? pq[r + static_cast<size_t>(c) * n] : 0.0;
+        }
+    if (!formQ) return;
+    __syncthreads();
+    for (int j = k - 1; j >= 0; --j) {  // dorg2r
+        double* cj = pq + static_cast<size_t>(j) * n;
+        const double t = tau[j];
+        for (int l = j + 1 + warp; l < k; l += nw) {  // H_j applied to Q's columns j + 1 .. k - 1 (rows j .. n - 1)
+            double* cl = pq + static_cast<size_t>(l) * n;
+            double w = lane == 0 ? cl[j] : 0.0;
+            for (int i = j + 1 + lane; i < n; i += 32) w = fma(cj[i], cl[i], w);
+            w = warp_sum(w) * t;
+            if (lane == 0) cl[j] -= w;
+            for (int i = j + 1 + lane; i < n; i += 32) cl[i] = fma(-w, cj[i], cl[i]);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            cj[i] = i < j ? 0.0 : (i == j ? 1.0 - t : -t * cj[i]);
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < n * k; i += blockDim.x) X[i] = pq[i];
+}
+
 // one inverse-iteration step for a single vector (one CTA, n <= 2048):
 // x <- s Y / ||Y|| with s making the first largest-magnitude entry positive
 // (svd.cpp:232-248); out[0] = ||x_new - x_old||, out[1] = ||Y||
@@ -433,16 +506,27 @@ bool precond_build_chol(Ctx& c, const double* SA, int64_t rows, int64_t n, int b
     fill_kernel<<<blocks(n), 256, 0, c.stream>>>(sig, n, 1.0);
     c.launches += 4;
 
+    // the single-CTA panel QR (panel_qr_kernel) where the n x k panel fits shared memory
+    auto panel_smem = [&](int k) { return sizeof(double) * (static_cast<size_t>(k) * n + 32); };
+    auto panel_fits = [&](int k) {
+        if (std::getenv("MSVD_PANEL_QR_CUSOLVER") || panel_smem(k) + 1024 > c.smem_optin) return false;
+        optin_smem(c, panel_qr_kernel);
+        return true;
+    };
     // Rayleigh-Ritz of the n x k block Xb through R: the small R factor of R Xb
     // (Householder) and its one-sided Jacobi SVD -> sgo (descending), W
     auto ritz = [&](const double* Xb, int k, double* sgo) {
         MSVD_BLAS(cublasDtrmm(c.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, in,
                               k, &one, R, in, Xb, in, Z, in));
-        MSVD_SOLVER(cusolverDnDgeqrf(c.solver, in, k, Z, in, tau, lw, lwork, info + 4));
-        MSVD_CUDA(cudaMemsetAsync(H, 0, sizeof(double) * k * k, c.stream));
-        MSVD_CUDA(cudaMemcpy2DAsync(H, sizeof(double) * k, Z, sizeof(double) * n, sizeof(double) * k, k,
-                                    cudaMemcpyDeviceToDevice, c.stream));
-        zero_lower_kernel<<<blocks(k * k), 256, 0, c.stream>>>(H, k);
+        if (panel_fits(k)) {
+            panel_qr_kernel<<<1, 1024, panel_smem(k), c.stream>>>(Z, in, k, H, 0);
+        } else {
+            MSVD_SOLVER(cusolverDnDgeqrf(c.solver, in, k, Z, in, tau, lw, lwork, info + 4));
+            MSVD_CUDA(cudaMemsetAsync(H, 0, sizeof(double) * k * k, c.stream));
+            MSVD_CUDA(cudaMemcpy2DAsync(H, sizeof(double) * k, Z, sizeof(double) * n, sizeof(double) * k, k,
+                                        cudaMemcpyDeviceToDevice, c.stream));
+            zero_lower_kernel<<<blocks(k * k), 256, 0, c.stream>>>(H, k);
+        }
         ++c.launches;
         launch_small_svd(c, H, k, sgo, W, st);
     };
@@ -481,6 +565,11 @@ bool precond_build_chol(Ctx& c, const double* SA, int64_t rows, int64_t n, int b
         MSVD_CUDA(cudaMemcpyAsync(dst, tmp, sizeof(double) * nn, cudaMemcpyDeviceToDevice, c.stream));
     };
     auto orth = [&](double* Xb, int k, int* inf) {  // Householder: robust for any conditioning
+        if (panel_fits(k)) {
+            panel_qr_kernel<<<1, 1024, panel_smem(k), c.stream>>>(Xb, in, k, nullptr, 1);
+            ++c.launches;
+            return;
+        }
         MSVD_SOLVER(cusolverDnDgeqrf(c.solver, in, k, Xb, in, tau, lw, lwork, inf));
         MSVD_SOLVER(cusolverDnDorgqr(c.solver, in, k, k, Xb, in, tau, lw, lwork, inf));
     };

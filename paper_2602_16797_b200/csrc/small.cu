@@ -258,12 +258,18 @@ __device__ bool jacobi_svd(double* Bm, double* V, int k, double* sig, double* Vs
                     const double aqq = warp_sum(bq * bq);
                     const double apq = warp_sum(bp * bq);
                     if (!(app == 0.0 || aqq == 0.0 || apq == 0.0)) {
-                        const double rel = fabs(apq) / sqrt(app * aqq);
-                        if (lane == 0) atomic_max_pos(worst_s, rel);
-                        if (rel > 1e-15) {
-                            const double tau = (aqq - app) / (2.0 * apq);
-                            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                            const double c = 1.0 / sqrt(1.0 + t * t);
+                        // svd.cpp:113-131 with the serial sqrt / divide chain shortened: the
+                        // cosine test |apq| / sqrt(app aqq) > 1e-15 squared (no sqrt, no
+                        // divide), t = sign(tau) / (|tau| + sqrt(1 + tau^2)) with tau =
+                        // zeta / (2 apq) written as 2 apq sign(zeta) / (|zeta| + sqrt(zeta^2 +
+                        // 4 apq^2)) (one sqrt, one divide), c = rsqrt(1 + t^2)
+                        const bool big = apq * apq > 1e-30 * (app * aqq);
+                        if (lane == 0 && big) *worst_s = 1.0;  // (every writer stores the same value)
+                        if (big) {
+                            const double zeta = aqq - app;
+                            const double t = (zeta >= 0.0 ? 2.0 : -2.0) * apq /
+                                             (fabs(zeta) + sqrt(fma(zeta, zeta, 4.0 * apq * apq)));
+                            const double c = rsqrt(fma(t, t, 1.0));
                             const double sn = c * t;
                             if (lane < k) {
                                 Bm[lane + p * KM] = c * bp - sn * bq;
