@@ -22,9 +22,8 @@ namespace {
 
 constexpr int kGramT = 128;    // threads per CTA (4 warps; static shared memory)
 constexpr int kGramW = kGramT / 32;
-// block_gram_reg_kernel: one CTA per SM (num_sms parts); 16 warps for k <= 8, 8 warps for the
-// register-heavier k > 8
-__host__ __device__ constexpr int gram_reg_threads(int k) { return k > 8 ? 256 : 512; }
+constexpr int kGramRegT = 512;  // block_gram_reg_kernel: 16 warps, one CTA per SM -> num_sms parts
+constexpr int kGramRegW = kGramRegT / 32;
 constexpr int kMaxEnt = (kMaxK * (kMaxK + 1) / 2 + 31) / 32;  // Gram entries per lane (<= 10)
 constexpr int kCholT = 512;    // chol_small_kernel threads
 
@@ -122,7 +121,7 @@ __global__ void __launch_bounds__(kGramT) block_gram_kernel(Cols T, int64_t m, i
 // [0, KH) and [KH, K) of the same rows (both halves load and transform the same 16 rows:
 // the same addresses, one transaction).
 template <int K>
-__global__ void __launch_bounds__(gram_reg_threads(K)) block_gram_reg_kernel(Cols T, int64_t m, const double* Rinv, double* Gpart,
+__global__ void __launch_bounds__(kGramRegT) block_gram_reg_kernel(Cols T, int64_t m, const double* Rinv, double* Gpart,
                                                                const int* disabled) {
     if (*disabled) return;
     constexpr int NE = K * (K + 1) / 2;
@@ -132,13 +131,12 @@ __global__ void __launch_bounds__(gram_reg_threads(K)) block_gram_reg_kernel(Col
     constexpr int NA = kHalves ? (NE0 > NE - NE0 ? NE0 : NE - NE0) : NE;  // accumulators per thread
     constexpr int ROWS = kHalves ? 16 : 32;
     __shared__ double ri[K * K];
-    __shared__ double wsum[gram_reg_threads(K) / 32][NE];
-    constexpr int kWarps = gram_reg_threads(K) / 32;
+    __shared__ double wsum[kGramRegW][NE];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (Rinv)
         for (int i = threadIdx.x; i < K * K; i += blockDim.x) ri[i] = Rinv[i];
     __syncthreads();
-    const int64_t gw = static_cast<int64_t>(blockIdx.x) * kWarps + warp, nw = static_cast<int64_t>(gridDim.x) * kWarps;
+    const int64_t gw = static_cast<int64_t>(blockIdx.x) * kGramRegW + warp, nw = static_cast<int64_t>(gridDim.x) * kGramRegW;
     const int64_t r0 = (m * gw) / nw, r1 = (m * (gw + 1)) / nw;
     const bool upper = kHalves && lane >= 16;
     // (volatile: R^-1 is re-read from shared memory per tile; hoisted into registers its
@@ -147,23 +145,12 @@ __global__ void __launch_bounds__(gram_reg_threads(K)) block_gram_reg_kernel(Col
     double acc[NA];
 #pragma unroll
     for (int e = 0; e < NA; ++e) acc[e] = 0.0;
-    // the next tile's row is loaded while the current one is accumulated
-    double tn[K];
-    {
-        const int64_t r = r0 + (lane & (ROWS - 1));
-#pragma unroll
-        for (int j = 0; j < K; ++j) tn[j] = r < r1 ? T.p[j][r] : 0.0;
-    }
 #pragma unroll 1
     for (int64_t base = r0; base < r1; base += ROWS) {
+        const int64_t r = base + (lane & (ROWS - 1));
         double t[K];
 #pragma unroll
-        for (int j = 0; j < K; ++j) t[j] = tn[j];
-        {
-            const int64_t r = base + ROWS + (lane & (ROWS - 1));
-#pragma unroll
-            for (int j = 0; j < K; ++j) tn[j] = r < r1 ? T.p[j][r] : 0.0;
-        }
+        for (int j = 0; j < K; ++j) t[j] = r < r1 ? T.p[j][r] : 0.0;
         if (Rinv) {
 #pragma unroll
             for (int j = K - 1; j >= 0; --j) {  // t <- t R^-1 (upper): column j uses t[0..j]
@@ -203,7 +190,7 @@ __global__ void __launch_bounds__(gram_reg_threads(K)) block_gram_reg_kernel(Col
     double* G = Gpart + static_cast<size_t>(blockIdx.x) * K * K;
     for (int e = threadIdx.x; e < NE; e += blockDim.x) {
         double v = wsum[0][e];
-        for (int w = 1; w < kWarps; ++w) v += wsum[w][e];
+        for (int w = 1; w < kGramRegW; ++w) v += wsum[w][e];
         int q = 0, base = 0;
         while (base + q + 1 <= e) {  // column q holds entries base .. base + q
             base += q + 1;
@@ -408,13 +395,13 @@ void launch_trial_cholqr(Ctx& c, Cols T, int64_t m, int k, TrialQr& q, const Col
     const int parts = static_cast<int>(reg ? rgrid : grid);
     auto gram = [&](const double* Rinv) {
         switch (k) {
-            case 2: block_gram_reg_kernel<2><<<rgrid, gram_reg_threads(2), 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
-            case 3: block_gram_reg_kernel<3><<<rgrid, gram_reg_threads(3), 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
-            case 4: block_gram_reg_kernel<4><<<rgrid, gram_reg_threads(4), 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
-            case 6: block_gram_reg_kernel<6><<<rgrid, gram_reg_threads(6), 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
-            case 8: block_gram_reg_kernel<8><<<rgrid, gram_reg_threads(8), 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
-            case 9: block_gram_reg_kernel<9><<<rgrid, gram_reg_threads(9), 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
-            case 12: block_gram_reg_kernel<12><<<rgrid, gram_reg_threads(12), 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 2: block_gram_reg_kernel<2><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 3: block_gram_reg_kernel<3><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 4: block_gram_reg_kernel<4><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 6: block_gram_reg_kernel<6><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 8: block_gram_reg_kernel<8><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 9: block_gram_reg_kernel<9><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
+            case 12: block_gram_reg_kernel<12><<<rgrid, kGramRegT, 0, c.stream>>>(T, m, Rinv, q.gpart, q.disabled); break;
             default: block_gram_kernel<<<grid, kGramT, 0, c.stream>>>(T, m, k, Rinv, q.gpart, q.disabled); break;
         }
     };
