@@ -25,9 +25,10 @@
 // warps: 16 warps leave 128 each) and the reduction latency of one group hides
 // behind the streaming FMAs of the others.
 //
-// With EX (the check refresh, solver.cpp:439 on the next pass) the ACC warps
-// also accumulate A^T E for the b columns E = A V' of the previous check
-// iterate: gpart holds [grid][2b][n].
+// With EX (the check refresh, solver.cpp:439 on the next pass) a second set of
+// ACC warps accumulates A^T E for the b columns E = A V' of the previous check
+// iterate (they take E from global memory and never wait for the DOT warps):
+// gpart holds [grid][2b][n].
 //
 // Every sum has a fixed order: the pass is bitwise repeatable.
 #include <string>
@@ -47,7 +48,7 @@ struct SplitSmem {
     uint64_t* ydone;
     unsigned* ticket;  // per stage: warps done with it
     double* ypart;  // [stages][TD][kYSlots]
-    double* ebuf;   // [acc warps][2][kYSlots]: the warp's summed y rows and (EX) its E rows
+    double* ebuf;   // [acc warps][kYSlots]: the warp's coefficient rows (summed y, or E)
     unsigned char* stage0;
 };
 
@@ -55,7 +56,7 @@ __host__ __device__ constexpr size_t split_bar_bytes(int stages) {
     return ((24 * static_cast<size_t>(stages) + 127) / 128) * 128;
 }
 __host__ __device__ constexpr size_t split_extra_bytes(int stages, int td, int acc_warps) {
-    return ((sizeof(double) * (static_cast<size_t>(stages) * td + 2 * acc_warps) * kYSlots + 127) / 128) * 128;
+    return ((sizeof(double) * (static_cast<size_t>(stages) * td + acc_warps) * kYSlots + 127) / 128) * 128;
 }
 
 // partial dot products of RG rows starting at `rows` (nr of them valid) against the
@@ -200,10 +201,15 @@ __global__ void __launch_bounds__(32 * G * (TD + TA), 1) apply_split_kernel(Appl
         // (no masks here: a pad column's or a re-read pair's accumulator is never stored)
         const int aw = cw - NDOT;
         const int grp = aw / TA, ha = aw % TA;
-        const int part = (npairs + TA - 1) / TA;
-        const int p0 = ha * part;
+        // EX: the TA members are two sets of TA / 2 -- role 0 accumulates A^T (A W) (it needs the
+        // dot warps' y), role 1 A^T E (E comes from global memory: it never waits for the dot
+        // warps and runs ahead of them, bounded only by the stage ring)
+        constexpr int TAH = EX ? TA / 2 : TA;
+        const int role = EX ? ha / TAH : 0, hh = ha % TAH;
+        const int part = (npairs + TAH - 1) / TAH;
+        const int p0 = hh * part;
         const int pend = min(npairs, p0 + part);
-        double ga[PLA][2][BG];
+        double ga[PLA][2][B];
         int off[PLA];
         bool keepy[PLA], mine[PLA];
 #pragma unroll
@@ -214,13 +220,12 @@ __global__ void __launch_bounds__(32 * G * (TD + TA), 1) apply_split_kernel(Appl
             off[i] = 2 * pc;
             keepy[i] = 2 * pc + 1 < n;
 #pragma unroll
-            for (int j = 0; j < BG; ++j) ga[i][0][j] = ga[i][1][j] = 0.0;
+            for (int j = 0; j < B; ++j) ga[i][0][j] = ga[i][1][j] = 0.0;
         }
-        // this warp's copy of the stage's y rows (the members' partials summed once per
-        // stage) and, with EX, of its E rows: [row][Bp], read back as broadcasts
-        double* yb = p.ebuf + static_cast<size_t>(aw) * 2 * kYSlots;
-        double* eb = yb + kYSlots;
-        // EX: lane l = row * Bp + j of the chunk's E values, one chunk ahead
+        // this warp's copy of the stage's coefficient rows -- y (the members' partials summed
+        // once per stage) or, role 1, its E rows: [row][Bp], read back as broadcasts
+        double* cb = p.ebuf + static_cast<size_t>(aw) * kYSlots;
+        // role 1: lane l = row * Bp + j of the chunk's E values, one chunk ahead
         double en = 0.0;
         auto ex_load = [&](int64_t cc) {
             if (!EX || cc >= nchunks) return;
@@ -229,42 +234,38 @@ __global__ void __launch_bounds__(32 * G * (TD + TA), 1) apply_split_kernel(Appl
             const int row = lane / Bp, j = lane % Bp;
             en = (row < rcc && j < B) ? ex.p[j][rr0 + row] : 0.0;
         };
-        ex_load(grp);
+        if (role == 1) ex_load(grp);
         int s = grp;
         uint32_t ph = 0;
         for (int64_t c = grp; c < nchunks; c += G) {
             const int64_t r0 = r_begin + c * g.rc;
             const int rc = static_cast<int>(min(static_cast<int64_t>(g.rc), r_end - r0));
-            if (EX) {
-                eb[lane] = en;  // (the previous chunk's reads ended at its closing __syncwarp)
+            if (role == 1) {
+                cb[lane] = en;  // (the previous chunk's reads ended at its closing __syncwarp)
                 ex_load(c + G);
+            } else {
+                mbar_wait(&p.ydone[s], ph);
             }
-            mbar_wait(&p.ydone[s], ph);
-            mbar_wait(&p.full[s], ph);  // complete already; this warp's own acquire of the TMA-written rows
-            {
+            mbar_wait(&p.full[s], ph);  // this warp's own acquire of the TMA-written rows
+            if (role == 0) {
                 const double* yp = p.ypart + static_cast<size_t>(s) * TD * kYSlots;
                 double t = yp[lane];
 #pragma unroll
                 for (int mm = 1; mm < TD; ++mm) t += yp[mm * kYSlots + lane];  // members in order: the same bits in every warp
-                yb[lane] = t;
+                cb[lane] = t;
                 const int row = lane / Bp, j = lane % Bp;
-                if (ha == 0 && row < rc && j < B) a.out.p[j][r0 + row] = t;  // the chunk's y = A W rows
+                if (hh == 0 && row < rc && j < B) a.out.p[j][r0 + row] = t;  // the chunk's y = A W rows
             }
             __syncwarp();
             const double* As = reinterpret_cast<const double*>(p.stage0 + s * g.stage_bytes);
 #pragma unroll 2
             for (int r = 0; r < rc; ++r) {
-                double y[Bp], e[Bp];
+                double y[Bp];
 #pragma unroll
                 for (int j2 = 0; j2 < Bp; j2 += 2) {
-                    const double2 t = *reinterpret_cast<const double2*>(yb + r * Bp + j2);
+                    const double2 t = *reinterpret_cast<const double2*>(cb + r * Bp + j2);
                     y[j2] = t.x;
                     y[j2 + 1] = t.y;
-                    if (EX) {
-                        const double2 u = *reinterpret_cast<const double2*>(eb + r * Bp + j2);
-                        e[j2] = u.x;
-                        e[j2 + 1] = u.y;
-                    }
                 }
                 const double* row = As + static_cast<int64_t>(r) * g.ld_s;
 #pragma unroll
@@ -274,10 +275,6 @@ __global__ void __launch_bounds__(32 * G * (TD + TA), 1) apply_split_kernel(Appl
                     for (int j = 0; j < B; ++j) {
                         ga[i][0][j] = fma(x.x, y[j], ga[i][0][j]);
                         ga[i][1][j] = fma(x.y, y[j], ga[i][1][j]);
-                        if constexpr (EX) {
-                            ga[i][0][B + j] = fma(x.x, e[j], ga[i][0][B + j]);
-                            ga[i][1][B + j] = fma(x.y, e[j], ga[i][1][B + j]);
-                        }
                     }
                 }
             }
@@ -296,9 +293,9 @@ __global__ void __launch_bounds__(32 * G * (TD + TA), 1) apply_split_kernel(Appl
             if (!mine[i]) continue;
             const int c0 = off[i];
 #pragma unroll
-            for (int j = 0; j < BG; ++j) {
-                red[(static_cast<size_t>(grp) * BG + j) * n + c0] = ga[i][0][j];
-                if (keepy[i]) red[(static_cast<size_t>(grp) * BG + j) * n + c0 + 1] = ga[i][1][j];
+            for (int j = 0; j < B; ++j) {
+                red[(static_cast<size_t>(grp) * BG + role * B + j) * n + c0] = ga[i][0][j];
+                if (keepy[i]) red[(static_cast<size_t>(grp) * BG + role * B + j) * n + c0 + 1] = ga[i][1][j];
             }
         }
     }
@@ -317,7 +314,7 @@ __global__ void __launch_bounds__(32 * G * (TD + TA), 1) apply_split_kernel(Appl
 template <int B, int PL, int G, bool EX>
 void split_launch(Ctx& c, const ApplyArgs& a, const Cols& ec) {
     constexpr int TD = 2, TA = EX ? 4 : 2;
-    constexpr int PLA = EX ? (PL > 1 ? PL / 2 : 1) : PL;
+    constexpr int PLA = PL;  // EX: two sets of two acc warps (A^T A W and A^T E), half a row each
     constexpr int RG = (B == 2 && PL == 8) ? 2 : 4;
     auto kernel = apply_split_kernel<B, PL, PLA, TD, TA, G, RG, EX>;
     optin_smem(c, kernel);
