@@ -96,6 +96,37 @@ def test_check_refresh_pass_repeatable(msvd, cuda, b, n, env, monkeypatch):
     print(f"[check refresh b={b} n={n} {env}] paths {sorted(paths)}: {REPEATS + 1} identical runs")
 
 
+@pytest.mark.parametrize("m", [1, 7, 150, 1001, 5000])
+@pytest.mark.parametrize("b,n", [(4, 500), (2, 1000), (3, 333), (2, 64)])
+def test_one_pass_passes_few_rows(msvd, cuda, b, n, m):
+    """Fewer rows than CTAs, partial stages, partial row groups: the one-pass pass and
+    the check-refresh pass against fp64 torch products."""
+    import torch
+
+    ldp = n + (n & 1)
+    g = torch.Generator(device=cuda).manual_seed(m + 13 * n + b)
+    a = torch.randn(m, ldp, dtype=torch.float64, device=cuda, generator=g)[:, :n]
+    w = torch.randn(n, b, dtype=torch.float64, device=cuda, generator=g)
+    e = torch.randn(m, b, dtype=torch.float64, device=cuda, generator=g)
+    op = msvd.DeviceDenseOperator(a)
+    aw, z = op.aw_gram(w)
+    try:
+        aw2, z2, ze = op.aw_gram_ex(w, e)
+    except msvd.Error as ex:  # a one-row view has ld = n: odd n has no TMA row stream, no such pass
+        assert m == 1 and n % 2 == 1 and "unsupported shape" in str(ex)
+        aw2, z2, ze = aw, z, a.t() @ e
+    aw_ref = a @ w
+    scale = max(aw_ref.abs().max().item(), 1e-300)
+    assert torch.allclose(aw, aw_ref, rtol=0, atol=1e-12 * scale)
+    assert torch.allclose(aw2, aw_ref, rtol=0, atol=1e-12 * scale)
+    z_ref = a.t() @ aw_ref
+    zs = max(z_ref.abs().max().item(), 1e-300)
+    assert torch.allclose(z, z_ref, rtol=0, atol=1e-11 * zs)
+    assert torch.allclose(z2, z_ref, rtol=0, atol=1e-11 * zs)
+    ze_ref = a.t() @ e
+    assert torch.allclose(ze, ze_ref, rtol=0, atol=1e-11 * max(ze_ref.abs().max().item(), 1e-300))
+
+
 @pytest.mark.parametrize("b,n,env", [(1, 1000, {}), (1, 999, {}), (5, 2000, {}), (8, 700, {}),
                                      (1, 1000, {"MSVD_STAGE_KB": "8"})])
 def test_apply_and_gram_repeatable(msvd, cuda, b, n, env, monkeypatch):
