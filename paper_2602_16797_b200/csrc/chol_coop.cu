@@ -10,10 +10,9 @@
 // doubling of the block size (the matrix padded with the identity to
 // 32 * 2^L columns so every level is a regular strided batch).
 //
-// chol_coop_kernel below is a cooperative right-looking blocked Cholesky on
-// 32 x 32 blocks; measured slower than potrf (3.4 vs 1.1 ms at n = 1000,
-// 96 grid-wide barriers), it is kept only behind MSVD_CHOL_COOP = 1.
-#include <cooperative_groups.h>
+// (A cooperative right-looking blocked Cholesky on 32 x 32 blocks measured
+// slower than potrf -- 3.4 vs 1.1 ms at n = 1000, 96 grid-wide barriers -- and
+// was removed in round 2.)
 
 #include <cstdlib>
 #include <string>
@@ -24,137 +23,7 @@
 namespace msvd {
 namespace {
 
-namespace cg = cooperative_groups;
-
 constexpr int kB = 32;        // block size
-constexpr int kCoopT = 256;   // threads per CTA (8 warps)
-
-// out (32 x 32 block, column ld) = s * A^T B for 32 x 32 blocks A, B (lane = column of out):
-// out(r, c) = s * sum_l A(l, r) B(l, c) [+ out(r, c) when acc]
-__device__ __forceinline__ void block_atb(const double* A, int lda, const double* B, int ldb, double* out, int ldo,
-                                          double s, bool acc, double* sh) {
-    const int lane = threadIdx.x & 31;
-    // A staged in shared memory (broadcast reads), B's column in registers
-    for (int i = lane; i < kB * kB; i += 32) sh[i] = A[(i % kB) + (i / kB) * static_cast<int64_t>(lda)];
-    double bc[kB];
-#pragma unroll
-    for (int l = 0; l < kB; ++l) bc[l] = B[l + lane * static_cast<int64_t>(ldb)];
-    __syncwarp();
-    for (int r = 0; r < kB; ++r) {
-        double t = 0.0;
-#pragma unroll
-        for (int l = 0; l < kB; ++l) t += sh[l + r * kB] * bc[l];
-        double* o = out + r + lane * static_cast<int64_t>(ldo);
-        *o = acc ? *o + s * t : s * t;
-    }
-    __syncwarp();
-}
-
-// G (np x np, column-major, upper triangle used) -> R (upper, in place, lower
-// zeroed) and Dinv[K] = R_KK^-1 for every diagonal block.  flag: 1 = success
-__global__ void __launch_bounds__(kCoopT, 1) chol_coop_kernel(double* G, int np, double* Dinv, int* flag) {
-    cg::grid_group grid = cg::this_grid();
-    extern __shared__ double shd[];  // 8 warps x one 32 x 32 staging block (64 KB, dynamic)
-    double* sh[8];
-    for (int w = 0; w < 8; ++w) sh[w] = shd + w * kB * kB;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int gw = blockIdx.x * 8 + warp, nwarps = gridDim.x * 8;
-    const int nb = np / kB;
-    for (int K = 0; K < nb; ++K) {
-        double* GKK = G + static_cast<int64_t>(K) * kB * (np + 1);
-        // A. diagonal block: warp 0 of CTA 0, lane = column
-        if (blockIdx.x == 0 && warp == 0) {
-            double col[kB];
-#pragma unroll
-            for (int i = 0; i < kB; ++i) col[i] = GKK[i + lane * static_cast<int64_t>(np)];
-            bool ok = true;
-#pragma unroll
-            for (int j = 0; j < kB; ++j) {
-                double d = 0.0;
-                if (lane == j) {
-                    double s = col[j];
-#pragma unroll
-                    for (int i = 0; i < j; ++i) s -= col[i] * col[i];
-                    d = s > 0.0 ? sqrt(s) : 0.0;
-                }
-                d = __shfl_sync(0xffffffffu, d, j);
-                if (!(d > 0.0)) ok = false;
-                double s = col[j];
-#pragma unroll
-                for (int i = 0; i < j; ++i) s -= __shfl_sync(0xffffffffu, col[i], j) * col[i];
-                if (lane == j) col[j] = d;
-                else if (lane > j) col[j] = d > 0.0 ? s / d : 0.0;
-            }
-            // write R_KK (upper, lower zeroed) and stage it for the inverse
-            double* R = sh[0];
-#pragma unroll
-            for (int i = 0; i < kB; ++i) {
-                const double v = i <= lane ? col[i] : 0.0;
-                GKK[i + lane * static_cast<int64_t>(np)] = v;
-                R[i + lane * kB] = v;
-            }
-            __syncwarp();
-            // Dinv_K column lane: back substitution R x = e_lane
-            double x[kB];
-#pragma unroll
-            for (int i = kB - 1; i >= 0; --i) {
-                double s = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-                for (int l = i + 1; l < kB; ++l) s -= R[i + l * kB] * x[l];
-                x[i] = i <= lane ? s / R[i + i * kB] : 0.0;
-            }
-            double* D = Dinv + static_cast<int64_t>(K) * kB * kB;
-#pragma unroll
-            for (int i = 0; i < kB; ++i) D[i + lane * kB] = x[i];
-            if (!ok && lane == 0) *flag = 0;
-            __syncwarp();
-        }
-        grid.sync();
-        // B. row panel: R_KJ = Dinv_K^T G_KJ for J > K
-        const double* D = Dinv + static_cast<int64_t>(K) * kB * kB;
-        for (int J = K + 1 + gw; J < nb; J += nwarps) {
-            double* GKJ = G + static_cast<int64_t>(K) * kB + static_cast<int64_t>(J) * kB * np;
-            // out = D^T GKJ, written back in place through a staging copy of GKJ
-            double* sB = sh[warp];
-            for (int i = lane; i < kB * kB; i += 32) sB[i] = GKJ[(i % kB) + (i / kB) * static_cast<int64_t>(np)];
-            __syncwarp();
-            double bc[kB];
-#pragma unroll
-            for (int l = 0; l < kB; ++l) bc[l] = sB[l + lane * kB];
-            __syncwarp();
-            for (int i = lane; i < kB * kB; i += 32) sB[i] = D[i];
-            __syncwarp();
-            for (int r = 0; r < kB; ++r) {
-                double t = 0.0;
-#pragma unroll
-                for (int l = 0; l < kB; ++l) t += sB[l + r * kB] * bc[l];
-                GKJ[r + lane * static_cast<int64_t>(np)] = t;
-            }
-            __syncwarp();
-        }
-        grid.sync();
-        // C. trailing update: G_IJ -= R_KI^T R_KJ for K < I <= J
-        const int nt = nb - K - 1;
-        const int tiles = nt * (nt + 1) / 2;
-        for (int t = gw; t < tiles; t += nwarps) {
-            // t -> (I, J), column-major over the upper triangle of the trailing blocks
-            int jj = 0, base = 0;
-            while (base + jj + 1 <= t) {
-                base += jj + 1;
-                ++jj;
-            }
-            const int I = K + 1 + (t - base), J = K + 1 + jj;
-            block_atb(G + static_cast<int64_t>(K) * kB + static_cast<int64_t>(I) * kB * np, np,
-                      G + static_cast<int64_t>(K) * kB + static_cast<int64_t>(J) * kB * np, np,
-                      G + static_cast<int64_t>(I) * kB + static_cast<int64_t>(J) * kB * np, np, -1.0, true, sh[warp]);
-        }
-        grid.sync();
-    }
-    // zero the strictly lower triangle
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < static_cast<int64_t>(np) * np;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        if (i % np > i / np) G[i] = 0.0;
-}
 
 // Dinv[K] = inverse of the upper triangular 32 x 32 diagonal block K of R
 // (one warp per block, lane = column, back substitution)
@@ -236,21 +105,7 @@ void chol_inverse(Ctx& c, const double* G, int64_t n, double* R, double* Rinv, d
     double* T = X + nn;         // np x np: GEMM scratch
     double* Dinv = T + nn;      // nb x 32 x 32
     pad_kernel<<<blocks_of(nn), 256, 0, c.stream>>>(G, n, np, Gp);
-    const char* ce = std::getenv("MSVD_CHOL_COOP");
-    if (ce && std::atoi(ce) == 1) {
-        const int one_i = 1;
-        MSVD_CUDA(cudaMemcpyAsync(dflag, &one_i, sizeof(int), cudaMemcpyHostToDevice, c.stream));
-        int per_sm = 0;
-        const size_t smem = sizeof(double) * 8 * kB * kB;
-        optin_smem(c, chol_coop_kernel);
-        MSVD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chol_coop_kernel, kCoopT, smem));
-        if (per_sm < 1) fail(MSVD_ERR_CUDA, "msvd: cooperative Cholesky kernel cannot be resident");
-        int npi = np;
-        void* args[] = {&Gp, &npi, &Dinv, &dflag};
-        MSVD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(chol_coop_kernel), c.num_sms, kCoopT, args,
-                                              smem, c.stream));
-        ++c.launches;
-    } else {
+    {
         if (!c.solver && cusolverDnCreate(&c.solver) != CUSOLVER_STATUS_SUCCESS) fail(MSVD_ERR_CUDA, "cusolverDnCreate");
         if (cusolverDnSetStream(c.solver, c.stream) != CUSOLVER_STATUS_SUCCESS) fail(MSVD_ERR_CUDA, "cusolverDnSetStream");
         int lwork = 0;
