@@ -731,6 +731,10 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
     if (o.store_iterates) emit(1, 0, {{Vb[0], b}});
     MSVD_CUDA(cudaEventRecord(c.ev[3], c.stream));
 
+    // early accept (tolerance-only stop, tol well above the images' drift ~1e-15):
+    // MSVD_EARLY_ACCEPT = 0 always confirms on the next pass
+    const bool early_accept = !o.use_stagnation && plan.tol >= 1e-13 &&
+                              !(std::getenv("MSVD_EARLY_ACCEPT") && std::atoi(std::getenv("MSVD_EARLY_ACCEPT")) == 0);
     int cur = 0;  // index of the current V / X / AV / AX buffers
     int status = 1;
     int last_row = 0;
@@ -834,7 +838,10 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
         }
         ca.V = Vb[nxt];
         ca.row = i + 1;
-        ca.check = check_it && !defer;
+        // a deferred check row whose image-based residual is already far under the
+        // tolerance stops here (control_kernel, check = 2): the speculative pass that
+        // would only confirm it is not launched (one pass of A per solve)
+        ca.check = check_it && !defer ? 1 : (defer && early_accept ? 2 : 0);
         launch_control(c, ca);
         last_row = i + 1;
         pending = defer;
@@ -860,6 +867,7 @@ void solve(msvd_matrix* M, const msvd_options& o, const msvd_truth* truth, msvd_
             const DevState h = read_state(c, st);
             if (h.stop) {
                 status = 0;
+                pending = false;
                 break;
             }
         }

@@ -827,7 +827,12 @@ __global__ void __launch_bounds__(256) control_kernel(ControlArgs a) {
     a.rows[a.row] = row;
     a.rh[a.row] = resid_s;
     a.th[a.row] = st->theta[0];
-    if (a.check) {
+    if (a.check == 2) {
+        // early accept of a deferred check row (tolerance-only stop): the residual from the
+        // carried images is within ~u sigma_1^2 of the exact one, so a value a factor four
+        // under the threshold decides the test without the refresh pass
+        st->stop = resid_s <= 0.25 * a.sigma1 * a.sigma1 * a.tol ? 1 : 0;
+    } else if (a.check) {
         int f[4];
         stop_rule(a.rh, a.th, a.row - 1, a.sigma1, a.tol, a.factor, a.use_stag, f);
         st->stop = f[3];
