@@ -225,7 +225,8 @@ __global__ void __launch_bounds__(256, kMinB) gather_slice_kernel(const double* 
                                                                  double* __restrict__ SA, DevState* st, int c0) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t s = static_cast<int64_t>(blockIdx.x) * 8 + warp;
-    if (s >= d) return;
+    c0 += 64 * static_cast<int>(blockIdx.y);  // several slices per launch (small d: fill the SMs)
+    if (s >= d || c0 >= n) return;
     const int64_t e0 = offs[s], e1 = offs[s + 1];
     // the lane's two columns (clamped to n - 1: loaded, result dropped)
     const int colA = c0 + lane, colB = c0 + lane + 32;
@@ -405,8 +406,11 @@ void sketch_dev(Ctx& c, const StreamGeom& g, int64_t row0, int64_t d, int zeta, 
     // algorithmic bytes, but 2.5 -> 8.9 ms: the fast warps idle)
     const int slice = 64;
     const unsigned grid = static_cast<unsigned>(ceil_div(d, 8));
-    for (int c0 = 0; c0 < g.n; c0 += slice) {
-        gather_slice_kernel<8, 4><<<grid, 256, sizeof(uint32_t) * 8 * kIdxCap, c.stream>>>(
+    // a small sketch (d / 8 CTAs of 4 * SMs slots) leaves the SMs half empty and each warp's
+    // chain of load latencies exposed: as many slices per launch as fit resident
+    const int per_launch = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, (4LL * c.num_sms) / grid)));
+    for (int c0 = 0; c0 < g.n; c0 += slice * per_launch) {
+        gather_slice_kernel<8, 4><<<dim3(grid, per_launch), 256, sizeof(uint32_t) * 8 * kIdxCap, c.stream>>>(
             g.A, static_cast<uint32_t>(g.ld * 8), g.n, d, L.offs, L.vals, L.val, SA, st, c0);
         MSVD_CUDA(cudaGetLastError());
         ++c.launches;

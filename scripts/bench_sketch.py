@@ -7,7 +7,7 @@ import os
 import subprocess
 import sys
 
-CASES = [(1_000_000, 1000, 4000), (500_000, 500, 2000), (2_000_000, 1000, 4000)]
+CASES = [(1_000_000, 1000, 4000), (500_000, 500, 2000), (1_000_000, 500, 1000), (10_000, 100, 200)]
 ENVS = [{}]
 
 
