@@ -364,7 +364,7 @@ bool precond_build_chol(Ctx& c, const double* SA, int64_t rows, int64_t n, int b
     MSVD_SOLVER(cusolverDnSetStream(c.solver, c.stream));
     const int in = static_cast<int>(n), ir = static_cast<int>(rows);
     // block widths (small_svd: <= 24): V0 for b = 1 needs only a small guard block
-    const int p = static_cast<int>(std::min<int64_t>(n, b == 1 ? 12 : std::min(24, b + 22)));
+    const int p = static_cast<int>(std::min<int64_t>(n, b == 1 ? 12 : std::min(24, b + 12)));  // b <= 4: at most 16 (the 16-wide small SVD)
     const int ps = static_cast<int>(std::min<int64_t>(n, 24));                    // sigma~_1 block
     const int64_t nn = n * n;
 
