@@ -98,6 +98,34 @@ __global__ void max_diag_kernel(const double* M, int64_t n, double* out) {
         out[0] = m > 0.0 ? m : 1.0;
     }
 }
+// out[0] = min |diag|, out[1] = max |diag| of an n x n matrix (one CTA)
+__global__ void diag_minmax_kernel(const double* M, int64_t n, double* out) {
+    __shared__ double rmin[32], rmax[32];
+    double lo = 1e300, hi = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double v = fabs(M[i + i * n]);
+        lo = v < lo || !(v == v) ? v : lo;  // (a NaN pivot sticks)
+        hi = fmax(hi, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+        lo = l2 < lo || !(l2 == l2) ? l2 : lo;
+        hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        rmin[threadIdx.x >> 5] = lo;
+        rmax[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            lo = rmin[w] < lo || !(rmin[w] == rmin[w]) ? rmin[w] : lo;
+            hi = fmax(hi, rmax[w]);
+        }
+        out[0] = lo;
+        out[1] = hi;
+    }
+}
 // deterministic start block: SplitMix64 (rng.hpp) uniform in [-1, 1), keyed per entry
 __global__ void start_block_kernel(double* X, int64_t count, uint64_t seed) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -438,6 +466,24 @@ bool precond_build_chol(Ctx& c, const double* SA, int64_t rows, int64_t n, int b
     mark();
     chol_inverse(c, R1, n, G, R1inv, cws, info + 5);  // R1 stays: G1 = SA^T SA, reused for sigma~_1
     mark();
+    {
+        // Early refusal (before the second pass, sigma~_1 and V0 are paid for): the Cholesky
+        // failed, or diag(R1) spans more than 1e10 -- min |r_jj| / max |r_jj| >= 1 / kappa(SA),
+        // so the sketch is too ill-conditioned for Cholesky QR2 (a floored or rank-deficient
+        // sketch such as C3's: 8 ms of a refused attempt before this check)
+        diag_minmax_kernel<<<1, 256, 0, c.stream>>>(G, n, resid);
+        ++c.launches;
+        int ok1 = 0;
+        double mm[2] = {0.0, 0.0};
+        MSVD_CUDA(cudaMemcpyAsync(&ok1, info + 5, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        MSVD_CUDA(cudaMemcpyAsync(mm, resid, sizeof(mm), cudaMemcpyDeviceToHost, c.stream));
+        MSVD_CUDA(cudaStreamSynchronize(c.stream));
+        if (ok1 != 1 || !(mm[0] > 1e-10 * mm[1])) {
+            if (timed) std::fprintf(stderr, "msvd chol route: refused after the first Cholesky (ok %d, diag %.3e .. %.3e)\n",
+                                    ok1, mm[0], mm[1]);
+            return false;
+        }
+    }
     MSVD_BLAS(cublasDtrmm(c.blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, ir, in,
                           &one, R1inv, in, SA, ir, Q, ir));  // Q = SA R1^-1
     mark();
